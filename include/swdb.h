@@ -1,0 +1,164 @@
+/*
+ * swdb.h -- C-ABI of the B200-native inter-task Smith-Waterman database search.
+ *
+ * The problem, as the paper states it (Section 4):
+ *   1. "Pre-processing stage: database sequences are pre-processed to allow
+ *      subsequent parallel computation."                       -> sw_db_load
+ *   2. "SW stage: alignments are carried out."                 -> sw_search
+ *   3. "Sorting stage: alignment scores are sorted in descending order."
+ *                                                              -> sw_topk
+ * Each alignment score is the Smith-Waterman local alignment score with
+ * affine gaps of PAPER.md:49-66 (Eqs. 1-3): the maximum over the H matrix of
+ *   H_ij = max{0, H_{i-1,j-1} + SM(q_i, d_j), E_ij, F_ij}
+ *   E_ij = max{H_{i,j-1} - Goe, E_{i,j-1} - Ge}
+ *   F_ij = max{H_{i-1,j} - Goe, F_{i-1,j} - Ge}
+ * with H, E, F = 0 when i = 0 or j = 0, Goe = gap_open + gap_extend and
+ * Ge = gap_extend, so a gap of length k costs gap_open + k*gap_extend
+ * (PAPER.md:66, 179).  The query is S1 (rows i), the database sequence S2
+ * (columns j).
+ *
+ * Conventions shared by every entry point
+ *   - Residue codes are uint8 in 0..23, alphabet "ARNDCQEGHILKMFPSTWYVBZX*"
+ *     (NCBI matrix order).  Codes >= 24 are rejected (SW_EINVAL).
+ *   - The substitution matrix is int8[24*24], row-major, indexed
+ *     matrix[query_code*24 + db_code].  It need not be symmetric.
+ *   - All functions return SW_OK (0) or a negative status; no C++ exception
+ *     or abort crosses this boundary.  sw_last_error() returns a message for
+ *     the most recent failing call of the calling thread.
+ *   - One database per process, held on the CUDA device that is current for
+ *     the calling thread at sw_db_load time.  Multi-GPU = one process per GPU,
+ *     each loading its own shard (the Python harness shards and merges).
+ *   - The library is not reentrant: calls must be serialised by the caller.
+ *   - Host pointers are only read during the call (inputs are copied); the
+ *     caller keeps ownership of every buffer it passes.
+ */
+#ifndef SWDB_H
+#define SWDB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SW_OK = 0,
+  SW_EINVAL = -1,  /* bad argument: NULL pointer, bad size, code >= 24, ... */
+  SW_ENOMEM = -2,  /* host or device allocation failed                    */
+  SW_ECUDA = -3,   /* CUDA runtime error (no device, launch failure, ...)  */
+  SW_ENODB = -4,   /* sw_search* called before a successful sw_db_load     */
+  SW_ESTATE = -5   /* sw_topk called before a successful search            */
+};
+
+#define SW_ALPHA 24
+
+/*
+ * sw_db_load -- pre-processing stage.
+ *   residues : host, uint8[offsets[count]]; sequence i is
+ *              residues[offsets[i] .. offsets[i+1]).  Codes < 24.
+ *   offsets  : host, int64[count+1], offsets[0] == 0, non-decreasing.
+ *              Zero-length sequences are accepted (they score 0).
+ *   count    : number of sequences, >= 1, < 2^31.
+ * Builds the device-resident, length-balanced, residue-interleaved stream
+ * image on the current CUDA device.  Replaces any
+ * previously loaded database; on error the previous database is kept.
+ * Not part of the timed search.
+ * Errors: SW_EINVAL (NULL, count < 1, bad offsets, code >= 24),
+ *         SW_ENOMEM, SW_ECUDA.
+ */
+int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count);
+
+/* Frees the database and all device buffers.  Safe to call at any time. */
+void sw_db_free(void);
+
+/* Number of sequences / total residues of the loaded database (0 if none). */
+int64_t sw_db_count(void);
+int64_t sw_db_residues(void);
+
+/*
+ * sw_search -- SW stage, synchronous, host buffers.
+ *   query      : host, uint8[qlen], codes < 24, qlen >= 1.
+ *   matrix     : host, int8[24*24], matrix[q*24 + d].
+ *   gap_open   : >= 0.   gap_extend : >= 0.   gap_open + gap_extend < 2^30.
+ *   scores_out : host, int32[count]; scores_out[i] = optimal local alignment
+ *                score of the query against database sequence i (original
+ *                load order), exact (saturated 16-bit lanes are re-scored in
+ *                32-bit).
+ * Copies the query and matrix to the device, runs the kernels on the
+ * library's stream and copies the scores back before returning.
+ * Errors: SW_ENODB, SW_EINVAL (NULL, qlen < 1, code >= 24, negative or too
+ *         large penalties, max|matrix| * min(qlen, longest) >= 2^30),
+ *         SW_ENOMEM, SW_ECUDA.
+ */
+int sw_search(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t gap_open,
+              int32_t gap_extend, int32_t *scores_out);
+
+/*
+ * sw_search_dev -- same as sw_search but stream-ordered and device-resident:
+ *   query, matrix : host pointers (copied, < 6 KB).
+ *   d_scores      : DEVICE pointer, int32[count], written in original order.
+ *   cuda_stream   : cudaStream_t to order the work on (NULL = legacy default).
+ * Returns once all work is enqueued; results are final when the stream
+ * reaches them.  sw_topk after sw_search_dev reads d_scores, which must stay
+ * allocated until then.
+ */
+int sw_search_dev(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t gap_open,
+                  int32_t gap_extend, int32_t *d_scores, void *cuda_stream);
+
+/*
+ * sw_topk -- sorting stage over the last search's scores.
+ *   k         : >= 0; min(k, count) results are written.
+ *   idx_out   : host, int64[k]: original database indices.
+ *   score_out : host, int32[k]: their scores.
+ * Order: score descending, ties by ascending index (reading R5).
+ * k >= count gives the complete sorted order.
+ * Returns the number of results written (>= 0) or a negative status
+ * (SW_EINVAL, SW_ESTATE, SW_ENOMEM, SW_ECUDA).
+ */
+int64_t sw_topk(int64_t k, int64_t *idx_out, int32_t *score_out);
+
+/*
+ * sw_topk_dev -- sorting stage on caller-provided DEVICE arrays (used to merge
+ * per-GPU candidates after the NCCL gather).
+ *   d_scores : device int32[n];  d_index : device int64[n] (distinct indices,
+ *              0 <= index < 2^32), or NULL meaning index = position.
+ *   k        : results wanted; d_idx_out int64[min(k,n)], d_score_out
+ *              int32[min(k,n)] are DEVICE pointers.
+ *   cuda_stream : stream to enqueue on (NULL = legacy default); synchronous
+ *              with respect to that stream on return.
+ * Returns min(k, n) or a negative status.
+ */
+int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, int64_t k,
+                    int64_t *d_idx_out, int32_t *d_score_out, void *cuda_stream);
+
+/*
+ * Statistics of the last search (for the benchmark report):
+ *   stats[0] = rows per query pass (G*R), stats[1] = passes,
+ *   stats[2] = G (lanes per group), stats[3] = R (rows per lane),
+ *   stats[4] = sequences flagged by the 16-bit saturation test and re-scored
+ *              in 32 bit, stats[5] = cells re-scored in 32 bit,
+ *   stats[6] = pair-columns streamed per pass, stats[7] = items.
+ * Returns the number of entries written (<= n).
+ */
+int sw_last_stats(int64_t *stats, int n);
+
+/*
+ * sw_set_tile -- override the (G, R) tile choice for subsequent searches
+ * (tests of tile invariance).  G in {8,16,32}; R must be
+ * one of the compiled row counts (sw_tile_supported).  G = 0 restores the
+ * automatic choice.  Returns SW_OK or SW_EINVAL.
+ */
+int sw_set_tile(int32_t G, int32_t R);
+int sw_tile_supported(int32_t G, int32_t R);
+
+/* Message for the most recent failing call on this thread ("" if none). */
+const char *sw_last_error(void);
+
+/* Library version string. */
+const char *sw_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SWDB_H */
