@@ -143,6 +143,16 @@ int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, 
 int sw_last_stats(int64_t *stats, int n);
 
 /*
+ * Device timing of the last search, from CUDA events recorded on the search
+ * stream (synchronises with it):
+ *   ms[0] = s16x2 pass kernels (start of the first pass .. end of the last),
+ *   ms[1] = whole search on the device (query-profile build .. end of the
+ *           32-bit re-scoring kernel).
+ * Returns the number of entries written (<= n) or a negative status.
+ */
+int sw_last_timing(float *ms, int n);
+
+/*
  * sw_set_tile -- override the (G, R) tile choice for subsequent searches
  * (tests of tile invariance).  G in {8,16,32}; R must be
  * one of the compiled row counts (sw_tile_supported).  G = 0 restores the

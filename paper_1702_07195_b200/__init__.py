@@ -1,0 +1,10 @@
+"""B200-native inter-task Smith-Waterman protein database search
+(arxiv 1702.07195 hot path): C-ABI library libswdb.so + thin binding.
+
+    from paper_1702_07195_b200 import sw_db_load, sw_search, sw_topk
+"""
+from .swdb import (  # noqa: F401
+    EXPORTS, SWError, library_path, load_library, sw_db_count, sw_db_free, sw_db_load,
+    sw_db_residues, sw_last_error, sw_last_stats, sw_last_timing, sw_search, sw_search_dev, sw_set_tile,
+    sw_tile_supported, sw_topk, sw_topk_dev, sw_version,
+)

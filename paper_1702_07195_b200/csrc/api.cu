@@ -1,0 +1,455 @@
+// C-ABI of the B200 Smith-Waterman database search (include/swdb.h).
+//
+// Pipeline per query:
+//   sw_db_load  : pre-processing stage -> device-resident stream image
+//   sw_search   : query profile build -> P s16x2 pass kernels
+//                 -> flag compaction -> exact s32 re-scoring of flagged
+//                 sequences -> scores in original order
+//   sw_topk     : sorting stage
+// All state lives in one process-wide object (one database per process; one
+// process per GPU for multi-GPU runs).  No exception crosses the ABI.
+#include "../../include/swdb.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "swdb_internal.h"
+
+using namespace swdb;
+
+namespace {
+
+thread_local std::string t_err;
+
+int fail(int code, const std::string &msg) {
+  t_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      return fail(_e == cudaErrorMemoryAllocation ? SW_ENOMEM : SW_ECUDA,                \
+                  std::string(#expr) + ": " + cudaGetErrorString(_e));                   \
+    }                                                                                    \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T *p = nullptr;
+  size_t n = 0;  // elements
+  cudaError_t ensure(size_t want) {
+    if (want <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(want, 1) * sizeof(T));
+    if (e == cudaSuccess) n = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct State {
+  bool loaded = false;
+  int device = -1;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  int64_t count = 0, total_res = 0, total_cols = 0, max_len = 0;
+  int num_items = 0;
+  // database image
+  DevBuf<uint32_t> stream_img;
+  DevBuf<Item> items;
+  DevBuf<int32_t> slots;
+  DevBuf<uint8_t> res;      // plain copy, original order (for s32 re-scoring)
+  DevBuf<int64_t> offs;
+  // per search
+  DevBuf<int32_t> scores;   // internal scores (sw_search)
+  DevBuf<uint8_t> flagged;
+  DevBuf<int32_t> flag_list;
+  DevBuf<int> counters;     // [0..P) pass cursors, [kMaxPass] flag count, [+1] sw32 cursor
+  DevBuf<int64_t> cells32;
+  DevBuf<uint8_t> query;
+  DevBuf<int8_t> matrix;
+  DevBuf<uint32_t> qp;
+  DevBuf<uint4> desc;
+  DevBuf<int32_t> qp32;
+  DevBuf<uint2> bnd;        // 2 * total_cols
+  DevBuf<uint2> scratch32;
+  DevBuf<uint64_t> keys;
+  DevBuf<uint64_t> keys2;
+  DevBuf<int64_t> tk_idx;
+  DevBuf<int32_t> tk_score;
+  int64_t scratch_stride = 0;
+  int sw32_grid = 0;
+  // last search
+  bool has_search = false;
+  const int32_t *last_scores = nullptr;
+  cudaStream_t last_stream = nullptr;
+  int last_G = 0, last_R = 0, last_P = 0;
+  int64_t last_flags = -1, last_cells32 = -1;
+  // forced tile
+  int force_G = 0, force_R = 0;
+  // timing events of the last search
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+  void release_all() {
+    stream_img.release(); items.release(); slots.release(); res.release(); offs.release();
+    scores.release(); flagged.release(); flag_list.release(); counters.release(); cells32.release();
+    query.release(); matrix.release(); qp.release(); desc.release(); qp32.release(); bnd.release();
+    scratch32.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
+    loaded = false;
+    has_search = false;
+    last_scores = nullptr;
+  }
+};
+
+State g;
+constexpr int kMaxPass = 4096;
+bool g_kernels_ready = false;
+
+int ensure_device_ready() {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (!g_kernels_ready) {
+    CUDA_TRY(init_kernels());
+    g_kernels_ready = true;
+  }
+  return SW_OK;
+}
+
+// Choose (G, R) for a query of m residues: minimise the issued lane-
+// instructions P * G * (5.5 R + overhead).
+int choose_tile(int m) {
+  if (g.force_G) {
+    int ti = find_tile(g.force_G, g.force_R);
+    if (ti >= 0) return ti;
+  }
+  double best = 1e300;
+  int bi = 0;
+  for (int i = 0; i < num_tiles(); ++i) {
+    const TileInfo ti = tile(i);
+    if (tile_ctas_per_sm(i) < 1) continue;
+    const int rows = ti.G * ti.R;
+    const int P = (m + rows - 1) / rows;
+    const double cost = (double)P * ti.G * (5.5 * ti.R + 12.0) + P * 200.0;
+    if (cost < best - 1e-9) {
+      best = cost;
+      bi = i;
+    }
+  }
+  return bi;
+}
+
+int validate_query(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t gap_open,
+                   int32_t gap_extend) {
+  if (!query || !matrix) return fail(SW_EINVAL, "query or matrix is NULL");
+  if (qlen < 1) return fail(SW_EINVAL, "qlen must be >= 1");
+  if (gap_open < 0 || gap_extend < 0) return fail(SW_EINVAL, "gap penalties must be >= 0");
+  if ((int64_t)gap_open + gap_extend >= (int64_t(1) << 30))
+    return fail(SW_EINVAL, "gap_open + gap_extend must be < 2^30");
+  for (int32_t i = 0; i < qlen; ++i)
+    if (query[i] >= kAlpha) return fail(SW_EINVAL, "query code >= 24 at position " + std::to_string(i));
+  int smax = 0;
+  for (int i = 0; i < kAlpha * kAlpha; ++i) smax = std::max(smax, std::abs((int)matrix[i]));
+  if ((int64_t)smax * std::min<int64_t>(qlen, std::max<int64_t>(g.max_len, 1)) >= (int64_t(1) << 30))
+    return fail(SW_EINVAL, "max|matrix| * min(qlen, longest sequence) must be < 2^30");
+  return SW_OK;
+}
+
+int search_impl(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t gap_open,
+                int32_t gap_extend, int32_t *d_scores, cudaStream_t st) {
+  int rc = validate_query(query, qlen, matrix, gap_open, gap_extend);
+  if (rc) return rc;
+  int dev = -1;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev != g.device) return fail(SW_EINVAL, "current CUDA device differs from the one sw_db_load used");
+
+  const int ti = choose_tile(qlen);
+  const TileInfo T = tile(ti);
+  const int rows = T.G * T.R;
+  const int P = (qlen + rows - 1) / rows;
+  if (P > kMaxPass) return fail(SW_EINVAL, "query too long");
+  const int K = (T.R + 3) / 4;
+  const int P32 = (qlen + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
+  const int mpad32 = P32 * 32 * kSW32Rows;
+  int smax = 1;
+  for (int i = 0; i < kAlpha * kAlpha; ++i) smax = std::max(smax, (int)matrix[i]);
+  const int thresh = 32768 - smax;
+  const int goe = gap_open + gap_extend, ge = gap_extend;
+
+  CUDA_TRY(g.query.ensure((size_t)qlen));
+  CUDA_TRY(g.matrix.ensure(kAlpha * kAlpha));
+  CUDA_TRY(g.qp.ensure((size_t)P * kNL * K * T.G * 4));
+  CUDA_TRY(g.desc.ensure((size_t)kNL * kNL * 2));
+  CUDA_TRY(g.qp32.ensure((size_t)kNL * mpad32));
+  if (P > 1) CUDA_TRY(g.bnd.ensure((size_t)g.total_cols * 2));
+
+  CUDA_TRY(cudaMemcpyAsync(g.query.p, query, (size_t)qlen, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(g.matrix.p, matrix, kAlpha * kAlpha, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(g.counters.p, 0, sizeof(int) * (kMaxPass + 2), st));
+  CUDA_TRY(cudaMemsetAsync(g.flagged.p, 0, (size_t)g.count, st));
+  CUDA_TRY(cudaMemsetAsync(g.cells32.p, 0, sizeof(int64_t), st));
+  if (!g.ev[0])
+    for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g.ev[i]));
+  CUDA_TRY(cudaEventRecord(g.ev[0], st));
+  CUDA_TRY(launch_qp_build(g.query.p, qlen, g.matrix.p, T.G, T.R, P, std::min(goe, 32767),
+                           std::min(ge, 32767), g.qp.p, g.desc.p, g.qp32.p, mpad32, st));
+
+  const int grid = g.num_sms * std::max(1, tile_ctas_per_sm(ti));
+  CUDA_TRY(cudaEventRecord(g.ev[1], st));
+  for (int pass = 0; pass < P; ++pass) {
+    SW16Params p;
+    p.stream = g.stream_img.p;
+    p.items = g.items.p;
+    p.num_items = g.num_items;
+    p.counter = g.counters.p + pass;
+    p.slots = g.slots.p;
+    p.qp = reinterpret_cast<const uint4 *>(g.qp.p);
+    p.desc = g.desc.p;
+    p.bnd_in = pass == 0 ? nullptr : g.bnd.p + (size_t)((pass - 1) & 1) * g.total_cols;
+    p.bnd_out = pass == P - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * g.total_cols;
+    p.scores = d_scores;
+    p.flagged = g.flagged.p;
+    p.pass = pass;
+    p.thresh = thresh;
+    p.zero = 0u;
+    CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
+  }
+  CUDA_TRY(cudaEventRecord(g.ev[2], st));
+  CUDA_TRY(launch_flag_compact(g.flagged.p, g.count, g.flag_list.p, g.counters.p + kMaxPass, st));
+  SW32Params q;
+  q.flag_list = g.flag_list.p;
+  q.flag_count = g.counters.p + kMaxPass;
+  q.cursor = g.counters.p + kMaxPass + 1;
+  q.res = g.res.p;
+  q.offs = g.offs.p;
+  q.qp32 = g.qp32.p;
+  q.mpad = mpad32;
+  q.passes = P32;
+  q.neg_goe = -goe;
+  q.neg_ge = -ge;
+  q.scratch = g.scratch32.p;
+  q.stride = g.scratch_stride;
+  q.scores = d_scores;
+  q.cells = g.cells32.p;
+  CUDA_TRY(launch_sw32(g.sw32_grid, q, st));
+  CUDA_TRY(cudaEventRecord(g.ev[3], st));
+
+  g.has_search = true;
+  g.last_scores = d_scores;
+  g.last_stream = st;
+  g.last_G = T.G;
+  g.last_R = T.R;
+  g.last_P = P;
+  g.last_flags = -1;
+  g.last_cells32 = -1;
+  return SW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *sw_last_error(void) { return t_err.c_str(); }
+const char *sw_version(void) { return "swdb-b200 0.1 (sm_100a)"; }
+
+void sw_db_free(void) {
+  if (g.loaded || g.stream) {
+    g.release_all();
+    if (g.stream) cudaStreamDestroy(g.stream);
+    g.stream = nullptr;
+  }
+  g.loaded = false;
+}
+
+int64_t sw_db_count(void) { return g.loaded ? g.count : 0; }
+int64_t sw_db_residues(void) { return g.loaded ? g.total_res : 0; }
+
+int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
+  t_err.clear();
+  std::string err;
+  if (validate_db(residues, offsets, count, err)) return fail(SW_EINVAL, err);
+  int rc = ensure_device_ready();
+  if (rc) return rc;
+  int dev = 0, nsm = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  // Items are sized for the number of lane groups that run concurrently with
+  // the widest-occupancy tile (4 groups per warp at G = 8, 16 warps per SM).
+  const int64_t target_groups = (int64_t)nsm * 16 * 2;
+  HostImage img;
+  try {
+    if (build_image(residues, offsets, count, target_groups, img, err)) return fail(SW_EINVAL, err);
+  } catch (const std::bad_alloc &) {
+    return fail(SW_ENOMEM, "host allocation failed in the pre-processor");
+  } catch (const std::exception &e) {
+    return fail(SW_EINVAL, e.what());
+  }
+  if (img.items.size() >= (size_t)INT_MAX) return fail(SW_EINVAL, "too many work items");
+  // replace the previous database
+  sw_db_free();
+  g.device = dev;
+  g.num_sms = nsm;
+  CUDA_TRY(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+  g.count = count;
+  g.total_res = offsets[count];
+  g.total_cols = img.total_cols;
+  g.max_len = img.max_len;
+  g.num_items = (int)img.items.size();
+  CUDA_TRY(g.stream_img.ensure(img.stream.size()));
+  CUDA_TRY(g.items.ensure(img.items.size()));
+  CUDA_TRY(g.slots.ensure(img.slots.size()));
+  CUDA_TRY(g.res.ensure((size_t)g.total_res));
+  CUDA_TRY(g.offs.ensure((size_t)count + 1));
+  CUDA_TRY(g.scores.ensure((size_t)count));
+  CUDA_TRY(g.flagged.ensure((size_t)count));
+  CUDA_TRY(g.flag_list.ensure((size_t)count));
+  CUDA_TRY(g.counters.ensure(kMaxPass + 2));
+  CUDA_TRY(g.cells32.ensure(1));
+  CUDA_TRY(cudaMemcpy(g.stream_img.p, img.stream.data(), img.stream.size() * sizeof(uint32_t),
+                      cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(g.items.p, img.items.data(), img.items.size() * sizeof(Item), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(g.slots.p, img.slots.data(), img.slots.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (g.total_res > 0)
+    CUDA_TRY(cudaMemcpy(g.res.p, residues, (size_t)g.total_res, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(g.offs.p, offsets, ((size_t)count + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  // s32 re-scoring scratch: one warp per 8 per SM, 2 boundary rows each
+  g.sw32_grid = nsm * 2;  // 2 CTAs x 8 warps per SM
+  g.scratch_stride = g.max_len + 64;
+  const int64_t nwarps32 = (int64_t)g.sw32_grid * (kSW32Threads / 32);
+  CUDA_TRY(g.scratch32.ensure((size_t)(nwarps32 * 2 * g.scratch_stride)));
+  CUDA_TRY(cudaDeviceSynchronize());
+  g.loaded = true;
+  return SW_OK;
+}
+
+int sw_search_dev(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t gap_open,
+                  int32_t gap_extend, int32_t *d_scores, void *cuda_stream) {
+  t_err.clear();
+  if (!g.loaded) return fail(SW_ENODB, "no database loaded");
+  if (!d_scores) return fail(SW_EINVAL, "d_scores is NULL");
+  return search_impl(query, qlen, matrix, gap_open, gap_extend, d_scores, (cudaStream_t)cuda_stream);
+}
+
+int sw_search(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t gap_open,
+              int32_t gap_extend, int32_t *scores_out) {
+  t_err.clear();
+  if (!g.loaded) return fail(SW_ENODB, "no database loaded");
+  if (!scores_out) return fail(SW_EINVAL, "scores_out is NULL");
+  int rc = search_impl(query, qlen, matrix, gap_open, gap_extend, g.scores.p, g.stream);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(scores_out, g.scores.p, (size_t)g.count * sizeof(int32_t),
+                           cudaMemcpyDeviceToHost, g.stream));
+  CUDA_TRY(cudaStreamSynchronize(g.stream));
+  return SW_OK;
+}
+
+int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, int64_t k,
+                    int64_t *d_idx_out, int32_t *d_score_out, void *cuda_stream) {
+  t_err.clear();
+  if (!d_scores || n < 0 || k < 0) return fail(SW_EINVAL, "bad arguments");
+  if (n >= (int64_t(1) << 32)) return fail(SW_EINVAL, "n must be < 2^32");
+  const int64_t kk = std::min(k, n);
+  if (kk == 0) return 0;
+  if (!d_idx_out || !d_score_out) return fail(SW_EINVAL, "output pointers are NULL");
+  int rc = ensure_device_ready();
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (kk <= 32) {
+    const int nw1 = (int)((std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)) + 7) / 8 * 8);
+    CUDA_TRY(g.keys.ensure((size_t)nw1 * kk));
+    CUDA_TRY(g.keys2.ensure((size_t)kk));
+    CUDA_TRY(launch_warp_topk(d_scores, d_index, nullptr, n, (int)kk, g.keys.p, nw1, st));
+    CUDA_TRY(launch_warp_topk(nullptr, nullptr, g.keys.p, (int64_t)nw1 * kk, (int)kk, g.keys2.p, 1, st));
+    CUDA_TRY(launch_decode_keys(g.keys2.p, kk, d_idx_out, d_score_out, st));
+  } else {
+    int64_t np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    if (np2 < 2) np2 = 2;
+    CUDA_TRY(g.keys.ensure((size_t)np2));
+    CUDA_TRY(launch_make_keys(d_scores, d_index, n, g.keys.p, np2, st));
+    CUDA_TRY(launch_bitonic_sort_desc(g.keys.p, np2, st));
+    CUDA_TRY(launch_decode_keys(g.keys.p, kk, d_idx_out, d_score_out, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return kk;
+}
+
+int64_t sw_topk(int64_t k, int64_t *idx_out, int32_t *score_out) {
+  t_err.clear();
+  if (k < 0) return fail(SW_EINVAL, "k must be >= 0");
+  if (!g.loaded || !g.has_search) return fail(SW_ESTATE, "no completed search");
+  const int64_t kk = std::min(k, g.count);
+  if (kk == 0) return 0;
+  if (!idx_out || !score_out) return fail(SW_EINVAL, "output pointers are NULL");
+  CUDA_TRY(g.tk_idx.ensure((size_t)kk));
+  CUDA_TRY(g.tk_score.ensure((size_t)kk));
+  int64_t r = sw_topk_dev(g.last_scores, nullptr, g.count, kk, g.tk_idx.p, g.tk_score.p, g.last_stream);
+  if (r < 0) return r;
+  CUDA_TRY(cudaMemcpy(idx_out, g.tk_idx.p, (size_t)kk * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(score_out, g.tk_score.p, (size_t)kk * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  return kk;
+}
+
+int sw_last_stats(int64_t *stats, int n) {
+  t_err.clear();
+  if (!stats || n < 0) return fail(SW_EINVAL, "bad arguments");
+  if (g.has_search && g.last_flags < 0) {
+    int fc = 0;
+    int64_t cells = 0;
+    CUDA_TRY(cudaStreamSynchronize(g.last_stream));
+    CUDA_TRY(cudaMemcpy(&fc, g.counters.p + kMaxPass, sizeof(int), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(&cells, g.cells32.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    g.last_flags = fc;
+    g.last_cells32 = cells;
+  }
+  const int64_t v[8] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
+                        g.last_flags, g.last_cells32, g.total_cols, g.num_items};
+  const int m = std::min(n, 8);
+  for (int i = 0; i < m; ++i) stats[i] = v[i];
+  return m;
+}
+
+int sw_last_timing(float *ms, int n) {
+  t_err.clear();
+  if (!ms || n < 0) return fail(SW_EINVAL, "bad arguments");
+  if (!g.has_search || !g.ev[0]) return fail(SW_ESTATE, "no completed search");
+  CUDA_TRY(cudaEventSynchronize(g.ev[3]));
+  float a = 0.f, b = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&a, g.ev[1], g.ev[2]));
+  CUDA_TRY(cudaEventElapsedTime(&b, g.ev[0], g.ev[3]));
+  const float v[2] = {a, b};
+  const int m = std::min(n, 2);
+  for (int i = 0; i < m; ++i) ms[i] = v[i];
+  return m;
+}
+
+int sw_set_tile(int32_t G, int32_t R) {
+  t_err.clear();
+  if (G == 0) {
+    g.force_G = g.force_R = 0;
+    return SW_OK;
+  }
+  if (find_tile(G, R) < 0) return fail(SW_EINVAL, "tile not compiled");
+  g.force_G = G;
+  g.force_R = R;
+  return SW_OK;
+}
+
+int sw_tile_supported(int32_t G, int32_t R) { return find_tile(G, R) >= 0 ? 1 : 0; }
+
+}  // extern "C"

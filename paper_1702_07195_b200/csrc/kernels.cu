@@ -1,0 +1,562 @@
+// sm_100a kernels of the inter-task Smith-Waterman database search.
+//
+// The recurrence (Eqs. 1-3), per cell (i = query row, j =
+// database column), in the equivalent relu form (readings R2, R6):
+//   H_ij = max{0, H_{i-1,j-1} + SM(q_i, d_j), E_ij, F_ij}
+//   E_{i,j+1} = max{E_ij - Ge, max(H_ij - Goe, 0)}
+//   F_{i+1,j} = max{F_ij - Ge, max(H_ij - Goe, 0)}
+//   S = max over all H_ij
+// is evaluated on packed s16x2 registers: each 32-bit value holds the same
+// cell of two different database sequences ("halves" A and B, inter-task
+// parallelism), with the Blackwell DPX instructions
+// VIADDMNMX.S16x2(.RELU) / VIMNMX.S16x2 / VIMNMX3.S16x2 -- 5.5 DPX per pair of
+// cells.  DPX adds wrap instead of saturating (R7): a sequence whose
+// 16-bit score reaches T = 32768 - smax is flagged and re-scored exactly by
+// the s32 kernel ("recalculated using the next wider integer
+// range").
+//
+// Mapping: a *group* of G lanes (G in 8/16/32)
+// is a systolic array over the query: lane t owns R consecutive query rows
+// of the current pass, keeps H and E of its rows in registers, and passes the
+// bottom-row (H, F), the column word and the running score chain to lane t+1
+// with one SHFL each per column.  A group streams one work item (two lane
+// streams of whole sequences separated by END/NUL columns) at a time, claimed
+// longest-first from an atomic counter (PAPER.md:119 dynamic distribution).
+// The substitution scores come from a query profile in shared
+// memory, one zero-extended int16 per (letter, row) word, so that packing the
+// two halves is one IMAD on the FMA pipe instead of a PRMT on the ALU pipe
+// (the ALU pipe is the bound: 64 lane-ops/clk/SM for DPX, measured).
+#include "kernels.cuh"
+
+#include <climits>
+#include <cstdio>
+
+namespace swdb {
+
+namespace {
+
+constexpr int kThreads = 512;
+constexpr uint32_t kNulWord = (uint32_t)((kNul * kNL + kNul) * kDescBytes);
+
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// s16x2 pass kernel: query rows [pass*G*R, (pass+1)*G*R) against every item.
+// ---------------------------------------------------------------------------
+template <int R, int G>
+__global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params p) {
+  constexpr int K = (R + 3) / 4;            // uint4 (4-row) chunks per lane
+  constexpr int QP_U4 = kNL * K * G;        // profile slice of one pass
+  constexpr int DESC_U4 = kNL * kNL * 2;
+  extern __shared__ uint4 smem[];
+  uint4 *s_desc = smem;
+  uint4 *s_qp = smem + DESC_U4;
+  {
+    const uint4 *gq = p.qp + (size_t)p.pass * QP_U4;
+    for (int i = threadIdx.x; i < DESC_U4; i += blockDim.x) s_desc[i] = p.desc[i];
+    for (int i = threadIdx.x; i < QP_U4; i += blockDim.x) s_qp[i] = gq[i];
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int t = lane & (G - 1);
+  const int gbase = lane & ~(G - 1);
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << gbase);
+  const bool first = t == 0;
+  const bool last = t == G - 1;
+  const uint32_t nfirst = first ? 0u : 1u;
+  const uint32_t zero = p.zero;
+  const char *desc_b = reinterpret_cast<const char *>(s_desc);
+  const char *qp_b = reinterpret_cast<const char *>(s_qp) + t * 16;
+  const bool has_bin = p.bnd_in != nullptr;
+  const bool has_bout = p.bnd_out != nullptr;
+
+  uint32_t H[R], E[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) { H[r] = 0u; E[r] = 0u; }
+  uint32_t S = 0u, hout = 0u, fout = 0u, sc = 0u, hprev = 0u;
+  uint32_t cw = kNulWord;
+
+  int64_t col0 = 0;
+  int s = 0, nsteps = 0;
+  int seqA = 0, seqB = 0, kA = 0, kB = 0;
+  bool done = false;
+  bool ld_on = false, st_on = false;
+  uint32_t sring[4] = {0u, 0u, 0u, 0u};
+  uint2 bring[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) bring[u] = make_uint2(0u, 0u);
+
+  for (;;) {
+    if (s >= nsteps) {  // group-uniform: claim the next work item
+      int it = 0;
+      if (first) it = atomicAdd(p.counter, 1);
+      it = __shfl_sync(gmask, it, gbase);
+      if (it < p.num_items) {
+        const Item item = p.items[it];
+        col0 = item.col_begin;
+        seqA = item.seqA;
+        seqB = item.seqB;
+        kA = 0;
+        kB = 0;
+        s = 0;
+        nsteps = (item.ncols + G - 1 + 3) & ~3;
+        ld_on = first;
+        st_on = last && has_bout;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          sring[u] = first ? p.stream[col0 + u] : 0u;
+          bring[u] = (first && has_bin) ? p.bnd_in[col0 + u] : make_uint2(0u, 0u);
+        }
+      } else {
+        done = true;
+        nsteps = INT_MAX;
+        ld_on = false;
+        st_on = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          sring[u] = first ? kNulWord : 0u;
+          bring[u] = make_uint2(0u, 0u);
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      // ---- inputs of this column from lane t-1 (lane 0: stream / boundary)
+      const uint32_t cw_up = __shfl_up_sync(0xffffffffu, cw, 1, G);
+      const uint32_t hu_up = __shfl_up_sync(0xffffffffu, hout, 1, G);
+      const uint32_t fu_up = __shfl_up_sync(0xffffffffu, fout, 1, G);
+      const uint32_t sc_up = __shfl_up_sync(0xffffffffu, sc, 1, G);
+      cw = imad(cw_up, nfirst, sring[u]);
+      const uint32_t hu = imad(hu_up, nfirst, bring[u].x);
+      uint32_t F = imad(fu_up, nfirst, bring[u].y);
+      const uint32_t sc_in = imad(sc_up, nfirst, 0u);
+      // prefetch 4 columns ahead (lane 0 only; NUL padding makes it in-bounds)
+      if (ld_on) {
+        sring[u] = p.stream[col0 + s + u + 4];
+        if (has_bin) bring[u] = p.bnd_in[col0 + s + u + 4];
+      }
+      // ---- column descriptor: profile offsets, gap penalties, END flags
+      const uint4 d0 = *reinterpret_cast<const uint4 *>(desc_b + cw);
+      const uint2 d1 = *reinterpret_cast<const uint2 *>(desc_b + cw + 16);
+      const char *pa = qp_b + d0.x;
+      const char *pb = qp_b + d0.y;
+      uint32_t hd = hprev;
+      hprev = hu;
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const uint4 a = *reinterpret_cast<const uint4 *>(pa + kk * G * 16);
+        const uint4 b = *reinterpret_cast<const uint4 *>(pb + kk * G * 16);
+        const uint32_t av[4] = {a.x, a.y, a.z, a.w};
+        const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = kk * 4 + e;
+          if (r < R) {
+            const uint32_t sub = imad(bv[e], 65536u, av[e]);   // (SM_A, SM_B)
+            uint32_t h = __viaddmax_s16x2_relu(hd, sub, E[r]);  // max(Hdiag+SM, E, 0)
+            h = __vmaxs2(h, F);                                 // Eq. 1
+            hd = H[r];
+            H[r] = h;
+            const uint32_t hg = __viaddmax_s16x2_relu(h, d0.z, zero);  // max(H-Goe, 0)
+            E[r] = __viaddmax_s16x2(E[r], d0.w, hg);                   // Eq. 2 (next column)
+            F = __viaddmax_s16x2(F, d0.w, hg);                         // Eq. 3 (next row)
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r + 1 < R; r += 2) S = __vimax3_s16x2(S, H[r], H[r + 1]);
+      if (R & 1) S = __vmaxs2(S, H[R - 1]);
+      hout = H[R - 1];
+      fout = F;
+      sc = __vmaxs2(sc_in, S);   // running max over lanes 0..t (valid at END columns)
+      S &= d1.x;                 // reset the half(s) whose sequence ended
+      if (st_on) p.bnd_out[col0 + s + u - (G - 1)] = make_uint2(hout, fout);
+      if (last && d1.y != 0u) {  // END column reached the last lane: emit
+        if (d1.y & 1u) {
+          const int orig = p.slots[seqA + kA];
+          ++kA;
+          const int v = (int)(sc & 0xffffu);
+          if (p.pass == 0) p.scores[orig] = v;
+          else p.scores[orig] = max(p.scores[orig], v);
+          if (v >= p.thresh) p.flagged[orig] = 1;
+        }
+        if (d1.y & 2u) {
+          const int orig = p.slots[seqB + kB];
+          ++kB;
+          const int v = (int)(sc >> 16);
+          if (p.pass == 0) p.scores[orig] = v;
+          else p.scores[orig] = max(p.scores[orig], v);
+          if (v >= p.thresh) p.flagged[orig] = 1;
+        }
+      }
+    }
+    s += 4;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exact s32 re-scoring of flagged sequences: one warp (G = 32
+// lanes x R rows) per sequence, read from the plain database copy; passes
+// over the query in-kernel with the (H, F) boundary in per-warp scratch.
+// ---------------------------------------------------------------------------
+template <int R>
+__global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) {
+  constexpr int K = (R + 3) / 4;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const bool first = lane == 0, last = lane == 31;
+  const int nfirst = first ? 0 : 1;
+  uint2 *buf0 = p.scratch + (size_t)gwarp * 2 * p.stride + 32;
+  uint2 *buf1 = buf0 + p.stride;
+  const int32_t *qp = p.qp32 + lane * R;
+  constexpr int kDummy = -(1 << 30);
+
+  for (;;) {
+    int idx = 0;
+    if (first) idx = atomicAdd(p.cursor, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= *p.flag_count) break;
+    const int orig = p.flag_list[idx];
+    const int64_t beg = p.offs[orig];
+    const int n = (int)(p.offs[orig + 1] - beg);
+    const uint8_t *res = p.res + beg;
+    int best = 0;
+    for (int pass = 0; pass < p.passes; ++pass) {
+      const uint2 *bin = pass == 0 ? nullptr : ((pass & 1) ? buf0 : buf1);
+      uint2 *bout = pass == p.passes - 1 ? nullptr : ((pass & 1) ? buf1 : buf0);
+      const int32_t *qpp = qp + pass * 32 * R;
+      int H[R], E[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) { H[r] = 0; E[r] = 0; }
+      int S = 0, hout = 0, fout = 0, hprev = 0, code = kNul;
+      const int nsteps = n + 31;
+      for (int c = 0; c < nsteps; ++c) {
+        const int code_up = __shfl_up_sync(0xffffffffu, code, 1);
+        const int hu_up = __shfl_up_sync(0xffffffffu, hout, 1);
+        const int fu_up = __shfl_up_sync(0xffffffffu, fout, 1);
+        int mycode = kNul, bh = 0, bf = 0;
+        if (first && c < n) {
+          mycode = res[c];
+          if (bin) { const uint2 b = bin[c]; bh = (int)b.x; bf = (int)b.y; }
+        }
+        code = first ? mycode : code_up;
+        const int hu = hu_up * nfirst + bh;
+        int F = fu_up * nfirst + bf;
+        const int32_t *q = qpp + code * p.mpad;
+        int hd = hprev;
+        hprev = hu;
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+          const int4 a = __ldg(reinterpret_cast<const int4 *>(q + kk * 4));
+          const int av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = kk * 4 + e;
+            if (r < R) {
+              int h = __viaddmax_s32_relu(hd, av[e], E[r]);
+              h = max(h, F);
+              hd = H[r];
+              H[r] = h;
+              const int hg = __viaddmax_s32_relu(h, p.neg_goe, 0);
+              E[r] = __viaddmax_s32(E[r], p.neg_ge, hg);
+              F = __viaddmax_s32(F, p.neg_ge, hg);
+            }
+          }
+        }
+#pragma unroll
+        for (int r = 0; r + 1 < R; r += 2) S = __vimax3_s32(S, H[r], H[r + 1]);
+        if (R & 1) S = max(S, H[R - 1]);
+        hout = H[R - 1];
+        fout = F;
+        if (last && bout) bout[c - 31] = make_uint2((uint32_t)hout, (uint32_t)fout);
+      }
+      best = max(best, S);
+      __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (first) {
+      p.scores[orig] = best;
+      if (p.cells) atomicAdd(reinterpret_cast<unsigned long long *>(p.cells),
+                             (unsigned long long)n * (unsigned long long)(p.passes * 32 * R));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Query profile ("auxiliary two-dimensional array of size
+// |q| x |Sigma|"), built per query in the layouts the kernels read.
+// ---------------------------------------------------------------------------
+__global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const int8_t *__restrict__ M,
+                                int G, int R, int P, int goe16, int ge16, uint32_t *qp16,
+                                uint4 *desc, int32_t *qp32, int mpad32) {
+  const int K = (R + 3) / 4;
+  const int64_t n16 = (int64_t)P * kNL * K * G * 4;
+  const int64_t ndesc = kNL * kNL;
+  const int64_t n32 = (int64_t)kNL * mpad32;
+  const int64_t total = n16 + ndesc + n32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n16) {
+      int64_t rest = i;
+      const int e = (int)(rest & 3); rest >>= 2;
+      const int t = (int)(rest % G); rest /= G;
+      const int kk = (int)(rest % K); rest /= K;
+      const int c = (int)(rest % kNL);
+      const int pass = (int)(rest / kNL);
+      const int rloc = 4 * kk + e;
+      const int64_t row = (int64_t)pass * G * R + (int64_t)t * R + rloc;
+      uint32_t v = 0x8000u;  // -32768: separator letters, phantom rows
+      if (rloc < R && row < m && c < kAlpha) v = (uint32_t)(uint16_t)(int16_t)M[q[row] * kAlpha + c];
+      qp16[i] = v;
+    } else if (i < n16 + ndesc) {
+      const int k = (int)(i - n16);
+      const int cA = k / kNL, cB = k % kNL;
+      const uint32_t offA = (uint32_t)(cA * K * G * 16), offB = (uint32_t)(cB * K * G * 16);
+      const int gA = cA >= kAlpha ? 32767 : goe16, gB = cB >= kAlpha ? 32767 : goe16;
+      const int eA = cA >= kAlpha ? 32767 : ge16, eB = cB >= kAlpha ? 32767 : ge16;
+      const uint32_t ngoe = (uint32_t)(uint16_t)(int16_t)(-gA) | ((uint32_t)(uint16_t)(int16_t)(-gB) << 16);
+      const uint32_t nge = (uint32_t)(uint16_t)(int16_t)(-eA) | ((uint32_t)(uint16_t)(int16_t)(-eB) << 16);
+      const uint32_t keep = (cA == kEnd ? 0u : 0xffffu) | (cB == kEnd ? 0u : 0xffff0000u);
+      const uint32_t flags = (cA == kEnd ? 1u : 0u) | (cB == kEnd ? 2u : 0u);
+      desc[2 * k] = make_uint4(offA, offB, ngoe, nge);
+      desc[2 * k + 1] = make_uint4(keep, flags, 0u, 0u);
+    } else {
+      const int64_t j = i - n16 - ndesc;
+      const int c = (int)(j / mpad32);
+      const int row = (int)(j % mpad32);
+      qp32[j] = (row < m && c < kAlpha) ? (int32_t)M[q[row] * kAlpha + c] : -(1 << 30);
+    }
+  }
+}
+
+__global__ void flag_compact_kernel(const uint8_t *__restrict__ flagged, int64_t count, int32_t *list,
+                                    int *n) {
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < count;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool f = i < count && flagged[i];
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (bal) {
+      const int lane = threadIdx.x & 31;
+      int pos = 0;
+      if (lane == 0) pos = atomicAdd(n, __popc(bal));
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      if (f) list[pos + __popc(bal & ((1u << lane) - 1u))] = (int32_t)i;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Sorting stage: keys = (score, -index) packed so that one
+// descending order of 64-bit keys is "score descending, index ascending".
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t make_key(int32_t score, uint64_t idx) {
+  return ((uint64_t)((uint32_t)score ^ 0x80000000u) << 32) | (uint64_t)(0xffffffffu - (uint32_t)idx);
+}
+
+__global__ void make_keys_kernel(const int32_t *scores, const int64_t *index, int64_t n, uint64_t *keys,
+                                 int64_t npad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npad;
+       i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = i < n ? make_key(scores[i], index ? (uint64_t)index[i] : (uint64_t)i) : 0ull;
+}
+
+__global__ void bitonic_step_kernel(uint64_t *keys, int64_t n, int64_t size, int64_t stride) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n / 2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = (i / stride) * stride * 2 + (i % stride);
+    const int64_t hi = lo + stride;
+    const bool desc = ((lo & size) == 0);  // descending blocks give a descending result
+    const uint64_t a = keys[lo], b = keys[hi];
+    if ((a < b) == desc) { keys[lo] = b; keys[hi] = a; }
+  }
+}
+
+__global__ void bitonic_local_kernel(uint64_t *keys, int64_t size, int64_t stride_hi) {
+  // all strides <= stride_hi (<= 1024) of one bitonic merge stage, in shared memory
+  __shared__ uint64_t sk[2048];
+  const int64_t base = (int64_t)blockIdx.x * 2048;
+  sk[threadIdx.x] = keys[base + threadIdx.x];
+  sk[threadIdx.x + 1024] = keys[base + threadIdx.x + 1024];
+  __syncthreads();
+  for (int64_t stride = stride_hi; stride > 0; stride >>= 1) {
+    const int i = threadIdx.x;
+    const int lo = (int)((i / stride) * stride * 2 + (i % stride));
+    const int hi = lo + (int)stride;
+    const bool desc = (((base + lo) & size) == 0);
+    const uint64_t a = sk[lo], b = sk[hi];
+    if ((a < b) == desc) { sk[lo] = b; sk[hi] = a; }
+    __syncthreads();
+  }
+  keys[base + threadIdx.x] = sk[threadIdx.x];
+  keys[base + threadIdx.x + 1024] = sk[threadIdx.x + 1024];
+}
+
+// Warp-level top-k (k <= 32): lane i holds the i-th largest key seen so far.
+__global__ void warp_topk_kernel(const int32_t *scores, const int64_t *index, const uint64_t *keys_in,
+                                 int64_t n, int k, uint64_t *out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint64_t L = 0ull;
+  uint64_t thr = 0ull;
+  for (int64_t base = gw * 32; base < n; base += nw * 32) {
+    const int64_t i = base + lane;
+    uint64_t key = 0ull;
+    if (i < n) key = keys_in ? keys_in[i] : make_key(scores[i], index ? (uint64_t)index[i] : (uint64_t)i);
+    unsigned cand = __ballot_sync(0xffffffffu, key > thr);
+    while (cand) {
+      const int src = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const uint64_t c = __shfl_sync(0xffffffffu, key, src);
+      if (c > thr) {
+        const int pos = __popc(__ballot_sync(0xffffffffu, L > c));
+        const uint64_t up = __shfl_up_sync(0xffffffffu, L, 1);
+        if (lane > pos) L = up;
+        if (lane == pos) L = c;
+        thr = __shfl_sync(0xffffffffu, L, k - 1);
+      }
+    }
+  }
+  if (lane < k) out[gw * k + lane] = L;
+}
+
+__global__ void decode_keys_kernel(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[i];
+    score[i] = (int32_t)((uint32_t)(key >> 32) ^ 0x80000000u);
+    idx[i] = (int64_t)(0xffffffffu - (uint32_t)(key & 0xffffffffull));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tile table.
+// ---------------------------------------------------------------------------
+using PassFn = void (*)(const SW16Params);
+
+template <int R, int G>
+constexpr int smem_of() {
+  return (kNL * kNL * 2 + kNL * ((R + 3) / 4) * G) * 16;
+}
+
+struct TileEntry {
+  int G, R, smem;
+  PassFn fn;
+  int ctas;
+};
+
+#define SW_TILE(G_, R_) {G_, R_, smem_of<R_, G_>(), sw16_pass_kernel<R_, G_>, 0}
+TileEntry g_tiles[] = {
+    SW_TILE(8, 8),   SW_TILE(8, 12),  SW_TILE(8, 16),  SW_TILE(8, 18),  SW_TILE(8, 20),
+    SW_TILE(8, 24),  SW_TILE(8, 28),  SW_TILE(8, 32),
+    SW_TILE(16, 8),  SW_TILE(16, 12), SW_TILE(16, 16), SW_TILE(16, 20), SW_TILE(16, 24),
+    SW_TILE(16, 28), SW_TILE(16, 29), SW_TILE(16, 32),
+    SW_TILE(32, 8),  SW_TILE(32, 12), SW_TILE(32, 15), SW_TILE(32, 16), SW_TILE(32, 20),
+    SW_TILE(32, 24), SW_TILE(32, 28), SW_TILE(32, 32),
+};
+#undef SW_TILE
+constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
+
+int grid_for(int64_t total, int threads) {
+  int64_t g = (total + threads - 1) / threads;
+  if (g > 148 * 32) g = 148 * 32;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace
+
+int num_tiles() { return kNumTiles; }
+TileInfo tile(int i) { return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem}; }
+int find_tile(int G, int R) {
+  for (int i = 0; i < kNumTiles; ++i)
+    if (g_tiles[i].G == G && g_tiles[i].R == R) return i;
+  return -1;
+}
+int tile_ctas_per_sm(int i) { return g_tiles[i].ctas; }
+
+cudaError_t init_kernels() {
+  for (int i = 0; i < kNumTiles; ++i) {
+    cudaError_t e = cudaFuncSetAttribute(g_tiles[i].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         g_tiles[i].smem);
+    if (e != cudaSuccess) return e;
+    int n = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, g_tiles[i].fn, kThreads, g_tiles[i].smem);
+    if (e != cudaSuccess) return e;
+    g_tiles[i].ctas = n;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_qp_build(const uint8_t *d_query, int m, const int8_t *d_matrix, int G, int R, int P,
+                            int goe16, int ge16, uint32_t *d_qp, uint4 *d_desc, int32_t *d_qp32,
+                            int mpad32, cudaStream_t st) {
+  const int K = (R + 3) / 4;
+  const int64_t total = (int64_t)P * kNL * K * G * 4 + kNL * kNL + (int64_t)kNL * mpad32;
+  qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_matrix, G, R, P, goe16, ge16, d_qp,
+                                                         d_desc, d_qp32, mpad32);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sw16_pass(int ti, int grid, const SW16Params &p, cudaStream_t st) {
+  g_tiles[ti].fn<<<grid, kThreads, g_tiles[ti].smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n, cudaStream_t st) {
+  flag_compact_kernel<<<grid_for(count, 256), 256, 0, st>>>(flagged, count, list, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st) {
+  sw32_kernel<kSW32Rows><<<grid, kSW32Threads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_make_keys(const int32_t *scores, const int64_t *index, int64_t n, uint64_t *keys,
+                             int64_t npad, cudaStream_t st) {
+  make_keys_kernel<<<grid_for(npad, 256), 256, 0, st>>>(scores, index, n, keys, npad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bitonic_sort_desc(uint64_t *keys, int64_t npow2, cudaStream_t st) {
+  for (int64_t size = 2; size <= npow2; size <<= 1) {
+    int64_t stride = size >> 1;
+    for (; stride > 1024; stride >>= 1) {
+      bitonic_step_kernel<<<grid_for(npow2 / 2, 256), 256, 0, st>>>(keys, npow2, size, stride);
+    }
+    if (npow2 >= 2048) {
+      bitonic_local_kernel<<<(unsigned)(npow2 / 2048), 1024, 0, st>>>(keys, size, stride);
+    } else {
+      for (; stride > 0; stride >>= 1)
+        bitonic_step_kernel<<<grid_for(npow2 / 2, 256), 256, 0, st>>>(keys, npow2, size, stride);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_warp_topk(const int32_t *scores, const int64_t *index, const uint64_t *keys_in, int64_t n,
+                             int k, uint64_t *out, int nwarps, cudaStream_t st) {
+  // exactly nwarps warps: out[] holds nwarps * k keys
+  const int threads = nwarps % 8 == 0 ? 256 : 32;
+  const int blocks = nwarps * 32 / threads;
+  warp_topk_kernel<<<blocks, threads, 0, st>>>(scores, index, keys_in, n, k, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score, cudaStream_t st) {
+  decode_keys_kernel<<<grid_for(k, 256), 256, 0, st>>>(keys, k, idx, score);
+  return cudaGetLastError();
+}
+
+}  // namespace swdb

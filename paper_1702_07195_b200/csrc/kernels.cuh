@@ -1,0 +1,77 @@
+// Kernel launch interface (host side of kernels.cu), used by api.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "swdb_internal.h"
+
+namespace swdb {
+
+struct SW16Params {
+  const uint32_t *stream;   // column words (descriptor byte offsets)
+  const Item *items;
+  int num_items;
+  int *counter;             // atomic item cursor for this pass (zeroed)
+  const int32_t *slots;     // slot -> original index
+  const uint4 *qp;          // query profile, all passes: [P][kNL][K][G] uint4
+  const uint4 *desc;        // descriptor table: [kNL*kNL][2] uint4
+  const uint2 *bnd_in;      // boundary (H,F) per column from the previous pass, or null
+  uint2 *bnd_out;           // boundary for the next pass, or null
+  int32_t *scores;          // original order
+  uint8_t *flagged;         // original order, 1 = 16-bit score >= thresh
+  int pass;
+  int thresh;               // 32768 - max(1, smax)
+  uint32_t zero;            // 0 (passed in so ptxas keeps it in a register)
+};
+
+struct SW32Params {
+  const int32_t *flag_list;
+  const int *flag_count;
+  int *cursor;
+  const uint8_t *res;       // plain database, original order
+  const int64_t *offs;
+  const int32_t *qp32;      // [kNL][mpad] int32
+  int mpad;
+  int passes;
+  int neg_goe, neg_ge;      // -(open+extend), -extend  (>= -2^30)
+  uint2 *scratch;           // per warp: 2 * stride
+  int64_t stride;           // >= max_len + 64
+  int32_t *scores;
+  int64_t *cells;           // re-scored cells (statistics), may be null
+};
+
+struct TileInfo {
+  int G, R;
+  int smem_bytes;           // dynamic shared memory of the pass kernel
+};
+
+// Compiled (G, R) tiles of the s16x2 pass kernel.
+int num_tiles();
+TileInfo tile(int i);
+int find_tile(int G, int R);  // index or -1
+
+// Prepares kernel attributes (max dynamic smem).  Returns cudaError_t.
+cudaError_t init_kernels();
+// Max resident CTAs per SM of tile i's kernel.
+int tile_ctas_per_sm(int i);
+
+cudaError_t launch_qp_build(const uint8_t *d_query, int m, const int8_t *d_matrix, int G, int R,
+                            int P, int goe16, int ge16, uint32_t *d_qp, uint4 *d_desc,
+                            int32_t *d_qp32, int mpad32, cudaStream_t st);
+cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cudaStream_t st);
+cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n,
+                                cudaStream_t st);
+constexpr int kSW32Rows = 16;         // rows per lane of the 32-bit kernel
+constexpr int kSW32Threads = 256;
+cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st);
+
+// Sorting stage.
+cudaError_t launch_make_keys(const int32_t *scores, const int64_t *index, int64_t n,
+                             uint64_t *keys, int64_t npad, cudaStream_t st);
+cudaError_t launch_bitonic_sort_desc(uint64_t *keys, int64_t npow2, cudaStream_t st);
+cudaError_t launch_warp_topk(const int32_t *scores, const int64_t *index, const uint64_t *keys_in,
+                             int64_t n, int k, uint64_t *out, int nwarps, cudaStream_t st);
+cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score,
+                               cudaStream_t st);
+
+}  // namespace swdb

@@ -1,0 +1,184 @@
+// Database pre-processor (host C++): "database sequences are
+// pre-processed to allow subsequent parallel computation" and PAPER.md:114
+// "database sequences are sorted by their lengths ... and padded with dummy
+// symbols.  This is done to favor memory pattern access and minimize workload
+// imbalances".
+//
+// B200 design: instead of padding every group of L
+// sequences to its longest member, each s16x2 lane half is a *stream* of
+// whole sequences separated by two separator columns (END, NUL); a work item
+// is a pair of such streams of equal length.  Items are filled
+// longest-sequence-first with a two-pointer pass over the length-sorted order
+// (longest remaining first, then shortest remaining to fill the tail), so the
+// padding per item is below the length of the shortest remaining sequence,
+// and item capacities shrink geometrically ("guided") so the dynamic
+// longest-first claim ("dynamically distributed ... as soon as
+// the threads become idle") ends with small items.
+#include "swdb_internal.h"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <thread>
+
+namespace swdb {
+
+int validate_db(const uint8_t *residues, const int64_t *offsets, int64_t count, std::string &err) {
+  if (!offsets) { err = "offsets is NULL"; return -1; }
+  if (count < 1) { err = "count must be >= 1"; return -1; }
+  if (count >= (int64_t(1) << 31) - 1) { err = "count must be < 2^31 - 1"; return -1; }
+  if (offsets[0] != 0) { err = "offsets[0] must be 0"; return -1; }
+  for (int64_t i = 0; i < count; ++i)
+    if (offsets[i + 1] < offsets[i]) {
+      err = "offsets must be non-decreasing (at index " + std::to_string(i) + ")";
+      return -1;
+    }
+  const int64_t total = offsets[count];
+  if (total > 0 && !residues) { err = "residues is NULL"; return -1; }
+  if (total >= (int64_t(1) << 40)) { err = "database too large"; return -1; }
+  // residue codes < 24, checked in parallel chunks
+  unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<int64_t> bad(nth, -1);
+  std::vector<std::thread> th;
+  const int64_t chunk = (total + nth - 1) / nth;
+  for (unsigned k = 0; k < nth; ++k)
+    th.emplace_back([&, k] {
+      const int64_t b = k * chunk, e = std::min(total, b + chunk);
+      for (int64_t i = b; i < e; ++i)
+        if (residues[i] >= kAlpha) { bad[k] = i; return; }
+    });
+  for (auto &t : th) t.join();
+  for (unsigned k = 0; k < nth; ++k)
+    if (bad[k] >= 0) {
+      err = "residue code >= 24 at position " + std::to_string(bad[k]);
+      return -1;
+    }
+  return 0;
+}
+
+namespace {
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
+                int64_t target_groups, HostImage &out, std::string &err) {
+  out = HostImage();
+  std::vector<int64_t> len(count);
+  int64_t total_stream = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    len[i] = offsets[i + 1] - offsets[i];
+    out.max_len = std::max(out.max_len, len[i]);
+    total_stream += len[i] + 2;  // residues, END, NUL
+  }
+  // Stable sort by length, descending (ties by original index).  The paper
+  // sorts ascending and processes groups in that order; we claim longest
+  // first to bound the tail of the dynamic schedule.
+  std::vector<int32_t> order(count);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return len[a] > len[b]; });
+
+  if (target_groups < 1) target_groups = 1;
+  int64_t remaining = (total_stream + 1) / 2;  // pair columns still to place
+  int64_t lo = 0, hi = count - 1;
+  std::vector<int32_t> halfA, halfB;
+  struct Tmp { int64_t ncols; int64_t slot0; int32_t nA, nB; };
+  std::vector<Tmp> tmp;
+  out.slots.reserve(count);
+  while (lo <= hi) {
+    int64_t cap = remaining / (target_groups * 3);
+    cap = std::max<int64_t>(256, std::min<int64_t>(8192, cap));
+    halfA.clear();
+    halfB.clear();
+    int64_t lA = 0, lB = 0;
+    {
+      int32_t s = order[lo++];
+      halfA.push_back(s);
+      lA = len[s] + 2;
+      cap = std::max(cap, lA);
+    }
+    for (;;) {
+      const bool toA = lA <= lB;
+      int64_t &l = toA ? lA : lB;
+      std::vector<int32_t> &h = toA ? halfA : halfB;
+      if (lo <= hi && l + len[order[lo]] + 2 <= cap) {
+        int32_t s = order[lo++];
+        h.push_back(s);
+        l += len[s] + 2;
+      } else if (lo <= hi && l + len[order[hi]] + 2 <= cap) {
+        int32_t s = order[hi--];
+        h.push_back(s);
+        l += len[s] + 2;
+      } else {
+        break;
+      }
+    }
+    const int64_t ncols = round_up(std::max(lA, lB), kColAlign);
+    Tmp t{ncols, (int64_t)out.slots.size(), (int32_t)halfA.size(), (int32_t)halfB.size()};
+    for (int32_t s : halfA) out.slots.push_back(s);
+    for (int32_t s : halfB) out.slots.push_back(s);
+    tmp.push_back(t);
+    remaining -= (lA + lB + 1) / 2;
+    if (remaining < 0) remaining = 0;
+  }
+  // claim order: longest item first (stable)
+  std::vector<int32_t> iorder(tmp.size());
+  std::iota(iorder.begin(), iorder.end(), 0);
+  std::stable_sort(iorder.begin(), iorder.end(),
+                   [&](int32_t a, int32_t b) { return tmp[a].ncols > tmp[b].ncols; });
+  int64_t col = kItemPad;
+  out.items.resize(tmp.size());
+  for (size_t k = 0; k < iorder.size(); ++k) {
+    const Tmp &t = tmp[iorder[k]];
+    Item &it = out.items[k];
+    it.col_begin = col;
+    it.ncols = (int32_t)t.ncols;
+    it.seqA = (int32_t)t.slot0;
+    it.nA = t.nA;
+    it.seqB = (int32_t)(t.slot0 + t.nA);
+    it.nB = t.nB;
+    it.pad = 0;
+    col += t.ncols + kItemPad;
+    if (t.ncols >= (int64_t(1) << 31)) { err = "sequence too long"; return -1; }
+  }
+  out.total_cols = col;
+  // Write the stream: column word per pair column.
+  out.stream.assign((size_t)col, column_word(kNul, kNul));
+  auto write_half = [&](const Item &it, int32_t slot0, int32_t n, int shift_is_b) {
+    int64_t c = it.col_begin;
+    for (int32_t k = 0; k < n; ++k) {
+      const int32_t s = out.slots[slot0 + k];
+      const uint8_t *r = residues + offsets[s];
+      for (int64_t j = 0; j < len[s]; ++j, ++c) {
+        uint32_t w = out.stream[c];
+        int cA = (int)(w / kDescBytes) / kNL, cB = (int)(w / kDescBytes) % kNL;
+        if (shift_is_b) cB = r[j]; else cA = r[j];
+        out.stream[c] = column_word(cA, cB);
+      }
+      for (int sep = 0; sep < 2; ++sep, ++c) {
+        uint32_t w = out.stream[c];
+        int cA = (int)(w / kDescBytes) / kNL, cB = (int)(w / kDescBytes) % kNL;
+        const int L = sep == 0 ? kEnd : kNul;
+        if (shift_is_b) cB = L; else cA = L;
+        out.stream[c] = column_word(cA, cB);
+      }
+    }
+  };
+  {
+    unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    const size_t ni = out.items.size();
+    for (unsigned k = 0; k < nth; ++k)
+      th.emplace_back([&, k] {
+        for (size_t i = k; i < ni; i += nth) {
+          const Item &it = out.items[i];
+          write_half(it, it.seqA, it.nA, 0);
+          write_half(it, it.seqB, it.nB, 1);
+        }
+      });
+    for (auto &t : th) t.join();
+  }
+  return 0;
+}
+
+}  // namespace swdb

@@ -1,0 +1,65 @@
+// Internal definitions shared by the host preprocessor (prep.cpp), the
+// kernels (kernels.cu) and the C-ABI (api.cu).  Not part of the public ABI.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace swdb {
+
+// Letters of the stream alphabet: 24 residue codes (SW_ALPHA), then two
+// separator letters used to concatenate many database sequences into one
+// lane stream:
+//   END  closes a sequence: substitution -32768 in every row and the gap
+//        penalties of the column forced to 32767, which zeroes E and F; the
+//        lane's running score S is emitted down the group and reset.
+//   NUL  follows END (and pads streams): substitution -32768, penalties
+//        32767; after it H, E and F are all 0, i.e. the column-0 boundary of
+//        PAPER.md:66 for the next sequence.
+constexpr int kAlpha = 24;
+constexpr int kEnd = 24;
+constexpr int kNul = 25;
+constexpr int kNL = 26;             // letters in the query profile / descriptor table
+constexpr int kDescBytes = 32;      // bytes per descriptor table entry
+constexpr int kColAlign = 4;        // item column counts are multiples of this
+// Columns of NUL padding after every item in the stream image (and before the
+// first): lets lane 0 prefetch past an item's end and lane G-1 store its
+// pipeline-fill columns without bounds predicates.  >= 32 - 1 + 4 + 4.
+constexpr int kItemPad = 40;
+
+// Column word of the s16x2 stream: byte offset of the descriptor of the
+// letter pair (cA, cB) = (cA * kNL + cB) * kDescBytes.  cA is the low 16-bit
+// lane ("half A"), cB the high lane ("half B").
+inline uint32_t column_word(int cA, int cB) { return (uint32_t)((cA * kNL + cB) * kDescBytes); }
+
+// A work item: two lane streams ("halves") of equal column count, each the
+// concatenation [seq, END, NUL, seq, END, NUL, ...] padded with NUL.
+struct Item {
+  int64_t col_begin;  // first column in the stream image
+  int32_t ncols;      // columns (multiple of kColAlign)
+  int32_t seqA;       // first slot of half A's sequences in the slot array
+  int32_t seqB;       // first slot of half B's sequences
+  int32_t nA;         // sequences in half A
+  int32_t nB;         // sequences in half B
+  int32_t pad;
+};
+static_assert(sizeof(Item) == 32, "Item layout");
+
+struct HostImage {
+  std::vector<uint32_t> stream;   // column words, total_cols
+  std::vector<Item> items;        // sorted by ncols descending (claim order)
+  std::vector<int32_t> slots;     // slot -> original sequence index
+  int64_t total_cols = 0;
+  int64_t max_len = 0;
+};
+
+// Pre-processing stage: validated input -> stream image.
+// target_groups: number of concurrently running lane groups to size items for.
+// Returns 0 or -1 (err set).
+int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
+                int64_t target_groups, HostImage &out, std::string &err);
+
+// Validation of the raw database (codes < 24, offsets monotone).
+int validate_db(const uint8_t *residues, const int64_t *offsets, int64_t count, std::string &err);
+
+}  // namespace swdb

@@ -1,0 +1,194 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle,
+element by element, bit-exact (integer scores).
+
+Sizes span several tiles, several query passes and ragged tails; the
+BASELINE.json configurations are checked in full where the oracle finishes in
+seconds (cfg0) and on seeded samples otherwise (cfg1 full size, in the
+launch configuration bench.py times).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import sw_inputs as si
+from sw_inputs import BLOSUM62, encode
+from tests.brute import expand
+
+pytestmark = pytest.mark.gpu
+
+sw = pytest.importorskip("paper_1702_07195_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+    sw.sw_set_tile(0)
+
+
+def _db(seqs):
+    return si.database_from_list(seqs)
+
+
+def _check_db(db, q, M=BLOSUM62, go=10, ge=2, label=""):
+    sw.sw_db_load(db.residues, db.offsets)
+    got = sw.sw_search(q, M, go, ge)
+    exp = oracle.batch(q, db.residues, db.offsets, M, go, ge)
+    bad = np.nonzero(got != exp)[0]
+    assert bad.size == 0, f"{label}: {bad.size} mismatches, first {bad[:5]} got {got[bad[:5]]} exp {exp[bad[:5]]}"
+    return got
+
+
+def test_hand_examples_on_gpu():
+    rows = [ln.rstrip("\n").split("\t") for ln in open("tests/golden/hand_examples.txt")
+            if ln.strip() and not ln.startswith("#")]
+    # one database per (query, gaps): every subject of that query
+    groups = {}
+    for r in rows:
+        groups.setdefault((r[0], int(r[2]), int(r[3])), []).append((r[1], int(r[4])))
+    for (qs, go, ge), subs in groups.items():
+        db = _db([encode(expand(s)) for s, _ in subs])
+        sw.sw_db_load(db.residues, db.offsets)
+        got = sw.sw_search(encode(expand(qs)), BLOSUM62, go, ge)
+        assert got.tolist() == [v for _, v in subs], (qs, go, ge)
+
+
+def test_random_small_databases_random_scoring():
+    rng = np.random.default_rng(1234)
+    for trial in range(12):
+        count = int(rng.integers(1, 400))
+        lens = rng.integers(0, 300, count)
+        seqs = [rng.integers(0, 24, int(L)).astype(np.uint8) for L in lens]
+        m = int(rng.integers(1, 1400))
+        q = rng.integers(0, 24, m).astype(np.uint8)
+        M = si.random_symmetric_matrix(rng) if trial % 2 == 0 else rng.integers(-4, 12, (24, 24)).astype(np.int8)
+        go, ge = int(rng.integers(0, 16)), int(rng.integers(0, 16))
+        _check_db(_db(seqs), q, M, go, ge, label=f"trial {trial} m={m} go={go} ge={ge}")
+
+
+def test_every_tile_is_exact():
+    rng = np.random.default_rng(7)
+    seqs = [si.rr_residues(rng, int(L)) for L in rng.integers(1, 500, 300)]
+    seqs += [np.zeros(0, np.uint8), si.rr_residues(rng, 3000)]
+    db = _db(seqs)
+    q = si.rr_residues(rng, 700)
+    exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
+    sw.sw_db_load(db.residues, db.offsets)
+    for G in (8, 16, 32):
+        for R in range(1, 33):
+            if not sw.sw_tile_supported(G, R):
+                continue
+            sw.sw_set_tile(G, R)
+            got = sw.sw_search(q, BLOSUM62, 10, 2)
+            st = sw.sw_last_stats()
+            assert (st["G"], st["R"]) == (G, R)
+            assert (got == exp).all(), (G, R, np.nonzero(got != exp)[0][:5])
+    sw.sw_set_tile(0)
+
+
+def test_config0_full_parity():
+    w = si.config0()
+    got = _check_db(w.db, w.queries[0], label="cfg0")
+    assert sw.sw_last_stats()["flagged"] == 0
+
+
+def test_saturation_boundary_and_rescoring():
+    # W^n vs W^n scores 11n: below, at and above T = 32768 - 11 = 32757
+    ns = [2977, 2978, 2979, 2980, 3000, 4000]
+    seqs = [encode("W" * n) for n in ns] + [encode("A" * 50)]
+    q = encode("W" * 4000)
+    got = _check_db(_db(seqs), q, label="W runs")
+    assert got[:len(ns)].tolist() == [11 * n for n in ns]
+    st = sw.sw_last_stats()
+    assert st["flagged"] == sum(1 for n in ns if 11 * n >= 32757)
+
+
+def test_adversarial_mixed_with_planted_copies():
+    w = si.config4(scale=0.002)   # 400 sequences incl. long ones and 8 planted copies
+    got = _check_db(w.db, w.queries[0], label="cfg4 small")
+    flagged_expected = int((got >= 32757).sum())
+    assert sw.sw_last_stats()["flagged"] == flagged_expected
+    assert (got[w.planted] >= 32757).all()
+
+
+def test_long_sequences_and_query_passes():
+    rng = np.random.default_rng(99)
+    seqs = [si.rr_residues(rng, int(L)) for L in (35000, 12000, 5000, 1, 2, 3)]
+    seqs += [si.rr_residues(rng, int(L)) for L in rng.integers(5, 200, 60)]
+    q = si.rr_residues(rng, 1500)
+    _check_db(_db(seqs), q, label="long")
+
+
+def test_topk_matches_oracle_sort_stage():
+    w = si.config0()
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    got = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
+    for k in (1, 10, 32, 33, 100, 5000, w.db.count, w.db.count + 10):
+        idx, sc = sw.sw_topk(k)
+        eidx, esc = oracle.topk(got, k)
+        assert (idx == eidx).all() and (sc == esc).all(), k
+
+
+def test_topk_dev_with_index_ties():
+    import torch
+    scores = torch.tensor([3, 9, 9, 1, 9], dtype=torch.int32, device="cuda")
+    index = torch.tensor([40, 11, 10, 7, 12], dtype=torch.int64, device="cuda")
+    oi = torch.empty(5, dtype=torch.int64, device="cuda")
+    os_ = torch.empty(5, dtype=torch.int32, device="cuda")
+    n = sw.sw_topk_dev(scores, index, 5, 4, oi, os_)
+    assert n == 4
+    assert oi[:4].tolist() == [10, 11, 12, 40]
+    assert os_[:4].tolist() == [9, 9, 9, 3]
+
+
+def test_search_dev_matches_search():
+    import torch
+    w = si.config0(scale=0.2)
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    host = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
+    d = torch.empty(w.db.count, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    sw.sw_search_dev(w.queries[0], BLOSUM62, 10, 2, d, s)
+    s.synchronize()
+    assert (d.cpu().numpy() == host).all()
+
+
+def test_error_paths_on_gpu():
+    w = si.config0(scale=0.01)
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    with pytest.raises(sw.SWError):
+        sw.sw_search(np.array([30], np.uint8), BLOSUM62, 10, 2)
+    with pytest.raises(sw.SWError):
+        sw.sw_search(np.zeros(0, np.uint8), BLOSUM62, 10, 2)
+    with pytest.raises(sw.SWError):
+        sw.sw_search(encode("AW"), BLOSUM62, -1, 2)
+    # a failed call leaves the database usable
+    got = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
+    exp = oracle.batch(w.queries[0], w.db.residues, w.db.offsets, BLOSUM62, 10, 2)
+    assert (got == exp).all()
+
+
+def test_config1_full_size_sampled():
+    """BASELINE.json configs[1] at full size (1 M sequences, query 464), in the
+    launch configuration bench.py times; oracle on a seeded sample of 3,000
+    sequences plus the 200 longest, and properties on all."""
+    w = si.config1()
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    got = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
+    assert got.min() >= 0
+    assert sw.sw_last_stats()["flagged"] == 0
+    rng = np.random.default_rng(2024)
+    L = w.db.lengths()
+    idx = np.unique(np.concatenate([rng.choice(w.db.count, 3000, replace=False), np.argsort(-L)[:200]]))
+    exp = oracle.batch(w.queries[0], w.db.residues, w.db.offsets, BLOSUM62, 10, 2, idx=idx)
+    assert (got[idx] == exp).all()
+    # upper bound: score <= sum over the query of its row maxima
+    ub = int(np.maximum(BLOSUM62[w.queries[0], :20].max(axis=1), 0).sum())
+    assert got.max() <= ub
+    # top-10 agrees with the oracle sort of the GPU scores
+    idx10, sc10 = sw.sw_topk(10)
+    eidx, esc = oracle.topk(got, 10)
+    assert (idx10 == eidx).all() and (sc10 == esc).all()
