@@ -84,10 +84,11 @@ struct State {
   DevBuf<int64_t> cells32;
   DevBuf<uint8_t> query;
   DevBuf<int8_t> matrix;
-  DevBuf<uint32_t> qp;
+  DevBuf<uint8_t> qp;
   DevBuf<uint4> desc;
   DevBuf<int32_t> qp32;
   DevBuf<uint2> bnd;        // 2 * total_cols
+  DevBuf<uint2> dummy;      // scratch for idle-lane stores (one 8-B slot per thread)
   DevBuf<uint2> scratch32;
   DevBuf<uint64_t> keys;
   DevBuf<uint64_t> keys2;
@@ -110,7 +111,7 @@ struct State {
     stream_img.release(); items.release(); slots.release(); res.release(); offs.release();
     scores.release(); flagged.release(); flag_list.release(); counters.release(); cells32.release();
     query.release(); matrix.release(); qp.release(); desc.release(); qp32.release(); bnd.release();
-    scratch32.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
+    scratch32.release(); dummy.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
     loaded = false;
     has_search = false;
     last_scores = nullptr;
@@ -125,6 +126,7 @@ int ensure_device_ready() {
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   if (!g_kernels_ready) {
+    if (const char *e = getenv("SWDB_QPM")) set_profile_mode(atoi(e));
     CUDA_TRY(init_kernels());
     g_kernels_ready = true;
   }
@@ -142,7 +144,7 @@ int choose_tile(int m) {
   int bi = 0;
   for (int i = 0; i < num_tiles(); ++i) {
     const TileInfo ti = tile(i);
-    if (tile_ctas_per_sm(i) < 1) continue;
+    if (ti.qpm != profile_mode() || tile_ctas_per_sm(i) < 1) continue;
     const int rows = ti.G * ti.R;
     const int P = (m + rows - 1) / rows;
     const double cost = (double)P * ti.G * (5.5 * ti.R + 12.0) + P * 200.0;
@@ -183,7 +185,6 @@ int search_impl(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_
   const int rows = T.G * T.R;
   const int P = (qlen + rows - 1) / rows;
   if (P > kMaxPass) return fail(SW_EINVAL, "query too long");
-  const int K = (T.R + 3) / 4;
   const int P32 = (qlen + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
   const int mpad32 = P32 * 32 * kSW32Rows;
   int smax = 1;
@@ -193,10 +194,14 @@ int search_impl(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_
 
   CUDA_TRY(g.query.ensure((size_t)qlen));
   CUDA_TRY(g.matrix.ensure(kAlpha * kAlpha));
-  CUDA_TRY(g.qp.ensure((size_t)P * kNL * K * T.G * 4));
-  CUDA_TRY(g.desc.ensure((size_t)kNL * kNL * 2));
+  CUDA_TRY(g.qp.ensure(qp_bytes(T.G, T.R, P, T.qpm)));
+  CUDA_TRY(g.desc.ensure((size_t)kNL * kNL));
   CUDA_TRY(g.qp32.ensure((size_t)kNL * mpad32));
-  if (P > 1) CUDA_TRY(g.bnd.ensure((size_t)g.total_cols * 2));
+  if (P > 1 && g.bnd.n < (size_t)g.total_cols * 2) {
+    CUDA_TRY(g.bnd.ensure((size_t)g.total_cols * 2));
+    // padding columns are only ever written with zeros; start from zeros
+    CUDA_TRY(cudaMemset(g.bnd.p, 0, g.bnd.n * sizeof(uint2)));
+  }
 
   CUDA_TRY(cudaMemcpyAsync(g.query.p, query, (size_t)qlen, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(g.matrix.p, matrix, kAlpha * kAlpha, cudaMemcpyHostToDevice, st));
@@ -206,8 +211,8 @@ int search_impl(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_
   if (!g.ev[0])
     for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g.ev[i]));
   CUDA_TRY(cudaEventRecord(g.ev[0], st));
-  CUDA_TRY(launch_qp_build(g.query.p, qlen, g.matrix.p, T.G, T.R, P, std::min(goe, 32767),
-                           std::min(ge, 32767), g.qp.p, g.desc.p, g.qp32.p, mpad32, st));
+  CUDA_TRY(launch_qp_build(g.query.p, qlen, g.matrix.p, T.G, T.R, P, T.qpm, g.qp.p, g.desc.p, g.qp32.p,
+                           mpad32, st));
 
   const int grid = g.num_sms * std::max(1, tile_ctas_per_sm(ti));
   CUDA_TRY(cudaEventRecord(g.ev[1], st));
@@ -222,11 +227,14 @@ int search_impl(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_
     p.desc = g.desc.p;
     p.bnd_in = pass == 0 ? nullptr : g.bnd.p + (size_t)((pass - 1) & 1) * g.total_cols;
     p.bnd_out = pass == P - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * g.total_cols;
+    p.dummy = g.dummy.p;
     p.scores = d_scores;
     p.flagged = g.flagged.p;
     p.pass = pass;
     p.thresh = thresh;
     p.zero = 0u;
+    p.dgoe = (uint32_t)(32767 - std::min(goe, 32767));
+    p.dge = (uint32_t)(32767 - std::min(ge, 32767));
     CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
   }
   CUDA_TRY(cudaEventRecord(g.ev[2], st));
@@ -320,6 +328,7 @@ int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
   CUDA_TRY(g.flag_list.ensure((size_t)count));
   CUDA_TRY(g.counters.ensure(kMaxPass + 2));
   CUDA_TRY(g.cells32.ensure(1));
+  CUDA_TRY(g.dummy.ensure((size_t)nsm * 4 * 1024));   // one slot per resident thread
   CUDA_TRY(cudaMemcpy(g.stream_img.p, img.stream.data(), img.stream.size() * sizeof(uint32_t),
                       cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(g.items.p, img.items.data(), img.items.size() * sizeof(Item), cudaMemcpyHostToDevice));

@@ -46,19 +46,56 @@ __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
 
 // ---------------------------------------------------------------------------
 // s16x2 pass kernel: query rows [pass*G*R, (pass+1)*G*R) against every item.
+//
+// Shared memory: descriptor table [kNL*kNL] x 16 B, then the profile slice of
+// this pass, int16, laid out [letter][8-row chunk][lane t][8 x int16] so that
+// the 8 lanes of a quarter-warp always hit 8 distinct 16-B bank groups.
+// Descriptor of letter pair (cA, cB): {offA | offB << 16 (profile offsets
+// in 16-B units), notsep bits (1 per non-separator half), END bits (0x8000 in a
+// half whose sequence ENDs: -32768 resets that half of S), 0}.  Only lane 0 of a group reads it; lanes
+// t > 0 receive it from lane t-1 with the column.
 // ---------------------------------------------------------------------------
-template <int R, int G>
+__device__ __forceinline__ uint32_t umulhi(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ void st_global_v2(uint2 *p, uint32_t a, uint32_t b) {
+  asm volatile("st.global.v2.u32 [%0], {%1, %2};" :: "l"(p), "r"(a), "r"(b) : "memory");
+}
+
+template <class T>
+__device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on the FMA pipe
+  uint64_t d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(n), "r"((uint32_t)sizeof(T)), "l"((uint64_t)p));
+  return reinterpret_cast<T *>(d);
+}
+
+// Profile modes (how the two halves' substitution scores are packed):
+//   QPM 0: one zero-extended int16 per (letter,row) 32-bit word (4 rows per
+//          16-B chunk); pack = IMAD(B, 65536, A)                [FMA pipe]
+//   QPM 1: int16 pairs (8 rows per chunk); pack with IMAD.HI/IMAD [FMA pipe]
+//   QPM 2: int16 pairs; pack with PRMT                           [ALU pipe]
+template <int R, int G, bool BIN, int QPM>
 __global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params p) {
-  constexpr int K = (R + 3) / 4;            // uint4 (4-row) chunks per lane
-  constexpr int QP_U4 = kNL * K * G;        // profile slice of one pass
-  constexpr int DESC_U4 = kNL * kNL * 2;
+  constexpr int RPC = QPM == 0 ? 4 : 8;     // rows per 16-B profile chunk
+  constexpr int KC = (R + RPC - 1) / RPC;   // chunks per lane
+  constexpr int LS = KC * G * 16;           // bytes per letter in the profile slice
+  constexpr int QP_U4 = kNL * LS / 16;
+  constexpr int DESC_U4 = kNL * kNL;
   extern __shared__ uint4 smem[];
-  uint4 *s_desc = smem;
-  uint4 *s_qp = smem + DESC_U4;
   {
     const uint4 *gq = p.qp + (size_t)p.pass * QP_U4;
-    for (int i = threadIdx.x; i < DESC_U4; i += blockDim.x) s_desc[i] = p.desc[i];
-    for (int i = threadIdx.x; i < QP_U4; i += blockDim.x) s_qp[i] = gq[i];
+    for (int i = threadIdx.x; i < DESC_U4; i += blockDim.x) smem[i] = p.desc[i];
+    for (int i = threadIdx.x; i < QP_U4; i += blockDim.x) smem[DESC_U4 + i] = gq[i];
   }
   __syncthreads();
 
@@ -70,22 +107,34 @@ __global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params
   const bool last = t == G - 1;
   const uint32_t nfirst = first ? 0u : 1u;
   const uint32_t zero = p.zero;
-  const char *desc_b = reinterpret_cast<const char *>(s_desc);
-  const char *qp_b = reinterpret_cast<const char *>(s_qp) + t * 16;
-  const bool has_bin = p.bnd_in != nullptr;
+  const uint32_t s_desc = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t s_qp = s_desc + DESC_U4 * 16 + t * 16;
+  const uint32_t pen_base = 0x80018001u;      // -32767 in both halves
+  const uint32_t dgoe = p.dgoe, dge = p.dge;  // 32767 - Goe, 32767 - Ge (clamped)
   const bool has_bout = p.bnd_out != nullptr;
+  const uint4 nul = lds128(s_desc + kNulWord);
+  const uint32_t emit_cmp = last ? 0u : 0xffffffffu;   // kp > emit_cmp <=> last lane at an END column
 
   uint32_t H[R], E[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) { H[r] = 0u; E[r] = 0u; }
   uint32_t S = 0u, hout = 0u, fout = 0u, sc = 0u, hprev = 0u;
-  uint32_t cw = kNulWord;
+  uint32_t w0 = nul.x, ns = nul.y, kp = nul.z;   // column chain (NUL)
+  uint32_t kneg = 0u;                            // kp of the previous column
+  uint4 dcur = make_uint4(0u, 0u, 0u, 0u);       // lane 0: descriptor of the current column
 
-  int64_t col0 = 0;
+  // Lane 0 prefetches the stream (and the boundary of the previous pass)
+  // 4 columns ahead; lane G-1 stores the boundary for the next pass.  When a
+  // group has no item left, the pointers stop advancing (increment 0) on the
+  // NUL padding at the start of the stream / a scratch word.
+  const uint32_t *sptr = p.stream;
+  const uint2 *bptr = p.bnd_in;
+  uint2 *const dummy = p.dummy + (blockIdx.x * blockDim.x + threadIdx.x);  // own slot: no contention
+  uint2 *optr = dummy;
+  uint32_t inc_s = 0u, inc_o = 0u;
   int s = 0, nsteps = 0;
   int seqA = 0, seqB = 0, kA = 0, kB = 0;
   bool done = false;
-  bool ld_on = false, st_on = false;
   uint32_t sring[4] = {0u, 0u, 0u, 0u};
   uint2 bring[4];
 #pragma unroll
@@ -98,29 +147,39 @@ __global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params
       it = __shfl_sync(gmask, it, gbase);
       if (it < p.num_items) {
         const Item item = p.items[it];
-        col0 = item.col_begin;
         seqA = item.seqA;
         seqB = item.seqB;
         kA = 0;
         kB = 0;
         s = 0;
         nsteps = (item.ncols + G - 1 + 3) & ~3;
-        ld_on = first;
-        st_on = last && has_bout;
+        inc_s = 4u;
+        sptr = p.stream + item.col_begin;
+        if (BIN) bptr = p.bnd_in + item.col_begin;
+        if (has_bout) {
+          optr = p.bnd_out + (item.col_begin - (G - 1));
+          inc_o = 4u;
+        }
+        if (first) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          sring[u] = first ? p.stream[col0 + u] : 0u;
-          bring[u] = (first && has_bin) ? p.bnd_in[col0 + u] : make_uint2(0u, 0u);
+          for (int u = 0; u < 4; ++u) {
+            sring[u] = __ldg(sptr + u);
+            if (BIN) bring[u] = __ldg(bptr + u);
+          }
+          dcur = lds128(s_desc + sring[0]);
         }
       } else {
         done = true;
         nsteps = INT_MAX;
-        ld_on = false;
-        st_on = false;
+        inc_s = 0u;
+        inc_o = 0u;
+        sptr = p.stream;          // NUL padding
+        if (BIN) bptr = p.bnd_in; // zeros (padding columns)
+        optr = dummy;
+        if (first) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          sring[u] = first ? kNulWord : 0u;
-          bring[u] = make_uint2(0u, 0u);
+          for (int u = 0; u < 4; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(0u, 0u); }
+          dcur = nul;
         }
       }
     }
@@ -128,58 +187,88 @@ __global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params
 
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      // ---- inputs of this column from lane t-1 (lane 0: stream / boundary)
-      const uint32_t cw_up = __shfl_up_sync(0xffffffffu, cw, 1, G);
+      // ---- the column arrives from lane t-1 (lane 0: from the stream)
+      const uint32_t w0_up = __shfl_up_sync(0xffffffffu, w0, 1, G);
+      const uint32_t ns_up = __shfl_up_sync(0xffffffffu, ns, 1, G);
+      const uint32_t kp_up = __shfl_up_sync(0xffffffffu, kp, 1, G);
       const uint32_t hu_up = __shfl_up_sync(0xffffffffu, hout, 1, G);
       const uint32_t fu_up = __shfl_up_sync(0xffffffffu, fout, 1, G);
       const uint32_t sc_up = __shfl_up_sync(0xffffffffu, sc, 1, G);
-      cw = imad(cw_up, nfirst, sring[u]);
+      w0 = imad(w0_up, nfirst, dcur.x);
+      ns = imad(ns_up, nfirst, dcur.y);
+      kp = imad(kp_up, nfirst, dcur.z);
       const uint32_t hu = imad(hu_up, nfirst, bring[u].x);
       uint32_t F = imad(fu_up, nfirst, bring[u].y);
       const uint32_t sc_in = imad(sc_up, nfirst, 0u);
-      // prefetch 4 columns ahead (lane 0 only; NUL padding makes it in-bounds)
-      if (ld_on) {
-        sring[u] = p.stream[col0 + s + u + 4];
-        if (has_bin) bring[u] = p.bnd_in[col0 + s + u + 4];
+      // ---- lane 0: descriptor of the next column; refill the stream ring
+      if (first) dcur = lds128(s_desc + sring[(u + 1) & 3]);
+      if (first) {
+        sring[u] = __ldg(sptr + u + 4);
+        if (BIN) bring[u] = __ldg(bptr + u + 4);
       }
-      // ---- column descriptor: profile offsets, gap penalties, END flags
-      const uint4 d0 = *reinterpret_cast<const uint4 *>(desc_b + cw);
-      const uint2 d1 = *reinterpret_cast<const uint2 *>(desc_b + cw + 16);
-      const char *pa = qp_b + d0.x;
-      const char *pb = qp_b + d0.y;
+      // ---- profile addresses and per-column gap penalties (FMA pipe)
+      const uint32_t offB = umulhi(w0, 65536u);           // profile offsets / 16
+      const uint32_t offA = imad(offB, 0xffff0000u, w0);
+      const uint32_t ngoe = imad(ns, dgoe, pen_base);   // -Goe, or -32767 in a separator half
+      const uint32_t nge = imad(ns, dge, pen_base);     // -Ge,  or -32767 in a separator half
+      const uint32_t aA = imad(offA, 16u, s_qp);
+      const uint32_t aB = imad(offB, 16u, s_qp);
       uint32_t hd = hprev;
       hprev = hu;
+      const uint32_t kneg_prev = kneg;   // -32768 in the half(s) whose sequence ended last column
+      kneg = kp;
 #pragma unroll
-      for (int kk = 0; kk < K; ++kk) {
-        const uint4 a = *reinterpret_cast<const uint4 *>(pa + kk * G * 16);
-        const uint4 b = *reinterpret_cast<const uint4 *>(pb + kk * G * 16);
+      for (int kk = 0; kk < KC; ++kk) {
+        const uint4 a = lds128(aA + kk * G * 16);
+        const uint4 b = lds128(aB + kk * G * 16);
         const uint32_t av[4] = {a.x, a.y, a.z, a.w};
         const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = kk * 4 + e;
-          if (r < R) {
-            const uint32_t sub = imad(bv[e], 65536u, av[e]);   // (SM_A, SM_B)
-            uint32_t h = __viaddmax_s16x2_relu(hd, sub, E[r]);  // max(Hdiag+SM, E, 0)
-            h = __vmaxs2(h, F);                                 // Eq. 1
-            hd = H[r];
-            H[r] = h;
-            const uint32_t hg = __viaddmax_s16x2_relu(h, d0.z, zero);  // max(H-Goe, 0)
-            E[r] = __viaddmax_s16x2(E[r], d0.w, hg);                   // Eq. 2 (next column)
-            F = __viaddmax_s16x2(F, d0.w, hg);                         // Eq. 3 (next row)
+        for (int j = 0; j < 4; ++j) {
+          const int r0 = kk * RPC + (QPM == 0 ? j : 2 * j);
+          if (r0 < R) {
+            uint32_t sub0, sub1 = 0u;
+            if (QPM == 0) {
+              sub0 = imad(bv[j], 65536u, av[j]);                 // (A_r0, B_r0)
+            } else if (QPM == 1) {
+              // (A_r0 | A_r1<<16), (B_r0 | B_r1<<16) -> (A_r0, B_r0), (A_r1, B_r1)
+              const uint32_t hiA = umulhi(av[j], 65536u);
+              const uint32_t hiB = umulhi(bv[j], 65536u);
+              sub0 = imad(imad(hiA, 0xffffffffu, bv[j]), 65536u, av[j]);
+              sub1 = imad(hiB, 65536u, hiA);
+            } else {
+              sub0 = __byte_perm(av[j], bv[j], 0x5410);
+              sub1 = __byte_perm(av[j], bv[j], 0x7632);
+            }
+#pragma unroll
+            for (int e = 0; e < (QPM == 0 ? 1 : 2); ++e) {
+              const int r = r0 + e;
+              if (r < R) {
+                const uint32_t sub = e ? sub1 : sub0;
+                uint32_t h = __viaddmax_s16x2_relu(hd, sub, E[r]);  // max(Hdiag+SM, E, 0)
+                h = __vmaxs2(h, F);                                 // Eq. 1
+                hd = H[r];
+                H[r] = h;
+                const uint32_t hg = __viaddmax_s16x2_relu(h, ngoe, zero);  // max(H-Goe, 0)
+                E[r] = __viaddmax_s16x2(E[r], nge, hg);                    // Eq. 2 (next column)
+                F = __viaddmax_s16x2(F, nge, hg);                          // Eq. 3 (next row)
+              }
+            }
           }
         }
       }
+      // S = max(S reset at the previous END, H_0 .. H_{R-1}); the reset adds
+      // -32768 to a half in [0, 32767] (no wrap), folded into the first max.
+      S = __viaddmax_s16x2(S, kneg_prev, H[0]);
 #pragma unroll
-      for (int r = 0; r + 1 < R; r += 2) S = __vimax3_s16x2(S, H[r], H[r + 1]);
-      if (R & 1) S = __vmaxs2(S, H[R - 1]);
+      for (int r = 1; r + 1 < R; r += 2) S = __vimax3_s16x2(S, H[r], H[r + 1]);
+      if ((R & 1) == 0) S = __vmaxs2(S, H[R - 1]);
       hout = H[R - 1];
       fout = F;
       sc = __vmaxs2(sc_in, S);   // running max over lanes 0..t (valid at END columns)
-      S &= d1.x;                 // reset the half(s) whose sequence ended
-      if (st_on) p.bnd_out[col0 + s + u - (G - 1)] = make_uint2(hout, fout);
-      if (last && d1.y != 0u) {  // END column reached the last lane: emit
-        if (d1.y & 1u) {
+      if (last) st_global_v2(optr + u, hout, fout);
+      if (kp > emit_cmp) {       // an END column reached the last lane: emit
+        if ((kp & 0xffffu) != 0u) {
           const int orig = p.slots[seqA + kA];
           ++kA;
           const int v = (int)(sc & 0xffffu);
@@ -187,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params
           else p.scores[orig] = max(p.scores[orig], v);
           if (v >= p.thresh) p.flagged[orig] = 1;
         }
-        if (d1.y & 2u) {
+        if ((kp >> 16) != 0u) {
           const int orig = p.slots[seqB + kB];
           ++kB;
           const int v = (int)(sc >> 16);
@@ -198,6 +287,9 @@ __global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params
       }
     }
     s += 4;
+    sptr = ptr_add(sptr, inc_s);
+    if (BIN) bptr = ptr_add(bptr, inc_s);
+    optr = ptr_add(optr, inc_o);
   }
 }
 
@@ -295,41 +387,39 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
 // |q| x |Sigma|"), built per query in the layouts the kernels read.
 // ---------------------------------------------------------------------------
 __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const int8_t *__restrict__ M,
-                                int G, int R, int P, int goe16, int ge16, uint32_t *qp16,
-                                uint4 *desc, int32_t *qp32, int mpad32) {
-  const int K = (R + 3) / 4;
-  const int64_t n16 = (int64_t)P * kNL * K * G * 4;
+                                int G, int R, int P, int rpc, uint8_t *qp, uint4 *desc, int32_t *qp32,
+                                int mpad32) {
+  // rpc = rows per 16-B chunk: 4 (32-bit zero-extended words) or 8 (int16)
+  const int KC = (R + rpc - 1) / rpc;
+  const int LS = KC * G * 16;
+  const int64_t nq = (int64_t)P * kNL * KC * G * rpc;
   const int64_t ndesc = kNL * kNL;
   const int64_t n32 = (int64_t)kNL * mpad32;
-  const int64_t total = n16 + ndesc + n32;
+  const int64_t total = nq + ndesc + n32;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < n16) {
+    if (i < nq) {
       int64_t rest = i;
-      const int e = (int)(rest & 3); rest >>= 2;
+      const int e = (int)(rest % rpc); rest /= rpc;
       const int t = (int)(rest % G); rest /= G;
-      const int kk = (int)(rest % K); rest /= K;
+      const int kk = (int)(rest % KC); rest /= KC;
       const int c = (int)(rest % kNL);
       const int pass = (int)(rest / kNL);
-      const int rloc = 4 * kk + e;
+      const int rloc = rpc * kk + e;
       const int64_t row = (int64_t)pass * G * R + (int64_t)t * R + rloc;
-      uint32_t v = 0x8000u;  // -32768: separator letters, phantom rows
-      if (rloc < R && row < m && c < kAlpha) v = (uint32_t)(uint16_t)(int16_t)M[q[row] * kAlpha + c];
-      qp16[i] = v;
-    } else if (i < n16 + ndesc) {
-      const int k = (int)(i - n16);
+      uint16_t v = 0x8000u;  // -32768: separator letters, phantom rows
+      if (rloc < R && row < m && c < kAlpha) v = (uint16_t)(int16_t)M[q[row] * kAlpha + c];
+      if (rpc == 8) reinterpret_cast<uint16_t *>(qp)[i] = v;
+      else reinterpret_cast<uint32_t *>(qp)[i] = (uint32_t)v;
+    } else if (i < nq + ndesc) {
+      const int k = (int)(i - nq);
       const int cA = k / kNL, cB = k % kNL;
-      const uint32_t offA = (uint32_t)(cA * K * G * 16), offB = (uint32_t)(cB * K * G * 16);
-      const int gA = cA >= kAlpha ? 32767 : goe16, gB = cB >= kAlpha ? 32767 : goe16;
-      const int eA = cA >= kAlpha ? 32767 : ge16, eB = cB >= kAlpha ? 32767 : ge16;
-      const uint32_t ngoe = (uint32_t)(uint16_t)(int16_t)(-gA) | ((uint32_t)(uint16_t)(int16_t)(-gB) << 16);
-      const uint32_t nge = (uint32_t)(uint16_t)(int16_t)(-eA) | ((uint32_t)(uint16_t)(int16_t)(-eB) << 16);
-      const uint32_t keep = (cA == kEnd ? 0u : 0xffffu) | (cB == kEnd ? 0u : 0xffff0000u);
-      const uint32_t flags = (cA == kEnd ? 1u : 0u) | (cB == kEnd ? 2u : 0u);
-      desc[2 * k] = make_uint4(offA, offB, ngoe, nge);
-      desc[2 * k + 1] = make_uint4(keep, flags, 0u, 0u);
+      const uint32_t offA = (uint32_t)(cA * LS / 16), offB = (uint32_t)(cB * LS / 16);
+      const uint32_t ns = (cA < kAlpha ? 1u : 0u) + (cB < kAlpha ? 65536u : 0u);
+      const uint32_t endneg = (cA == kEnd ? 0x8000u : 0u) | (cB == kEnd ? 0x80000000u : 0u);
+      desc[k] = make_uint4(offA | (offB << 16), ns, endneg, 0u);
     } else {
-      const int64_t j = i - n16 - ndesc;
+      const int64_t j = i - nq - ndesc;
       const int c = (int)(j / mpad32);
       const int row = (int)(j % mpad32);
       qp32[j] = (row < m && c < kAlpha) ? (int32_t)M[q[row] * kAlpha + c] : -(1 << 30);
@@ -442,28 +532,32 @@ __global__ void decode_keys_kernel(const uint64_t *keys, int64_t k, int64_t *idx
 // ---------------------------------------------------------------------------
 using PassFn = void (*)(const SW16Params);
 
-template <int R, int G>
+template <int R, int G, int QPM>
 constexpr int smem_of() {
-  return (kNL * kNL * 2 + kNL * ((R + 3) / 4) * G) * 16;
+  return (kNL * kNL + kNL * ((R + (QPM == 0 ? 4 : 8) - 1) / (QPM == 0 ? 4 : 8)) * G) * 16;
 }
 
 struct TileEntry {
-  int G, R, smem;
-  PassFn fn;
+  int G, R, qpm, smem;
+  PassFn fn0, fn1;   // pass 0 / passes > 0 (boundary input)
   int ctas;
 };
 
-#define SW_TILE(G_, R_) {G_, R_, smem_of<R_, G_>(), sw16_pass_kernel<R_, G_>, 0}
-TileEntry g_tiles[] = {
-    SW_TILE(8, 8),   SW_TILE(8, 12),  SW_TILE(8, 16),  SW_TILE(8, 18),  SW_TILE(8, 20),
-    SW_TILE(8, 24),  SW_TILE(8, 28),  SW_TILE(8, 32),
-    SW_TILE(16, 8),  SW_TILE(16, 12), SW_TILE(16, 16), SW_TILE(16, 20), SW_TILE(16, 24),
-    SW_TILE(16, 28), SW_TILE(16, 29), SW_TILE(16, 32),
-    SW_TILE(32, 8),  SW_TILE(32, 12), SW_TILE(32, 15), SW_TILE(32, 16), SW_TILE(32, 20),
-    SW_TILE(32, 24), SW_TILE(32, 28), SW_TILE(32, 32),
-};
+#define SW_TILE(G_, R_, M_)                                                                  \
+  {G_, R_, M_, smem_of<R_, G_, M_>(), sw16_pass_kernel<R_, G_, false, M_>,                 \
+   sw16_pass_kernel<R_, G_, true, M_>, 0}
+#define SW_TILES(M_)                                                                          \
+  SW_TILE(8, 8, M_), SW_TILE(8, 16, M_), SW_TILE(8, 18, M_), SW_TILE(8, 24, M_),              \
+  SW_TILE(8, 29, M_), SW_TILE(8, 32, M_),                                                     \
+  SW_TILE(16, 8, M_), SW_TILE(16, 12, M_), SW_TILE(16, 16, M_), SW_TILE(16, 18, M_),          \
+  SW_TILE(16, 24, M_), SW_TILE(16, 29, M_), SW_TILE(16, 32, M_),                              \
+  SW_TILE(32, 8, M_), SW_TILE(32, 12, M_), SW_TILE(32, 15, M_), SW_TILE(32, 16, M_),          \
+  SW_TILE(32, 18, M_), SW_TILE(32, 24, M_), SW_TILE(32, 29, M_), SW_TILE(32, 32, M_)
+TileEntry g_tiles[] = {SW_TILES(0), SW_TILES(1), SW_TILES(2)};
+#undef SW_TILES
 #undef SW_TILE
 constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
+int g_qpm = 0;   // profile mode used for automatic and forced tiles
 
 int grid_for(int64_t total, int threads) {
   int64_t g = (total + threads - 1) / threads;
@@ -475,39 +569,50 @@ int grid_for(int64_t total, int threads) {
 }  // namespace
 
 int num_tiles() { return kNumTiles; }
-TileInfo tile(int i) { return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem}; }
+TileInfo tile(int i) { return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem, g_tiles[i].qpm}; }
 int find_tile(int G, int R) {
   for (int i = 0; i < kNumTiles; ++i)
-    if (g_tiles[i].G == G && g_tiles[i].R == R) return i;
+    if (g_tiles[i].G == G && g_tiles[i].R == R && g_tiles[i].qpm == g_qpm) return i;
   return -1;
 }
+void set_profile_mode(int m) { g_qpm = m; }
+int profile_mode() { return g_qpm; }
 int tile_ctas_per_sm(int i) { return g_tiles[i].ctas; }
 
 cudaError_t init_kernels() {
   for (int i = 0; i < kNumTiles; ++i) {
-    cudaError_t e = cudaFuncSetAttribute(g_tiles[i].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         g_tiles[i].smem);
+    for (PassFn fn : {g_tiles[i].fn0, g_tiles[i].fn1}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g_tiles[i].smem);
+      if (e != cudaSuccess) return e;
+    }
+    int n0 = 0, n1 = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n0, g_tiles[i].fn0, kThreads, g_tiles[i].smem);
     if (e != cudaSuccess) return e;
-    int n = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, g_tiles[i].fn, kThreads, g_tiles[i].smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, g_tiles[i].fn1, kThreads, g_tiles[i].smem);
     if (e != cudaSuccess) return e;
-    g_tiles[i].ctas = n;
+    g_tiles[i].ctas = n0 < n1 ? n0 : n1;
   }
   return cudaSuccess;
 }
 
+size_t qp_bytes(int G, int R, int P, int qpm) {
+  const int rpc = qpm == 0 ? 4 : 8;
+  return (size_t)P * kNL * ((R + rpc - 1) / rpc) * G * 16;
+}
+
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const int8_t *d_matrix, int G, int R, int P,
-                            int goe16, int ge16, uint32_t *d_qp, uint4 *d_desc, int32_t *d_qp32,
-                            int mpad32, cudaStream_t st) {
-  const int K = (R + 3) / 4;
-  const int64_t total = (int64_t)P * kNL * K * G * 4 + kNL * kNL + (int64_t)kNL * mpad32;
-  qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_matrix, G, R, P, goe16, ge16, d_qp,
-                                                         d_desc, d_qp32, mpad32);
+                            int qpm, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int mpad32,
+                            cudaStream_t st) {
+  const int rpc = qpm == 0 ? 4 : 8;
+  const int64_t total = (int64_t)P * kNL * ((R + rpc - 1) / rpc) * G * rpc + kNL * kNL + (int64_t)kNL * mpad32;
+  qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_matrix, G, R, P, rpc, d_qp, d_desc,
+                                                         d_qp32, mpad32);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sw16_pass(int ti, int grid, const SW16Params &p, cudaStream_t st) {
-  g_tiles[ti].fn<<<grid, kThreads, g_tiles[ti].smem, st>>>(p);
+  PassFn fn = p.bnd_in ? g_tiles[ti].fn1 : g_tiles[ti].fn0;
+  fn<<<grid, kThreads, g_tiles[ti].smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -13,15 +13,17 @@ struct SW16Params {
   int num_items;
   int *counter;             // atomic item cursor for this pass (zeroed)
   const int32_t *slots;     // slot -> original index
-  const uint4 *qp;          // query profile, all passes: [P][kNL][K][G] uint4
-  const uint4 *desc;        // descriptor table: [kNL*kNL][2] uint4
+  const uint4 *qp;          // int16 query profile, all passes: [P][kNL][K8][G][8]
+  const uint4 *desc;        // descriptor table: [kNL*kNL] uint4
   const uint2 *bnd_in;      // boundary (H,F) per column from the previous pass, or null
   uint2 *bnd_out;           // boundary for the next pass, or null
+  uint2 *dummy;             // one 8-B scratch slot per launched thread (idle-lane stores)
   int32_t *scores;          // original order
   uint8_t *flagged;         // original order, 1 = 16-bit score >= thresh
   int pass;
   int thresh;               // 32768 - max(1, smax)
   uint32_t zero;            // 0 (passed in so ptxas keeps it in a register)
+  uint32_t dgoe, dge;       // 32767 - min(Goe, 32767), 32767 - min(Ge, 32767)
 };
 
 struct SW32Params {
@@ -43,12 +45,16 @@ struct SW32Params {
 struct TileInfo {
   int G, R;
   int smem_bytes;           // dynamic shared memory of the pass kernel
+  int qpm;                  // profile mode (see kernels.cu)
 };
 
 // Compiled (G, R) tiles of the s16x2 pass kernel.
 int num_tiles();
 TileInfo tile(int i);
-int find_tile(int G, int R);  // index or -1
+int find_tile(int G, int R);  // index or -1 (in the current profile mode)
+void set_profile_mode(int m);
+int profile_mode();
+size_t qp_bytes(int G, int R, int P, int qpm);
 
 // Prepares kernel attributes (max dynamic smem).  Returns cudaError_t.
 cudaError_t init_kernels();
@@ -56,8 +62,8 @@ cudaError_t init_kernels();
 int tile_ctas_per_sm(int i);
 
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const int8_t *d_matrix, int G, int R,
-                            int P, int goe16, int ge16, uint32_t *d_qp, uint4 *d_desc,
-                            int32_t *d_qp32, int mpad32, cudaStream_t st);
+                            int P, int qpm, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int mpad32,
+                            cudaStream_t st);
 cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cudaStream_t st);
 cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n,
                                 cudaStream_t st);
