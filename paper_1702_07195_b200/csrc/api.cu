@@ -74,6 +74,8 @@ struct State {
   DevBuf<uint32_t> stream_img;
   DevBuf<Item> items;
   DevBuf<int32_t> slots;
+  DevBuf<int64_t> endcol;   // per sequence: 2 * END column + half
+  DevBuf<uint32_t> sc_out;  // per column: score chain value (one pass)
   DevBuf<uint8_t> res;      // plain copy, original order (for s32 re-scoring)
   DevBuf<int64_t> offs;
   // per search
@@ -108,7 +110,7 @@ struct State {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
   void release_all() {
-    stream_img.release(); items.release(); slots.release(); res.release(); offs.release();
+    stream_img.release(); items.release(); slots.release(); endcol.release(); sc_out.release(); res.release(); offs.release();
     scores.release(); flagged.release(); flag_list.release(); counters.release(); cells32.release();
     query.release(); matrix.release(); qp.release(); desc.release(); qp32.release(); bnd.release();
     scratch32.release(); dummy.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
@@ -144,7 +146,7 @@ int choose_tile(int m) {
   int bi = 0;
   for (int i = 0; i < num_tiles(); ++i) {
     const TileInfo ti = tile(i);
-    if (ti.qpm != profile_mode() || tile_ctas_per_sm(i) < 1) continue;
+    if (ti.qpm != (profile_mode() == 3 ? 0 : profile_mode()) || tile_ctas_per_sm(i) < 1) continue;
     const int rows = ti.G * ti.R;
     const int P = (m + rows - 1) / rows;
     const double cost = (double)P * ti.G * (5.5 * ti.R + 12.0) + P * 200.0;
@@ -222,20 +224,19 @@ int search_impl(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_
     p.items = g.items.p;
     p.num_items = g.num_items;
     p.counter = g.counters.p + pass;
-    p.slots = g.slots.p;
     p.qp = reinterpret_cast<const uint4 *>(g.qp.p);
     p.desc = g.desc.p;
     p.bnd_in = pass == 0 ? nullptr : g.bnd.p + (size_t)((pass - 1) & 1) * g.total_cols;
     p.bnd_out = pass == P - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * g.total_cols;
     p.dummy = g.dummy.p;
-    p.scores = d_scores;
-    p.flagged = g.flagged.p;
+    p.sc_out = g.sc_out.p;
     p.pass = pass;
     p.thresh = thresh;
     p.zero = 0u;
     p.dgoe = (uint32_t)(32767 - std::min(goe, 32767));
     p.dge = (uint32_t)(32767 - std::min(ge, 32767));
     CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
+    CUDA_TRY(launch_sw16_gather(g.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p, pass, thresh, st));
   }
   CUDA_TRY(cudaEventRecord(g.ev[2], st));
   CUDA_TRY(launch_flag_compact(g.flagged.p, g.count, g.flag_list.p, g.counters.p + kMaxPass, st));
@@ -321,6 +322,8 @@ int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
   CUDA_TRY(g.stream_img.ensure(img.stream.size()));
   CUDA_TRY(g.items.ensure(img.items.size()));
   CUDA_TRY(g.slots.ensure(img.slots.size()));
+  CUDA_TRY(g.endcol.ensure(img.endcol.size()));
+  CUDA_TRY(g.sc_out.ensure((size_t)img.total_cols));
   CUDA_TRY(g.res.ensure((size_t)g.total_res));
   CUDA_TRY(g.offs.ensure((size_t)count + 1));
   CUDA_TRY(g.scores.ensure((size_t)count));
@@ -333,6 +336,7 @@ int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
                       cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(g.items.p, img.items.data(), img.items.size() * sizeof(Item), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(g.slots.p, img.slots.data(), img.slots.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(g.endcol.p, img.endcol.data(), img.endcol.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   if (g.total_res > 0)
     CUDA_TRY(cudaMemcpy(g.res.p, residues, (size_t)g.total_res, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(g.offs.p, offsets, ((size_t)count + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));

@@ -72,6 +72,10 @@ __device__ __forceinline__ void st_global_v2(uint2 *p, uint32_t a, uint32_t b) {
   asm volatile("st.global.v2.u32 [%0], {%1, %2};" :: "l"(p), "r"(a), "r"(b) : "memory");
 }
 
+__device__ __forceinline__ void st_global_u32(uint32_t *p, uint32_t a) {
+  asm volatile("st.global.u32 [%0], %1;" :: "l"(p), "r"(a) : "memory");
+}
+
 template <class T>
 __device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on the FMA pipe
   uint64_t d;
@@ -84,8 +88,15 @@ __device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on
 //          16-B chunk); pack = IMAD(B, 65536, A)                [FMA pipe]
 //   QPM 1: int16 pairs (8 rows per chunk); pack with IMAD.HI/IMAD [FMA pipe]
 //   QPM 2: int16 pairs; pack with PRMT                           [ALU pipe]
-template <int R, int G, bool BIN, int QPM>
-__global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params p) {
+//
+// Lane roles inside a group (shuffles rotate: lane 0 receives from lane G-1):
+//   lane G-1 after computing its column: stores the column's score chain value
+//   (and the pass boundary), then overwrites its outgoing registers with the
+//   inputs of lane 0's next column -- the stream descriptor (loaded from smem
+//   early in the step, once its own copy is consumed) and the boundary of the
+//   previous pass (prefetched 4 columns ahead).  No per-lane selects at lane 0.
+template <int R, int G, bool BIN, int QPM, int NT>
+__global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   constexpr int RPC = QPM == 0 ? 4 : 8;     // rows per 16-B profile chunk
   constexpr int KC = (R + RPC - 1) / RPC;   // chunks per lane
   constexpr int LS = KC * G * 16;           // bytes per letter in the profile slice
@@ -102,38 +113,36 @@ __global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params
   const int lane = threadIdx.x & 31;
   const int t = lane & (G - 1);
   const int gbase = lane & ~(G - 1);
+  const int src = gbase + ((t + G - 1) & (G - 1));   // lane t-1; lane 0 <- lane G-1
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << gbase);
-  const bool first = t == 0;
   const bool last = t == G - 1;
-  const uint32_t nfirst = first ? 0u : 1u;
+  const uint32_t nlast = last ? 0u : 1u;
   const uint32_t zero = p.zero;
   const uint32_t s_desc = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t s_qp = s_desc + DESC_U4 * 16 + t * 16;
   const uint32_t pen_base = 0x80018001u;      // -32767 in both halves
   const uint32_t dgoe = p.dgoe, dge = p.dge;  // 32767 - Goe, 32767 - Ge (clamped)
-  const bool has_bout = p.bnd_out != nullptr;
+  const bool bout = last && p.bnd_out != nullptr;
   const uint4 nul = lds128(s_desc + kNulWord);
-  const uint32_t emit_cmp = last ? 0u : 0xffffffffu;   // kp > emit_cmp <=> last lane at an END column
 
   uint32_t H[R], E[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) { H[r] = 0u; E[r] = 0u; }
   uint32_t S = 0u, hout = 0u, fout = 0u, sc = 0u, hprev = 0u;
   uint32_t w0 = nul.x, ns = nul.y, kp = nul.z;   // column chain (NUL)
-  uint32_t kneg = 0u;                            // kp of the previous column
-  uint4 dcur = make_uint4(0u, 0u, 0u, 0u);       // lane 0: descriptor of the current column
+  uint32_t kneg = 0u;                            // END bits of the previous column
 
-  // Lane 0 prefetches the stream (and the boundary of the previous pass)
-  // 4 columns ahead; lane G-1 stores the boundary for the next pass.  When a
-  // group has no item left, the pointers stop advancing (increment 0) on the
-  // NUL padding at the start of the stream / a scratch word.
+  // Lane G-1 prefetches the stream and the previous pass's boundary 4 columns
+  // ahead, and stores per column the score chain value (sc_out) and the
+  // boundary for the next pass.  A group without items keeps feeding NUL
+  // columns; its pointers stop (increment 0) on the NUL padding / own slot.
+  uint2 *const dummy = p.dummy + (blockIdx.x * blockDim.x + threadIdx.x);
   const uint32_t *sptr = p.stream;
   const uint2 *bptr = p.bnd_in;
-  uint2 *const dummy = p.dummy + (blockIdx.x * blockDim.x + threadIdx.x);  // own slot: no contention
-  uint2 *optr = dummy;
-  uint32_t inc_s = 0u, inc_o = 0u;
-  int s = 0, nsteps = 0;
-  int seqA = 0, seqB = 0, kA = 0, kB = 0;
+  uint32_t *scp = reinterpret_cast<uint32_t *>(dummy);
+  uint2 *bop = dummy;
+  uint32_t inc = 0u;
+  int rem = 0;                                   // steps left in the current item
   bool done = false;
   uint32_t sring[4] = {0u, 0u, 0u, 0u};
   uint2 bring[4];
@@ -141,45 +150,50 @@ __global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params
   for (int u = 0; u < 4; ++u) bring[u] = make_uint2(0u, 0u);
 
   for (;;) {
-    if (s >= nsteps) {  // group-uniform: claim the next work item
+    if (rem <= 0) {  // group-uniform: claim the next work item
       int it = 0;
-      if (first) it = atomicAdd(p.counter, 1);
-      it = __shfl_sync(gmask, it, gbase);
+      if (last) it = atomicAdd(p.counter, 1);
+      it = __shfl_sync(gmask, it, gbase + G - 1);
       if (it < p.num_items) {
-        const Item item = p.items[it];
-        seqA = item.seqA;
-        seqB = item.seqB;
-        kA = 0;
-        kB = 0;
-        s = 0;
-        nsteps = (item.ncols + G - 1 + 3) & ~3;
-        inc_s = 4u;
-        sptr = p.stream + item.col_begin;
-        if (BIN) bptr = p.bnd_in + item.col_begin;
-        if (has_bout) {
-          optr = p.bnd_out + (item.col_begin - (G - 1));
-          inc_o = 4u;
-        }
-        if (first) {
+        const int64_t c0 = p.items[it].col_begin;
+        const int ncols = p.items[it].ncols;
+        rem = (ncols + G - 1 + 3) & ~3;
+        inc = 4u;
+        sptr = p.stream + c0;
+        if (BIN) bptr = p.bnd_in + c0;
+        scp = p.sc_out + (c0 - (G - 1));
+        if (p.bnd_out) bop = p.bnd_out + (c0 - (G - 1));
+        if (last) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             sring[u] = __ldg(sptr + u);
             if (BIN) bring[u] = __ldg(bptr + u);
           }
-          dcur = lds128(s_desc + sring[0]);
+          const uint4 d = lds128(s_desc + sring[0]);   // lane 0's first column
+          w0 = d.x;
+          ns = d.y;
+          kp = d.z;
+          hout = bring[0].x;
+          fout = bring[0].y;
+          sc = 0u;
         }
       } else {
         done = true;
-        nsteps = INT_MAX;
-        inc_s = 0u;
-        inc_o = 0u;
-        sptr = p.stream;          // NUL padding
-        if (BIN) bptr = p.bnd_in; // zeros (padding columns)
-        optr = dummy;
-        if (first) {
+        rem = INT_MAX;
+        inc = 0u;
+        sptr = p.stream;                   // NUL padding
+        if (BIN) bptr = p.bnd_in;          // zero padding
+        scp = reinterpret_cast<uint32_t *>(dummy);
+        bop = dummy;
+        if (last) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(0u, 0u); }
-          dcur = nul;
+          w0 = nul.x;
+          ns = nul.y;
+          kp = nul.z;
+          hout = 0u;
+          fout = 0u;
+          sc = 0u;
         }
       }
     }
@@ -187,25 +201,13 @@ __global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params
 
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      // ---- the column arrives from lane t-1 (lane 0: from the stream)
-      const uint32_t w0_up = __shfl_up_sync(0xffffffffu, w0, 1, G);
-      const uint32_t ns_up = __shfl_up_sync(0xffffffffu, ns, 1, G);
-      const uint32_t kp_up = __shfl_up_sync(0xffffffffu, kp, 1, G);
-      const uint32_t hu_up = __shfl_up_sync(0xffffffffu, hout, 1, G);
-      const uint32_t fu_up = __shfl_up_sync(0xffffffffu, fout, 1, G);
-      const uint32_t sc_up = __shfl_up_sync(0xffffffffu, sc, 1, G);
-      w0 = imad(w0_up, nfirst, dcur.x);
-      ns = imad(ns_up, nfirst, dcur.y);
-      kp = imad(kp_up, nfirst, dcur.z);
-      const uint32_t hu = imad(hu_up, nfirst, bring[u].x);
-      uint32_t F = imad(fu_up, nfirst, bring[u].y);
-      const uint32_t sc_in = imad(sc_up, nfirst, 0u);
-      // ---- lane 0: descriptor of the next column; refill the stream ring
-      if (first) dcur = lds128(s_desc + sring[(u + 1) & 3]);
-      if (first) {
-        sring[u] = __ldg(sptr + u + 4);
-        if (BIN) bring[u] = __ldg(bptr + u + 4);
-      }
+      // ---- this column's inputs from lane t-1 (lane 0: from lane G-1)
+      w0 = __shfl_sync(0xffffffffu, w0, src);
+      ns = __shfl_sync(0xffffffffu, ns, src);
+      kp = __shfl_sync(0xffffffffu, kp, src);
+      const uint32_t hu = __shfl_sync(0xffffffffu, hout, src);
+      uint32_t F = __shfl_sync(0xffffffffu, fout, src);
+      const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
       // ---- profile addresses and per-column gap penalties (FMA pipe)
       const uint32_t offB = umulhi(w0, 65536u);           // profile offsets / 16
       const uint32_t offA = imad(offB, 0xffff0000u, w0);
@@ -213,10 +215,19 @@ __global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params
       const uint32_t nge = imad(ns, dge, pen_base);     // -Ge,  or -32767 in a separator half
       const uint32_t aA = imad(offA, 16u, s_qp);
       const uint32_t aB = imad(offB, 16u, s_qp);
-      uint32_t hd = hprev;
-      hprev = hu;
       const uint32_t kneg_prev = kneg;   // -32768 in the half(s) whose sequence ended last column
       kneg = kp;
+      // ---- lane G-1: lane 0's next column descriptor; refill the rings
+      if (last) {
+        const uint4 d = lds128(s_desc + sring[(u + 1) & 3]);
+        w0 = d.x;
+        ns = d.y;
+        kp = d.z;
+        sring[u] = __ldg(sptr + u + 4);
+        if (BIN) bring[u] = __ldg(bptr + u + 4);
+      }
+      uint32_t hd = hprev;
+      hprev = hu;
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
         const uint4 a = lds128(aA + kk * G * 16);
@@ -263,33 +274,36 @@ __global__ void __launch_bounds__(kThreads, 1) sw16_pass_kernel(const SW16Params
 #pragma unroll
       for (int r = 1; r + 1 < R; r += 2) S = __vimax3_s16x2(S, H[r], H[r + 1]);
       if ((R & 1) == 0) S = __vmaxs2(S, H[R - 1]);
-      hout = H[R - 1];
-      fout = F;
-      sc = __vmaxs2(sc_in, S);   // running max over lanes 0..t (valid at END columns)
-      if (last) st_global_v2(optr + u, hout, fout);
-      if (kp > emit_cmp) {       // an END column reached the last lane: emit
-        if ((kp & 0xffffu) != 0u) {
-          const int orig = p.slots[seqA + kA];
-          ++kA;
-          const int v = (int)(sc & 0xffffu);
-          if (p.pass == 0) p.scores[orig] = v;
-          else p.scores[orig] = max(p.scores[orig], v);
-          if (v >= p.thresh) p.flagged[orig] = 1;
-        }
-        if ((kp >> 16) != 0u) {
-          const int orig = p.slots[seqB + kB];
-          ++kB;
-          const int v = (int)(sc >> 16);
-          if (p.pass == 0) p.scores[orig] = v;
-          else p.scores[orig] = max(p.scores[orig], v);
-          if (v >= p.thresh) p.flagged[orig] = 1;
-        }
-      }
+      const uint32_t so = __vmaxs2(sc_in, S);   // max over lanes 0..t (read at END columns)
+      if (last) st_global_u32(scp + u, so);
+      if (bout) st_global_v2(bop + u, H[R - 1], F);
+      // outgoing registers; lane G-1 hands over lane 0's next-column inputs
+      hout = imad(H[R - 1], nlast, bring[(u + 1) & 3].x);
+      fout = imad(F, nlast, bring[(u + 1) & 3].y);
+      sc = imad(so, nlast, 0u);
     }
-    s += 4;
-    sptr = ptr_add(sptr, inc_s);
-    if (BIN) bptr = ptr_add(bptr, inc_s);
-    optr = ptr_add(optr, inc_o);
+    rem -= 4;
+    sptr = ptr_add(sptr, inc);
+    if (BIN) bptr = ptr_add(bptr, inc);
+    scp = ptr_add(scp, inc);
+    bop = ptr_add(bop, inc);
+  }
+}
+
+// Scores of one pass from the per-column score chain: the value at a
+// sequence's END column.  Max over passes;
+// flag the 16-bit saturation test.
+__global__ void sw16_gather_kernel(const int64_t *__restrict__ endcol, int64_t count,
+                                   const uint32_t *__restrict__ sc_out, int32_t *scores, uint8_t *flagged,
+                                   int pass, int thresh) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = endcol[i];
+    const uint32_t w = sc_out[e >> 1];
+    const int v = (int)((e & 1) ? (w >> 16) : (w & 0xffffu));
+    const int prev = pass == 0 ? 0 : scores[i];
+    scores[i] = max(prev, v);
+    if (v >= thresh) flagged[i] = 1;
   }
 }
 
@@ -538,14 +552,15 @@ constexpr int smem_of() {
 }
 
 struct TileEntry {
-  int G, R, qpm, smem;
+  int G, R, qpm, nt, smem;
   PassFn fn0, fn1;   // pass 0 / passes > 0 (boundary input)
   int ctas;
 };
 
-#define SW_TILE(G_, R_, M_)                                                                  \
-  {G_, R_, M_, smem_of<R_, G_, M_>(), sw16_pass_kernel<R_, G_, false, M_>,                 \
-   sw16_pass_kernel<R_, G_, true, M_>, 0}
+#define SW_TILE_NT(G_, R_, M_, NT_)                                                         \
+  {G_, R_, M_, NT_, smem_of<R_, G_, M_>(), sw16_pass_kernel<R_, G_, false, M_, NT_>,       \
+   sw16_pass_kernel<R_, G_, true, M_, NT_>, 0}
+#define SW_TILE(G_, R_, M_) SW_TILE_NT(G_, R_, M_, 512)
 #define SW_TILES(M_)                                                                          \
   SW_TILE(8, 8, M_), SW_TILE(8, 16, M_), SW_TILE(8, 18, M_), SW_TILE(8, 24, M_),              \
   SW_TILE(8, 29, M_), SW_TILE(8, 32, M_),                                                     \
@@ -553,9 +568,21 @@ struct TileEntry {
   SW_TILE(16, 24, M_), SW_TILE(16, 29, M_), SW_TILE(16, 32, M_),                              \
   SW_TILE(32, 8, M_), SW_TILE(32, 12, M_), SW_TILE(32, 15, M_), SW_TILE(32, 16, M_),          \
   SW_TILE(32, 18, M_), SW_TILE(32, 24, M_), SW_TILE(32, 29, M_), SW_TILE(32, 32, M_)
-TileEntry g_tiles[] = {SW_TILES(0), SW_TILES(1), SW_TILES(2)};
+TileEntry g_tiles[] = {SW_TILES(0), SW_TILES(1), SW_TILES(2),
+                       // occupancy experiments (mode 3 = mode 0 kernels at other block sizes)
+                       {16, 29, 3, 384, smem_of<29, 16, 0>(), sw16_pass_kernel<29, 16, false, 0, 384>,
+                        sw16_pass_kernel<29, 16, true, 0, 384>, 0},
+                       {32, 15, 3, 640, smem_of<15, 32, 0>(), sw16_pass_kernel<15, 32, false, 0, 640>,
+                        sw16_pass_kernel<15, 32, true, 0, 640>, 0},
+                       {32, 12, 3, 640, smem_of<12, 32, 0>(), sw16_pass_kernel<12, 32, false, 0, 640>,
+                        sw16_pass_kernel<12, 32, true, 0, 640>, 0},
+                       {16, 12, 3, 640, smem_of<12, 16, 0>(), sw16_pass_kernel<12, 16, false, 0, 640>,
+                        sw16_pass_kernel<12, 16, true, 0, 640>, 0},
+                       {32, 16, 3, 640, smem_of<16, 32, 0>(), sw16_pass_kernel<16, 32, false, 0, 640>,
+                        sw16_pass_kernel<16, 32, true, 0, 640>, 0}};
 #undef SW_TILES
 #undef SW_TILE
+#undef SW_TILE_NT
 constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
 int g_qpm = 0;   // profile mode used for automatic and forced tiles
 
@@ -569,10 +596,13 @@ int grid_for(int64_t total, int threads) {
 }  // namespace
 
 int num_tiles() { return kNumTiles; }
-TileInfo tile(int i) { return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem, g_tiles[i].qpm}; }
+TileInfo tile(int i) { return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem, g_tiles[i].qpm == 3 ? 0 : g_tiles[i].qpm}; }
 int find_tile(int G, int R) {
   for (int i = 0; i < kNumTiles; ++i)
     if (g_tiles[i].G == G && g_tiles[i].R == R && g_tiles[i].qpm == g_qpm) return i;
+  if (g_qpm == 3)
+    for (int i = 0; i < kNumTiles; ++i)
+      if (g_tiles[i].G == G && g_tiles[i].R == R && g_tiles[i].qpm == 0) return i;
   return -1;
 }
 void set_profile_mode(int m) { g_qpm = m; }
@@ -586,9 +616,9 @@ cudaError_t init_kernels() {
       if (e != cudaSuccess) return e;
     }
     int n0 = 0, n1 = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n0, g_tiles[i].fn0, kThreads, g_tiles[i].smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n0, g_tiles[i].fn0, g_tiles[i].nt, g_tiles[i].smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, g_tiles[i].fn1, kThreads, g_tiles[i].smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, g_tiles[i].fn1, g_tiles[i].nt, g_tiles[i].smem);
     if (e != cudaSuccess) return e;
     g_tiles[i].ctas = n0 < n1 ? n0 : n1;
   }
@@ -612,7 +642,13 @@ cudaError_t launch_qp_build(const uint8_t *d_query, int m, const int8_t *d_matri
 
 cudaError_t launch_sw16_pass(int ti, int grid, const SW16Params &p, cudaStream_t st) {
   PassFn fn = p.bnd_in ? g_tiles[ti].fn1 : g_tiles[ti].fn0;
-  fn<<<grid, kThreads, g_tiles[ti].smem, st>>>(p);
+  fn<<<grid, g_tiles[ti].nt, g_tiles[ti].smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
+                               uint8_t *flagged, int pass, int thresh, cudaStream_t st) {
+  sw16_gather_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, scores, flagged, pass, thresh);
   return cudaGetLastError();
 }
 

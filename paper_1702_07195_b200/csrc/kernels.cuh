@@ -12,14 +12,12 @@ struct SW16Params {
   const Item *items;
   int num_items;
   int *counter;             // atomic item cursor for this pass (zeroed)
-  const int32_t *slots;     // slot -> original index
   const uint4 *qp;          // int16 query profile, all passes: [P][kNL][K8][G][8]
   const uint4 *desc;        // descriptor table: [kNL*kNL] uint4
   const uint2 *bnd_in;      // boundary (H,F) per column from the previous pass, or null
   uint2 *bnd_out;           // boundary for the next pass, or null
   uint2 *dummy;             // one 8-B scratch slot per launched thread (idle-lane stores)
-  int32_t *scores;          // original order
-  uint8_t *flagged;         // original order, 1 = 16-bit score >= thresh
+  uint32_t *sc_out;         // per column: score chain value at the last lane
   int pass;
   int thresh;               // 32768 - max(1, smax)
   uint32_t zero;            // 0 (passed in so ptxas keeps it in a register)
@@ -65,6 +63,8 @@ cudaError_t launch_qp_build(const uint8_t *d_query, int m, const int8_t *d_matri
                             int P, int qpm, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int mpad32,
                             cudaStream_t st);
 cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cudaStream_t st);
+cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
+                               uint8_t *flagged, int pass, int thresh, cudaStream_t st);
 cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n,
                                 cudaStream_t st);
 constexpr int kSW32Rows = 16;         // rows per lane of the 32-bit kernel

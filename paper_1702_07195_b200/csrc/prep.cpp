@@ -144,6 +144,7 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
   out.total_cols = col;
   // Write the stream: column word per pair column.
   out.stream.assign((size_t)col, column_word(kNul, kNul));
+  out.endcol.assign((size_t)count, -1);
   auto write_half = [&](const Item &it, int32_t slot0, int32_t n, int shift_is_b) {
     int64_t c = it.col_begin;
     for (int32_t k = 0; k < n; ++k) {
@@ -155,6 +156,7 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
         if (shift_is_b) cB = r[j]; else cA = r[j];
         out.stream[c] = column_word(cA, cB);
       }
+      out.endcol[s] = 2 * c + shift_is_b;   // the END column of sequence s
       for (int sep = 0; sep < 2; ++sep, ++c) {
         uint32_t w = out.stream[c];
         int cA = (int)(w / kDescBytes) / kNL, cB = (int)(w / kDescBytes) % kNL;

@@ -49,6 +49,7 @@ struct HostImage {
   std::vector<uint32_t> stream;   // column words, total_cols
   std::vector<Item> items;        // sorted by ncols descending (claim order)
   std::vector<int32_t> slots;     // slot -> original sequence index
+  std::vector<int64_t> endcol;    // per original sequence: 2 * (END column) + half (0 = A, 1 = B)
   int64_t total_cols = 0;
   int64_t max_len = 0;
 };
