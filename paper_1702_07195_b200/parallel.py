@@ -69,3 +69,24 @@ def gather_to_root(t, world: int, rank: int, dist):
         return out
     dist.gather(t, dst=0)
     return None
+
+
+def assemble_scores(gathered, shards, total: int) -> np.ndarray:
+    """Rank 0: scatter the gathered (padded) per-rank score vectors back to the
+    original database order using the static shard index maps."""
+    out = np.empty(total, dtype=np.int32)
+    for sc, idx in zip(gathered, shards):
+        sc = np.asarray(sc)
+        out[idx] = sc[: idx.size]
+    return out
+
+
+def pad_to(a, n: int):
+    """Pad a 1-D numpy array or torch tensor to length n with zeros (equal-count gather)."""
+    if hasattr(a, "new_zeros"):
+        out = a.new_zeros(n)
+        out[: a.numel()] = a
+        return out
+    out = np.zeros(n, dtype=a.dtype)
+    out[: a.size] = a
+    return out
