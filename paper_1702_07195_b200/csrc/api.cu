@@ -247,7 +247,6 @@ int search_impl(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_
   q.res = g.res.p;
   q.offs = g.offs.p;
   q.qp32 = g.qp32.p;
-  q.mpad = mpad32;
   q.passes = P32;
   q.neg_goe = -goe;
   q.neg_ge = -ge;

@@ -308,64 +308,90 @@ __global__ void sw16_gather_kernel(const int64_t *__restrict__ endcol, int64_t c
 }
 
 // ---------------------------------------------------------------------------
-// Exact s32 re-scoring of flagged sequences: one warp (G = 32
-// lanes x R rows) per sequence, read from the plain database copy; passes
-// over the query in-kernel with the (H, F) boundary in per-warp scratch.
+// Exact s32 re-scoring of flagged sequences ("recalculated using
+// the next wider integer range").  One warp (G = 32 lanes x R rows) per
+// flagged sequence, read from the plain database copy.  The warps of a CTA
+// step through the query passes together so that the pass's int32 profile
+// slice sits in shared memory ([letter][4-row chunk][lane][16 B]); the pass
+// boundary (H, F) goes through per-warp scratch.
 // ---------------------------------------------------------------------------
 template <int R>
 __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) {
-  constexpr int K = (R + 3) / 4;
+  constexpr int K4 = R / 4;
+  constexpr int SLICE_U4 = kNL * K4 * 32;
+  extern __shared__ uint4 sq[];
+  __shared__ int s_base;
   const int lane = threadIdx.x & 31;
-  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const int gwarp = blockIdx.x * nw + warp;
   const bool first = lane == 0, last = lane == 31;
   const int nfirst = first ? 0 : 1;
   uint2 *buf0 = p.scratch + (size_t)gwarp * 2 * p.stride + 32;
   uint2 *buf1 = buf0 + p.stride;
-  const int32_t *qp = p.qp32 + lane * R;
-  constexpr int kDummy = -(1 << 30);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sq) + lane * 16;
+  const int nflag = *p.flag_count;
 
   for (;;) {
-    int idx = 0;
-    if (first) idx = atomicAdd(p.cursor, 1);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
-    if (idx >= *p.flag_count) break;
-    const int orig = p.flag_list[idx];
-    const int64_t beg = p.offs[orig];
-    const int n = (int)(p.offs[orig + 1] - beg);
-    const uint8_t *res = p.res + beg;
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = atomicAdd(p.cursor, nw);
+    __syncthreads();
+    const int base = s_base;
+    if (base >= nflag) break;                      // CTA-uniform
+    const int idx = base + warp;
+    const bool active = idx < nflag;
+    int orig = 0, n = 0;
+    const uint8_t *res = p.res;
+    if (active) {
+      orig = p.flag_list[idx];
+      const int64_t b = p.offs[orig];
+      n = (int)(p.offs[orig + 1] - b);
+      res = p.res + b;
+    }
     int best = 0;
     for (int pass = 0; pass < p.passes; ++pass) {
+      __syncthreads();
+      const uint4 *g = reinterpret_cast<const uint4 *>(p.qp32) + (size_t)pass * SLICE_U4;
+      for (int i = threadIdx.x; i < SLICE_U4; i += blockDim.x) sq[i] = g[i];
+      __syncthreads();
+      if (!active) continue;
       const uint2 *bin = pass == 0 ? nullptr : ((pass & 1) ? buf0 : buf1);
       uint2 *bout = pass == p.passes - 1 ? nullptr : ((pass & 1) ? buf1 : buf0);
-      const int32_t *qpp = qp + pass * 32 * R;
       int H[R], E[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) { H[r] = 0; E[r] = 0; }
       int S = 0, hout = 0, fout = 0, hprev = 0, code = kNul;
-      const int nsteps = n + 31;
-      for (int c = 0; c < nsteps; ++c) {
-        const int code_up = __shfl_up_sync(0xffffffffu, code, 1);
-        const int hu_up = __shfl_up_sync(0xffffffffu, hout, 1);
-        const int fu_up = __shfl_up_sync(0xffffffffu, fout, 1);
-        int mycode = kNul, bh = 0, bf = 0;
-        if (first && c < n) {
-          mycode = res[c];
-          if (bin) { const uint2 b = bin[c]; bh = (int)b.x; bf = (int)b.y; }
-        }
-        code = first ? mycode : code_up;
-        const int hu = hu_up * nfirst + bh;
-        int F = fu_up * nfirst + bf;
-        const int32_t *q = qpp + code * p.mpad;
-        int hd = hprev;
-        hprev = hu;
+      int cring[4];
 #pragma unroll
-        for (int kk = 0; kk < K; ++kk) {
-          const int4 a = __ldg(reinterpret_cast<const int4 *>(q + kk * 4));
-          const int av[4] = {a.x, a.y, a.z, a.w};
+      for (int u = 0; u < 4; ++u) cring[u] = (first && u < n) ? (int)res[u] : kNul;
+      const int nsteps = (n + 31 + 3) & ~3;
+      for (int c0 = 0; c0 < nsteps; c0 += 4) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int r = kk * 4 + e;
-            if (r < R) {
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u;
+          const int code_up = __shfl_up_sync(0xffffffffu, code, 1);
+          const int hu_up = __shfl_up_sync(0xffffffffu, hout, 1);
+          const int fu_up = __shfl_up_sync(0xffffffffu, fout, 1);
+          int bh = 0, bf = 0;
+          if (first && bin && c < n) {
+            const uint2 b = bin[c];
+            bh = (int)b.x;
+            bf = (int)b.y;
+          }
+          code = first ? cring[u] : code_up;
+          if (first) cring[u] = (c + 4 < n) ? (int)res[c + 4] : kNul;
+          const int hu = hu_up * nfirst + bh;
+          int F = fu_up * nfirst + bf;
+          const uint32_t qa = sbase + (uint32_t)code * (K4 * 32 * 16);
+          int hd = hprev;
+          hprev = hu;
+#pragma unroll
+          for (int kk = 0; kk < K4; ++kk) {
+            const uint4 a = lds128(qa + kk * 32 * 16);
+            const int av[4] = {(int)a.x, (int)a.y, (int)a.z, (int)a.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int r = kk * 4 + e;
               int h = __viaddmax_s32_relu(hd, av[e], E[r]);
               h = max(h, F);
               hd = H[r];
@@ -375,23 +401,24 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
               F = __viaddmax_s32(F, p.neg_ge, hg);
             }
           }
-        }
 #pragma unroll
-        for (int r = 0; r + 1 < R; r += 2) S = __vimax3_s32(S, H[r], H[r + 1]);
-        if (R & 1) S = max(S, H[R - 1]);
-        hout = H[R - 1];
-        fout = F;
-        if (last && bout) bout[c - 31] = make_uint2((uint32_t)hout, (uint32_t)fout);
+          for (int r = 0; r + 1 < R; r += 2) S = __vimax3_s32(S, H[r], H[r + 1]);
+          hout = H[R - 1];
+          fout = F;
+          if (last && bout) bout[c - 31] = make_uint2((uint32_t)hout, (uint32_t)fout);
+        }
       }
       best = max(best, S);
       __syncwarp();
     }
+    if (active) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if (first) {
-      p.scores[orig] = best;
-      if (p.cells) atomicAdd(reinterpret_cast<unsigned long long *>(p.cells),
-                             (unsigned long long)n * (unsigned long long)(p.passes * 32 * R));
+      for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (first) {
+        p.scores[orig] = best;
+        if (p.cells) atomicAdd(reinterpret_cast<unsigned long long *>(p.cells),
+                               (unsigned long long)n * (unsigned long long)(p.passes * 32 * R));
+      }
     }
   }
 }
@@ -433,9 +460,15 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const int8
       const uint32_t endneg = (cA == kEnd ? 0x8000u : 0u) | (cB == kEnd ? 0x80000000u : 0u);
       desc[k] = make_uint4(offA | (offB << 16), ns, endneg, 0u);
     } else {
+      // s32 profile, pass-slice layout [pass][letter][4-row chunk][lane][4]
       const int64_t j = i - nq - ndesc;
-      const int c = (int)(j / mpad32);
-      const int row = (int)(j % mpad32);
+      int64_t rest = j;
+      const int e = (int)(rest & 3); rest >>= 2;
+      const int ln = (int)(rest & 31); rest >>= 5;
+      const int kk = (int)(rest % (kSW32Rows / 4)); rest /= (kSW32Rows / 4);
+      const int c = (int)(rest % kNL);
+      const int pass = (int)(rest / kNL);
+      const int row = pass * 32 * kSW32Rows + ln * kSW32Rows + kk * 4 + e;
       qp32[j] = (row < m && c < kAlpha) ? (int32_t)M[q[row] * kAlpha + c] : -(1 << 30);
     }
   }
@@ -658,7 +691,14 @@ cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *
 }
 
 cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st) {
-  sw32_kernel<kSW32Rows><<<grid, kSW32Threads, 0, st>>>(p);
+  constexpr int smem = kNL * (kSW32Rows / 4) * 32 * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(sw32_kernel<kSW32Rows>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  sw32_kernel<kSW32Rows><<<grid, kSW32Threads, smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -30,8 +30,7 @@ struct SW32Params {
   int *cursor;
   const uint8_t *res;       // plain database, original order
   const int64_t *offs;
-  const int32_t *qp32;      // [kNL][mpad] int32
-  int mpad;
+  const int32_t *qp32;      // [pass][kNL][kSW32Rows/4][32 lanes][4] int32
   int passes;
   int neg_goe, neg_ge;      // -(open+extend), -extend  (>= -2^30)
   uint2 *scratch;           // per warp: 2 * stride
