@@ -21,12 +21,14 @@ constexpr int CHAINS = 8;
 constexpr int ITERS = 2048;
 
 enum Op { ADDMAX_RELU, ADDMAX, MAX2, MAX3, ADDMAX_S32, PRMT_OP, IADD3_OP, LOP3_OP, IMAD_OP,
-          MIX_DPX_PRMT, MIX_DPX_IMAD, MIX_DPX_IADD3, CELL, SHFL_OP, NUM_OPS };
+          MIX_DPX_PRMT, MIX_DPX_IMAD, MIX_DPX_IADD3, CELL, SHFL_OP,
+          MIX_DPX3_IMAD1, MIX_DPX_IMADIMM, MIX_DPX_IMADHALF, ADDMAX_RZ, MIX_DPX_MOV, NUM_OPS };
 static const char* kNames[] = {"viaddmax_s16x2_relu", "viaddmax_s16x2", "vmax_s16x2", "vimax3_s16x2",
   "viaddmax_s32_relu", "prmt", "iadd3", "lop3", "imad", "mix_dpx_prmt_1to1", "mix_dpx_imad_1to1",
-  "mix_dpx_iadd3_1to1", "cellpair_R8", "shfl_up"};
+  "mix_dpx_iadd3_1to1", "cellpair_R8", "shfl_up", "mix_dpx3_imad1", "mix_dpx_imad_imm_1to1",
+  "mix_dpx2_imad1", "viaddmax_relu_rz", "mix_dpx_mov_1to1"};
 // thread-ops counted per chain per iteration for each op
-static const int kOpsPerIter[] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 0, 2};
+static const int kOpsPerIter[] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 0, 2, 4, 2, 3, 1, 2};
 
 template <int OP>
 __global__ void __launch_bounds__(256) bench(const unsigned* __restrict__ in, unsigned* out,
@@ -83,6 +85,32 @@ __global__ void __launch_bounds__(256) bench(const unsigned* __restrict__ in, un
         else if constexpr (OP == MIX_DPX_IMAD) n[k] = __viaddmax_s16x2(x, y, c) * y + c;
         else if constexpr (OP == MIX_DPX_IADD3) n[k] = __viaddmax_s16x2(x, y, c) + y + b;
         else if constexpr (OP == SHFL_OP) n[k] = __shfl_up_sync(0xffffffffu, x, 1) ^ y;
+        else if constexpr (OP == MIX_DPX3_IMAD1) {
+          uint32_t t1 = __viaddmax_s16x2(x, y, c);
+          uint32_t t2 = __viaddmax_s16x2_relu(t1, b, y);
+          uint32_t t3 = __vimax3_s16x2(t2, x, c);
+          uint32_t m;
+          asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(m) : "r"(t3), "r"(y), "r"(b));
+          n[k] = m;
+        }
+        else if constexpr (OP == MIX_DPX_IMADIMM) {
+          uint32_t m;
+          asm("mad.lo.u32 %0, %1, 65536, %2;" : "=r"(m) : "r"(__viaddmax_s16x2(x, y, c)), "r"(y));
+          n[k] = m;
+        }
+        else if constexpr (OP == MIX_DPX_IMADHALF) {
+          uint32_t t1 = __viaddmax_s16x2(x, y, c);
+          uint32_t t2 = __viaddmax_s16x2_relu(t1, b, y);
+          uint32_t m;
+          asm("mad.lo.u32 %0, %1, 65536, %2;" : "=r"(m) : "r"(t2), "r"(x));
+          n[k] = m;
+        }
+        else if constexpr (OP == ADDMAX_RZ) n[k] = __viaddmax_s16x2_relu(x, y, 0u);
+        else if constexpr (OP == MIX_DPX_MOV) {
+          uint32_t m;
+          asm volatile("mov.b32 %0, %1;" : "=r"(m) : "r"(__viaddmax_s16x2(x, y, c)));
+          n[k] = m;
+        }
       }
 #pragma unroll
       for (int k = 0; k < CHAINS; ++k) a[k] = n[k];
@@ -140,7 +168,7 @@ int main() {
   CK(cudaMalloc(&d_out, (size_t)nsm * 8 * 256 * sizeof(unsigned)));
   CK(cudaMalloc(&d_cyc, (size_t)nsm * 8 * sizeof(long long)));
   printf("{\"device_sms\": %d}\n", nsm);
-  for (int bps : {4, 8}) {
+  for (int bps : {2, 4}) {
     run<ADDMAX_RELU>(nsm, bps, d_in, d_out, d_cyc);
     run<ADDMAX>(nsm, bps, d_in, d_out, d_cyc);
     run<MAX2>(nsm, bps, d_in, d_out, d_cyc);
@@ -155,6 +183,11 @@ int main() {
     run<MIX_DPX_IADD3>(nsm, bps, d_in, d_out, d_cyc);
     run<CELL>(nsm, bps, d_in, d_out, d_cyc);
     run<SHFL_OP>(nsm, bps, d_in, d_out, d_cyc);
+    run<MIX_DPX3_IMAD1>(nsm, bps, d_in, d_out, d_cyc);
+    run<MIX_DPX_IMADIMM>(nsm, bps, d_in, d_out, d_cyc);
+    run<MIX_DPX_IMADHALF>(nsm, bps, d_in, d_out, d_cyc);
+    run<ADDMAX_RZ>(nsm, bps, d_in, d_out, d_cyc);
+    run<MIX_DPX_MOV>(nsm, bps, d_in, d_out, d_cyc);
   }
   return 0;
 }

@@ -95,8 +95,9 @@ __device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on
 //   inputs of lane 0's next column -- the stream descriptor (loaded from smem
 //   early in the step, once its own copy is consumed) and the boundary of the
 //   previous pass (prefetched 4 columns ahead).  No per-lane selects at lane 0.
-template <int R, int G, bool BIN, int QPM, int NT>
+template <int R, int G, bool BIN, int QPM, int NT, int U>
 __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
+  static_assert(U == 1 || U == 2 || U == 4, "U: columns per unrolled block / prefetch distance");
   constexpr int RPC = QPM == 0 ? 4 : 8;     // rows per 16-B profile chunk
   constexpr int KC = (R + RPC - 1) / RPC;   // chunks per lane
   constexpr int LS = KC * G * 16;           // bytes per letter in the profile slice
@@ -144,10 +145,10 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   uint32_t inc = 0u;
   int rem = 0;                                   // steps left in the current item
   bool done = false;
-  uint32_t sring[4] = {0u, 0u, 0u, 0u};
-  uint2 bring[4];
+  uint32_t sring[U];
+  uint2 bring[U];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) bring[u] = make_uint2(0u, 0u);
+  for (int u = 0; u < U; ++u) { sring[u] = 0u; bring[u] = make_uint2(0u, 0u); }
 
   for (;;) {
     if (rem <= 0) {  // group-uniform: claim the next work item
@@ -157,24 +158,26 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       if (it < p.num_items) {
         const int64_t c0 = p.items[it].col_begin;
         const int ncols = p.items[it].ncols;
-        rem = (ncols + G - 1 + 3) & ~3;
-        inc = 4u;
+        rem = (ncols + G - 1 + U - 1) & ~(U - 1);
+        inc = (uint32_t)U;
         sptr = p.stream + c0;
         if (BIN) bptr = p.bnd_in + c0;
         scp = p.sc_out + (c0 - (G - 1));
         if (p.bnd_out) bop = p.bnd_out + (c0 - (G - 1));
         if (last) {
+          // ring slot x % U holds column x; columns 1..U are prefetched here
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            sring[u] = __ldg(sptr + u);
-            if (BIN) bring[u] = __ldg(bptr + u);
+          for (int u = 1; u <= U; ++u) {
+            sring[u % U] = __ldg(sptr + u);
+            if (BIN) bring[u % U] = __ldg(bptr + u);
           }
-          const uint4 d = lds128(s_desc + sring[0]);   // lane 0's first column
+          const uint4 d = lds128(s_desc + __ldg(sptr));   // lane 0's first column
           w0 = d.x;
           ns = d.y;
           kp = d.z;
-          hout = bring[0].x;
-          fout = bring[0].y;
+          const uint2 b0 = BIN ? __ldg(bptr) : make_uint2(0u, 0u);
+          hout = b0.x;
+          fout = b0.y;
           sc = 0u;
         }
       } else {
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         bop = dummy;
         if (last) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(0u, 0u); }
+          for (int u = 0; u < U; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(0u, 0u); }
           w0 = nul.x;
           ns = nul.y;
           kp = nul.z;
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
     if (__all_sync(0xffffffffu, done)) break;
 
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       // ---- this column's inputs from lane t-1 (lane 0: from lane G-1)
       w0 = __shfl_sync(0xffffffffu, w0, src);
       ns = __shfl_sync(0xffffffffu, ns, src);
@@ -217,14 +220,18 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       const uint32_t aB = imad(offB, 16u, s_qp);
       const uint32_t kneg_prev = kneg;   // -32768 in the half(s) whose sequence ended last column
       kneg = kp;
-      // ---- lane G-1: lane 0's next column descriptor; refill the rings
+      // ---- lane G-1: lane 0's next column (s+u+1) descriptor; refill its ring slot
+      uint2 bnext = make_uint2(0u, 0u);
       if (last) {
-        const uint4 d = lds128(s_desc + sring[(u + 1) & 3]);
+        const uint4 d = lds128(s_desc + sring[(u + 1) % U]);
         w0 = d.x;
         ns = d.y;
         kp = d.z;
-        sring[u] = __ldg(sptr + u + 4);
-        if (BIN) bring[u] = __ldg(bptr + u + 4);
+        sring[(u + 1) % U] = __ldg(sptr + u + 1 + U);
+        if (BIN) {
+          bnext = bring[(u + 1) % U];
+          bring[(u + 1) % U] = __ldg(bptr + u + 1 + U);
+        }
       }
       uint32_t hd = hprev;
       hprev = hu;
@@ -260,7 +267,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
                 h = __vmaxs2(h, F);                                 // Eq. 1
                 hd = H[r];
                 H[r] = h;
-                const uint32_t hg = __viaddmax_s16x2_relu(h, ngoe, zero);  // max(H-Goe, 0)
+                const uint32_t hg = __viaddmax_s16x2_relu(h, ngoe, ngoe);  // max(H-Goe, 0): ngoe <= 0, one register read fewer
                 E[r] = __viaddmax_s16x2(E[r], nge, hg);                    // Eq. 2 (next column)
                 F = __viaddmax_s16x2(F, nge, hg);                          // Eq. 3 (next row)
               }
@@ -278,11 +285,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       if (last) st_global_u32(scp + u, so);
       if (bout) st_global_v2(bop + u, H[R - 1], F);
       // outgoing registers; lane G-1 hands over lane 0's next-column inputs
-      hout = imad(H[R - 1], nlast, bring[(u + 1) & 3].x);
-      fout = imad(F, nlast, bring[(u + 1) & 3].y);
+      hout = imad(H[R - 1], nlast, bnext.x);
+      fout = imad(F, nlast, bnext.y);
       sc = imad(so, nlast, 0u);
     }
-    rem -= 4;
+    rem -= U;
     sptr = ptr_add(sptr, inc);
     if (BIN) bptr = ptr_add(bptr, inc);
     scp = ptr_add(scp, inc);
@@ -590,9 +597,13 @@ struct TileEntry {
   int ctas;
 };
 
-#define SW_TILE_NT(G_, R_, M_, NT_)                                                         \
-  {G_, R_, M_, NT_, smem_of<R_, G_, M_>(), sw16_pass_kernel<R_, G_, false, M_, NT_>,       \
-   sw16_pass_kernel<R_, G_, true, M_, NT_>, 0}
+#define SW_TILE_NTU(G_, R_, M_, NT_, U_)                                                     \
+  {G_, R_, M_, NT_, smem_of<R_, G_, M_>(), sw16_pass_kernel<R_, G_, false, M_, NT_, U_>,   \
+   sw16_pass_kernel<R_, G_, true, M_, NT_, U_>, 0}
+#define SW_TILE_NT(G_, R_, M_, NT_) SW_TILE_NTU(G_, R_, M_, NT_, 4)
+#define SW_TILE_X(G_, R_, NT_, U_)                                                             \
+  {G_, R_, 3, NT_, smem_of<R_, G_, 0>(), sw16_pass_kernel<R_, G_, false, 0, NT_, U_>,      \
+   sw16_pass_kernel<R_, G_, true, 0, NT_, U_>, 0}
 #define SW_TILE(G_, R_, M_) SW_TILE_NT(G_, R_, M_, 512)
 #define SW_TILES(M_)                                                                          \
   SW_TILE(8, 8, M_), SW_TILE(8, 16, M_), SW_TILE(8, 18, M_), SW_TILE(8, 24, M_),              \
@@ -602,20 +613,14 @@ struct TileEntry {
   SW_TILE(32, 8, M_), SW_TILE(32, 12, M_), SW_TILE(32, 15, M_), SW_TILE(32, 16, M_),          \
   SW_TILE(32, 18, M_), SW_TILE(32, 24, M_), SW_TILE(32, 29, M_), SW_TILE(32, 32, M_)
 TileEntry g_tiles[] = {SW_TILES(0), SW_TILES(1), SW_TILES(2),
-                       // occupancy experiments (mode 3 = mode 0 kernels at other block sizes)
-                       {16, 29, 3, 384, smem_of<29, 16, 0>(), sw16_pass_kernel<29, 16, false, 0, 384>,
-                        sw16_pass_kernel<29, 16, true, 0, 384>, 0},
-                       {32, 15, 3, 640, smem_of<15, 32, 0>(), sw16_pass_kernel<15, 32, false, 0, 640>,
-                        sw16_pass_kernel<15, 32, true, 0, 640>, 0},
-                       {32, 12, 3, 640, smem_of<12, 32, 0>(), sw16_pass_kernel<12, 32, false, 0, 640>,
-                        sw16_pass_kernel<12, 32, true, 0, 640>, 0},
-                       {16, 12, 3, 640, smem_of<12, 16, 0>(), sw16_pass_kernel<12, 16, false, 0, 640>,
-                        sw16_pass_kernel<12, 16, true, 0, 640>, 0},
-                       {32, 16, 3, 640, smem_of<16, 32, 0>(), sw16_pass_kernel<16, 32, false, 0, 640>,
-                        sw16_pass_kernel<16, 32, true, 0, 640>, 0}};
+                       // experiments (mode 3 = mode-0 profile with other block sizes / unrolls)
+                       SW_TILE_X(16, 29, 384, 1), SW_TILE_X(32, 15, 512, 1), SW_TILE_X(16, 16, 512, 1),
+                       SW_TILE_X(32, 16, 512, 2), SW_TILE_X(16, 24, 384, 2), SW_TILE_X(32, 29, 384, 1)};
 #undef SW_TILES
 #undef SW_TILE
 #undef SW_TILE_NT
+#undef SW_TILE_NTU
+#undef SW_TILE_X
 constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
 int g_qpm = 0;   // profile mode used for automatic and forced tiles
 
