@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--config", type=int, default=CONFIG_INDEX)
     ap.add_argument("--scale", type=float, default=1.0, help="(dev) shrink the workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="initialise the NCCL process group even at world size 1 (exercises the gather path)")
     return ap.parse_args()
 
 
@@ -224,8 +226,13 @@ def run_ours(args):
     assert torch.cuda.is_available(), "bench needs a CUDA device"
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29531")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if rank == 0:
         swbuild.build()
@@ -252,7 +259,7 @@ def run_ours(args):
     d_tk_i = torch.empty(TOPK, dtype=torch.int64, device=dev)
     d_tk_s = torch.empty(TOPK, dtype=torch.int32, device=dev)
     nmax = count
-    if world > 1:
+    if dist:
         t = torch.tensor([count], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         nmax = int(t.item())
@@ -265,7 +272,7 @@ def run_ours(args):
         sw.sw_search_dev(q, w.matrix, w.gap_open, w.gap_extend, d_scores, stream)
         sw.sw_topk_dev(d_scores, d_gidx, count, TOPK, d_tk_i, d_tk_s, stream)
         n = 0
-        if world > 1:
+        if dist:
             with torch.cuda.stream(stream):
                 d_pad[:count].copy_(d_scores)
                 all_sc = gather_to_root(d_pad, world, rank, dist)
@@ -283,7 +290,8 @@ def run_ours(args):
         step()
     stream.synchronize()
     st = sw.sw_last_stats()
-    per_step_kernels = 1 + st["passes"] + 2 + 3   # qp build, passes, compact, sw32, top-k (2 + decode)
+    # qp build, P x (pass kernel + score gather), flag compact, s32 re-score, top-k (2 + decode)
+    per_step_kernels = 1 + 2 * st["passes"] + 2 + 3
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
