@@ -135,8 +135,10 @@ int ensure_device_ready() {
   return SW_OK;
 }
 
-// Choose (G, R) for a query of m residues: minimise the issued lane-
-// instructions P * G * (5.5 R + overhead).
+// Choose (G, R) for a query of m residues: minimise the predicted pass time
+// P * G * R / eff(G, R) (rows computed, incl. phantom rows of the last pass,
+// over the tile's measured full-row throughput) plus a per-pass constant
+// (DESIGN.md "Tile choice").
 int choose_tile(int m) {
   if (g.force_G) {
     int ti = find_tile(g.force_G, g.force_R);
@@ -146,11 +148,11 @@ int choose_tile(int m) {
   int bi = 0;
   for (int i = 0; i < num_tiles(); ++i) {
     const TileInfo ti = tile(i);
-    if (ti.qpm != (profile_mode() == 3 ? 0 : profile_mode()) || tile_ctas_per_sm(i) < 1) continue;
+    if (ti.qpm != (profile_mode() >= 3 ? 0 : profile_mode()) || tile_ctas_per_sm(i) < 1) continue;
     const int rows = ti.G * ti.R;
     const int P = (m + rows - 1) / rows;
-    const double cost = (double)P * ti.G * (5.5 * ti.R + 12.0) + P * 200.0;
-    if (cost < best - 1e-9) {
+    const double cost = (double)P * rows / ti.eff + P * 0.002;
+    if (cost < best - 1e-12) {
       best = cost;
       bi = i;
     }
@@ -452,6 +454,7 @@ int sw_last_timing(float *ms, int n) {
 
 int sw_set_tile(int32_t G, int32_t R) {
   t_err.clear();
+  if (const char *e = getenv("SWDB_QPM")) set_profile_mode(atoi(e));
   if (G == 0) {
     g.force_G = g.force_R = 0;
     return SW_OK;

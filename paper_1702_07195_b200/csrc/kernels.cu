@@ -51,14 +51,20 @@ __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
 // this pass, int16, laid out [letter][8-row chunk][lane t][8 x int16] so that
 // the 8 lanes of a quarter-warp always hit 8 distinct 16-B bank groups.
 // Descriptor of letter pair (cA, cB): {offA | offB << 16 (profile offsets
-// in 16-B units), notsep bits (1 per non-separator half), END bits (0x8000 in a
-// half whose sequence ENDs: -32768 resets that half of S), 0}.  Only lane 0 of a group reads it; lanes
+// in 16-B units), notsep bits (1 per non-separator half), END bits (0x8000 in
+// a half whose sequence ENDs; informational), 0}.  Only lane 0 of a group reads it; lanes
 // t > 0 receive it from lane t-1 with the column.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t umulhi(uint32_t a, uint32_t b) {
   uint32_t d;
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -71,6 +77,12 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 __device__ __forceinline__ void st_global_v2(uint2 *p, uint32_t a, uint32_t b) {
   asm volatile("st.global.v2.u32 [%0], {%1, %2};" :: "l"(p), "r"(a), "r"(b) : "memory");
 }
+
+__device__ __forceinline__ void st_global_v4(uint4 *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+__device__ __forceinline__ void st_global_v2(uint2 *p, uint32_t a, uint32_t b);
 
 __device__ __forceinline__ void st_global_u32(uint32_t *p, uint32_t a) {
   asm volatile("st.global.u32 [%0], %1;" :: "l"(p), "r"(a) : "memory");
@@ -130,8 +142,8 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
   for (int r = 0; r < R; ++r) { H[r] = 0u; E[r] = 0u; }
   uint32_t S = 0u, hout = 0u, fout = 0u, sc = 0u, hprev = 0u;
-  uint32_t w0 = nul.x, ns = nul.y, kp = nul.z;   // column chain (NUL)
-  uint32_t kneg = 0u;                            // END bits of the previous column
+  uint32_t w0 = nul.x, ns = nul.y;               // column chain (NUL)
+  uint32_t kneg = 0u;                            // S-reset value after the previous column
 
   // Lane G-1 prefetches the stream and the previous pass's boundary 4 columns
   // ahead, and stores per column the score chain value (sc_out) and the
@@ -174,7 +186,6 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           const uint4 d = lds128(s_desc + __ldg(sptr));   // lane 0's first column
           w0 = d.x;
           ns = d.y;
-          kp = d.z;
           const uint2 b0 = BIN ? __ldg(bptr) : make_uint2(0u, 0u);
           hout = b0.x;
           fout = b0.y;
@@ -193,7 +204,6 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           for (int u = 0; u < U; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(0u, 0u); }
           w0 = nul.x;
           ns = nul.y;
-          kp = nul.z;
           hout = 0u;
           fout = 0u;
           sc = 0u;
@@ -207,7 +217,6 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       // ---- this column's inputs from lane t-1 (lane 0: from lane G-1)
       w0 = __shfl_sync(0xffffffffu, w0, src);
       ns = __shfl_sync(0xffffffffu, ns, src);
-      kp = __shfl_sync(0xffffffffu, kp, src);
       const uint32_t hu = __shfl_sync(0xffffffffu, hout, src);
       uint32_t F = __shfl_sync(0xffffffffu, fout, src);
       const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
@@ -218,15 +227,16 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       const uint32_t nge = imad(ns, dge, pen_base);     // -Ge,  or -32767 in a separator half
       const uint32_t aA = imad(offA, 16u, s_qp);
       const uint32_t aB = imad(offB, 16u, s_qp);
-      const uint32_t kneg_prev = kneg;   // -32768 in the half(s) whose sequence ended last column
-      kneg = kp;
+      // S is reset after every separator column (END: the score was just read
+      // from the chain; NUL: S is already 0): -32768 in each separator half.
+      const uint32_t kneg_prev = kneg;
+      kneg = imad(ns, 0xffff8000u, 0x80008000u);
       // ---- lane G-1: lane 0's next column (s+u+1) descriptor; refill its ring slot
       uint2 bnext = make_uint2(0u, 0u);
       if (last) {
-        const uint4 d = lds128(s_desc + sring[(u + 1) % U]);
+        const uint2 d = lds64(s_desc + sring[(u + 1) % U]);
         w0 = d.x;
         ns = d.y;
-        kp = d.z;
         sring[(u + 1) % U] = __ldg(sptr + u + 1 + U);
         if (BIN) {
           bnext = bring[(u + 1) % U];
@@ -601,28 +611,74 @@ struct TileEntry {
   {G_, R_, M_, NT_, smem_of<R_, G_, M_>(), sw16_pass_kernel<R_, G_, false, M_, NT_, U_>,   \
    sw16_pass_kernel<R_, G_, true, M_, NT_, U_>, 0}
 #define SW_TILE_NT(G_, R_, M_, NT_) SW_TILE_NTU(G_, R_, M_, NT_, 4)
-#define SW_TILE_X(G_, R_, NT_, U_)                                                             \
-  {G_, R_, 3, NT_, smem_of<R_, G_, 0>(), sw16_pass_kernel<R_, G_, false, 0, NT_, U_>,      \
-   sw16_pass_kernel<R_, G_, true, 0, NT_, U_>, 0}
 #define SW_TILE(G_, R_, M_) SW_TILE_NT(G_, R_, M_, 512)
 #define SW_TILES(M_)                                                                          \
-  SW_TILE(8, 8, M_), SW_TILE(8, 16, M_), SW_TILE(8, 18, M_), SW_TILE(8, 24, M_),              \
-  SW_TILE(8, 29, M_), SW_TILE(8, 32, M_),                                                     \
+  SW_TILE(8, 8, M_), SW_TILE(8, 12, M_), SW_TILE(8, 16, M_), SW_TILE(8, 18, M_),              \
+  SW_TILE(8, 20, M_), SW_TILE(8, 22, M_), SW_TILE(8, 24, M_), SW_TILE(8, 26, M_),             \
+  SW_TILE(8, 28, M_), SW_TILE(8, 29, M_), SW_TILE(8, 30, M_), SW_TILE(8, 32, M_),             \
   SW_TILE(16, 8, M_), SW_TILE(16, 12, M_), SW_TILE(16, 16, M_), SW_TILE(16, 18, M_),          \
-  SW_TILE(16, 24, M_), SW_TILE(16, 29, M_), SW_TILE(16, 32, M_),                              \
+  SW_TILE(16, 20, M_), SW_TILE(16, 22, M_), SW_TILE(16, 24, M_), SW_TILE(16, 26, M_),         \
+  SW_TILE(16, 28, M_), SW_TILE(16, 29, M_), SW_TILE(16, 30, M_), SW_TILE(16, 32, M_),         \
   SW_TILE(32, 8, M_), SW_TILE(32, 12, M_), SW_TILE(32, 15, M_), SW_TILE(32, 16, M_),          \
-  SW_TILE(32, 18, M_), SW_TILE(32, 24, M_), SW_TILE(32, 29, M_), SW_TILE(32, 32, M_)
-TileEntry g_tiles[] = {SW_TILES(0), SW_TILES(1), SW_TILES(2),
-                       // experiments (mode 3 = mode-0 profile with other block sizes / unrolls)
-                       SW_TILE_X(16, 29, 384, 1), SW_TILE_X(32, 15, 512, 1), SW_TILE_X(16, 16, 512, 1),
-                       SW_TILE_X(32, 16, 512, 2), SW_TILE_X(16, 24, 384, 2), SW_TILE_X(32, 29, 384, 1)};
+  SW_TILE(32, 18, M_), SW_TILE(32, 20, M_), SW_TILE(32, 22, M_), SW_TILE(32, 24, M_),         \
+  SW_TILE(32, 26, M_), SW_TILE(32, 28, M_), SW_TILE(32, 29, M_), SW_TILE(32, 30, M_),         \
+  SW_TILE(32, 32, M_)
+TileEntry g_tiles[] = {SW_TILES(0)};
 #undef SW_TILES
 #undef SW_TILE
 #undef SW_TILE_NT
 #undef SW_TILE_NTU
-#undef SW_TILE_X
 constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
 int g_qpm = 0;   // profile mode used for automatic and forced tiles
+
+// Measured full-row throughput (GCUPS, pass kernel, 1 B200, query of exactly
+// G*R residues vs configs[1] at 0.3 scale; profiles/r01_tile_calibration.jsonl).
+// Used by the tile choice: time ~ P * G * R / eff.
+struct TileEff { int G, R; float gcups; };
+const TileEff kTileEff[] = {
+    {8, 8, 4242.f},
+    {8, 12, 4694.f},
+    {8, 16, 4944.f},
+    {8, 18, 4979.f},
+    {8, 20, 5108.f},
+    {8, 22, 5179.f},
+    {8, 24, 5200.f},
+    {8, 26, 5156.f},
+    {8, 28, 5212.f},
+    {8, 29, 5155.f},
+    {8, 30, 5215.f},
+    {8, 32, 5290.f},
+    {16, 8, 4312.f},
+    {16, 12, 4747.f},
+    {16, 16, 4991.f},
+    {16, 18, 5088.f},
+    {16, 20, 5157.f},
+    {16, 22, 5225.f},
+    {16, 24, 5243.f},
+    {16, 26, 5205.f},
+    {16, 28, 5260.f},
+    {16, 29, 5203.f},
+    {16, 30, 5263.f},
+    {16, 32, 5329.f},
+    {32, 8, 4260.f},
+    {32, 12, 4779.f},
+    {32, 15, 4937.f},
+    {32, 16, 4927.f},
+    {32, 18, 5099.f},
+    {32, 20, 5075.f},
+    {32, 22, 5005.f},
+    {32, 24, 5108.f},
+    {32, 26, 5112.f},
+    {32, 28, 5139.f},
+    {32, 29, 5189.f},
+    {32, 30, 5094.f},
+    {32, 32, 5214.f}};
+
+float tile_eff(int G, int R) {
+  for (const TileEff &e : kTileEff)
+    if (e.G == G && e.R == R) return e.gcups;
+  return 4000.f;   // uncalibrated tile: pessimistic
+}
 
 int grid_for(int64_t total, int threads) {
   int64_t g = (total + threads - 1) / threads;
@@ -634,11 +690,14 @@ int grid_for(int64_t total, int threads) {
 }  // namespace
 
 int num_tiles() { return kNumTiles; }
-TileInfo tile(int i) { return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem, g_tiles[i].qpm == 3 ? 0 : g_tiles[i].qpm}; }
+TileInfo tile(int i) {
+  return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem, g_tiles[i].qpm >= 3 ? 0 : g_tiles[i].qpm,
+                  tile_eff(g_tiles[i].G, g_tiles[i].R)};
+}
 int find_tile(int G, int R) {
   for (int i = 0; i < kNumTiles; ++i)
     if (g_tiles[i].G == G && g_tiles[i].R == R && g_tiles[i].qpm == g_qpm) return i;
-  if (g_qpm == 3)
+  if (g_qpm >= 3)
     for (int i = 0; i < kNumTiles; ++i)
       if (g_tiles[i].G == G && g_tiles[i].R == R && g_tiles[i].qpm == 0) return i;
   return -1;

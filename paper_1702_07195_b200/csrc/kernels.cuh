@@ -43,6 +43,7 @@ struct TileInfo {
   int G, R;
   int smem_bytes;           // dynamic shared memory of the pass kernel
   int qpm;                  // profile mode (see kernels.cu)
+  float eff;                // measured full-row GCUPS of the pass kernel
 };
 
 // Compiled (G, R) tiles of the s16x2 pass kernel.

@@ -24,7 +24,8 @@ constexpr int kDescBytes = 16;      // bytes per descriptor table entry
 constexpr int kColAlign = 4;        // item column counts are multiples of this
 // Columns of NUL padding after every item in the stream image (and before the
 // first): lets lane 0 prefetch past an item's end and lane G-1 store its
-// pipeline-fill columns without bounds predicates.  >= 32 - 1 + 4 + 4.
+// pipeline-fill columns without bounds predicates.  >= (32 - 1) + 2U + 1;
+// a multiple of 4.
 constexpr int kItemPad = 40;
 
 // Column word of the s16x2 stream: byte offset of the descriptor of the
