@@ -106,6 +106,28 @@ int sw_search_dev(const uint8_t *query, int32_t qlen, const int8_t *matrix, int3
                   int32_t gap_extend, int32_t *d_scores, void *cuda_stream);
 
 /*
+ * sw_search_batch -- several queries against the database (SW stage for each).
+ *   queries   : host, uint8, the nq queries concatenated; query k is
+ *               queries[qoffsets[k] .. qoffsets[k+1]).
+ *   qoffsets  : host, int64[nq+1], qoffsets[0] == 0, every query length >= 1.
+ *   nq        : >= 1.
+ *   matrix, gap_open, gap_extend : as for sw_search.
+ *   scores_out: host, int32[nq * count]; scores_out[k*count + i] = score of
+ *               query k against database sequence i.
+ * Queries are sorted by length and paired: each pair is scored in ONE pass
+ * over a one-sequence-per-column image, query 1 in the low and query 2 in
+ * the high 16-bit half of every register (multi-query packing, SURVEY.md
+ * 8(f) NEXT-2); results are identical to nq calls of sw_search.
+ * sw_topk afterwards ranks query 0.  Errors as for sw_search.
+ */
+int sw_search_batch(const uint8_t *queries, const int64_t *qoffsets, int32_t nq, const int8_t *matrix,
+                    int32_t gap_open, int32_t gap_extend, int32_t *scores_out);
+
+/* Stream-ordered batch search into a DEVICE array d_scores[nq * count]. */
+int sw_search_batch_dev(const uint8_t *queries, const int64_t *qoffsets, int32_t nq, const int8_t *matrix,
+                        int32_t gap_open, int32_t gap_extend, int32_t *d_scores, void *cuda_stream);
+
+/*
  * sw_topk -- sorting stage over the last search's scores.
  *   k         : >= 0; min(k, count) results are written.
  *   idx_out   : host, int64[k]: original database indices.

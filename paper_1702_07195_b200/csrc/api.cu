@@ -63,34 +63,47 @@ struct DevBuf {
   }
 };
 
+// A device-resident stream image.
+struct Image {
+  DevBuf<uint32_t> stream;  // column words
+  DevBuf<Item> items;
+  DevBuf<int64_t> endcol;   // per sequence: 2 * END column + half
+  int64_t total_cols = 0;
+  int num_items = 0;
+  void release() {
+    stream.release(); items.release(); endcol.release();
+    total_cols = 0;
+    num_items = 0;
+  }
+};
+
 struct State {
   bool loaded = false;
   int device = -1;
   int num_sms = 0;
   cudaStream_t stream = nullptr;
-  int64_t count = 0, total_res = 0, total_cols = 0, max_len = 0;
-  int num_items = 0;
-  // database image
-  DevBuf<uint32_t> stream_img;
-  DevBuf<Item> items;
-  DevBuf<int32_t> slots;
-  DevBuf<int64_t> endcol;   // per sequence: 2 * END column + half
+  int64_t count = 0, total_res = 0, max_len = 0;
+  // img[0]: two sequences per column (one query); img[1]: one sequence per
+  // column (query pairs)
+  Image img[2];
+  int64_t max_cols = 0;
   DevBuf<uint32_t> sc_out;  // per column: score chain value (one pass)
   DevBuf<uint8_t> res;      // plain copy, original order (for s32 re-scoring)
   DevBuf<int64_t> offs;
   // per search
   DevBuf<int32_t> scores;   // internal scores (sw_search)
-  DevBuf<uint8_t> flagged;
-  DevBuf<int32_t> flag_list;
-  DevBuf<int> counters;     // [0..P) pass cursors, [kMaxPass] flag count, [+1] sw32 cursor
+  DevBuf<int32_t> bscores;  // internal scores (sw_search_batch)
+  DevBuf<uint8_t> flagged, flagged2;
+  DevBuf<int32_t> flag_list, flag_list2;
+  DevBuf<int> counters;     // [0..P) pass cursors, [kMaxPass..+3] flag counts / cursors
   DevBuf<int64_t> cells32;
-  DevBuf<uint8_t> query;
+  DevBuf<uint8_t> query, query2;
   DevBuf<int8_t> matrix;
   DevBuf<uint8_t> qp;
   DevBuf<uint4> desc;
-  DevBuf<int32_t> qp32;
-  DevBuf<uint2> bnd;        // 2 * total_cols
-  DevBuf<uint2> dummy;      // scratch for idle-lane stores (one 8-B slot per thread)
+  DevBuf<int32_t> qp32, qp32b;
+  DevBuf<uint2> bnd;        // 2 * max_cols
+  DevBuf<uint2> dummy;      // scratch for idle-lane stores (16-B slot per thread)
   DevBuf<uint2> scratch32;
   DevBuf<uint64_t> keys;
   DevBuf<uint64_t> keys2;
@@ -102,7 +115,7 @@ struct State {
   bool has_search = false;
   const int32_t *last_scores = nullptr;
   cudaStream_t last_stream = nullptr;
-  int last_G = 0, last_R = 0, last_P = 0;
+  int last_G = 0, last_R = 0, last_P = 0, last_mode = 0;
   int64_t last_flags = -1, last_cells32 = -1;
   // forced tile
   int force_G = 0, force_R = 0;
@@ -110,9 +123,12 @@ struct State {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
   void release_all() {
-    stream_img.release(); items.release(); slots.release(); endcol.release(); sc_out.release(); res.release(); offs.release();
-    scores.release(); flagged.release(); flag_list.release(); counters.release(); cells32.release();
-    query.release(); matrix.release(); qp.release(); desc.release(); qp32.release(); bnd.release();
+    img[0].release(); img[1].release();
+    sc_out.release(); res.release(); offs.release();
+    scores.release(); bscores.release(); flagged.release(); flagged2.release(); flag_list.release();
+    flag_list2.release(); counters.release(); cells32.release();
+    query.release(); query2.release(); matrix.release(); qp.release(); desc.release(); qp32.release();
+    qp32b.release(); bnd.release();
     scratch32.release(); dummy.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
     loaded = false;
     has_search = false;
@@ -128,7 +144,6 @@ int ensure_device_ready() {
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   if (!g_kernels_ready) {
-    if (const char *e = getenv("SWDB_QPM")) set_profile_mode(atoi(e));
     CUDA_TRY(init_kernels());
     g_kernels_ready = true;
   }
@@ -139,16 +154,16 @@ int ensure_device_ready() {
 // P * G * R / eff(G, R) (rows computed, incl. phantom rows of the last pass,
 // over the tile's measured full-row throughput) plus a per-pass constant
 // (DESIGN.md "Tile choice").
-int choose_tile(int m) {
+int choose_tile(int m, int qpm) {
   if (g.force_G) {
-    int ti = find_tile(g.force_G, g.force_R);
+    int ti = find_tile_mode(g.force_G, g.force_R, qpm);
     if (ti >= 0) return ti;
   }
   double best = 1e300;
-  int bi = 0;
+  int bi = -1;
   for (int i = 0; i < num_tiles(); ++i) {
     const TileInfo ti = tile(i);
-    if (ti.qpm != (profile_mode() >= 3 ? 0 : profile_mode()) || tile_ctas_per_sm(i) < 1) continue;
+    if (ti.qpm != qpm || tile_ctas_per_sm(i) < 1) continue;
     const int rows = ti.G * ti.R;
     const int P = (m + rows - 1) / rows;
     const double cost = (double)P * rows / ti.eff + P * 0.002;
@@ -176,60 +191,72 @@ int validate_query(const uint8_t *query, int32_t qlen, const int8_t *matrix, int
   return SW_OK;
 }
 
-int search_impl(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t gap_open,
-                int32_t gap_extend, int32_t *d_scores, cudaStream_t st) {
-  int rc = validate_query(query, qlen, matrix, gap_open, gap_extend);
+// One query (q2 == nullptr) against the database image of sequence pairs, or
+// a query pair (q, q2) against the image of single sequences.  Stream-ordered
+// on st; scores (and scores2) are device arrays in original database order.
+int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, const int8_t *matrix,
+                int32_t gap_open, int32_t gap_extend, int32_t *d_scores, int32_t *d_scores2, cudaStream_t st) {
+  int rc = validate_query(q, m, matrix, gap_open, gap_extend);
   if (rc) return rc;
+  if (q2 && (rc = validate_query(q2, m2, matrix, gap_open, gap_extend))) return rc;
   int dev = -1;
   CUDA_TRY(cudaGetDevice(&dev));
   if (dev != g.device) return fail(SW_EINVAL, "current CUDA device differs from the one sw_db_load used");
 
-  const int ti = choose_tile(qlen);
+  const bool pair = q2 != nullptr;
+  const int mode = pair ? 3 : 0;
+  const Image &I = g.img[pair ? 1 : 0];
+  const int mm = pair ? std::max(m, m2) : m;
+  const int ti = choose_tile(mm, mode);
+  if (ti < 0) return fail(SW_ECUDA, "no runnable kernel tile");
   const TileInfo T = tile(ti);
   const int rows = T.G * T.R;
-  const int P = (qlen + rows - 1) / rows;
+  const int P = (mm + rows - 1) / rows;
   if (P > kMaxPass) return fail(SW_EINVAL, "query too long");
-  const int P32 = (qlen + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
-  const int mpad32 = P32 * 32 * kSW32Rows;
+  const int P32max = (mm + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
   int smax = 1;
   for (int i = 0; i < kAlpha * kAlpha; ++i) smax = std::max(smax, (int)matrix[i]);
   const int thresh = 32768 - smax;
   const int goe = gap_open + gap_extend, ge = gap_extend;
 
-  CUDA_TRY(g.query.ensure((size_t)qlen));
+  CUDA_TRY(g.query.ensure((size_t)m));
+  if (pair) CUDA_TRY(g.query2.ensure((size_t)m2));
   CUDA_TRY(g.matrix.ensure(kAlpha * kAlpha));
   CUDA_TRY(g.qp.ensure(qp_bytes(T.G, T.R, P, T.qpm)));
   CUDA_TRY(g.desc.ensure((size_t)kNL * kNL));
-  CUDA_TRY(g.qp32.ensure((size_t)kNL * mpad32));
-  if (P > 1 && g.bnd.n < (size_t)g.total_cols * 2) {
-    CUDA_TRY(g.bnd.ensure((size_t)g.total_cols * 2));
+  CUDA_TRY(g.qp32.ensure((size_t)kNL * P32max * 32 * kSW32Rows));
+  if (pair) CUDA_TRY(g.qp32b.ensure((size_t)kNL * P32max * 32 * kSW32Rows));
+  if (P > 1 && g.bnd.n < (size_t)g.max_cols * 2) {
+    CUDA_TRY(g.bnd.ensure((size_t)g.max_cols * 2));
     // padding columns are only ever written with zeros; start from zeros
     CUDA_TRY(cudaMemset(g.bnd.p, 0, g.bnd.n * sizeof(uint2)));
   }
 
-  CUDA_TRY(cudaMemcpyAsync(g.query.p, query, (size_t)qlen, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(g.query.p, q, (size_t)m, cudaMemcpyHostToDevice, st));
+  if (pair) CUDA_TRY(cudaMemcpyAsync(g.query2.p, q2, (size_t)m2, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(g.matrix.p, matrix, kAlpha * kAlpha, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemsetAsync(g.counters.p, 0, sizeof(int) * (kMaxPass + 2), st));
+  CUDA_TRY(cudaMemsetAsync(g.counters.p, 0, sizeof(int) * (kMaxPass + 4), st));
   CUDA_TRY(cudaMemsetAsync(g.flagged.p, 0, (size_t)g.count, st));
+  if (pair) CUDA_TRY(cudaMemsetAsync(g.flagged2.p, 0, (size_t)g.count, st));
   CUDA_TRY(cudaMemsetAsync(g.cells32.p, 0, sizeof(int64_t), st));
   if (!g.ev[0])
     for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g.ev[i]));
   CUDA_TRY(cudaEventRecord(g.ev[0], st));
-  CUDA_TRY(launch_qp_build(g.query.p, qlen, g.matrix.p, T.G, T.R, P, T.qpm, g.qp.p, g.desc.p, g.qp32.p,
-                           mpad32, st));
+  CUDA_TRY(launch_qp_build(g.query.p, m, pair ? g.query2.p : nullptr, m2, g.matrix.p, T.G, T.R, P, g.qp.p,
+                           g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr, st));
 
   const int grid = g.num_sms * std::max(1, tile_ctas_per_sm(ti));
   CUDA_TRY(cudaEventRecord(g.ev[1], st));
   for (int pass = 0; pass < P; ++pass) {
     SW16Params p;
-    p.stream = g.stream_img.p;
-    p.items = g.items.p;
-    p.num_items = g.num_items;
+    p.stream = I.stream.p;
+    p.items = I.items.p;
+    p.num_items = I.num_items;
     p.counter = g.counters.p + pass;
     p.qp = reinterpret_cast<const uint4 *>(g.qp.p);
     p.desc = g.desc.p;
-    p.bnd_in = pass == 0 ? nullptr : g.bnd.p + (size_t)((pass - 1) & 1) * g.total_cols;
-    p.bnd_out = pass == P - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * g.total_cols;
+    p.bnd_in = pass == 0 ? nullptr : g.bnd.p + (size_t)((pass - 1) & 1) * I.total_cols;
+    p.bnd_out = pass == P - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * I.total_cols;
     p.dummy = g.dummy.p;
     p.sc_out = g.sc_out.p;
     p.pass = pass;
@@ -238,25 +265,30 @@ int search_impl(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_
     p.dgoe = (uint32_t)(32767 - std::min(goe, 32767));
     p.dge = (uint32_t)(32767 - std::min(ge, 32767));
     CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
-    CUDA_TRY(launch_sw16_gather(g.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p, pass, thresh, st));
+    CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p, pair ? d_scores2 : nullptr,
+                                pair ? g.flagged2.p : nullptr, pass, thresh, st));
   }
   CUDA_TRY(cudaEventRecord(g.ev[2], st));
-  CUDA_TRY(launch_flag_compact(g.flagged.p, g.count, g.flag_list.p, g.counters.p + kMaxPass, st));
-  SW32Params q;
-  q.flag_list = g.flag_list.p;
-  q.flag_count = g.counters.p + kMaxPass;
-  q.cursor = g.counters.p + kMaxPass + 1;
-  q.res = g.res.p;
-  q.offs = g.offs.p;
-  q.qp32 = g.qp32.p;
-  q.passes = P32;
-  q.neg_goe = -goe;
-  q.neg_ge = -ge;
-  q.scratch = g.scratch32.p;
-  q.stride = g.scratch_stride;
-  q.scores = d_scores;
-  q.cells = g.cells32.p;
-  CUDA_TRY(launch_sw32(g.sw32_grid, q, st));
+  // exact s32 re-scoring of every sequence whose 16-bit score saturated
+  for (int k = 0; k < (pair ? 2 : 1); ++k) {
+    CUDA_TRY(launch_flag_compact(k ? g.flagged2.p : g.flagged.p, g.count, k ? g.flag_list2.p : g.flag_list.p,
+                                 g.counters.p + kMaxPass + 2 * k, st));
+    SW32Params q;
+    q.flag_list = k ? g.flag_list2.p : g.flag_list.p;
+    q.flag_count = g.counters.p + kMaxPass + 2 * k;
+    q.cursor = g.counters.p + kMaxPass + 2 * k + 1;
+    q.res = g.res.p;
+    q.offs = g.offs.p;
+    q.qp32 = k ? g.qp32b.p : g.qp32.p;
+    q.passes = ((k ? m2 : m) + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
+    q.neg_goe = -goe;
+    q.neg_ge = -ge;
+    q.scratch = g.scratch32.p;
+    q.stride = g.scratch_stride;
+    q.scores = k ? d_scores2 : d_scores;
+    q.cells = g.cells32.p;
+    CUDA_TRY(launch_sw32(g.sw32_grid, q, st));
+  }
   CUDA_TRY(cudaEventRecord(g.ev[3], st));
 
   g.has_search = true;
@@ -265,8 +297,53 @@ int search_impl(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_
   g.last_G = T.G;
   g.last_R = T.R;
   g.last_P = P;
+  g.last_mode = mode;
   g.last_flags = -1;
   g.last_cells32 = -1;
+  return SW_OK;
+}
+
+int search_impl(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t gap_open,
+                int32_t gap_extend, int32_t *d_scores, cudaStream_t st) {
+  return search_core(query, qlen, nullptr, 0, matrix, gap_open, gap_extend, d_scores, nullptr, st);
+}
+
+int validate_batch(const uint8_t *queries, const int64_t *qoffsets, int32_t nq) {
+  if (!queries || !qoffsets) return fail(SW_EINVAL, "queries or qoffsets is NULL");
+  if (nq < 1) return fail(SW_EINVAL, "nq must be >= 1");
+  if (qoffsets[0] != 0) return fail(SW_EINVAL, "qoffsets[0] must be 0");
+  for (int32_t k = 0; k < nq; ++k)
+    if (qoffsets[k + 1] - qoffsets[k] < 1 || qoffsets[k + 1] - qoffsets[k] >= (int64_t(1) << 31))
+      return fail(SW_EINVAL, "query " + std::to_string(k) + " has length < 1 or >= 2^31");
+  return SW_OK;
+}
+
+// Batch: queries sorted by length, consecutive ones paired into the two 16-bit
+// halves (one pass over the single-sequence image serves both); an odd one
+// left over runs alone.
+int batch_impl(const uint8_t *queries, const int64_t *qoffsets, int32_t nq, const int8_t *matrix,
+               int32_t gap_open, int32_t gap_extend, int32_t *d_scores, cudaStream_t st) {
+  int rc = validate_batch(queries, qoffsets, nq);
+  if (rc) return rc;
+  std::vector<int32_t> order(nq);
+  for (int32_t k = 0; k < nq; ++k) order[k] = k;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+    return qoffsets[x + 1] - qoffsets[x] > qoffsets[y + 1] - qoffsets[y];
+  });
+  for (int32_t k = 0; k < nq; k += 2) {
+    const int32_t a = order[k];
+    const uint8_t *qa = queries + qoffsets[a];
+    const int32_t ma = (int32_t)(qoffsets[a + 1] - qoffsets[a]);
+    if (k + 1 < nq) {
+      const int32_t b = order[k + 1];
+      rc = search_core(qa, ma, queries + qoffsets[b], (int32_t)(qoffsets[b + 1] - qoffsets[b]), matrix, gap_open,
+                       gap_extend, d_scores + (size_t)a * g.count, d_scores + (size_t)b * g.count, st);
+    } else {
+      rc = search_core(qa, ma, nullptr, 0, matrix, gap_open, gap_extend, d_scores + (size_t)a * g.count, nullptr, st);
+    }
+    if (rc) return rc;
+  }
+  g.last_scores = d_scores;   // sw_topk after a batch ranks query 0
   return SW_OK;
 }
 
@@ -301,15 +378,17 @@ int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
   // Items are sized for the number of lane groups that run concurrently with
   // the widest-occupancy tile (4 groups per warp at G = 8, 16 warps per SM).
   const int64_t target_groups = (int64_t)nsm * 16 * 2;
-  HostImage img;
+  HostImage himg[2];
   try {
-    if (build_image(residues, offsets, count, target_groups, img, err)) return fail(SW_EINVAL, err);
+    for (int k = 0; k < 2; ++k)
+      if (build_image(residues, offsets, count, target_groups, k == 1, himg[k], err)) return fail(SW_EINVAL, err);
   } catch (const std::bad_alloc &) {
     return fail(SW_ENOMEM, "host allocation failed in the pre-processor");
   } catch (const std::exception &e) {
     return fail(SW_EINVAL, e.what());
   }
-  if (img.items.size() >= (size_t)INT_MAX) return fail(SW_EINVAL, "too many work items");
+  for (int k = 0; k < 2; ++k)
+    if (himg[k].items.size() >= (size_t)INT_MAX) return fail(SW_EINVAL, "too many work items");
   // replace the previous database
   sw_db_free();
   g.device = dev;
@@ -317,27 +396,31 @@ int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
   CUDA_TRY(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
   g.count = count;
   g.total_res = offsets[count];
-  g.total_cols = img.total_cols;
-  g.max_len = img.max_len;
-  g.num_items = (int)img.items.size();
-  CUDA_TRY(g.stream_img.ensure(img.stream.size()));
-  CUDA_TRY(g.items.ensure(img.items.size()));
-  CUDA_TRY(g.slots.ensure(img.slots.size()));
-  CUDA_TRY(g.endcol.ensure(img.endcol.size()));
-  CUDA_TRY(g.sc_out.ensure((size_t)img.total_cols));
+  g.max_len = himg[0].max_len;
+  g.max_cols = std::max(himg[0].total_cols, himg[1].total_cols);
+  for (int k = 0; k < 2; ++k) {
+    Image &I = g.img[k];
+    const HostImage &H = himg[k];
+    I.total_cols = H.total_cols;
+    I.num_items = (int)H.items.size();
+    CUDA_TRY(I.stream.ensure(H.stream.size()));
+    CUDA_TRY(I.items.ensure(H.items.size()));
+    CUDA_TRY(I.endcol.ensure(H.endcol.size()));
+    CUDA_TRY(cudaMemcpy(I.stream.p, H.stream.data(), H.stream.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(I.items.p, H.items.data(), H.items.size() * sizeof(Item), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(I.endcol.p, H.endcol.data(), H.endcol.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  CUDA_TRY(g.sc_out.ensure((size_t)g.max_cols));
   CUDA_TRY(g.res.ensure((size_t)g.total_res));
   CUDA_TRY(g.offs.ensure((size_t)count + 1));
   CUDA_TRY(g.scores.ensure((size_t)count));
   CUDA_TRY(g.flagged.ensure((size_t)count));
+  CUDA_TRY(g.flagged2.ensure((size_t)count));
   CUDA_TRY(g.flag_list.ensure((size_t)count));
-  CUDA_TRY(g.counters.ensure(kMaxPass + 2));
+  CUDA_TRY(g.flag_list2.ensure((size_t)count));
+  CUDA_TRY(g.counters.ensure(kMaxPass + 4));
   CUDA_TRY(g.cells32.ensure(1));
-  CUDA_TRY(g.dummy.ensure((size_t)nsm * 4 * 1024));   // one slot per resident thread
-  CUDA_TRY(cudaMemcpy(g.stream_img.p, img.stream.data(), img.stream.size() * sizeof(uint32_t),
-                      cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(g.items.p, img.items.data(), img.items.size() * sizeof(Item), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(g.slots.p, img.slots.data(), img.slots.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(g.endcol.p, img.endcol.data(), img.endcol.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(g.dummy.ensure((size_t)nsm * 4 * 1024));   // one 16-B slot per resident thread
   if (g.total_res > 0)
     CUDA_TRY(cudaMemcpy(g.res.p, residues, (size_t)g.total_res, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(g.offs.p, offsets, ((size_t)count + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
@@ -426,13 +509,17 @@ int sw_last_stats(int64_t *stats, int n) {
     int fc = 0;
     int64_t cells = 0;
     CUDA_TRY(cudaStreamSynchronize(g.last_stream));
+    int fc2 = 0;
     CUDA_TRY(cudaMemcpy(&fc, g.counters.p + kMaxPass, sizeof(int), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(&fc2, g.counters.p + kMaxPass + 2, sizeof(int), cudaMemcpyDeviceToHost));
+    fc += fc2;
     CUDA_TRY(cudaMemcpy(&cells, g.cells32.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
     g.last_flags = fc;
     g.last_cells32 = cells;
   }
+  const Image &I = g.img[g.last_mode == 3 ? 1 : 0];
   const int64_t v[8] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
-                        g.last_flags, g.last_cells32, g.total_cols, g.num_items};
+                        g.last_flags, g.last_cells32, I.total_cols, I.num_items};
   const int m = std::min(n, 8);
   for (int i = 0; i < m; ++i) stats[i] = v[i];
   return m;
@@ -454,17 +541,39 @@ int sw_last_timing(float *ms, int n) {
 
 int sw_set_tile(int32_t G, int32_t R) {
   t_err.clear();
-  if (const char *e = getenv("SWDB_QPM")) set_profile_mode(atoi(e));
   if (G == 0) {
     g.force_G = g.force_R = 0;
     return SW_OK;
   }
-  if (find_tile(G, R) < 0) return fail(SW_EINVAL, "tile not compiled");
+  if (find_tile_mode(G, R, 0) < 0 || find_tile_mode(G, R, 3) < 0) return fail(SW_EINVAL, "tile not compiled");
   g.force_G = G;
   g.force_R = R;
   return SW_OK;
 }
 
-int sw_tile_supported(int32_t G, int32_t R) { return find_tile(G, R) >= 0 ? 1 : 0; }
+int sw_tile_supported(int32_t G, int32_t R) { return find_tile_mode(G, R, 0) >= 0 ? 1 : 0; }
+
+int sw_search_batch_dev(const uint8_t *queries, const int64_t *qoffsets, int32_t nq, const int8_t *matrix,
+                        int32_t gap_open, int32_t gap_extend, int32_t *d_scores, void *cuda_stream) {
+  t_err.clear();
+  if (!g.loaded) return fail(SW_ENODB, "no database loaded");
+  if (!d_scores) return fail(SW_EINVAL, "d_scores is NULL");
+  return batch_impl(queries, qoffsets, nq, matrix, gap_open, gap_extend, d_scores, (cudaStream_t)cuda_stream);
+}
+
+int sw_search_batch(const uint8_t *queries, const int64_t *qoffsets, int32_t nq, const int8_t *matrix,
+                    int32_t gap_open, int32_t gap_extend, int32_t *scores_out) {
+  t_err.clear();
+  if (!g.loaded) return fail(SW_ENODB, "no database loaded");
+  if (!scores_out) return fail(SW_EINVAL, "scores_out is NULL");
+  if (nq < 1) return fail(SW_EINVAL, "nq must be >= 1");
+  CUDA_TRY(g.bscores.ensure((size_t)nq * g.count));
+  int rc = batch_impl(queries, qoffsets, nq, matrix, gap_open, gap_extend, g.bscores.p, g.stream);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(scores_out, g.bscores.p, (size_t)nq * g.count * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                           g.stream));
+  CUDA_TRY(cudaStreamSynchronize(g.stream));
+  return SW_OK;
+}
 
 }  // extern "C"

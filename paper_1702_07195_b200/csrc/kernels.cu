@@ -95,11 +95,16 @@ __device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on
   return reinterpret_cast<T *>(d);
 }
 
-// Profile modes (how the two halves' substitution scores are packed):
-//   QPM 0: one zero-extended int16 per (letter,row) 32-bit word (4 rows per
-//          16-B chunk); pack = IMAD(B, 65536, A)                [FMA pipe]
-//   QPM 1: int16 pairs (8 rows per chunk); pack with IMAD.HI/IMAD [FMA pipe]
-//   QPM 2: int16 pairs; pack with PRMT                           [ALU pipe]
+// Profile modes (what the two 16-bit halves of a register hold):
+//   QPM 0: two database sequences, one query.  Profile: one zero-extended
+//          int16 per (letter,row) 32-bit word, 4 rows per 16-B chunk; the two
+//          halves' scores are packed with one IMAD(B, 65536, A) (FMA pipe).
+//          (int16-pair profiles packed with PRMT or IMAD.HI were measured
+//          slower: profiles/r01_tile_calibration.jsonl.)
+//   QPM 3: one database sequence, two queries (multi-query packing, SURVEY
+//          8(f) NEXT-2).  Profile word = (SM[q1_r][c], SM[q2_r][c]): no
+//          packing at all; the stream holds one sequence per column (column
+//          word of the letter pair (c, c)).
 //
 // Lane roles inside a group (shuffles rotate: lane 0 receives from lane G-1):
 //   lane G-1 after computing its column: stores the column's score chain value
@@ -110,7 +115,8 @@ __device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on
 template <int R, int G, bool BIN, int QPM, int NT, int U>
 __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   static_assert(U == 1 || U == 2 || U == 4, "U: columns per unrolled block / prefetch distance");
-  constexpr int RPC = QPM == 0 ? 4 : 8;     // rows per 16-B profile chunk
+  static_assert(QPM == 0 || QPM == 3, "profile mode");
+  constexpr int RPC = 4;                    // rows per 16-B profile chunk
   constexpr int KC = (R + RPC - 1) / RPC;   // chunks per lane
   constexpr int LS = KC * G * 16;           // bytes per letter in the profile slice
   constexpr int QP_U4 = kNL * LS / 16;
@@ -248,31 +254,20 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
         const uint4 a = lds128(aA + kk * G * 16);
-        const uint4 b = lds128(aB + kk * G * 16);
+        const uint4 b = QPM == 0 ? lds128(aB + kk * G * 16) : make_uint4(0u, 0u, 0u, 0u);
         const uint32_t av[4] = {a.x, a.y, a.z, a.w};
         const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int r0 = kk * RPC + (QPM == 0 ? j : 2 * j);
+          const int r0 = kk * RPC + j;
           if (r0 < R) {
-            uint32_t sub0, sub1 = 0u;
-            if (QPM == 0) {
-              sub0 = imad(bv[j], 65536u, av[j]);                 // (A_r0, B_r0)
-            } else if (QPM == 1) {
-              // (A_r0 | A_r1<<16), (B_r0 | B_r1<<16) -> (A_r0, B_r0), (A_r1, B_r1)
-              const uint32_t hiA = umulhi(av[j], 65536u);
-              const uint32_t hiB = umulhi(bv[j], 65536u);
-              sub0 = imad(imad(hiA, 0xffffffffu, bv[j]), 65536u, av[j]);
-              sub1 = imad(hiB, 65536u, hiA);
-            } else {
-              sub0 = __byte_perm(av[j], bv[j], 0x5410);
-              sub1 = __byte_perm(av[j], bv[j], 0x7632);
-            }
+            // QPM 0: (SM(q_r, dA), SM(q_r, dB)); QPM 3: (SM(q1_r, d), SM(q2_r, d))
+            const uint32_t sub0 = QPM == 0 ? imad(bv[j], 65536u, av[j]) : av[j];
 #pragma unroll
-            for (int e = 0; e < (QPM == 0 ? 1 : 2); ++e) {
+            for (int e = 0; e < 1; ++e) {
               const int r = r0 + e;
               if (r < R) {
-                const uint32_t sub = e ? sub1 : sub0;
+                const uint32_t sub = sub0;
                 uint32_t h = __viaddmax_s16x2_relu(hd, sub, E[r]);  // max(Hdiag+SM, E, 0)
                 h = __vmaxs2(h, F);                                 // Eq. 1
                 hd = H[r];
@@ -312,15 +307,22 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 // flag the 16-bit saturation test.
 __global__ void sw16_gather_kernel(const int64_t *__restrict__ endcol, int64_t count,
                                    const uint32_t *__restrict__ sc_out, int32_t *scores, uint8_t *flagged,
-                                   int pass, int thresh) {
+                                   int32_t *scores2, uint8_t *flagged2, int pass, int thresh) {
+  // scores2 == nullptr: two sequences per column, the END column's half is the
+  // sequence's.  scores2 != nullptr (query pair): both halves belong to the
+  // sequence, low half = query 1, high half = query 2.
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = endcol[i];
     const uint32_t w = sc_out[e >> 1];
-    const int v = (int)((e & 1) ? (w >> 16) : (w & 0xffffu));
-    const int prev = pass == 0 ? 0 : scores[i];
-    scores[i] = max(prev, v);
+    const int v = (int)((!scores2 && (e & 1)) ? (w >> 16) : (w & 0xffffu));
+    scores[i] = max(pass == 0 ? 0 : scores[i], v);
     if (v >= thresh) flagged[i] = 1;
+    if (scores2) {
+      const int v2 = (int)(w >> 16);
+      scores2[i] = max(pass == 0 ? 0 : scores2[i], v2);
+      if (v2 >= thresh) flagged2[i] = 1;
+    }
   }
 }
 
@@ -444,31 +446,37 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
 // Query profile ("auxiliary two-dimensional array of size
 // |q| x |Sigma|"), built per query in the layouts the kernels read.
 // ---------------------------------------------------------------------------
-__global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const int8_t *__restrict__ M,
-                                int G, int R, int P, int rpc, uint8_t *qp, uint4 *desc, int32_t *qp32,
-                                int mpad32) {
-  // rpc = rows per 16-B chunk: 4 (32-bit zero-extended words) or 8 (int16)
-  const int KC = (R + rpc - 1) / rpc;
+__global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint8_t *__restrict__ q2, int m2,
+                                const int8_t *__restrict__ M, int G, int R, int P, uint32_t *qp, uint4 *desc,
+                                int32_t *qp32, int32_t *qp32b) {
+  // q2 == nullptr: one query; profile word = zero-extended int16 (QPM 0).
+  // q2 != nullptr: query pair; profile word = (SM[q_r][c], SM[q2_r][c]) (QPM 3).
+  const int KC = (R + 3) / 4;
   const int LS = KC * G * 16;
-  const int64_t nq = (int64_t)P * kNL * KC * G * rpc;
+  const int mm = q2 ? max(m, m2) : m;
+  const int P32 = (mm + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
+  const int64_t nq = (int64_t)P * kNL * KC * G * 4;
   const int64_t ndesc = kNL * kNL;
-  const int64_t n32 = (int64_t)kNL * mpad32;
+  const int64_t n32 = (int64_t)kNL * P32 * 32 * kSW32Rows;
   const int64_t total = nq + ndesc + n32;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (i < nq) {
       int64_t rest = i;
-      const int e = (int)(rest % rpc); rest /= rpc;
+      const int e = (int)(rest & 3); rest >>= 2;
       const int t = (int)(rest % G); rest /= G;
       const int kk = (int)(rest % KC); rest /= KC;
       const int c = (int)(rest % kNL);
       const int pass = (int)(rest / kNL);
-      const int rloc = rpc * kk + e;
+      const int rloc = 4 * kk + e;
       const int64_t row = (int64_t)pass * G * R + (int64_t)t * R + rloc;
-      uint16_t v = 0x8000u;  // -32768: separator letters, phantom rows
-      if (rloc < R && row < m && c < kAlpha) v = (uint16_t)(int16_t)M[q[row] * kAlpha + c];
-      if (rpc == 8) reinterpret_cast<uint16_t *>(qp)[i] = v;
-      else reinterpret_cast<uint32_t *>(qp)[i] = (uint32_t)v;
+      // -32768 (0x8000): separator letters and phantom rows
+      uint32_t lo = 0x8000u, hi = 0x8000u;
+      if (rloc < R && c < kAlpha) {
+        if (row < m) lo = (uint16_t)(int16_t)M[q[row] * kAlpha + c];
+        if (q2 && row < m2) hi = (uint16_t)(int16_t)M[q2[row] * kAlpha + c];
+      }
+      qp[i] = q2 ? (lo | (hi << 16)) : lo;
     } else if (i < nq + ndesc) {
       const int k = (int)(i - nq);
       const int cA = k / kNL, cB = k % kNL;
@@ -477,7 +485,7 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const int8
       const uint32_t endneg = (cA == kEnd ? 0x8000u : 0u) | (cB == kEnd ? 0x80000000u : 0u);
       desc[k] = make_uint4(offA | (offB << 16), ns, endneg, 0u);
     } else {
-      // s32 profile, pass-slice layout [pass][letter][4-row chunk][lane][4]
+      // s32 profile(s), pass-slice layout [pass][letter][4-row chunk][lane][4]
       const int64_t j = i - nq - ndesc;
       int64_t rest = j;
       const int e = (int)(rest & 3); rest >>= 2;
@@ -487,6 +495,7 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const int8
       const int pass = (int)(rest / kNL);
       const int row = pass * 32 * kSW32Rows + ln * kSW32Rows + kk * 4 + e;
       qp32[j] = (row < m && c < kAlpha) ? (int32_t)M[q[row] * kAlpha + c] : -(1 << 30);
+      if (q2) qp32b[j] = (row < m2 && c < kAlpha) ? (int32_t)M[q2[row] * kAlpha + c] : -(1 << 30);
     }
   }
 }
@@ -598,7 +607,7 @@ using PassFn = void (*)(const SW16Params);
 
 template <int R, int G, int QPM>
 constexpr int smem_of() {
-  return (kNL * kNL + kNL * ((R + (QPM == 0 ? 4 : 8) - 1) / (QPM == 0 ? 4 : 8)) * G) * 16;
+  return (kNL * kNL + kNL * ((R + 3) / 4) * G) * 16;
 }
 
 struct TileEntry {
@@ -623,13 +632,12 @@ struct TileEntry {
   SW_TILE(32, 18, M_), SW_TILE(32, 20, M_), SW_TILE(32, 22, M_), SW_TILE(32, 24, M_),         \
   SW_TILE(32, 26, M_), SW_TILE(32, 28, M_), SW_TILE(32, 29, M_), SW_TILE(32, 30, M_),         \
   SW_TILE(32, 32, M_)
-TileEntry g_tiles[] = {SW_TILES(0)};
+TileEntry g_tiles[] = {SW_TILES(0), SW_TILES(3)};
 #undef SW_TILES
 #undef SW_TILE
 #undef SW_TILE_NT
 #undef SW_TILE_NTU
 constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
-int g_qpm = 0;   // profile mode used for automatic and forced tiles
 
 // Measured full-row throughput (GCUPS, pass kernel, 1 B200, query of exactly
 // G*R residues vs configs[1] at 0.3 scale; profiles/r01_tile_calibration.jsonl).
@@ -691,19 +699,15 @@ int grid_for(int64_t total, int threads) {
 
 int num_tiles() { return kNumTiles; }
 TileInfo tile(int i) {
-  return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem, g_tiles[i].qpm >= 3 ? 0 : g_tiles[i].qpm,
+  return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem, g_tiles[i].qpm,
                   tile_eff(g_tiles[i].G, g_tiles[i].R)};
 }
-int find_tile(int G, int R) {
+int find_tile_mode(int G, int R, int qpm) {
   for (int i = 0; i < kNumTiles; ++i)
-    if (g_tiles[i].G == G && g_tiles[i].R == R && g_tiles[i].qpm == g_qpm) return i;
-  if (g_qpm >= 3)
-    for (int i = 0; i < kNumTiles; ++i)
-      if (g_tiles[i].G == G && g_tiles[i].R == R && g_tiles[i].qpm == 0) return i;
+    if (g_tiles[i].G == G && g_tiles[i].R == R && g_tiles[i].qpm == qpm) return i;
   return -1;
 }
-void set_profile_mode(int m) { g_qpm = m; }
-int profile_mode() { return g_qpm; }
+int find_tile(int G, int R) { return find_tile_mode(G, R, 0); }
 int tile_ctas_per_sm(int i) { return g_tiles[i].ctas; }
 
 cudaError_t init_kernels() {
@@ -723,17 +727,19 @@ cudaError_t init_kernels() {
 }
 
 size_t qp_bytes(int G, int R, int P, int qpm) {
-  const int rpc = qpm == 0 ? 4 : 8;
-  return (size_t)P * kNL * ((R + rpc - 1) / rpc) * G * 16;
+  (void)qpm;
+  return (size_t)P * kNL * ((R + 3) / 4) * G * 16;
 }
 
-cudaError_t launch_qp_build(const uint8_t *d_query, int m, const int8_t *d_matrix, int G, int R, int P,
-                            int qpm, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int mpad32,
+cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,
+                            int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
                             cudaStream_t st) {
-  const int rpc = qpm == 0 ? 4 : 8;
-  const int64_t total = (int64_t)P * kNL * ((R + rpc - 1) / rpc) * G * rpc + kNL * kNL + (int64_t)kNL * mpad32;
-  qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_matrix, G, R, P, rpc, d_qp, d_desc,
-                                                         d_qp32, mpad32);
+  const int mm = d_query2 ? (m > m2 ? m : m2) : m;
+  const int P32 = (mm + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
+  const int64_t total = (int64_t)P * kNL * ((R + 3) / 4) * G * 4 + kNL * kNL + (int64_t)kNL * P32 * 32 * kSW32Rows;
+  qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_query2, m2, d_matrix, G, R, P,
+                                                         reinterpret_cast<uint32_t *>(d_qp), d_desc, d_qp32,
+                                                         d_qp32b);
   return cudaGetLastError();
 }
 
@@ -744,8 +750,10 @@ cudaError_t launch_sw16_pass(int ti, int grid, const SW16Params &p, cudaStream_t
 }
 
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
-                               uint8_t *flagged, int pass, int thresh, cudaStream_t st) {
-  sw16_gather_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, scores, flagged, pass, thresh);
+                               uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
+                               cudaStream_t st) {
+  sw16_gather_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, scores, flagged, scores2, flagged2,
+                                                            pass, thresh);
   return cudaGetLastError();
 }
 

@@ -49,9 +49,8 @@ struct TileInfo {
 // Compiled (G, R) tiles of the s16x2 pass kernel.
 int num_tiles();
 TileInfo tile(int i);
-int find_tile(int G, int R);  // index or -1 (in the current profile mode)
-void set_profile_mode(int m);
-int profile_mode();
+int find_tile(int G, int R);                // index or -1 (profile mode 0)
+int find_tile_mode(int G, int R, int qpm);  // index or -1
 size_t qp_bytes(int G, int R, int P, int qpm);
 
 // Prepares kernel attributes (max dynamic smem).  Returns cudaError_t.
@@ -59,12 +58,14 @@ cudaError_t init_kernels();
 // Max resident CTAs per SM of tile i's kernel.
 int tile_ctas_per_sm(int i);
 
-cudaError_t launch_qp_build(const uint8_t *d_query, int m, const int8_t *d_matrix, int G, int R,
-                            int P, int qpm, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int mpad32,
+// d_query2 != nullptr: query-pair profile (QPM 3) and a second s32 profile.
+cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,
+                            int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
                             cudaStream_t st);
 cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cudaStream_t st);
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
-                               uint8_t *flagged, int pass, int thresh, cudaStream_t st);
+                               uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
+                               cudaStream_t st);
 cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n,
                                 cudaStream_t st);
 constexpr int kSW32Rows = 16;         // rows per lane of the 32-bit kernel

@@ -61,7 +61,7 @@ inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 }  // namespace
 
 int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
-                int64_t target_groups, HostImage &out, std::string &err) {
+                int64_t target_groups, bool single, HostImage &out, std::string &err) {
   out = HostImage();
   std::vector<int64_t> len(count);
   int64_t total_stream = 0;
@@ -79,7 +79,8 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
                    [&](int32_t a, int32_t b) { return len[a] > len[b]; });
 
   if (target_groups < 1) target_groups = 1;
-  int64_t remaining = (total_stream + 1) / 2;  // pair columns still to place
+  // columns still to place (pair columns: two sequences per column)
+  int64_t remaining = single ? total_stream : (total_stream + 1) / 2;
   int64_t lo = 0, hi = count - 1;
   std::vector<int32_t> halfA, halfB;
   struct Tmp { int64_t ncols; int64_t slot0; int32_t nA, nB; };
@@ -98,7 +99,7 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
       cap = std::max(cap, lA);
     }
     for (;;) {
-      const bool toA = lA <= lB;
+      const bool toA = single || lA <= lB;
       int64_t &l = toA ? lA : lB;
       std::vector<int32_t> &h = toA ? halfA : halfB;
       if (lo <= hi && l + len[order[lo]] + 2 <= cap) {
@@ -118,7 +119,7 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
     for (int32_t s : halfA) out.slots.push_back(s);
     for (int32_t s : halfB) out.slots.push_back(s);
     tmp.push_back(t);
-    remaining -= (lA + lB + 1) / 2;
+    remaining -= single ? lA : (lA + lB + 1) / 2;
     if (remaining < 0) remaining = 0;
   }
   // claim order: longest item first (stable)
@@ -145,25 +146,23 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
   // Write the stream: column word per pair column.
   out.stream.assign((size_t)col, column_word(kNul, kNul));
   out.endcol.assign((size_t)count, -1);
-  auto write_half = [&](const Item &it, int32_t slot0, int32_t n, int shift_is_b) {
+  // half: 0 = A (low 16 bits), 1 = B (high), 2 = both (single-sequence image)
+  auto write_half = [&](const Item &it, int32_t slot0, int32_t n, int half) {
     int64_t c = it.col_begin;
+    auto put = [&](int64_t col, int letter) {
+      uint32_t w = out.stream[col];
+      int cA = (int)(w / kDescBytes) / kNL, cB = (int)(w / kDescBytes) % kNL;
+      if (half != 1) cA = letter;
+      if (half != 0) cB = letter;
+      out.stream[col] = column_word(cA, cB);
+    };
     for (int32_t k = 0; k < n; ++k) {
       const int32_t s = out.slots[slot0 + k];
       const uint8_t *r = residues + offsets[s];
-      for (int64_t j = 0; j < len[s]; ++j, ++c) {
-        uint32_t w = out.stream[c];
-        int cA = (int)(w / kDescBytes) / kNL, cB = (int)(w / kDescBytes) % kNL;
-        if (shift_is_b) cB = r[j]; else cA = r[j];
-        out.stream[c] = column_word(cA, cB);
-      }
-      out.endcol[s] = 2 * c + shift_is_b;   // the END column of sequence s
-      for (int sep = 0; sep < 2; ++sep, ++c) {
-        uint32_t w = out.stream[c];
-        int cA = (int)(w / kDescBytes) / kNL, cB = (int)(w / kDescBytes) % kNL;
-        const int L = sep == 0 ? kEnd : kNul;
-        if (shift_is_b) cB = L; else cA = L;
-        out.stream[c] = column_word(cA, cB);
-      }
+      for (int64_t j = 0; j < len[s]; ++j, ++c) put(c, r[j]);
+      out.endcol[s] = 2 * c + (half == 1 ? 1 : 0);   // the END column of sequence s
+      put(c++, kEnd);
+      put(c++, kNul);
     }
   };
   {
@@ -174,8 +173,12 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
       th.emplace_back([&, k] {
         for (size_t i = k; i < ni; i += nth) {
           const Item &it = out.items[i];
-          write_half(it, it.seqA, it.nA, 0);
-          write_half(it, it.seqB, it.nB, 1);
+          if (single) {
+            write_half(it, it.seqA, it.nA, 2);
+          } else {
+            write_half(it, it.seqA, it.nA, 0);
+            write_half(it, it.seqB, it.nB, 1);
+          }
         }
       });
     for (auto &t : th) t.join();

@@ -58,8 +58,10 @@ struct HostImage {
 // Pre-processing stage: validated input -> stream image.
 // target_groups: number of concurrently running lane groups to size items for.
 // Returns 0 or -1 (err set).
+// single = false: two sequences per column (halves A/B, one query);
+// single = true: one sequence per column in both halves (query pairs).
 int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
-                int64_t target_groups, HostImage &out, std::string &err);
+                int64_t target_groups, bool single, HostImage &out, std::string &err);
 
 // Validation of the raw database (codes < 24, offsets monotone).
 int validate_db(const uint8_t *residues, const int64_t *offsets, int64_t count, std::string &err);

@@ -20,7 +20,7 @@ _NAMES = {SW_EINVAL: "SW_EINVAL", SW_ENOMEM: "SW_ENOMEM", SW_ECUDA: "SW_ECUDA",
           SW_ENODB: "SW_ENODB", SW_ESTATE: "SW_ESTATE"}
 
 EXPORTS = ["sw_db_load", "sw_db_free", "sw_db_count", "sw_db_residues", "sw_search",
-           "sw_search_dev", "sw_topk", "sw_topk_dev", "sw_last_stats", "sw_last_timing", "sw_set_tile",
+           "sw_search_dev", "sw_search_batch", "sw_search_batch_dev", "sw_topk", "sw_topk_dev", "sw_last_stats", "sw_last_timing", "sw_set_tile",
            "sw_tile_supported", "sw_last_error", "sw_version"]
 
 
@@ -54,6 +54,8 @@ def load_library():
         "sw_db_residues": (i64, []),
         "sw_search": (ctypes.c_int, [p, i32, p, i32, i32, p]),
         "sw_search_dev": (ctypes.c_int, [p, i32, p, i32, i32, p, p]),
+        "sw_search_batch": (ctypes.c_int, [p, p, i32, p, i32, i32, p]),
+        "sw_search_batch_dev": (ctypes.c_int, [p, p, i32, p, i32, i32, p, p]),
         "sw_topk": (i64, [i64, p, p]),
         "sw_topk_dev": (i64, [p, p, i64, i64, p, p, p]),
         "sw_last_stats": (ctypes.c_int, [p, ctypes.c_int]),
@@ -151,6 +153,32 @@ def sw_search_dev(query, matrix, gap_open: int, gap_extend: int, d_scores, strea
     m = _matrix(matrix)
     _check(load_library().sw_search_dev(_ptr(q), int(q.size), _ptr(m), int(gap_open), int(gap_extend),
                                         _dev_ptr(d_scores), _stream_ptr(stream)))
+
+
+def _pack_queries(queries):
+    qs = [_u8(q) for q in queries]
+    offs = np.zeros(len(qs) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum([q.size for q in qs])
+    cat = np.ascontiguousarray(np.concatenate(qs) if qs else np.zeros(0, np.uint8))
+    return cat, offs
+
+
+def sw_search_batch(queries, matrix, gap_open: int, gap_extend: int) -> np.ndarray:
+    """Scores of every query (list of uint8 arrays) -> int32[nq, count]."""
+    cat, offs = _pack_queries(queries)
+    m = _matrix(matrix)
+    n = sw_db_count()
+    out = np.empty((len(queries), n), dtype=np.int32)
+    _check(load_library().sw_search_batch(_ptr(cat), _ptr(offs), len(queries), _ptr(m), int(gap_open),
+                                          int(gap_extend), _ptr(out)))
+    return out
+
+
+def sw_search_batch_dev(queries, matrix, gap_open: int, gap_extend: int, d_scores, stream=None) -> None:
+    cat, offs = _pack_queries(queries)
+    m = _matrix(matrix)
+    _check(load_library().sw_search_batch_dev(_ptr(cat), _ptr(offs), len(queries), _ptr(m), int(gap_open),
+                                              int(gap_extend), _dev_ptr(d_scores), _stream_ptr(stream)))
 
 
 def sw_topk(k: int):

@@ -192,3 +192,46 @@ def test_config1_full_size_sampled():
     idx10, sc10 = sw.sw_topk(10)
     eidx, esc = oracle.topk(got, 10)
     assert (idx10 == eidx).all() and (sc10 == esc).all()
+
+
+# ---- multi-query packing: query pairs in the two halves
+def test_batch_random_queries_match_oracle():
+    rng = np.random.default_rng(4242)
+    for trial in range(4):
+        seqs = [rng.integers(0, 24, int(L)).astype(np.uint8) for L in rng.integers(0, 400, 300)]
+        seqs.append(si.rr_residues(rng, 3000))
+        db = _db(seqs)
+        nq = int(rng.integers(1, 6))
+        qs = [rng.integers(0, 24, int(rng.integers(1, 1300))).astype(np.uint8) for _ in range(nq)]
+        M = si.random_symmetric_matrix(rng)
+        go, ge = int(rng.integers(0, 16)), int(rng.integers(0, 16))
+        sw.sw_db_load(db.residues, db.offsets)
+        got = sw.sw_search_batch(qs, M, go, ge)
+        for k, q in enumerate(qs):
+            exp = oracle.batch(q, db.residues, db.offsets, M, go, ge)
+            assert (got[k] == exp).all(), (trial, k, len(q), np.nonzero(got[k] != exp)[0][:5])
+
+
+def test_batch_with_saturating_pair():
+    seqs = [encode("W" * n) for n in (100, 2977, 2978, 3500)] + [encode("AC" * 40)]
+    db = _db(seqs)
+    qs = [encode("W" * 3600), encode("AC" * 30), encode("W" * 3000)]
+    sw.sw_db_load(db.residues, db.offsets)
+    got = sw.sw_search_batch(qs, BLOSUM62, 10, 2)
+    for k, q in enumerate(qs):
+        exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
+        assert (got[k] == exp).all(), k
+    assert got[0][3] == 11 * 3500
+
+
+def test_batch_equals_single_searches_cfg3_lengths():
+    w = si.config0(scale=0.3)
+    rng = si.rng_for(3, 2)
+    qs = [si.rr_residues(rng, L) for L in si.CFG3_QUERY_LENGTHS[::4]]   # 144 .. 4917
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    got = sw.sw_search_batch(qs, BLOSUM62, 10, 2)
+    for k, q in enumerate(qs):
+        single = sw.sw_search(q, BLOSUM62, 10, 2)
+        assert (got[k] == single).all(), k
+    exp = oracle.batch(qs[1], w.db.residues, w.db.offsets, BLOSUM62, 10, 2)
+    assert (got[1] == exp).all()

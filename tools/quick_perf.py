@@ -27,3 +27,18 @@ for q in w.queries[:3]:
         stats = sw.sw_last_stats()
         print(json.dumps({"m": len(q), "tile": [stats["G"], stats["R"]], "passes": stats["passes"], "ms": round(ms, 3),
                           "gcups": round(len(q) * w.db.total_residues / (ms * 1e6), 1), "flagged": stats["flagged"], "items": stats["items"]}), flush=True)
+if len(sys.argv) > 4 and sys.argv[4] == "batch":
+    sw.sw_set_tile(0)
+    rng = si.rng_for(1, 9)
+    qs = [w.queries[0], si.rr_residues(rng, len(w.queries[0]))]
+    dd = torch.empty(2 * w.db.count, dtype=torch.int32, device='cuda')
+    for _ in range(2): sw.sw_search_batch_dev(qs, si.BLOSUM62, 10, 2, dd, st)
+    st.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(5): sw.sw_search_batch_dev(qs, si.BLOSUM62, 10, 2, dd, st)
+    e1.record(st); st.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    s = sw.sw_last_stats()
+    print(json.dumps({"batch_pair_m": [len(q) for q in qs], "tile": [s["G"], s["R"]], "ms": round(ms, 3),
+                      "gcups": round(sum(len(q) for q in qs) * w.db.total_residues / (ms * 1e6), 1)}), flush=True)
