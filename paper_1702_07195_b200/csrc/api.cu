@@ -228,7 +228,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   if (pair) CUDA_TRY(g.qp32b.ensure((size_t)kNL * P32max * 32 * kSW32Rows));
   if (P > 1 && g.bnd.n < (size_t)g.max_cols * 2) {
     CUDA_TRY(g.bnd.ensure((size_t)g.max_cols * 2));
-    // padding columns are only ever written with zeros; start from zeros
+    // (columns past an item's end are never read: the kernel substitutes 0)
     CUDA_TRY(cudaMemset(g.bnd.p, 0, g.bnd.n * sizeof(uint2)));
   }
 

@@ -162,6 +162,8 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   uint2 *bop = dummy;
   uint32_t inc = 0u;
   int rem = 0;                                   // steps left in the current item
+  int bcols = 0;  // BIN: boundary columns left to read (columns >= ncols read as 0: the
+                  // boundary buffer's padding may hold another image's or search's data)
   bool done = false;
   uint32_t sring[U];
   uint2 bring[U];
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         inc = (uint32_t)U;
         sptr = p.stream + c0;
         if (BIN) bptr = p.bnd_in + c0;
+        bcols = ncols;
         scp = p.sc_out + (c0 - (G - 1));
         if (p.bnd_out) bop = p.bnd_out + (c0 - (G - 1));
         if (last) {
@@ -187,12 +190,12 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
           for (int u = 1; u <= U; ++u) {
             sring[u % U] = __ldg(sptr + u);
-            if (BIN) bring[u % U] = __ldg(bptr + u);
+            if (BIN) bring[u % U] = u < ncols ? __ldg(bptr + u) : make_uint2(0u, 0u);
           }
           const uint4 d = lds128(s_desc + __ldg(sptr));   // lane 0's first column
           w0 = d.x;
           ns = d.y;
-          const uint2 b0 = BIN ? __ldg(bptr) : make_uint2(0u, 0u);
+          const uint2 b0 = BIN ? __ldg(bptr) : make_uint2(0u, 0u);   // ncols >= 4
           hout = b0.x;
           fout = b0.y;
           sc = 0u;
@@ -201,6 +204,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         done = true;
         rem = INT_MAX;
         inc = 0u;
+        bcols = 0;
         sptr = p.stream;                   // NUL padding
         if (BIN) bptr = p.bnd_in;          // zero padding
         scp = reinterpret_cast<uint32_t *>(dummy);
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         sring[(u + 1) % U] = __ldg(sptr + u + 1 + U);
         if (BIN) {
           bnext = bring[(u + 1) % U];
-          bring[(u + 1) % U] = __ldg(bptr + u + 1 + U);
+          bring[(u + 1) % U] = (u + 1 + U < bcols) ? __ldg(bptr + u + 1 + U) : make_uint2(0u, 0u);
         }
       }
       uint32_t hd = hprev;
@@ -295,6 +299,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       sc = imad(so, nlast, 0u);
     }
     rem -= U;
+    if (BIN) bcols -= U;
     sptr = ptr_add(sptr, inc);
     if (BIN) bptr = ptr_add(bptr, inc);
     scp = ptr_add(scp, inc);

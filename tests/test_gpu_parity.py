@@ -235,3 +235,21 @@ def test_batch_equals_single_searches_cfg3_lengths():
         assert (got[k] == single).all(), k
     exp = oracle.batch(qs[1], w.db.residues, w.db.offsets, BLOSUM62, 10, 2)
     assert (got[1] == exp).all()
+
+
+def test_single_after_batch_multipass_no_stale_boundary():
+    """Regression: a multi-pass single-query search after a batch search on the
+    same database must not read the other image's pass boundaries from the
+    shared buffer's padding columns."""
+    w = si.config2(scale=0.01)
+    rng = si.rng_for(3, 2)
+    qs = [si.rr_residues(rng, L) for L in (705, 1267, 2109)]
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    sw.sw_search_batch(qs, BLOSUM62, 10, 2)
+    for G, R in ((8, 30), (16, 22), (32, 29)):
+        sw.sw_set_tile(G, R)
+        for q in qs:
+            got = sw.sw_search(q, BLOSUM62, 10, 2)
+            exp = oracle.batch(q, w.db.residues, w.db.offsets, BLOSUM62, 10, 2)
+            assert (got == exp).all(), (G, R, len(q), int((got != exp).sum()))
+    sw.sw_set_tile(0)

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--sample", type=int, default=1500)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--queries", type=str, default="")
+    ap.add_argument("--batch", action="store_true", help="also time sw_search_batch over all queries")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     cores = os.cpu_count()
@@ -78,6 +79,28 @@ def main():
                 "cells32": stats["cells32"], "parity_checked": int(idx.size), "parity_mismatches": bad,
                 "oracle_s": round(tq, 1), "max_score": int(got.max())}), flush=True)
             assert bad == 0, f"config {c} query {qi}: {bad} mismatches"
+        if args.batch and len(w.queries) > 1:
+            dd = torch.empty(len(w.queries) * w.db.count, dtype=torch.int32, device="cuda")
+            sw.sw_search_batch_dev(w.queries, w.matrix, w.gap_open, w.gap_extend, dd, st)
+            st.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            sw.sw_search_batch_dev(w.queries, w.matrix, w.gap_open, w.gap_extend, dd, st)
+            e1.record(st)
+            st.synchronize()
+            ms = e0.elapsed_time(e1)
+            allsc = dd.view(len(w.queries), w.db.count).cpu().numpy()
+            # parity of the batch against the single-query path on every query (exact)
+            mism = 0
+            for qi, q in enumerate(w.queries):
+                sw.sw_search_dev(q, w.matrix, w.gap_open, w.gap_extend, d, st)
+                st.synchronize()
+                mism += int((d.cpu().numpy() != allsc[qi]).sum())
+            cells = sum(len(q) for q in w.queries) * w.db.total_residues
+            print(json.dumps({"config": c, "batch_queries": len(w.queries), "ms": round(ms, 1),
+                              "gcups": round(cells / (ms * 1e6), 1), "batch_vs_single_mismatches": mism}), flush=True)
+            assert mism == 0
 
 
 if __name__ == "__main__":
