@@ -150,10 +150,10 @@ int ensure_device_ready() {
   return SW_OK;
 }
 
-// Choose (G, R) for a query of m residues: minimise the predicted pass time
-// P * G * R / eff(G, R) (rows computed, incl. phantom rows of the last pass,
-// over the tile's measured full-row throughput) plus a per-pass constant
-// (DESIGN.md "Tile choice").
+// Choose (G, R) for a query of m residues: minimise the predicted time
+// G*R * (1/eff0 + (P-1)/eff1) -- rows computed, incl. the phantom rows of the
+// last pass, over the tile's measured full-row throughput of a first pass and
+// of a boundary-reading pass -- plus a per-pass constant.
 int choose_tile(int m, int qpm) {
   if (g.force_G) {
     int ti = find_tile_mode(g.force_G, g.force_R, qpm);
@@ -166,7 +166,7 @@ int choose_tile(int m, int qpm) {
     if (ti.qpm != qpm || tile_ctas_per_sm(i) < 1) continue;
     const int rows = ti.G * ti.R;
     const int P = (m + rows - 1) / rows;
-    const double cost = (double)P * rows / ti.eff + P * 0.002;
+    const double cost = (double)rows * (1.0 / ti.eff0 + (P - 1) / ti.eff1) + P * 0.002;
     if (cost < best - 1e-12) {
       best = cost;
       bi = i;

@@ -644,53 +644,55 @@ TileEntry g_tiles[] = {SW_TILES(0), SW_TILES(3)};
 #undef SW_TILE_NTU
 constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
 
-// Measured full-row throughput (GCUPS, pass kernel, 1 B200, query of exactly
-// G*R residues vs configs[1] at 0.3 scale; profiles/r01_tile_calibration.jsonl).
-// Used by the tile choice: time ~ P * G * R / eff.
-struct TileEff { int G, R; float gcups; };
+// Measured full-row throughput (GCUPS) of each tile's pass kernel on one
+// B200 (configs[1] at 0.5 scale; tools/calibrate_tiles.py,
+// profiles/r01_tile_calibration.jsonl): eff0 = first pass (query of G*R),
+// eff1 = a pass reading the previous pass's boundary (2*G*R minus G*R).
+// The tile choice predicts time ~ G*R * (1/eff0 + (P-1)/eff1).
+struct TileEff { int G, R; float eff0, eff1; };
 const TileEff kTileEff[] = {
-    {8, 8, 4242.f},
-    {8, 12, 4694.f},
-    {8, 16, 4944.f},
-    {8, 18, 4979.f},
-    {8, 20, 5108.f},
-    {8, 22, 5179.f},
-    {8, 24, 5200.f},
-    {8, 26, 5156.f},
-    {8, 28, 5212.f},
-    {8, 29, 5155.f},
-    {8, 30, 5215.f},
-    {8, 32, 5290.f},
-    {16, 8, 4312.f},
-    {16, 12, 4747.f},
-    {16, 16, 4991.f},
-    {16, 18, 5088.f},
-    {16, 20, 5157.f},
-    {16, 22, 5225.f},
-    {16, 24, 5243.f},
-    {16, 26, 5205.f},
-    {16, 28, 5260.f},
-    {16, 29, 5203.f},
-    {16, 30, 5263.f},
-    {16, 32, 5329.f},
-    {32, 8, 4260.f},
-    {32, 12, 4779.f},
-    {32, 15, 4937.f},
-    {32, 16, 4927.f},
-    {32, 18, 5099.f},
-    {32, 20, 5075.f},
-    {32, 22, 5005.f},
-    {32, 24, 5108.f},
-    {32, 26, 5112.f},
-    {32, 28, 5139.f},
-    {32, 29, 5189.f},
-    {32, 30, 5094.f},
-    {32, 32, 5214.f}};
+    {8, 8, 4344.f, 3415.f},
+    {8, 12, 4785.f, 4362.f},
+    {8, 16, 5040.f, 4707.f},
+    {8, 18, 5091.f, 4899.f},
+    {8, 20, 5197.f, 4901.f},
+    {8, 22, 5301.f, 5056.f},
+    {8, 24, 5311.f, 5176.f},
+    {8, 26, 5261.f, 5157.f},
+    {8, 28, 5297.f, 5229.f},
+    {8, 29, 5237.f, 5184.f},
+    {8, 30, 5289.f, 5238.f},
+    {8, 32, 5377.f, 4948.f},
+    {16, 8, 4390.f, 3550.f},
+    {16, 12, 4820.f, 4457.f},
+    {16, 16, 5058.f, 4774.f},
+    {16, 18, 5154.f, 4939.f},
+    {16, 20, 5224.f, 4985.f},
+    {16, 22, 5295.f, 5082.f},
+    {16, 24, 5304.f, 5174.f},
+    {16, 26, 5279.f, 5156.f},
+    {16, 28, 5335.f, 5205.f},
+    {16, 29, 5279.f, 5230.f},
+    {16, 30, 5337.f, 5264.f},
+    {16, 32, 5412.f, 5016.f},
+    {32, 8, 4346.f, 3638.f},
+    {32, 12, 4863.f, 4378.f},
+    {32, 15, 5027.f, 4646.f},
+    {32, 16, 5019.f, 4713.f},
+    {32, 18, 5184.f, 4853.f},
+    {32, 20, 5159.f, 5002.f},
+    {32, 22, 5088.f, 4971.f},
+    {32, 24, 5191.f, 5014.f},
+    {32, 26, 5198.f, 5065.f},
+    {32, 28, 5224.f, 5105.f},
+    {32, 29, 5274.f, 5032.f},
+    {32, 30, 5183.f, 5217.f},
+    {32, 32, 5300.f, 5153.f}};
 
-float tile_eff(int G, int R) {
+TileEff tile_eff(int G, int R) {
   for (const TileEff &e : kTileEff)
-    if (e.G == G && e.R == R) return e.gcups;
-  return 4000.f;   // uncalibrated tile: pessimistic
+    if (e.G == G && e.R == R) return e;
+  return TileEff{G, R, 4000.f, 3500.f};   // uncalibrated tile: pessimistic
 }
 
 int grid_for(int64_t total, int threads) {
@@ -704,8 +706,8 @@ int grid_for(int64_t total, int threads) {
 
 int num_tiles() { return kNumTiles; }
 TileInfo tile(int i) {
-  return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem, g_tiles[i].qpm,
-                  tile_eff(g_tiles[i].G, g_tiles[i].R)};
+  const TileEff e = tile_eff(g_tiles[i].G, g_tiles[i].R);
+  return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem, g_tiles[i].qpm, e.eff0, e.eff1};
 }
 int find_tile_mode(int G, int R, int qpm) {
   for (int i = 0; i < kNumTiles; ++i)

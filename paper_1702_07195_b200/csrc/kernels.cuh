@@ -43,7 +43,7 @@ struct TileInfo {
   int G, R;
   int smem_bytes;           // dynamic shared memory of the pass kernel
   int qpm;                  // profile mode (see kernels.cu)
-  float eff;                // measured full-row GCUPS of the pass kernel
+  float eff0, eff1;         // measured full-row GCUPS: first pass / boundary-reading pass
 };
 
 // Compiled (G, R) tiles of the s16x2 pass kernel.
