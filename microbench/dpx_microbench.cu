@@ -22,13 +22,14 @@ constexpr int ITERS = 2048;
 
 enum Op { ADDMAX_RELU, ADDMAX, MAX2, MAX3, ADDMAX_S32, PRMT_OP, IADD3_OP, LOP3_OP, IMAD_OP,
           MIX_DPX_PRMT, MIX_DPX_IMAD, MIX_DPX_IADD3, CELL, SHFL_OP,
-          MIX_DPX3_IMAD1, MIX_DPX_IMADIMM, MIX_DPX_IMADHALF, ADDMAX_RZ, MIX_DPX_MOV, NUM_OPS };
+          MIX_DPX3_IMAD1, MIX_DPX_IMADIMM, MIX_DPX_IMADHALF, ADDMAX_RZ, MIX_DPX_MOV, CELL_U8X4,
+          CELL_S16X2_EMU, NUM_OPS };
 static const char* kNames[] = {"viaddmax_s16x2_relu", "viaddmax_s16x2", "vmax_s16x2", "vimax3_s16x2",
   "viaddmax_s32_relu", "prmt", "iadd3", "lop3", "imad", "mix_dpx_prmt_1to1", "mix_dpx_imad_1to1",
   "mix_dpx_iadd3_1to1", "cellpair_R8", "shfl_up", "mix_dpx3_imad1", "mix_dpx_imad_imm_1to1",
-  "mix_dpx2_imad1", "viaddmax_relu_rz", "mix_dpx_mov_1to1"};
+  "mix_dpx2_imad1", "viaddmax_relu_rz", "mix_dpx_mov_1to1", "cell_u8x4_R8", "cell_s16x2_sat_emul_R8"};
 // thread-ops counted per chain per iteration for each op
-static const int kOpsPerIter[] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 0, 2, 4, 2, 3, 1, 2};
+static const int kOpsPerIter[] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 0, 2, 4, 2, 3, 1, 2, 0, 0};
 
 template <int OP>
 __global__ void __launch_bounds__(256) bench(const unsigned* __restrict__ in, unsigned* out,
@@ -62,6 +63,64 @@ __global__ void __launch_bounds__(256) bench(const unsigned* __restrict__ in, un
       }
 #pragma unroll
       for (int r = 0; r < 8; r += 2) S = __vimax3_s16x2(S, H[r], H[r + 1]);
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = H[r] ^ E[r];
+    a[0] ^= S;
+  } else if constexpr (OP == CELL_U8X4) {
+    // NEXT-4: the paper's 8-bit lanes as 4 x u8 per register,
+    // biased unsigned saturating arithmetic (SWIPE/Farrar style):
+    //   h = subs(adds(hd, sub+bias), bias); h = max(h, E, F); S = max(S, h)
+    //   hg = subs(h, Goe); E = max(subs(E, Ge), hg); F = max(subs(F, Ge), hg)
+    // No DPX form exists for 8-bit lanes: __vaddus4 / __vsubus4 / __vmaxu4 are
+    // multi-instruction emulations.  8 rows x 1 column x 4 lanes per iteration.
+    unsigned H[8], E[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) { H[r] = a[r]; E[r] = a[r] ^ b; }
+    unsigned S = 0, bias = in[11] | 0x04040404u, goe = 0x0c0c0c0cu, ge = 0x02020202u;
+    unsigned A0 = in[14], B0 = in[15];
+    for (int it = 0; it < ITERS; ++it) {
+      unsigned F = b, hd = c;
+      A0 += it; B0 ^= it;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        unsigned sub = __byte_perm(A0, B0, 0x5410 + r);
+        unsigned h = __vsubus4(__vaddus4(hd, sub), bias);
+        h = __vmaxu4(__vmaxu4(h, E[r]), F);
+        hd = H[r];
+        H[r] = h;
+        S = __vmaxu4(S, h);
+        unsigned hg = __vsubus4(h, goe);
+        E[r] = __vmaxu4(__vsubus4(E[r], ge), hg);
+        F = __vmaxu4(__vsubus4(F, ge), hg);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = H[r] ^ E[r];
+    a[0] ^= S;
+  } else if constexpr (OP == CELL_S16X2_EMU) {
+    // 16-bit lanes with the paper's *saturating* adds (__vaddss2 emulation)
+    // instead of wrapping DPX: same recurrence, 8 rows x 2 lanes per iteration.
+    unsigned H[8], E[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) { H[r] = a[r]; E[r] = a[r] ^ b; }
+    unsigned S = 0, ngoe = in[12], nge = in[13];
+    unsigned A0 = in[14], B0 = in[15];
+    for (int it = 0; it < ITERS; ++it) {
+      unsigned F = b, hd = c;
+      A0 += it; B0 ^= it;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        unsigned sub = __byte_perm(A0, B0, 0x5410 + r);
+        unsigned h = __vmaxs2(__vmaxs2(__vaddss2(hd, sub), E[r]), F);
+        h = __vmaxs2(h, 0u);
+        hd = H[r];
+        H[r] = h;
+        S = __vmaxs2(S, h);
+        unsigned hg = __vmaxs2(__vaddss2(h, ngoe), 0u);
+        E[r] = __vmaxs2(__vaddss2(E[r], nge), hg);
+        F = __vmaxs2(__vaddss2(F, nge), hg);
+      }
     }
 #pragma unroll
     for (int r = 0; r < 8; ++r) a[r] = H[r] ^ E[r];
@@ -145,6 +204,8 @@ int run(int nsm, int blocks_per_sm, unsigned* d_in, unsigned* d_out, long long* 
   delete[] h;
   double ops_per_thread;
   if (OP == CELL) ops_per_thread = (double)ITERS * (8 * 5 + 8 /*prmt*/ + 4 /*max3*/);  // 5 DPX + 1 PRMT per row, 0.5 VIMNMX3
+  else if (OP == CELL_U8X4) ops_per_thread = (double)ITERS * 8 * 4;       // CELLS (4 lanes x 8 rows)
+  else if (OP == CELL_S16X2_EMU) ops_per_thread = (double)ITERS * 8 * 2;  // CELLS (2 lanes x 8 rows)
   else ops_per_thread = (double)ITERS * CHAINS * kOpsPerIter[OP];
   double ops_per_sm = ops_per_thread * threads * blocks_per_sm;
   double per_clk = ops_per_sm / (double)mx;          // thread-ops / clk / SM (all blocks concurrent)
@@ -188,6 +249,8 @@ int main() {
     run<MIX_DPX_IMADHALF>(nsm, bps, d_in, d_out, d_cyc);
     run<ADDMAX_RZ>(nsm, bps, d_in, d_out, d_cyc);
     run<MIX_DPX_MOV>(nsm, bps, d_in, d_out, d_cyc);
+    run<CELL_U8X4>(nsm, bps, d_in, d_out, d_cyc);
+    run<CELL_S16X2_EMU>(nsm, bps, d_in, d_out, d_cyc);
   }
   return 0;
 }

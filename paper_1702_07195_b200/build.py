@@ -26,6 +26,8 @@ HEADERS = ["kernels.cuh", "swdb_internal.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                      "-I" + os.path.join(ROOT, "include")]
+if os.environ.get("SW_ABLATE"):   # performance experiments only (wrong results)
+    NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ABLATE=" + os.environ["SW_ABLATE"]]
 
 
 def _nvcc() -> str:

@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
         const uint4 a = lds128(aA + kk * G * 16);
-        const uint4 b = QPM == 0 ? lds128(aB + kk * G * 16) : make_uint4(0u, 0u, 0u, 0u);
+        const uint4 b = (QPM == 0 && SW_ABLATE < 2) ? lds128(aB + kk * G * 16) : make_uint4(0u, 0u, 0u, 0u);
         const uint32_t av[4] = {a.x, a.y, a.z, a.w};
         const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
@@ -266,7 +266,12 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           const int r0 = kk * RPC + j;
           if (r0 < R) {
             // QPM 0: (SM(q_r, dA), SM(q_r, dB)); QPM 3: (SM(q1_r, d), SM(q2_r, d))
-            const uint32_t sub0 = QPM == 0 ? imad(bv[j], 65536u, av[j]) : av[j];
+#ifndef SW_ABLATE
+#define SW_ABLATE 0
+#endif
+            // SW_ABLATE (performance experiments only; results are wrong): 1 = no
+            // half packing, 2 = no B profile load and no packing
+            const uint32_t sub0 = (QPM == 0 && SW_ABLATE == 0) ? imad(bv[j], 65536u, av[j]) : av[j];
 #pragma unroll
             for (int e = 0; e < 1; ++e) {
               const int r = r0 + e;
