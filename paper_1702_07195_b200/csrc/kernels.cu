@@ -31,6 +31,11 @@
 #include <climits>
 #include <cstdio>
 
+// SW_ABLATE (performance experiments only, wrong results): see the pass kernel.
+#ifndef SW_ABLATE
+#define SW_ABLATE 0
+#endif
+
 namespace swdb {
 
 namespace {
@@ -266,9 +271,6 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           const int r0 = kk * RPC + j;
           if (r0 < R) {
             // QPM 0: (SM(q_r, dA), SM(q_r, dB)); QPM 3: (SM(q1_r, d), SM(q2_r, d))
-#ifndef SW_ABLATE
-#define SW_ABLATE 0
-#endif
             // SW_ABLATE (performance experiments only; results are wrong): 1 = no
             // half packing, 2 = no B profile load and no packing
             const uint32_t sub0 = (QPM == 0 && SW_ABLATE == 0) ? imad(bv[j], 65536u, av[j]) : av[j];
