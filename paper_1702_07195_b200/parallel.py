@@ -60,8 +60,9 @@ def merge_topk_host(scores_list, index_list, k: int):
 
 
 def gather_to_root(t, world: int, rank: int, dist):
-    """Gather equal-shape tensors to rank 0 (returns list on rank 0, else None)."""
-    if world == 1:
+    """Gather equal-shape tensors to rank 0 (returns list on rank 0, else None).
+    With a process group (dist given) the collective runs even at world size 1."""
+    if dist is None:
         return [t]
     if rank == 0:
         out = [t.new_empty(t.shape) for _ in range(world)]
