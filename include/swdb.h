@@ -68,6 +68,26 @@ enum {
  */
 int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count);
 
+/*
+ * sw_db_load_streamed -- pre-processing stage for a database that need not fit
+ * in device memory ("larger genomic
+ * databases that do not fit in MCDRAM").  Same arguments and validation as
+ * sw_db_load, plus
+ *   chunk_bytes : >= 1, the device memory budget of one chunk of the stream
+ *                 image (two chunk buffers are allocated).
+ * The sequence-pair image is kept in pinned HOST memory and split into chunks
+ * of consecutive work items; every search copies chunk k+1 host->device on a
+ * separate stream while the pass kernels run on chunk k.  Residues for 32-bit
+ * re-scoring are read from mapped host memory.  sw_search / sw_search_dev /
+ * sw_topk work unchanged; sw_search_batch(_dev) returns SW_EINVAL (it needs a
+ * resident database).  Per-sequence arrays (scores, offsets) stay on the
+ * device.
+ */
+int sw_db_load_streamed(const uint8_t *residues, const int64_t *offsets, int64_t count, int64_t chunk_bytes);
+
+/* Number of chunks of a streamed database (0 for a resident one). */
+int64_t sw_db_chunks(void);
+
 /* Frees the database and all device buffers.  Safe to call at any time. */
 void sw_db_free(void);
 

@@ -95,7 +95,9 @@ struct State {
   DevBuf<int32_t> bscores;  // internal scores (sw_search_batch)
   DevBuf<uint8_t> flagged, flagged2;
   DevBuf<int32_t> flag_list, flag_list2;
-  DevBuf<int> counters;     // [0..P) pass cursors, [kMaxPass..+3] flag counts / cursors
+  DevBuf<int> counters;     // [kMaxPass..+3] flag counts / cursors
+  DevBuf<int> pcounters;    // per (chunk, pass) item cursors
+  const uint8_t *res_dev = nullptr;  // residues for s32 re-scoring (device or mapped host)
   DevBuf<int64_t> cells32;
   DevBuf<uint8_t> query, query2;
   DevBuf<int8_t> matrix;
@@ -104,6 +106,8 @@ struct State {
   DevBuf<int32_t> qp32, qp32b;
   DevBuf<uint2> bnd;        // 2 * max_cols
   DevBuf<uint2> dummy;      // scratch for idle-lane stores (16-B slot per thread)
+  DevBuf<uint32_t> nulcols; // 16 NUL column words
+  DevBuf<uint2> zerocols;   // 16 zero boundary columns
   DevBuf<uint2> scratch32;
   DevBuf<uint64_t> keys;
   DevBuf<uint64_t> keys2;
@@ -121,15 +125,49 @@ struct State {
   int force_G = 0, force_R = 0;
   // timing events of the last search
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // ---- streamed (out-of-core) database, SURVEY 8(f) NEXT-3
+  struct Chunk {
+    int item_begin, item_end;   // items [begin, end)
+    int64_t col_begin, col_end; // image columns [begin, end), padding included
+    int64_t seq_begin, seq_end; // entries in cseq_idx / cseq_endcol
+  };
+  bool streamed = false;
+  std::vector<Chunk> chunks;
+  int64_t chunk_span = 0;       // max columns of a chunk
+  uint32_t *h_stream = nullptr; // pinned host image
+  uint8_t *h_res = nullptr;     // pinned, mapped host copy of the residues (s32 re-scoring)
+  DevBuf<uint32_t> cbuf[2];     // device chunk buffers (double-buffered)
+  DevBuf<int32_t> cseq_idx;     // sequences grouped by chunk
+  DevBuf<int64_t> cseq_endcol;  // their END columns (global image columns)
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+
+  void release_streamed() {
+    if (h_stream) cudaFreeHost(h_stream);
+    if (h_res) cudaFreeHost(h_res);
+    h_stream = nullptr;
+    h_res = nullptr;
+    cbuf[0].release(); cbuf[1].release(); cseq_idx.release(); cseq_endcol.release();
+    for (int k = 0; k < 2; ++k) {
+      if (ev_copied[k]) cudaEventDestroy(ev_copied[k]);
+      if (ev_free[k]) cudaEventDestroy(ev_free[k]);
+      ev_copied[k] = ev_free[k] = nullptr;
+    }
+    if (copy_st) cudaStreamDestroy(copy_st);
+    copy_st = nullptr;
+    chunks.clear();
+    streamed = false;
+  }
 
   void release_all() {
+    release_streamed();
     img[0].release(); img[1].release();
     sc_out.release(); res.release(); offs.release();
     scores.release(); bscores.release(); flagged.release(); flagged2.release(); flag_list.release();
-    flag_list2.release(); counters.release(); cells32.release();
+    flag_list2.release(); counters.release(); pcounters.release(); cells32.release();
     query.release(); query2.release(); matrix.release(); qp.release(); desc.release(); qp32.release();
     qp32b.release(); bnd.release();
-    scratch32.release(); dummy.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
+    scratch32.release(); dummy.release(); nulcols.release(); zerocols.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
     loaded = false;
     has_search = false;
     last_scores = nullptr;
@@ -204,6 +242,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   if (dev != g.device) return fail(SW_EINVAL, "current CUDA device differs from the one sw_db_load used");
 
   const bool pair = q2 != nullptr;
+  if (pair && g.streamed) return fail(SW_EINVAL, "query pairs / batch search need a resident database");
   const int mode = pair ? 3 : 0;
   const Image &I = g.img[pair ? 1 : 0];
   const int mm = pair ? std::max(m, m2) : m;
@@ -226,11 +265,6 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(g.desc.ensure((size_t)kNL * kNL));
   CUDA_TRY(g.qp32.ensure((size_t)kNL * P32max * 32 * kSW32Rows));
   if (pair) CUDA_TRY(g.qp32b.ensure((size_t)kNL * P32max * 32 * kSW32Rows));
-  if (P > 1 && g.bnd.n < (size_t)g.max_cols * 2) {
-    CUDA_TRY(g.bnd.ensure((size_t)g.max_cols * 2));
-    // (columns past an item's end are never read: the kernel substitutes 0)
-    CUDA_TRY(cudaMemset(g.bnd.p, 0, g.bnd.n * sizeof(uint2)));
-  }
 
   CUDA_TRY(cudaMemcpyAsync(g.query.p, q, (size_t)m, cudaMemcpyHostToDevice, st));
   if (pair) CUDA_TRY(cudaMemcpyAsync(g.query2.p, q2, (size_t)m2, cudaMemcpyHostToDevice, st));
@@ -246,27 +280,66 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
                            g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr, st));
 
   const int grid = g.num_sms * std::max(1, tile_ctas_per_sm(ti));
+  // resident database: one "chunk" (the whole image); streamed database: the
+  // image's chunks are copied host->device on copy_st into two buffers,
+  // overlapping the passes of the previous chunk
+  const bool strm = g.streamed;
+  const int nch = strm ? (int)g.chunks.size() : 1;
+  const int64_t span = strm ? g.chunk_span : I.total_cols;
+  CUDA_TRY(g.pcounters.ensure((size_t)nch * P));
+  CUDA_TRY(cudaMemsetAsync(g.pcounters.p, 0, sizeof(int) * (size_t)nch * P, st));
+  if (P > 1 && g.bnd.n < (size_t)span * 2) CUDA_TRY(g.bnd.ensure((size_t)span * 2));
   CUDA_TRY(cudaEventRecord(g.ev[1], st));
-  for (int pass = 0; pass < P; ++pass) {
-    SW16Params p;
-    p.stream = I.stream.p;
-    p.items = I.items.p;
-    p.num_items = I.num_items;
-    p.counter = g.counters.p + pass;
-    p.qp = reinterpret_cast<const uint4 *>(g.qp.p);
-    p.desc = g.desc.p;
-    p.bnd_in = pass == 0 ? nullptr : g.bnd.p + (size_t)((pass - 1) & 1) * I.total_cols;
-    p.bnd_out = pass == P - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * I.total_cols;
-    p.dummy = g.dummy.p;
-    p.sc_out = g.sc_out.p;
-    p.pass = pass;
-    p.thresh = thresh;
-    p.zero = 0u;
-    p.dgoe = (uint32_t)(32767 - std::min(goe, 32767));
-    p.dge = (uint32_t)(32767 - std::min(ge, 32767));
-    CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
-    CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p, pair ? d_scores2 : nullptr,
-                                pair ? g.flagged2.p : nullptr, pass, thresh, st));
+  for (int k = 0; k < nch; ++k) {
+    const uint32_t *stream_base = I.stream.p;
+    const Item *items = I.items.p;
+    int nitems = I.num_items;
+    int64_t base = 0;
+    const int b = k & 1;
+    if (strm) {
+      const State::Chunk &c = g.chunks[k];
+      // the buffer is free once the passes of the chunk that used it last are done
+      CUDA_TRY(cudaStreamWaitEvent(g.copy_st, g.ev_free[b], 0));
+      CUDA_TRY(cudaMemcpyAsync(g.cbuf[b].p, g.h_stream + c.col_begin, (size_t)(c.col_end - c.col_begin) * 4,
+                               cudaMemcpyHostToDevice, g.copy_st));
+      CUDA_TRY(cudaEventRecord(g.ev_copied[b], g.copy_st));
+      CUDA_TRY(cudaStreamWaitEvent(st, g.ev_copied[b], 0));
+      base = c.col_begin;
+      stream_base = g.cbuf[b].p - base;     // so that item.col_begin indexes the buffer
+      items = I.items.p + c.item_begin;
+      nitems = c.item_end - c.item_begin;
+    }
+    for (int pass = 0; pass < P; ++pass) {
+      SW16Params p;
+      p.stream = stream_base;
+      p.items = items;
+      p.num_items = nitems;
+      p.counter = g.pcounters.p + (size_t)k * P + pass;
+      p.qp = reinterpret_cast<const uint4 *>(g.qp.p);
+      p.desc = g.desc.p;
+      p.bnd_in = pass == 0 ? nullptr : g.bnd.p + (size_t)((pass - 1) & 1) * span - base;
+      p.bnd_out = pass == P - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * span - base;
+      p.dummy = g.dummy.p;
+      p.nul_stream = g.nulcols.p;
+      p.zero_bnd = g.zerocols.p;
+      p.sc_out = g.sc_out.p - base;
+      p.pass = pass;
+      p.thresh = thresh;
+      p.zero = 0u;
+      p.dgoe = (uint32_t)(32767 - std::min(goe, 32767));
+      p.dge = (uint32_t)(32767 - std::min(ge, 32767));
+      CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
+      if (strm) {
+        const State::Chunk &c = g.chunks[k];
+        CUDA_TRY(launch_sw16_gather(g.cseq_endcol.p + c.seq_begin, c.seq_end - c.seq_begin, g.sc_out.p - base,
+                                    d_scores, g.flagged.p, nullptr, nullptr, pass, thresh, st,
+                                    g.cseq_idx.p + c.seq_begin));
+      } else {
+        CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p,
+                                    pair ? d_scores2 : nullptr, pair ? g.flagged2.p : nullptr, pass, thresh, st));
+      }
+    }
+    if (strm) CUDA_TRY(cudaEventRecord(g.ev_free[b], st));
   }
   CUDA_TRY(cudaEventRecord(g.ev[2], st));
   // exact s32 re-scoring of every sequence whose 16-bit score saturated
@@ -277,7 +350,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     q.flag_list = k ? g.flag_list2.p : g.flag_list.p;
     q.flag_count = g.counters.p + kMaxPass + 2 * k;
     q.cursor = g.counters.p + kMaxPass + 2 * k + 1;
-    q.res = g.res.p;
+    q.res = g.res_dev;
     q.offs = g.offs.p;
     q.qp32 = k ? g.qp32b.p : g.qp32.p;
     q.passes = ((k ? m2 : m) + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
@@ -366,10 +439,20 @@ void sw_db_free(void) {
 int64_t sw_db_count(void) { return g.loaded ? g.count : 0; }
 int64_t sw_db_residues(void) { return g.loaded ? g.total_res : 0; }
 
-int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
+}  // extern "C"
+
+namespace {
+
+// chunk_bytes == 0: resident database (both images on the device).
+// chunk_bytes  > 0: streamed database: the sequence-pair image stays in
+// pinned host memory, split into chunks of at most chunk_bytes of stream,
+// copied to the device during every search.
+int load_impl(const uint8_t *residues, const int64_t *offsets, int64_t count, int64_t chunk_bytes) {
   t_err.clear();
   std::string err;
   if (validate_db(residues, offsets, count, err)) return fail(SW_EINVAL, err);
+  if (chunk_bytes < 0) return fail(SW_EINVAL, "chunk_bytes must be >= 0");
+  const bool strm = chunk_bytes > 0;
   int rc = ensure_device_ready();
   if (rc) return rc;
   int dev = 0, nsm = 0;
@@ -379,15 +462,16 @@ int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
   // the widest-occupancy tile (4 groups per warp at G = 8, 16 warps per SM).
   const int64_t target_groups = (int64_t)nsm * 16 * 2;
   HostImage himg[2];
+  const int nimg = strm ? 1 : 2;
   try {
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < nimg; ++k)
       if (build_image(residues, offsets, count, target_groups, k == 1, himg[k], err)) return fail(SW_EINVAL, err);
   } catch (const std::bad_alloc &) {
     return fail(SW_ENOMEM, "host allocation failed in the pre-processor");
   } catch (const std::exception &e) {
     return fail(SW_EINVAL, e.what());
   }
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < nimg; ++k)
     if (himg[k].items.size() >= (size_t)INT_MAX) return fail(SW_EINVAL, "too many work items");
   // replace the previous database
   sw_db_free();
@@ -398,20 +482,90 @@ int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
   g.total_res = offsets[count];
   g.max_len = himg[0].max_len;
   g.max_cols = std::max(himg[0].total_cols, himg[1].total_cols);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < nimg; ++k) {
     Image &I = g.img[k];
     const HostImage &H = himg[k];
     I.total_cols = H.total_cols;
     I.num_items = (int)H.items.size();
-    CUDA_TRY(I.stream.ensure(H.stream.size()));
     CUDA_TRY(I.items.ensure(H.items.size()));
+    CUDA_TRY(cudaMemcpy(I.items.p, H.items.data(), H.items.size() * sizeof(Item), cudaMemcpyHostToDevice));
+    if (strm) continue;
+    CUDA_TRY(I.stream.ensure(H.stream.size()));
     CUDA_TRY(I.endcol.ensure(H.endcol.size()));
     CUDA_TRY(cudaMemcpy(I.stream.p, H.stream.data(), H.stream.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(I.items.p, H.items.data(), H.items.size() * sizeof(Item), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(I.endcol.p, H.endcol.data(), H.endcol.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   }
-  CUDA_TRY(g.sc_out.ensure((size_t)g.max_cols));
-  CUDA_TRY(g.res.ensure((size_t)g.total_res));
+  if (strm) {
+    const HostImage &H = himg[0];
+    const int64_t chunk_cols = std::max<int64_t>(chunk_bytes / 4, 1);
+    // chunks: maximal runs of consecutive items whose columns (with the NUL
+    // padding on both sides) fit chunk_cols; an item longer than that is a
+    // chunk of its own
+    std::vector<int32_t> item_chunk(H.items.size());
+    int64_t span = 0;
+    for (size_t b = 0; b < H.items.size();) {
+      State::Chunk c;
+      c.item_begin = (int)b;
+      c.col_begin = H.items[b].col_begin - kItemPad;
+      size_t e = b + 1;
+      while (e < H.items.size() &&
+             H.items[e].col_begin + H.items[e].ncols + kItemPad - c.col_begin <= chunk_cols)
+        ++e;
+      c.item_end = (int)e;
+      c.col_end = H.items[e - 1].col_begin + H.items[e - 1].ncols + kItemPad;
+      for (size_t i = b; i < e; ++i) item_chunk[i] = (int32_t)g.chunks.size();
+      span = std::max(span, c.col_end - c.col_begin);
+      g.chunks.push_back(c);
+      b = e;
+    }
+    g.chunk_span = span;
+    // per chunk: its sequences (original index) and their END columns
+    std::vector<int64_t> cnt(g.chunks.size() + 1, 0);
+    for (size_t i = 0; i < H.items.size(); ++i) cnt[item_chunk[i] + 1] += H.items[i].nA + H.items[i].nB;
+    for (size_t k = 0; k < g.chunks.size(); ++k) cnt[k + 1] += cnt[k];
+    std::vector<int32_t> idx((size_t)count);
+    std::vector<int64_t> ecol((size_t)count);
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (size_t i = 0; i < H.items.size(); ++i) {
+      const Item &it = H.items[i];
+      for (int32_t s = 0; s < it.nA + it.nB; ++s) {
+        const int32_t orig = H.slots[it.seqA + s];
+        const int64_t pos = fill[item_chunk[i]]++;
+        idx[pos] = orig;
+        ecol[pos] = H.endcol[orig];
+      }
+    }
+    for (size_t k = 0; k < g.chunks.size(); ++k) {
+      g.chunks[k].seq_begin = cnt[k];
+      g.chunks[k].seq_end = cnt[k + 1];
+    }
+    CUDA_TRY(g.cseq_idx.ensure((size_t)count));
+    CUDA_TRY(g.cseq_endcol.ensure((size_t)count));
+    CUDA_TRY(cudaMemcpy(g.cseq_idx.p, idx.data(), idx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(g.cseq_endcol.p, ecol.data(), ecol.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaHostAlloc(&g.h_stream, H.stream.size() * sizeof(uint32_t), cudaHostAllocDefault));
+    std::memcpy(g.h_stream, H.stream.data(), H.stream.size() * sizeof(uint32_t));
+    for (int k = 0; k < 2; ++k) {
+      CUDA_TRY(g.cbuf[k].ensure((size_t)span));
+      CUDA_TRY(cudaEventCreateWithFlags(&g.ev_copied[k], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&g.ev_free[k], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaStreamCreateWithFlags(&g.copy_st, cudaStreamNonBlocking));
+    CUDA_TRY(g.sc_out.ensure((size_t)span));
+    // residues for the (rare) s32 re-scoring: read over the host link
+    CUDA_TRY(cudaHostAlloc(&g.h_res, std::max<size_t>((size_t)g.total_res, 1), cudaHostAllocMapped));
+    if (g.total_res > 0) std::memcpy(g.h_res, residues, (size_t)g.total_res);
+    uint8_t *dres = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dres), g.h_res, 0));
+    g.res_dev = dres;
+    g.streamed = true;
+  } else {
+    CUDA_TRY(g.sc_out.ensure((size_t)g.max_cols));
+    CUDA_TRY(g.res.ensure((size_t)g.total_res));
+    if (g.total_res > 0)
+      CUDA_TRY(cudaMemcpy(g.res.p, residues, (size_t)g.total_res, cudaMemcpyHostToDevice));
+    g.res_dev = g.res.p;
+  }
   CUDA_TRY(g.offs.ensure((size_t)count + 1));
   CUDA_TRY(g.scores.ensure((size_t)count));
   CUDA_TRY(g.flagged.ensure((size_t)count));
@@ -421,8 +575,13 @@ int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
   CUDA_TRY(g.counters.ensure(kMaxPass + 4));
   CUDA_TRY(g.cells32.ensure(1));
   CUDA_TRY(g.dummy.ensure((size_t)nsm * 4 * 1024));   // one 16-B slot per resident thread
-  if (g.total_res > 0)
-    CUDA_TRY(cudaMemcpy(g.res.p, residues, (size_t)g.total_res, cudaMemcpyHostToDevice));
+  {
+    CUDA_TRY(g.nulcols.ensure(16));
+    CUDA_TRY(g.zerocols.ensure(16));
+    std::vector<uint32_t> nw(16, column_word(kNul, kNul));
+    CUDA_TRY(cudaMemcpy(g.nulcols.p, nw.data(), 16 * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemset(g.zerocols.p, 0, 16 * sizeof(uint2)));
+  }
   CUDA_TRY(cudaMemcpy(g.offs.p, offsets, ((size_t)count + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
   // s32 re-scoring scratch: one warp per 8 per SM, 2 boundary rows each
   g.sw32_grid = nsm * 2;  // 2 CTAs x 8 warps per SM
@@ -433,6 +592,24 @@ int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
   g.loaded = true;
   return SW_OK;
 }
+
+}  // namespace
+
+extern "C" {
+
+int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count) {
+  return load_impl(residues, offsets, count, 0);
+}
+
+int sw_db_load_streamed(const uint8_t *residues, const int64_t *offsets, int64_t count, int64_t chunk_bytes) {
+  if (chunk_bytes < 1) {
+    t_err = "chunk_bytes must be >= 1";
+    return SW_EINVAL;
+  }
+  return load_impl(residues, offsets, count, chunk_bytes);
+}
+
+int64_t sw_db_chunks(void) { return g.loaded && g.streamed ? (int64_t)g.chunks.size() : 0; }
 
 int sw_search_dev(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t gap_open,
                   int32_t gap_extend, int32_t *d_scores, void *cuda_stream) {

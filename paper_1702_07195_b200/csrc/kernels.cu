@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   // boundary for the next pass.  A group without items keeps feeding NUL
   // columns; its pointers stop (increment 0) on the NUL padding / own slot.
   uint2 *const dummy = p.dummy + (blockIdx.x * blockDim.x + threadIdx.x);
-  const uint32_t *sptr = p.stream;
-  const uint2 *bptr = p.bnd_in;
+  const uint32_t *sptr = p.nul_stream;
+  const uint2 *bptr = p.zero_bnd;
   uint32_t *scp = reinterpret_cast<uint32_t *>(dummy);
   uint2 *bop = dummy;
   uint32_t inc = 0u;
@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         rem = INT_MAX;
         inc = 0u;
         bcols = 0;
-        sptr = p.stream;                   // NUL padding
-        if (BIN) bptr = p.bnd_in;          // zero padding
+        sptr = p.nul_stream;               // NUL columns
+        if (BIN) bptr = p.zero_bnd;        // zero boundary
         scp = reinterpret_cast<uint32_t *>(dummy);
         bop = dummy;
         if (last) {
@@ -319,21 +319,25 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 // flag the 16-bit saturation test.
 __global__ void sw16_gather_kernel(const int64_t *__restrict__ endcol, int64_t count,
                                    const uint32_t *__restrict__ sc_out, int32_t *scores, uint8_t *flagged,
-                                   int32_t *scores2, uint8_t *flagged2, int pass, int thresh) {
+                                   int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
+                                   const int32_t *__restrict__ seq_idx) {
   // scores2 == nullptr: two sequences per column, the END column's half is the
   // sequence's.  scores2 != nullptr (query pair): both halves belong to the
   // sequence, low half = query 1, high half = query 2.
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
+    // seq_idx (streamed databases): entry i describes original sequence seq_idx[i]
+    // and endcol is relative to the current chunk
+    const int64_t o = seq_idx ? (int64_t)seq_idx[i] : i;
     const int64_t e = endcol[i];
     const uint32_t w = sc_out[e >> 1];
     const int v = (int)((!scores2 && (e & 1)) ? (w >> 16) : (w & 0xffffu));
-    scores[i] = max(pass == 0 ? 0 : scores[i], v);
-    if (v >= thresh) flagged[i] = 1;
+    scores[o] = max(pass == 0 ? 0 : scores[o], v);
+    if (v >= thresh) flagged[o] = 1;
     if (scores2) {
       const int v2 = (int)(w >> 16);
-      scores2[i] = max(pass == 0 ? 0 : scores2[i], v2);
-      if (v2 >= thresh) flagged2[i] = 1;
+      scores2[o] = max(pass == 0 ? 0 : scores2[o], v2);
+      if (v2 >= thresh) flagged2[o] = 1;
     }
   }
 }
@@ -765,9 +769,10 @@ cudaError_t launch_sw16_pass(int ti, int grid, const SW16Params &p, cudaStream_t
 
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
-                               cudaStream_t st) {
+                               cudaStream_t st, const int32_t *seq_idx) {
+  if (count <= 0) return cudaSuccess;
   sw16_gather_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, scores, flagged, scores2, flagged2,
-                                                            pass, thresh);
+                                                            pass, thresh, seq_idx);
   return cudaGetLastError();
 }
 

@@ -16,7 +16,9 @@ struct SW16Params {
   const uint4 *desc;        // descriptor table: [kNL*kNL] uint4
   const uint2 *bnd_in;      // boundary (H,F) per column from the previous pass, or null
   uint2 *bnd_out;           // boundary for the next pass, or null
-  uint2 *dummy;             // one 8-B scratch slot per launched thread (idle-lane stores)
+  uint2 *dummy;             // one 16-B scratch slot per launched thread (idle-lane stores)
+  const uint32_t *nul_stream;  // >= 16 NUL column words (groups without items)
+  const uint2 *zero_bnd;       // >= 16 zero boundary columns
   uint32_t *sc_out;         // per column: score chain value at the last lane
   int pass;
   int thresh;               // 32768 - max(1, smax)
@@ -65,7 +67,7 @@ cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_quer
 cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cudaStream_t st);
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
-                               cudaStream_t st);
+                               cudaStream_t st, const int32_t *seq_idx = nullptr);
 cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n,
                                 cudaStream_t st);
 constexpr int kSW32Rows = 16;         // rows per lane of the 32-bit kernel

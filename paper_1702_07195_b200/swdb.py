@@ -19,7 +19,7 @@ SW_OK, SW_EINVAL, SW_ENOMEM, SW_ECUDA, SW_ENODB, SW_ESTATE = 0, -1, -2, -3, -4, 
 _NAMES = {SW_EINVAL: "SW_EINVAL", SW_ENOMEM: "SW_ENOMEM", SW_ECUDA: "SW_ECUDA",
           SW_ENODB: "SW_ENODB", SW_ESTATE: "SW_ESTATE"}
 
-EXPORTS = ["sw_db_load", "sw_db_free", "sw_db_count", "sw_db_residues", "sw_search",
+EXPORTS = ["sw_db_load", "sw_db_load_streamed", "sw_db_chunks", "sw_db_free", "sw_db_count", "sw_db_residues", "sw_search",
            "sw_search_dev", "sw_search_batch", "sw_search_batch_dev", "sw_topk", "sw_topk_dev", "sw_last_stats", "sw_last_timing", "sw_set_tile",
            "sw_tile_supported", "sw_last_error", "sw_version"]
 
@@ -49,6 +49,8 @@ def load_library():
     p, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     sig = {
         "sw_db_load": (ctypes.c_int, [p, p, i64]),
+        "sw_db_load_streamed": (ctypes.c_int, [p, p, i64, i64]),
+        "sw_db_chunks": (i64, []),
         "sw_db_free": (None, []),
         "sw_db_count": (i64, []),
         "sw_db_residues": (i64, []),
@@ -123,6 +125,19 @@ def sw_db_load(residues, offsets) -> None:
     offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
     count = int(offs.size - 1)
     _check(load_library().sw_db_load(_ptr(res) if res.size else None, _ptr(offs), count))
+
+
+def sw_db_load_streamed(residues, offsets, chunk_bytes: int) -> None:
+    """Out-of-core database: the image stays in pinned host memory and is
+    streamed to the device in chunks of <= chunk_bytes during each search."""
+    res = _u8(residues)
+    offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    _check(load_library().sw_db_load_streamed(_ptr(res) if res.size else None, _ptr(offs), int(offs.size - 1),
+                                              int(chunk_bytes)))
+
+
+def sw_db_chunks() -> int:
+    return int(load_library().sw_db_chunks())
 
 
 def sw_db_free() -> None:

@@ -58,6 +58,12 @@ def test_db_load_validation(lib, res, offs, msg):
     assert msg in str(e.value)
 
 
+def test_streamed_load_validation(lib):
+    with pytest.raises(sw.SWError) as e:
+        sw.sw_db_load_streamed(np.array([1, 2, 3], np.uint8), np.array([0, 3]), 0)
+    assert e.value.code == -1
+
+
 def test_search_before_load_is_enodb(lib):
     sw.sw_db_free()
     with pytest.raises(sw.SWError) as e:

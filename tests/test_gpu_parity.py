@@ -253,3 +253,29 @@ def test_single_after_batch_multipass_no_stale_boundary():
             exp = oracle.batch(q, w.db.residues, w.db.offsets, BLOSUM62, 10, 2)
             assert (got == exp).all(), (G, R, len(q), int((got != exp).sum()))
     sw.sw_set_tile(0)
+
+
+# ---- out-of-core streamed database
+def test_streamed_database_matches_resident_and_oracle():
+    rng = np.random.default_rng(555)
+    seqs = [si.rr_residues(rng, int(L)) for L in rng.integers(0, 600, 3000)]
+    seqs += [si.rr_residues(rng, 9000), encode("W" * 3100), encode("W" * 2000)]
+    db = _db(seqs)
+    queries = [si.rr_residues(rng, 300), si.rr_residues(rng, 1700), encode("W" * 3100)]
+    sw.sw_db_load_streamed(db.residues, db.offsets, 64 * 1024)     # many small chunks
+    assert sw.sw_db_chunks() > 4
+    for q in queries:
+        got = sw.sw_search(q, BLOSUM62, 10, 2)
+        exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
+        assert (got == exp).all(), (len(q), int((got != exp).sum()))
+        again = sw.sw_search(q, BLOSUM62, 10, 2)
+        assert (again == got).all()
+        idx, sc = sw.sw_topk(10)
+        eidx, esc = oracle.topk(exp, 10)
+        assert (idx == eidx).all() and (sc == esc).all()
+    with pytest.raises(sw.SWError):
+        sw.sw_search_batch(queries[:2], BLOSUM62, 10, 2)
+    sw.sw_db_load(db.residues, db.offsets)
+    assert sw.sw_db_chunks() == 0
+    assert (sw.sw_search(queries[1], BLOSUM62, 10, 2) ==
+            oracle.batch(queries[1], db.residues, db.offsets, BLOSUM62, 10, 2)).all()
