@@ -321,6 +321,8 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       p.bnd_out = pass == P - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * span - base;
       p.dummy = g.dummy.p;
       p.nul_stream = g.nulcols.p;
+      p.col_lo = base;
+      p.col_hi = strm ? g.chunks[k].col_end : I.total_cols;
       p.zero_bnd = g.zerocols.p;
       p.sc_out = g.sc_out.p - base;
       p.pass = pass;

@@ -35,6 +35,18 @@
 #ifndef SW_ABLATE
 #define SW_ABLATE 0
 #endif
+// SW_DEBUG: device-side bounds checks on every global / shared access of the
+// pass kernel (a debug build; compute-sanitizer is not available on the GPU
+// pool).  A violation traps with a device assert.
+#ifndef SW_DEBUG
+#define SW_DEBUG 0
+#endif
+#if SW_DEBUG
+#include <cassert>
+#define SW_CHECK(cond) assert(cond)
+#else
+#define SW_CHECK(cond) ((void)0)
+#endif
 
 namespace swdb {
 
@@ -252,9 +264,14 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         const uint2 d = lds64(s_desc + sring[(u + 1) % U]);
         w0 = d.x;
         ns = d.y;
+        SW_CHECK(sptr == p.nul_stream ? (u + 1 + U < 16)
+                                      : (sptr + u + 1 + U - p.stream >= p.col_lo &&
+                                         sptr + u + 1 + U - p.stream < p.col_hi));
         sring[(u + 1) % U] = __ldg(sptr + u + 1 + U);
         if (BIN) {
           bnext = bring[(u + 1) % U];
+          SW_CHECK(u + 1 + U >= bcols || (bptr + u + 1 + U - p.bnd_in >= p.col_lo &&
+                                           bptr + u + 1 + U - p.bnd_in < p.col_hi));
           bring[(u + 1) % U] = (u + 1 + U < bcols) ? __ldg(bptr + u + 1 + U) : make_uint2(0u, 0u);
         }
       }
@@ -262,6 +279,8 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       hprev = hu;
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
+        SW_CHECK(aA + kk * G * 16 + 16 <= s_desc + (DESC_U4 + QP_U4) * 16 &&
+                 aB + kk * G * 16 + 16 <= s_desc + (DESC_U4 + QP_U4) * 16);
         const uint4 a = lds128(aA + kk * G * 16);
         const uint4 b = (QPM == 0 && SW_ABLATE < 2) ? lds128(aB + kk * G * 16) : make_uint4(0u, 0u, 0u, 0u);
         const uint32_t av[4] = {a.x, a.y, a.z, a.w};
@@ -298,6 +317,9 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       for (int r = 1; r + 1 < R; r += 2) S = __vimax3_s16x2(S, H[r], H[r + 1]);
       if ((R & 1) == 0) S = __vmaxs2(S, H[R - 1]);
       const uint32_t so = __vmaxs2(sc_in, S);   // max over lanes 0..t (read at END columns)
+      SW_CHECK(!last || scp == reinterpret_cast<uint32_t *>(dummy) ||
+               (scp + u - p.sc_out >= p.col_lo && scp + u - p.sc_out < p.col_hi));
+      SW_CHECK(!bout || bop == dummy || (bop + u - p.bnd_out >= p.col_lo && bop + u - p.bnd_out < p.col_hi));
       if (last) st_global_u32(scp + u, so);
       if (bout) st_global_v2(bop + u, H[R - 1], F);
       // outgoing registers; lane G-1 hands over lane 0's next-column inputs

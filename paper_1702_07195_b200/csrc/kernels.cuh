@@ -19,6 +19,7 @@ struct SW16Params {
   uint2 *dummy;             // one 16-B scratch slot per launched thread (idle-lane stores)
   const uint32_t *nul_stream;  // >= 16 NUL column words (groups without items)
   const uint2 *zero_bnd;       // >= 16 zero boundary columns
+  int64_t col_lo, col_hi;      // valid column range of stream / bnd / sc_out (SW_DEBUG checks)
   uint32_t *sc_out;         // per column: score chain value at the last lane
   int pass;
   int thresh;               // 32768 - max(1, smax)
