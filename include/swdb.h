@@ -179,7 +179,10 @@ int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, 
  *   stats[2] = G (lanes per group), stats[3] = R (rows per lane),
  *   stats[4] = sequences flagged by the 16-bit saturation test and re-scored
  *              in 32 bit, stats[5] = cells re-scored in 32 bit,
- *   stats[6] = pair-columns streamed per pass, stats[7] = items.
+ *   stats[6] = pair-columns streamed per pass, stats[7] = items,
+ *   stats[8] = the 16-bit flag threshold T in score units: a sequence is
+ *              re-scored in 32 bit iff its 16-bit score is >= T, and every
+ *              sequence whose exact score is >= T is (R7).
  * Returns the number of entries written (<= n).
  */
 int sw_last_stats(int64_t *stats, int n);

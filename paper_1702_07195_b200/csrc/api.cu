@@ -120,7 +120,7 @@ struct State {
   const int32_t *last_scores = nullptr;
   cudaStream_t last_stream = nullptr;
   int last_G = 0, last_R = 0, last_P = 0, last_mode = 0;
-  int64_t last_flags = -1, last_cells32 = -1;
+  int64_t last_flags = -1, last_cells32 = -1, last_thresh = 0;
   // forced tile
   int force_G = 0, force_R = 0;
   // timing events of the last search
@@ -255,7 +255,8 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int P32max = (mm + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
   int smax = 1;
   for (int i = 0; i < kAlpha * kAlpha; ++i) smax = std::max(smax, (int)matrix[i]);
-  const int thresh = 32768 - smax;
+  const int thresh = 32768 - smax;   // stored 16-bit units (R7)
+  g.last_thresh = thresh - kBias16;  // in score units
   const int goe = gap_open + gap_extend, ge = gap_extend;
 
   CUDA_TRY(g.query.ensure((size_t)m));
@@ -328,6 +329,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       p.pass = pass;
       p.thresh = thresh;
       p.zero = 0u;
+      p.one = 1u;
       p.dgoe = (uint32_t)(32767 - std::min(goe, 32767));
       p.dge = (uint32_t)(32767 - std::min(ge, 32767));
       CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
@@ -582,7 +584,10 @@ int load_impl(const uint8_t *residues, const int64_t *offsets, int64_t count, in
     CUDA_TRY(g.zerocols.ensure(16));
     std::vector<uint32_t> nw(16, column_word(kNul, kNul));
     CUDA_TRY(cudaMemcpy(g.nulcols.p, nw.data(), 16 * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemset(g.zerocols.p, 0, 16 * sizeof(uint2)));
+    {
+      std::vector<uint2> zc(16, make_uint2((uint32_t)kBias16 * 0x10001u, (uint32_t)kBias16 * 0x10001u));
+      CUDA_TRY(cudaMemcpy(g.zerocols.p, zc.data(), 16 * sizeof(uint2), cudaMemcpyHostToDevice));
+    }
   }
   CUDA_TRY(cudaMemcpy(g.offs.p, offsets, ((size_t)count + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
   // s32 re-scoring scratch: one warp per 8 per SM, 2 boundary rows each
@@ -697,9 +702,9 @@ int sw_last_stats(int64_t *stats, int n) {
     g.last_cells32 = cells;
   }
   const Image &I = g.img[g.last_mode == 3 ? 1 : 0];
-  const int64_t v[8] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
-                        g.last_flags, g.last_cells32, I.total_cols, I.num_items};
-  const int m = std::min(n, 8);
+  const int64_t v[9] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
+                        g.last_flags, g.last_cells32, I.total_cols, I.num_items, g.last_thresh};
+  const int m = std::min(n, 9);
   for (int i = 0; i < m; ++i) stats[i] = v[i];
   return m;
 }

@@ -53,6 +53,7 @@ namespace swdb {
 namespace {
 
 constexpr int kThreads = 512;
+constexpr uint32_t kB2 = (uint32_t)kBias16 * 0x10001u;   // the stored zero, both halves
 constexpr uint32_t kNulWord = (uint32_t)((kNul * kNL + kNul) * kDescBytes);
 
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
@@ -161,10 +162,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   const bool bout = last && p.bnd_out != nullptr;
   const uint4 nul = lds128(s_desc + kNulWord);
 
+  const uint32_t one = p.one;
   uint32_t H[R], E[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) { H[r] = 0u; E[r] = 0u; }
-  uint32_t S = 0u, hout = 0u, fout = 0u, sc = 0u, hprev = 0u;
+  for (int r = 0; r < R; ++r) { H[r] = kB2; E[r] = kB2; }
+  uint32_t S = 0u, hout = kB2, fout = kB2, sc = 0u, hprev = kB2;
   uint32_t w0 = nul.x, ns = nul.y;               // column chain (NUL)
   uint32_t kneg = 0u;                            // S-reset value after the previous column
 
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   uint32_t sring[U];
   uint2 bring[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) { sring[u] = 0u; bring[u] = make_uint2(0u, 0u); }
+  for (int u = 0; u < U; ++u) { sring[u] = 0u; bring[u] = make_uint2(kB2, kB2); }
 
   for (;;) {
     if (rem <= 0) {  // group-uniform: claim the next work item
@@ -207,12 +209,12 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
           for (int u = 1; u <= U; ++u) {
             sring[u % U] = __ldg(sptr + u);
-            if (BIN) bring[u % U] = u < ncols ? __ldg(bptr + u) : make_uint2(0u, 0u);
+            if (BIN) bring[u % U] = u < ncols ? __ldg(bptr + u) : make_uint2(kB2, kB2);
           }
           const uint4 d = lds128(s_desc + __ldg(sptr));   // lane 0's first column
           w0 = d.x;
           ns = d.y;
-          const uint2 b0 = BIN ? __ldg(bptr) : make_uint2(0u, 0u);   // ncols >= 4
+          const uint2 b0 = BIN ? __ldg(bptr) : make_uint2(kB2, kB2);   // ncols >= 4
           hout = b0.x;
           fout = b0.y;
           sc = 0u;
@@ -228,11 +230,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         bop = dummy;
         if (last) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(0u, 0u); }
+          for (int u = 0; u < U; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(kB2, kB2); }
           w0 = nul.x;
           ns = nul.y;
-          hout = 0u;
-          fout = 0u;
+          hout = kB2;
+          fout = kB2;
           sc = 0u;
         }
       }
@@ -259,8 +261,9 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       const uint32_t kneg_prev = kneg;
       kneg = imad(ns, 0xffff8000u, 0x80008000u);
       // ---- lane G-1: lane 0's next column (s+u+1) descriptor; refill its ring slot
-      uint2 bnext = make_uint2(0u, 0u);
+      uint2 bnext = make_uint2(0u, 0u);   // added to the outgoing (H, F) of lanes t < G-1: 0
       if (last) {
+        bnext = make_uint2(kB2, kB2);      // lane 0's boundary without a previous pass
         const uint2 d = lds64(s_desc + sring[(u + 1) % U]);
         w0 = d.x;
         ns = d.y;
@@ -272,7 +275,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           bnext = bring[(u + 1) % U];
           SW_CHECK(u + 1 + U >= bcols || (bptr + u + 1 + U - p.bnd_in >= p.col_lo &&
                                            bptr + u + 1 + U - p.bnd_in < p.col_hi));
-          bring[(u + 1) % U] = (u + 1 + U < bcols) ? __ldg(bptr + u + 1 + U) : make_uint2(0u, 0u);
+          bring[(u + 1) % U] = (u + 1 + U < bcols) ? __ldg(bptr + u + 1 + U) : make_uint2(kB2, kB2);
         }
       }
       uint32_t hd = hprev;
@@ -298,13 +301,26 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
               const int r = r0 + e;
               if (r < R) {
                 const uint32_t sub = sub0;
-                uint32_t h = __viaddmax_s16x2_relu(hd, sub, E[r]);  // max(Hdiag+SM, E, 0)
-                h = __vmaxs2(h, F);                                 // Eq. 1
-                hd = H[r];
-                H[r] = h;
-                const uint32_t hg = __viaddmax_s16x2_relu(h, ngoe, ngoe);  // max(H-Goe, 0): ngoe <= 0, one register read fewer
-                E[r] = __viaddmax_s16x2(E[r], nge, hg);                    // Eq. 2 (next column)
-                F = __viaddmax_s16x2(F, nge, hg);                          // Eq. 3 (next row)
+                uint32_t h;
+                if (kArith == 1) {
+                  // biased: H, E, F >= kB2 halfwise, so Hdiag + SM never crosses a
+                  // half boundary and is one 32-bit add (FMA pipe); E >= kB2
+                  // makes the 0 of Eq. 1 implicit
+                  h = __vimax3_s16x2(imad(hd, one, sub), E[r], F);     // Eq. 1
+                  hd = H[r];
+                  H[r] = h;
+                  const uint32_t hg = __viaddmax_s16x2(h, ngoe, kB2);  // max(H-Goe, 0)
+                  E[r] = __viaddmax_s16x2(E[r], nge, hg);              // Eq. 2 (next column)
+                  F = __viaddmax_s16x2(F, nge, hg);                    // Eq. 3 (next row)
+                } else {
+                  h = __viaddmax_s16x2_relu(hd, sub, E[r]);  // max(Hdiag+SM, E, 0)
+                  h = __vmaxs2(h, F);                        // Eq. 1
+                  hd = H[r];
+                  H[r] = h;
+                  const uint32_t hg = __viaddmax_s16x2_relu(h, ngoe, ngoe);  // max(H-Goe, 0): ngoe <= 0, one register read fewer
+                  E[r] = __viaddmax_s16x2(E[r], nge, hg);                    // Eq. 2 (next column)
+                  F = __viaddmax_s16x2(F, nge, hg);                          // Eq. 3 (next row)
+                }
               }
             }
           }
@@ -354,11 +370,11 @@ __global__ void sw16_gather_kernel(const int64_t *__restrict__ endcol, int64_t c
     const int64_t e = endcol[i];
     const uint32_t w = sc_out[e >> 1];
     const int v = (int)((!scores2 && (e & 1)) ? (w >> 16) : (w & 0xffffu));
-    scores[o] = max(pass == 0 ? 0 : scores[o], v);
+    scores[o] = max(pass == 0 ? 0 : scores[o], v - kBias16);
     if (v >= thresh) flagged[o] = 1;
     if (scores2) {
       const int v2 = (int)(w >> 16);
-      scores2[o] = max(pass == 0 ? 0 : scores2[o], v2);
+      scores2[o] = max(pass == 0 ? 0 : scores2[o], v2 - kBias16);
       if (v2 >= thresh) flagged2[o] = 1;
     }
   }
@@ -508,13 +524,16 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
       const int pass = (int)(rest / kNL);
       const int rloc = 4 * kk + e;
       const int64_t row = (int64_t)pass * G * R + (int64_t)t * R + rloc;
-      // -32768 (0x8000): separator letters and phantom rows
-      uint32_t lo = 0x8000u, hi = 0x8000u;
+      // kDummy16: separator letters and phantom rows
+      int lo = kDummy16, hi = kDummy16;
       if (rloc < R && c < kAlpha) {
-        if (row < m) lo = (uint16_t)(int16_t)M[q[row] * kAlpha + c];
-        if (q2 && row < m2) hi = (uint16_t)(int16_t)M[q2[row] * kAlpha + c];
+        if (row < m) lo = M[q[row] * kAlpha + c];
+        if (q2 && row < m2) hi = M[q2[row] * kAlpha + c];
       }
-      qp[i] = q2 ? (lo | (hi << 16)) : lo;
+      if (kArith == 1)   // the 32-bit integer hi * 65536 + lo (added to H_diag as one 32-bit add)
+        qp[i] = q2 ? (uint32_t)(hi * 65536 + lo) : (uint32_t)lo;
+      else               // zero-extended halves
+        qp[i] = q2 ? ((uint32_t)(uint16_t)lo | ((uint32_t)(uint16_t)hi << 16)) : (uint32_t)(uint16_t)lo;
     } else if (i < nq + ndesc) {
       const int k = (int)(i - nq);
       const int cA = k / kNL, cB = k % kNL;

@@ -5,7 +5,23 @@
 
 #include "swdb_internal.h"
 
+// SW_ARITH selects the s16x2 cell arithmetic of the pass kernel:
+//   1 (default): "biased" form.  Every 16-bit value is stored as x + kBias16
+//     (kBias16 = 16384), so the diagonal add H_diag + SM can run as a plain
+//     32-bit add on the FMA pipe (no carry between the halves is possible) and
+//     Eq. 1 becomes one VIMNMX3 on the ALU pipe: 4.5 ALU + 2 FMA instructions
+//     per pair of cells instead of 5.5 ALU + 1 FMA.  Exact below
+//     32768 - smax - kBias16 (= 16373 for BLOSUM62); above, flagged.
+//   0: the plain relu form, 5.5 DPX per pair of cells, exact below 32768 - smax.
+#ifndef SW_ARITH
+#define SW_ARITH 1
+#endif
+
 namespace swdb {
+
+constexpr int kArith = SW_ARITH;
+constexpr int kBias16 = kArith == 1 ? 16384 : 0;   // stored = value + kBias16 (per half)
+constexpr int kDummy16 = kArith == 1 ? -16384 : -32768;   // separator / phantom-row score
 
 struct SW16Params {
   const uint32_t *stream;   // column words (descriptor byte offsets)
@@ -24,6 +40,7 @@ struct SW16Params {
   int pass;
   int thresh;               // 32768 - max(1, smax)
   uint32_t zero;            // 0 (passed in so ptxas keeps it in a register)
+  uint32_t one;             // 1 (passed in: keeps 32-bit adds on the FMA pipe as IMAD)
   uint32_t dgoe, dge;       // 32767 - min(Goe, 32767), 32767 - min(Ge, 32767)
 };
 
@@ -69,6 +86,7 @@ cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cuda
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
                                cudaStream_t st, const int32_t *seq_idx = nullptr);
+// thresh: in stored 16-bit units (32768 - smax); scores are stored - kBias16.
 cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n,
                                 cudaStream_t st);
 constexpr int kSW32Rows = 16;         // rows per lane of the 32-bit kernel
