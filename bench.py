@@ -35,7 +35,10 @@ METRIC = "GCUPS (giga cell updates/sec) at 1/2/4/8 B200, % of int/DPX roofline"
 CONFIG_INDEX = 1
 TOPK = 10
 ALU_LANE_OPS_PER_CLK_PER_SM = 64      # measured (profiles/r01_dpx_microbench.jsonl); guide: rt_SMSP=2
-DPX_PER_CELL = 2.75                   # 5.5 DPX per s16x2 pair of cells
+# ALU-pipe instructions per cell of the 16-bit pass kernel:
+# biased arithmetic 4.5 per s16x2 pair of cells (VIMNMX3 + 3 VIADDMNMX + 1/2
+# VIMNMX3; the diagonal add runs on the FMA pipe), relu form 5.5 DPX.
+ALU_PER_CELL = {1: 2.25, 0: 2.75}
 
 
 def parse():
@@ -358,14 +361,15 @@ def run_ours(args):
     kms = float(np.mean(kernel_ms))
     achieved = len(q) * local_res / (kms * 1e6)          # GCUPS of the pass kernels, this rank
     f_max = float(peaks.get("sm_max_mhz", 1965.0))
-    peak = nsm * f_max * 1e6 * ALU_LANE_OPS_PER_CLK_PER_SM / DPX_PER_CELL / 1e9
+    alu_per_cell = ALU_PER_CELL[int(sw.sw_last_stats()["arith"])]
+    peak = nsm * f_max * 1e6 * ALU_LANE_OPS_PER_CLK_PER_SM / alu_per_cell / 1e9
     f_obs = clk.get("sm_mhz")
     roof = {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "GCUPS",
             "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
             "kernel": "sw16_pass_kernel", "kernel_ms": round(kms, 4),
             "kernel_share_of_step": round(kms / ms_step, 4),
             "peak_basis": f"{nsm} SMs x {f_max:.0f} MHz (sm_max_mhz, {peaks_src}) x "
-                          f"{ALU_LANE_OPS_PER_CLK_PER_SM} ALU lane-ops/clk/SM / {DPX_PER_CELL} DPX per cell",
+                          f"{ALU_LANE_OPS_PER_CLK_PER_SM} ALU lane-ops/clk/SM / {alu_per_cell} ALU instructions per cell",
             "frac_at_observed_clock": (round(achieved / (peak * f_obs / f_max), 4) if f_obs else None)}
 
     cpu = None

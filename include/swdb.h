@@ -182,7 +182,10 @@ int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, 
  *   stats[6] = pair-columns streamed per pass, stats[7] = items,
  *   stats[8] = the 16-bit flag threshold T in score units: a sequence is
  *              re-scored in 32 bit iff its 16-bit score is >= T, and every
- *              sequence whose exact score is >= T is (R7).
+ *              sequence whose exact score is >= T is (R7),
+ *   stats[9] = cell arithmetic of the 16-bit kernel: 1 = biased (4.5 ALU +
+ *              2 FMA instructions per pair of cells), 0 = relu form (5.5 ALU
+ *              + 1 FMA).
  * Returns the number of entries written (<= n).
  */
 int sw_last_stats(int64_t *stats, int n);

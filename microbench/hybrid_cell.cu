@@ -34,9 +34,9 @@
   fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
 
 constexpr int ITERS = 1024;
-enum Var { DPX, HA, HB, HBF, MIX, HB_I, HBF_I, MIX_I, HA_I, NUM_VARS };
+enum Var { DPX, HA, HB, HBF, MIX, HB_I, HBF_I, MIX_I, HA_I, HAINT, HAINT_T, HA_I_T, NUM_VARS };
 static const char *kNames[] = {"dpx", "hybA_biased", "hybB_fp16", "hybB_fp16_fmarelu", "mix_AB_biased",
-                               "hybB_fp16_imm", "hybB_fp16_fmarelu_imm", "mix_AB_biased_imm", "hybA_biased_imm"};
+                               "hybB_fp16_imm", "hybB_fp16_fmarelu_imm", "mix_AB_biased_imm", "hybA_biased_imm", "hybA_int_imad", "hybA_int_imad_Stree", "hybA_biased_imm_Stree"};
 
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -67,7 +67,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 }
 
 template <int VAR, int R, bool LDS>
-__global__ void __launch_bounds__(256, (R <= 8 ? 4 : 2)) bench(const uint32_t *__restrict__ in, uint32_t *out, long long *cycles) {
+__global__ void __launch_bounds__(256, (R <= 8 ? 4 : 2)) bench(const uint32_t *__restrict__ in, uint32_t *out, long long *cycles, uint32_t one_p) {
   __shared__ uint4 prof[8 * (R / 4) * 32];
   for (int i = threadIdx.x; i < 8 * (R / 4) * 32; i += blockDim.x)
     prof[i] = make_uint4(in[i & 15], in[(i + 1) & 15], in[(i + 2) & 15], in[(i + 3) & 15]);
@@ -104,10 +104,16 @@ __global__ void __launch_bounds__(256, (R <= 8 ? 4 : 2)) bench(const uint32_t *_
           const uint32_t hg = __viaddmax_s16x2_relu(h, ngoe, ngoe);
           E[r] = __viaddmax_s16x2(E[r], nge, hg);
           F = __viaddmax_s16x2(F, nge, hg);
-        } else if (VAR == HA || VAR == HA_I || ((VAR == MIX || VAR == MIX_I) && (r & 1) == 0)) {
+        } else if (VAR == HAINT || VAR == HAINT_T) {
+          h = __vimax3_s16x2(imad(hd, one_p, sub), E[r], F);
+          hd = H[r]; H[r] = h;
+          const uint32_t hg = __viaddmax_s16x2(h, ngoe, 0x40004000u);
+          E[r] = __viaddmax_s16x2(E[r], nge, hg);
+          F = __viaddmax_s16x2(F, nge, hg);
+        } else if (VAR == HA || VAR == HA_I || VAR == HA_I_T || ((VAR == MIX || VAR == MIX_I) && (r & 1) == 0)) {
           h = __vimax3_s16x2(hadd2(hd, sub), E[r], F);
           hd = H[r]; H[r] = h;
-          const uint32_t hg = __viaddmax_s16x2(h, ngoe, VAR == HA_I ? 0x64006400u : bias);
+          const uint32_t hg = __viaddmax_s16x2(h, ngoe, (VAR == HA_I || VAR == HA_I_T) ? 0x64006400u : bias);
           E[r] = __viaddmax_s16x2(E[r], nge, hg);
           F = __viaddmax_s16x2(F, nge, hg);
         } else if (VAR == MIX || VAR == MIX_I) {
@@ -131,8 +137,29 @@ __global__ void __launch_bounds__(256, (R <= 8 ? 4 : 2)) bench(const uint32_t *_
         }
       }
     }
+    if (VAR == HAINT_T || VAR == HA_I_T) {   // S as a tree of VIMNMX3 (depth log3 R)
+      uint32_t m[R];
+      int n = R;
+#pragma unroll
+      for (int r = 0; r < R; ++r) m[r] = H[r];
+#pragma unroll
+      for (int lvl = 0; lvl < 6; ++lvl) {
+        if (n > 1) {
+          int k = 0;
+#pragma unroll
+          for (int i = 0; i + 2 < 32; i += 3) {
+            if (i + 2 < n) m[k++] = __vimax3_s16x2(m[i], m[i + 1], m[i + 2]);
+            else if (i + 1 < n) m[k++] = __vmaxs2(m[i], m[i + 1]);
+            else if (i < n) m[k++] = m[i];
+          }
+          n = k;
+        }
+      }
+      S = __vmaxs2(S, m[0]);
+    } else {
 #pragma unroll
     for (int r = 0; r < R; r += 2) S = __vimax3_s16x2(S, H[r], H[r + 1]);
+    }
     b ^= F;
     c += S;
   }
@@ -207,10 +234,10 @@ int run(int nsm, int bps, uint32_t *d_in, uint32_t *d_out, long long *d_cyc) {
   const int threads = 256, blocks = nsm * bps;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
-  bench<VAR, R, LDS><<<blocks, threads>>>(d_in, d_out, d_cyc);
+  bench<VAR, R, LDS><<<blocks, threads>>>(d_in, d_out, d_cyc, 1u);
   CK(cudaDeviceSynchronize());
   cudaEventRecord(e0);
-  bench<VAR, R, LDS><<<blocks, threads>>>(d_in, d_out, d_cyc);
+  bench<VAR, R, LDS><<<blocks, threads>>>(d_in, d_out, d_cyc, 1u);
   cudaEventRecord(e1);
   CK(cudaEventSynchronize(e1));
   float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
@@ -239,6 +266,9 @@ void run_all(int nsm, uint32_t *d_in, uint32_t *d_out, long long *d_cyc, int bps
     run<HBF_I, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
     run<MIX_I, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
     run<HA_I, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
+    run<HAINT, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
+    run<HAINT_T, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
+    run<HA_I_T, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
   }
 }
 

@@ -30,6 +30,8 @@ if os.environ.get("SW_ABLATE"):   # performance experiments only (wrong results)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ABLATE=" + os.environ["SW_ABLATE"]]
 if os.environ.get("SW_ARITH"):    # cell arithmetic (kernels.cuh): 1 biased (default), 0 relu DPX
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ARITH=" + os.environ["SW_ARITH"]]
+if os.environ.get("SW_NTMODE"):   # threads per CTA by tile (experiment, kernels.cu)
+    NVCC_FLAGS = NVCC_FLAGS + ["-DSW_NTMODE=" + os.environ["SW_NTMODE"]]
 if os.environ.get("SW_DEBUG"):    # device-side bounds checks (slow; debug builds)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_DEBUG=1"]
 

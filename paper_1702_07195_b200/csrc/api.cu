@@ -69,10 +69,12 @@ struct Image {
   DevBuf<Item> items;
   DevBuf<int64_t> endcol;   // per sequence: 2 * END column + half
   int64_t total_cols = 0;
+  int64_t max_item_cols = 0;  // longest work item (columns)
   int num_items = 0;
   void release() {
     stream.release(); items.release(); endcol.release();
     total_cols = 0;
+    max_item_cols = 0;
     num_items = 0;
   }
 };
@@ -192,7 +194,14 @@ int ensure_device_ready() {
 // G*R * (1/eff0 + (P-1)/eff1) -- rows computed, incl. the phantom rows of the
 // last pass, over the tile's measured full-row throughput of a first pass and
 // of a boundary-reading pass -- plus a per-pass constant.
-int choose_tile(int m, int qpm) {
+// Tile choice: predicted time per database residue of a query of m rows,
+//   rows * (1/eff0 + (P-1)/eff1) / balance + P * const,
+// eff0/eff1 the measured full-row throughput of the tile (kernels.cu).  A pass
+// lasts at least as long as its longest work item, which one group of G lanes
+// processes alone (the intra-task part of the kernel); balance = min(1,
+// average columns per group / (1.15 * longest item)) charges tiles with many
+// small groups for that tail (cfg4: 5-35 k residue sequences).
+int choose_tile(int m, int qpm, const Image &I) {
   if (g.force_G) {
     int ti = find_tile_mode(g.force_G, g.force_R, qpm);
     if (ti >= 0) return ti;
@@ -204,7 +213,10 @@ int choose_tile(int m, int qpm) {
     if (ti.qpm != qpm || tile_ctas_per_sm(i) < 1) continue;
     const int rows = ti.G * ti.R;
     const int P = (m + rows - 1) / rows;
-    const double cost = (double)rows * (1.0 / ti.eff0 + (P - 1) / ti.eff1) + P * 0.002;
+    const double groups = (double)g.num_sms * tile_ctas_per_sm(i) * tile_threads(i) / ti.G;
+    const double avg_cols = (double)I.total_cols / groups;
+    const double balance = I.max_item_cols > 0 ? std::min(1.0, avg_cols / (1.15 * (double)I.max_item_cols)) : 1.0;
+    const double cost = (double)rows * (1.0 / ti.eff0 + (P - 1) / ti.eff1) / balance + P * 0.002;
     if (cost < best - 1e-12) {
       best = cost;
       bi = i;
@@ -246,7 +258,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int mode = pair ? 3 : 0;
   const Image &I = g.img[pair ? 1 : 0];
   const int mm = pair ? std::max(m, m2) : m;
-  const int ti = choose_tile(mm, mode);
+  const int ti = choose_tile(mm, mode, I);
   if (ti < 0) return fail(SW_ECUDA, "no runnable kernel tile");
   const TileInfo T = tile(ti);
   const int rows = T.G * T.R;
@@ -491,6 +503,8 @@ int load_impl(const uint8_t *residues, const int64_t *offsets, int64_t count, in
     const HostImage &H = himg[k];
     I.total_cols = H.total_cols;
     I.num_items = (int)H.items.size();
+    I.max_item_cols = 0;
+    for (const Item &it : H.items) I.max_item_cols = std::max<int64_t>(I.max_item_cols, it.ncols);
     CUDA_TRY(I.items.ensure(H.items.size()));
     CUDA_TRY(cudaMemcpy(I.items.p, H.items.data(), H.items.size() * sizeof(Item), cudaMemcpyHostToDevice));
     if (strm) continue;
@@ -702,9 +716,9 @@ int sw_last_stats(int64_t *stats, int n) {
     g.last_cells32 = cells;
   }
   const Image &I = g.img[g.last_mode == 3 ? 1 : 0];
-  const int64_t v[9] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
-                        g.last_flags, g.last_cells32, I.total_cols, I.num_items, g.last_thresh};
-  const int m = std::min(n, 9);
+  const int64_t v[10] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
+                         g.last_flags, g.last_cells32, I.total_cols, I.num_items, g.last_thresh, kArith};
+  const int m = std::min(n, 10);
   for (int i = 0; i < m; ++i) stats[i] = v[i];
   return m;
 }

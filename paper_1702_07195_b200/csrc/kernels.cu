@@ -677,7 +677,13 @@ struct TileEntry {
   {G_, R_, M_, NT_, smem_of<R_, G_, M_>(), sw16_pass_kernel<R_, G_, false, M_, NT_, U_>,   \
    sw16_pass_kernel<R_, G_, true, M_, NT_, U_>, 0}
 #define SW_TILE_NT(G_, R_, M_, NT_) SW_TILE_NTU(G_, R_, M_, NT_, 4)
-#define SW_TILE(G_, R_, M_) SW_TILE_NT(G_, R_, M_, 512)
+// SW_NTMODE (experiment): 0 = 512 threads (16 warps) for every tile; 1 = more
+// warps for the smaller R (768 threads up to R = 18, 640 up to R = 24).
+#ifndef SW_NTMODE
+#define SW_NTMODE 0
+#endif
+#define SW_NT_OF(R_) (SW_NTMODE == 1 ? ((R_) <= 18 ? 768 : (R_) <= 24 ? 640 : 512) : 512)
+#define SW_TILE(G_, R_, M_) SW_TILE_NT(G_, R_, M_, SW_NT_OF(R_))
 #define SW_TILES(M_)                                                                          \
   SW_TILE(8, 8, M_), SW_TILE(8, 12, M_), SW_TILE(8, 16, M_), SW_TILE(8, 18, M_),              \
   SW_TILE(8, 20, M_), SW_TILE(8, 22, M_), SW_TILE(8, 24, M_), SW_TILE(8, 26, M_),             \
@@ -697,49 +703,49 @@ TileEntry g_tiles[] = {SW_TILES(0), SW_TILES(3)};
 constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
 
 // Measured full-row throughput (GCUPS) of each tile's pass kernel on one
-// B200 (configs[1] at 0.5 scale; tools/calibrate_tiles.py,
-// profiles/r01_tile_calibration.jsonl): eff0 = first pass (query of G*R),
+// B200, biased arithmetic (configs[1] at 0.3 scale; tools/calibrate_tiles.py,
+// profiles/r01_tile_calibration_biased.jsonl): eff0 = first pass (query of G*R),
 // eff1 = a pass reading the previous pass's boundary (2*G*R minus G*R).
 // The tile choice predicts time ~ G*R * (1/eff0 + (P-1)/eff1).
 struct TileEff { int G, R; float eff0, eff1; };
 const TileEff kTileEff[] = {
-    {8, 8, 4344.f, 3415.f},
-    {8, 12, 4785.f, 4362.f},
-    {8, 16, 5040.f, 4707.f},
-    {8, 18, 5091.f, 4899.f},
-    {8, 20, 5197.f, 4901.f},
-    {8, 22, 5301.f, 5056.f},
-    {8, 24, 5311.f, 5176.f},
-    {8, 26, 5261.f, 5157.f},
-    {8, 28, 5297.f, 5229.f},
-    {8, 29, 5237.f, 5184.f},
-    {8, 30, 5289.f, 5238.f},
-    {8, 32, 5377.f, 4948.f},
-    {16, 8, 4390.f, 3550.f},
-    {16, 12, 4820.f, 4457.f},
-    {16, 16, 5058.f, 4774.f},
-    {16, 18, 5154.f, 4939.f},
-    {16, 20, 5224.f, 4985.f},
-    {16, 22, 5295.f, 5082.f},
-    {16, 24, 5304.f, 5174.f},
-    {16, 26, 5279.f, 5156.f},
-    {16, 28, 5335.f, 5205.f},
-    {16, 29, 5279.f, 5230.f},
-    {16, 30, 5337.f, 5264.f},
-    {16, 32, 5412.f, 5016.f},
-    {32, 8, 4346.f, 3638.f},
-    {32, 12, 4863.f, 4378.f},
-    {32, 15, 5027.f, 4646.f},
-    {32, 16, 5019.f, 4713.f},
-    {32, 18, 5184.f, 4853.f},
-    {32, 20, 5159.f, 5002.f},
-    {32, 22, 5088.f, 4971.f},
-    {32, 24, 5191.f, 5014.f},
-    {32, 26, 5198.f, 5065.f},
-    {32, 28, 5224.f, 5105.f},
-    {32, 29, 5274.f, 5032.f},
-    {32, 30, 5183.f, 5217.f},
-    {32, 32, 5300.f, 5153.f}};
+    {8, 8, 4389.5f, 3408.8f},
+    {8, 12, 4966.9f, 4168.2f},
+    {8, 16, 5259.9f, 4805.2f},
+    {8, 18, 5379.2f, 4889.6f},
+    {8, 20, 5477.4f, 5138.6f},
+    {8, 22, 5518.4f, 5159.2f},
+    {8, 24, 5631.3f, 5374.1f},
+    {8, 26, 5625.2f, 5339.2f},
+    {8, 28, 5671.0f, 5441.1f},
+    {8, 29, 5690.3f, 5437.5f},
+    {8, 30, 5784.8f, 5422.8f},
+    {8, 32, 5709.8f, 5463.9f},
+    {16, 8, 4452.6f, 3497.9f},
+    {16, 12, 5025.1f, 4259.5f},
+    {16, 16, 5324.0f, 4893.3f},
+    {16, 18, 5435.9f, 4959.8f},
+    {16, 20, 5517.0f, 5195.7f},
+    {16, 22, 5550.3f, 5241.6f},
+    {16, 24, 5668.9f, 5434.2f},
+    {16, 26, 5666.7f, 5381.2f},
+    {16, 28, 5721.0f, 5493.5f},
+    {16, 29, 5729.9f, 5508.8f},
+    {16, 30, 5831.6f, 5466.7f},
+    {16, 32, 5746.5f, 5496.7f},
+    {32, 8, 4404.6f, 3668.1f},
+    {32, 12, 5053.5f, 4357.2f},
+    {32, 15, 5220.7f, 4809.7f},
+    {32, 16, 5174.7f, 4845.5f},
+    {32, 18, 5431.1f, 5056.3f},
+    {32, 20, 5525.3f, 5180.1f},
+    {32, 22, 5579.1f, 5151.0f},
+    {32, 24, 5544.8f, 5248.8f},
+    {32, 26, 5583.6f, 5233.2f},
+    {32, 28, 5631.5f, 5415.7f},
+    {32, 29, 5418.3f, 5407.7f},
+    {32, 30, 5539.0f, 5324.0f},
+    {32, 32, 5570.3f, 5446.3f}};
 
 TileEff tile_eff(int G, int R) {
   for (const TileEff &e : kTileEff)
@@ -768,6 +774,7 @@ int find_tile_mode(int G, int R, int qpm) {
 }
 int find_tile(int G, int R) { return find_tile_mode(G, R, 0); }
 int tile_ctas_per_sm(int i) { return g_tiles[i].ctas; }
+int tile_threads(int i) { return g_tiles[i].nt; }
 
 cudaError_t init_kernels() {
   for (int i = 0; i < kNumTiles; ++i) {

@@ -77,6 +77,8 @@ size_t qp_bytes(int G, int R, int P, int qpm);
 cudaError_t init_kernels();
 // Max resident CTAs per SM of tile i's kernel.
 int tile_ctas_per_sm(int i);
+// Threads per CTA of tile i's kernel.
+int tile_threads(int i);
 
 // d_query2 != nullptr: query-pair profile (QPM 3) and a second s32 profile.
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,

@@ -211,10 +211,10 @@ def sw_topk_dev(d_scores, d_index, n: int, k: int, d_idx_out, d_score_out, strea
 
 
 def sw_last_stats() -> dict:
-    a = np.zeros(9, dtype=np.int64)
-    _check(load_library().sw_last_stats(_ptr(a), 9))
+    a = np.zeros(10, dtype=np.int64)
+    _check(load_library().sw_last_stats(_ptr(a), 10))
     keys = ["rows_per_pass", "passes", "G", "R", "flagged", "cells32", "pair_columns", "items",
-            "flag_threshold"]
+            "flag_threshold", "arith"]
     return {k: int(v) for k, v in zip(keys, a)}
 
 
