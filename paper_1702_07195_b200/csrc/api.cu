@@ -290,7 +290,8 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g.ev[i]));
   CUDA_TRY(cudaEventRecord(g.ev[0], st));
   CUDA_TRY(launch_qp_build(g.query.p, m, pair ? g.query2.p : nullptr, m2, g.matrix.p, T.G, T.R, P, g.qp.p,
-                           g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr, st));
+                           g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr,
+                           (uint32_t)(32767 - std::min(goe, 32767)), (uint32_t)(32767 - std::min(ge, 32767)), st));
 
   const int grid = g.num_sms * std::max(1, tile_ctas_per_sm(ti));
   // resident database: one "chunk" (the whole image); streamed database: the
@@ -665,11 +666,12 @@ int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, 
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)cuda_stream;
   if (kk <= 32) {
-    const int nw1 = (int)((std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)) + 7) / 8 * 8);
-    CUDA_TRY(g.keys.ensure((size_t)nw1 * kk));
+    // one block per SM (at most), each warp >= 4 batches of 32 scores
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, g.num_sms > 0 ? g.num_sms : 148));
+    CUDA_TRY(g.keys.ensure((size_t)nb * kk));
     CUDA_TRY(g.keys2.ensure((size_t)kk));
-    CUDA_TRY(launch_warp_topk(d_scores, d_index, nullptr, n, (int)kk, g.keys.p, nw1, st));
-    CUDA_TRY(launch_warp_topk(nullptr, nullptr, g.keys.p, (int64_t)nw1 * kk, (int)kk, g.keys2.p, 1, st));
+    CUDA_TRY(launch_block_topk(d_scores, d_index, nullptr, n, (int)kk, g.keys.p, nb, st));
+    CUDA_TRY(launch_block_topk(nullptr, nullptr, g.keys.p, (int64_t)nb * kk, (int)kk, g.keys2.p, 1, st));
     CUDA_TRY(launch_decode_keys(g.keys2.p, kk, d_idx_out, d_score_out, st));
   } else {
     int64_t np2 = 1;

@@ -31,6 +31,17 @@
 #include <climits>
 #include <cstdio>
 
+// SW_PENSHFL: 1 = the per-column gap penalties and S-reset words come from the
+// descriptor table (built per query) and travel lane to lane by shuffle; 0 =
+// each lane computes them from the separator bits with three IMADs.
+#ifndef SW_PENSHFL
+#define SW_PENSHFL 1
+#endif
+// SW_ROWAHEAD: 1 = biased rows form the next row's diagonal add before the
+// current row's H is overwritten (see the pass kernel); 0 = plain row order.
+#ifndef SW_ROWAHEAD
+#define SW_ROWAHEAD 1
+#endif
 // SW_ABLATE (performance experiments only, wrong results): see the pass kernel.
 #ifndef SW_ABLATE
 #define SW_ABLATE 0
@@ -154,6 +165,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << gbase);
   const bool last = t == G - 1;
   const uint32_t nlast = last ? 0u : 1u;
+  const uint32_t bdef = last ? kB2 : 0u;   // lane 0's boundary without a previous pass (via lane G-1)
   const uint32_t zero = p.zero;
   const uint32_t s_desc = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t s_qp = s_desc + DESC_U4 * 16 + t * 16;
@@ -169,6 +181,9 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   uint32_t S = 0u, hout = kB2, fout = kB2, sc = 0u, hprev = kB2;
   uint32_t w0 = nul.x, ns = nul.y;               // column chain (NUL)
   uint32_t kneg = 0u;                            // S-reset value after the previous column
+#if SW_PENSHFL
+  uint32_t ngoe = nul.y, nge = nul.z, knext = nul.w;   // descriptor penalty words of the column chain
+#endif
 
   // Lane G-1 prefetches the stream and the previous pass's boundary 4 columns
   // ahead, and stores per column the score chain value (sc_out) and the
@@ -214,6 +229,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           const uint4 d = lds128(s_desc + __ldg(sptr));   // lane 0's first column
           w0 = d.x;
           ns = d.y;
+#if SW_PENSHFL
+          ngoe = d.y;
+          nge = d.z;
+          knext = d.w;
+#endif
           const uint2 b0 = BIN ? __ldg(bptr) : make_uint2(kB2, kB2);   // ncols >= 4
           hout = b0.x;
           fout = b0.y;
@@ -233,6 +253,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           for (int u = 0; u < U; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(kB2, kB2); }
           w0 = nul.x;
           ns = nul.y;
+#if SW_PENSHFL
+          ngoe = nul.y;
+          nge = nul.z;
+          knext = nul.w;
+#endif
           hout = kB2;
           fout = kB2;
           sc = 0u;
@@ -245,28 +270,44 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
     for (int u = 0; u < U; ++u) {
       // ---- this column's inputs from lane t-1 (lane 0: from lane G-1)
       w0 = __shfl_sync(0xffffffffu, w0, src);
+#if SW_PENSHFL
+      ngoe = __shfl_sync(0xffffffffu, ngoe, src);
+      nge = __shfl_sync(0xffffffffu, nge, src);
+      knext = __shfl_sync(0xffffffffu, knext, src);
+#else
       ns = __shfl_sync(0xffffffffu, ns, src);
+#endif
       const uint32_t hu = __shfl_sync(0xffffffffu, hout, src);
       uint32_t F = __shfl_sync(0xffffffffu, fout, src);
       const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
       // ---- profile addresses and per-column gap penalties (FMA pipe)
       const uint32_t offB = umulhi(w0, 65536u);           // profile offsets / 16
       const uint32_t offA = imad(offB, 0xffff0000u, w0);
+#if !SW_PENSHFL
       const uint32_t ngoe = imad(ns, dgoe, pen_base);   // -Goe, or -32767 in a separator half
       const uint32_t nge = imad(ns, dge, pen_base);     // -Ge,  or -32767 in a separator half
+#endif
       const uint32_t aA = imad(offA, 16u, s_qp);
       const uint32_t aB = imad(offB, 16u, s_qp);
       // S is reset after every separator column (END: the score was just read
       // from the chain; NUL: S is already 0): -32768 in each separator half.
       const uint32_t kneg_prev = kneg;
+#if SW_PENSHFL
+      kneg = knext;
+#else
       kneg = imad(ns, 0xffff8000u, 0x80008000u);
+#endif
       // ---- lane G-1: lane 0's next column (s+u+1) descriptor; refill its ring slot
-      uint2 bnext = make_uint2(0u, 0u);   // added to the outgoing (H, F) of lanes t < G-1: 0
+      uint2 bnext = make_uint2(bdef, bdef);   // added to the outgoing (H, F): 0 for lanes t < G-1
+      // descriptor of lane 0's next column: loaded after the rows with
+      // SW_PENSHFL (lane G-1 still needs its own column's penalty words)
+      const uint32_t dnext = sring[(u + 1) % U];
       if (last) {
-        bnext = make_uint2(kB2, kB2);      // lane 0's boundary without a previous pass
-        const uint2 d = lds64(s_desc + sring[(u + 1) % U]);
+#if !SW_PENSHFL
+        const uint2 d = lds64(s_desc + dnext);
         w0 = d.x;
         ns = d.y;
+#endif
         SW_CHECK(sptr == p.nul_stream ? (u + 1 + U < 16)
                                       : (sptr + u + 1 + U - p.stream >= p.col_lo &&
                                          sptr + u + 1 + U - p.stream < p.col_hi));
@@ -280,6 +321,44 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       }
       uint32_t hd = hprev;
       hprev = hu;
+      if (kArith == 1 && SW_ROWAHEAD && SW_ABLATE == 0) {
+        // Biased rows with the diagonal add one row ahead: t(r+1) = H_old[r] + P(r+1)
+        // is formed before H[r] is overwritten, so the new H can take the old H's
+        // register (no per-column rotation of the H registers, which otherwise
+        // costs a register permutation at every loop back-edge).
+        // P(r) = SM(q_r, dB) * 65536 + SM(q_r, dA) (QPM 0) or the profile word (QPM 3).
+        uint4 ca = lds128(aA), cb = QPM == 0 ? lds128(aB) : make_uint4(0u, 0u, 0u, 0u);
+        uint32_t tcur = imad(hd, one, QPM == 0 ? imad(cb.x, 65536u, ca.x) : ca.x);
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+          SW_CHECK(aA + kk * G * 16 + 16 <= s_desc + (DESC_U4 + QP_U4) * 16 &&
+                   aB + kk * G * 16 + 16 <= s_desc + (DESC_U4 + QP_U4) * 16);
+          uint4 na = make_uint4(0u, 0u, 0u, 0u), nb = make_uint4(0u, 0u, 0u, 0u);
+          if (kk + 1 < KC) {
+            na = lds128(aA + (kk + 1) * G * 16);
+            if (QPM == 0) nb = lds128(aB + (kk + 1) * G * 16);
+          }
+          const uint32_t av[8] = {ca.x, ca.y, ca.z, ca.w, na.x, na.y, na.z, na.w};
+          const uint32_t bv[8] = {cb.x, cb.y, cb.z, cb.w, nb.x, nb.y, nb.z, nb.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = kk * RPC + j;
+            if (r < R) {
+              uint32_t tnext = 0u;
+              if (r + 1 < R)
+                tnext = imad(H[r], one, QPM == 0 ? imad(bv[j + 1], 65536u, av[j + 1]) : av[j + 1]);
+              const uint32_t h = __vimax3_s16x2(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
+              H[r] = h;
+              const uint32_t hg = __viaddmax_s16x2(h, ngoe, kB2);  // max(H-Goe, 0)
+              E[r] = __viaddmax_s16x2(E[r], nge, hg);              // Eq. 2 (next column)
+              F = __viaddmax_s16x2(F, nge, hg);                    // Eq. 3 (next row)
+              tcur = tnext;
+            }
+          }
+          ca = na;
+          cb = nb;
+        }
+      } else {
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
         SW_CHECK(aA + kk * G * 16 + 16 <= s_desc + (DESC_U4 + QP_U4) * 16 &&
@@ -326,6 +405,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           }
         }
       }
+      }
       // S = max(S reset at the previous END, H_0 .. H_{R-1}); the reset adds
       // -32768 to a half in [0, 32767] (no wrap), folded into the first max.
       S = __viaddmax_s16x2(S, kneg_prev, H[0]);
@@ -336,6 +416,15 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       SW_CHECK(!last || scp == reinterpret_cast<uint32_t *>(dummy) ||
                (scp + u - p.sc_out >= p.col_lo && scp + u - p.sc_out < p.col_hi));
       SW_CHECK(!bout || bop == dummy || (bop + u - p.bnd_out >= p.col_lo && bop + u - p.bnd_out < p.col_hi));
+#if SW_PENSHFL
+      if (last) {
+        const uint4 d = lds128(s_desc + dnext);
+        w0 = d.x;
+        ngoe = d.y;
+        nge = d.z;
+        knext = d.w;
+      }
+#endif
       if (last) st_global_u32(scp + u, so);
       if (bout) st_global_v2(bop + u, H[R - 1], F);
       // outgoing registers; lane G-1 hands over lane 0's next-column inputs
@@ -502,7 +591,7 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
 // ---------------------------------------------------------------------------
 __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint8_t *__restrict__ q2, int m2,
                                 const int8_t *__restrict__ M, int G, int R, int P, uint32_t *qp, uint4 *desc,
-                                int32_t *qp32, int32_t *qp32b) {
+                                int32_t *qp32, int32_t *qp32b, uint32_t dgoe, uint32_t dge) {
   // q2 == nullptr: one query; profile word = zero-extended int16 (QPM 0).
   // q2 != nullptr: query pair; profile word = (SM[q_r][c], SM[q2_r][c]) (QPM 3).
   const int KC = (R + 3) / 4;
@@ -539,8 +628,14 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
       const int cA = k / kNL, cB = k % kNL;
       const uint32_t offA = (uint32_t)(cA * LS / 16), offB = (uint32_t)(cB * LS / 16);
       const uint32_t ns = (cA < kAlpha ? 1u : 0u) + (cB < kAlpha ? 65536u : 0u);
-      const uint32_t endneg = (cA == kEnd ? 0x8000u : 0u) | (cB == kEnd ? 0x80000000u : 0u);
-      desc[k] = make_uint4(offA | (offB << 16), ns, endneg, 0u);
+#if SW_PENSHFL
+      // per half: -Goe / -Ge, or -32767 in a separator half (zeroes E and F); S
+      // reset -32768 after a separator half
+      desc[k] = make_uint4(offA | (offB << 16), ns * dgoe + 0x80018001u, ns * dge + 0x80018001u,
+                           ns * 0xffff8000u + 0x80008000u);
+#else
+      desc[k] = make_uint4(offA | (offB << 16), ns, 0u, 0u);   // separator bits (1 per non-separator half)
+#endif
     } else {
       // s32 profile(s), pass-slice layout [pass][letter][4-row chunk][lane][4]
       const int64_t j = i - nq - ndesc;
@@ -620,33 +715,56 @@ __global__ void bitonic_local_kernel(uint64_t *keys, int64_t size, int64_t strid
   keys[base + threadIdx.x + 1024] = sk[threadIdx.x + 1024];
 }
 
-// Warp-level top-k (k <= 32): lane i holds the i-th largest key seen so far.
-__global__ void warp_topk_kernel(const int32_t *scores, const int64_t *index, const uint64_t *keys_in,
-                                 int64_t n, int k, uint64_t *out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  uint64_t L = 0ull;
-  uint64_t thr = 0ull;
-  for (int64_t base = gw * 32; base < n; base += nw * 32) {
-    const int64_t i = base + lane;
-    uint64_t key = 0ull;
-    if (i < n) key = keys_in ? keys_in[i] : make_key(scores[i], index ? (uint64_t)index[i] : (uint64_t)i);
-    unsigned cand = __ballot_sync(0xffffffffu, key > thr);
-    while (cand) {
-      const int src = __ffs(cand) - 1;
-      cand &= cand - 1;
-      const uint64_t c = __shfl_sync(0xffffffffu, key, src);
-      if (c > thr) {
-        const int pos = __popc(__ballot_sync(0xffffffffu, L > c));
-        const uint64_t up = __shfl_up_sync(0xffffffffu, L, 1);
-        if (lane > pos) L = up;
-        if (lane == pos) L = c;
-        thr = __shfl_sync(0xffffffffu, L, k - 1);
-      }
+// Block-level top-k (k <= 32), the sorting stage's fast path: every warp keeps
+// a lane-distributed sorted list of the k best keys of a strided slice (lane i
+// holds the i-th largest), with the next batch's load issued before the
+// current batch is inserted; warp 0 then merges the block's lists from shared
+// memory.  Launched twice: a grid over the scores, then one block over the
+// grid's lists.
+__device__ __forceinline__ void warp_topk_insert(uint64_t key, uint64_t &L, uint64_t &thr, int k, int lane) {
+  unsigned cand = __ballot_sync(0xffffffffu, key > thr);
+  while (cand) {
+    const int src = __ffs(cand) - 1;
+    cand &= cand - 1;
+    const uint64_t c = __shfl_sync(0xffffffffu, key, src);
+    if (c > thr) {
+      const int pos = __popc(__ballot_sync(0xffffffffu, L > c));
+      const uint64_t up = __shfl_up_sync(0xffffffffu, L, 1);
+      if (lane > pos) L = up;
+      if (lane == pos) L = c;
+      thr = __shfl_sync(0xffffffffu, L, k - 1);
     }
   }
-  if (lane < k) out[gw * k + lane] = L;
+}
+
+__global__ void __launch_bounds__(1024) block_topk_kernel(const int32_t *scores, const int64_t *index,
+                                                          const uint64_t *keys_in, int64_t n, int k,
+                                                          uint64_t *out) {
+  __shared__ uint64_t s_lists[32 * 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t stride = (int64_t)gridDim.x * nwarps * 32;
+  auto load = [&](int64_t i) -> uint64_t {
+    if (i >= n) return 0ull;
+    return keys_in ? keys_in[i] : make_key(scores[i], index ? (uint64_t)index[i] : (uint64_t)i);
+  };
+  uint64_t L = 0ull, thr = 0ull;
+  int64_t i = gw * 32 + lane;
+  uint64_t key = load(i);
+  for (int64_t base = gw * 32; base < n; base += stride) {
+    const uint64_t next = load(i + stride);   // in flight while this batch is inserted
+    warp_topk_insert(key, L, thr, k, lane);
+    key = next;
+    i += stride;
+  }
+  s_lists[warp * 32 + lane] = lane < k ? L : 0ull;
+  __syncthreads();
+  if (warp == 0) {
+    L = 0ull;
+    thr = 0ull;
+    for (int w = 0; w < nwarps; ++w) warp_topk_insert(s_lists[w * 32 + lane], L, thr, k, lane);
+    if (lane < k) out[(int64_t)blockIdx.x * k + lane] = L;
+  }
 }
 
 __global__ void decode_keys_kernel(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score) {
@@ -676,7 +794,10 @@ struct TileEntry {
 #define SW_TILE_NTU(G_, R_, M_, NT_, U_)                                                     \
   {G_, R_, M_, NT_, smem_of<R_, G_, M_>(), sw16_pass_kernel<R_, G_, false, M_, NT_, U_>,   \
    sw16_pass_kernel<R_, G_, true, M_, NT_, U_>, 0}
-#define SW_TILE_NT(G_, R_, M_, NT_) SW_TILE_NTU(G_, R_, M_, NT_, 4)
+#ifndef SW_UNROLL
+#define SW_UNROLL 4   // columns per unrolled block = lane G-1's prefetch distance
+#endif
+#define SW_TILE_NT(G_, R_, M_, NT_) SW_TILE_NTU(G_, R_, M_, NT_, SW_UNROLL)
 // SW_NTMODE (experiment): 0 = 512 threads (16 warps) for every tile; 1 = more
 // warps for the smaller R (768 threads up to R = 18, 640 up to R = 24).
 #ifndef SW_NTMODE
@@ -799,13 +920,13 @@ size_t qp_bytes(int G, int R, int P, int qpm) {
 
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,
                             int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
-                            cudaStream_t st) {
+                            uint32_t dgoe, uint32_t dge, cudaStream_t st) {
   const int mm = d_query2 ? (m > m2 ? m : m2) : m;
   const int P32 = (mm + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
   const int64_t total = (int64_t)P * kNL * ((R + 3) / 4) * G * 4 + kNL * kNL + (int64_t)kNL * P32 * 32 * kSW32Rows;
   qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_query2, m2, d_matrix, G, R, P,
                                                          reinterpret_cast<uint32_t *>(d_qp), d_desc, d_qp32,
-                                                         d_qp32b);
+                                                         d_qp32b, dgoe, dge);
   return cudaGetLastError();
 }
 
@@ -865,12 +986,9 @@ cudaError_t launch_bitonic_sort_desc(uint64_t *keys, int64_t npow2, cudaStream_t
   return cudaSuccess;
 }
 
-cudaError_t launch_warp_topk(const int32_t *scores, const int64_t *index, const uint64_t *keys_in, int64_t n,
-                             int k, uint64_t *out, int nwarps, cudaStream_t st) {
-  // exactly nwarps warps: out[] holds nwarps * k keys
-  const int threads = nwarps % 8 == 0 ? 256 : 32;
-  const int blocks = nwarps * 32 / threads;
-  warp_topk_kernel<<<blocks, threads, 0, st>>>(scores, index, keys_in, n, k, out);
+cudaError_t launch_block_topk(const int32_t *scores, const int64_t *index, const uint64_t *keys_in, int64_t n,
+                              int k, uint64_t *out, int blocks, cudaStream_t st) {
+  block_topk_kernel<<<blocks, 1024, 0, st>>>(scores, index, keys_in, n, k, out);
   return cudaGetLastError();
 }
 

@@ -83,7 +83,8 @@ int tile_threads(int i);
 // d_query2 != nullptr: query-pair profile (QPM 3) and a second s32 profile.
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,
                             int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
-                            cudaStream_t st);
+                            uint32_t dgoe, uint32_t dge, cudaStream_t st);
+// dgoe, dge = 32767 - min(Goe, 32767), 32767 - min(Ge, 32767) (descriptor penalty words)
 cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cudaStream_t st);
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
@@ -99,8 +100,10 @@ cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st);
 cudaError_t launch_make_keys(const int32_t *scores, const int64_t *index, int64_t n,
                              uint64_t *keys, int64_t npad, cudaStream_t st);
 cudaError_t launch_bitonic_sort_desc(uint64_t *keys, int64_t npow2, cudaStream_t st);
-cudaError_t launch_warp_topk(const int32_t *scores, const int64_t *index, const uint64_t *keys_in,
-                             int64_t n, int k, uint64_t *out, int nwarps, cudaStream_t st);
+// k <= 32: `blocks` blocks of 1024 threads; out[] holds blocks * k keys, each
+// block's k best in descending order.
+cudaError_t launch_block_topk(const int32_t *scores, const int64_t *index, const uint64_t *keys_in, int64_t n,
+                              int k, uint64_t *out, int blocks, cudaStream_t st);
 cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score,
                                cudaStream_t st);
 
