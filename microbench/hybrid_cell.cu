@@ -34,9 +34,9 @@
   fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
 
 constexpr int ITERS = 1024;
-enum Var { DPX, HA, HB, HBF, MIX, HB_I, HBF_I, MIX_I, HA_I, HAINT, HAINT_T, HA_I_T, NUM_VARS };
+enum Var { DPX, HA, HB, HBF, MIX, HB_I, HBF_I, MIX_I, HA_I, HAINT, HAINT_T, HA_I_T, HC, HMIX2, HMIX3, NUM_VARS };
 static const char *kNames[] = {"dpx", "hybA_biased", "hybB_fp16", "hybB_fp16_fmarelu", "mix_AB_biased",
-                               "hybB_fp16_imm", "hybB_fp16_fmarelu_imm", "mix_AB_biased_imm", "hybA_biased_imm", "hybA_int_imad", "hybA_int_imad_Stree", "hybA_biased_imm_Stree"};
+                               "hybB_fp16_imm", "hybB_fp16_fmarelu_imm", "mix_AB_biased_imm", "hybA_biased_imm", "hybA_int_imad", "hybA_int_imad_Stree", "hybA_biased_imm_Stree", "hybC_int_fmaroute", "hybAC_mix_1to1", "hybAC_mix_2to1"};
 
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(256, (R <= 8 ? 4 : 2)) bench(const uint32_t *_
   for (int i = threadIdx.x; i < 8 * (R / 4) * 32; i += blockDim.x)
     prof[i] = make_uint4(in[i & 15], in[(i + 1) & 15], in[(i + 2) & 15], in[(i + 3) & 15]);
   const uint32_t ngoe = in[12], nge = in[13], bias = in[4], one = in[5];
+  const uint32_t ngoe32 = in[8] * 0xfff4fff4u, nge32 = in[8] * 0xfffefffeu;
   const uint32_t ngoe_h = in[6], nge_h = in[7];
   uint32_t H[R], E[R];
 #pragma unroll
@@ -104,7 +105,15 @@ __global__ void __launch_bounds__(256, (R <= 8 ? 4 : 2)) bench(const uint32_t *_
           const uint32_t hg = __viaddmax_s16x2_relu(h, ngoe, ngoe);
           E[r] = __viaddmax_s16x2(E[r], nge, hg);
           F = __viaddmax_s16x2(F, nge, hg);
-        } else if (VAR == HAINT || VAR == HAINT_T) {
+        } else if (VAR == HC || (VAR == HMIX2 && (r & 1)) || (VAR == HMIX3 && r % 3 == 2)) {
+          // FMA route: u = h - Goe, e1 = E - Ge, f1 = F - Ge as 32-bit adds (no borrow:
+          // values >= B = 16384 >= the clamped penalties); 3 max3 with the floor B
+          h = __vimax3_s16x2(imad(hd, one_p, sub), E[r], F);
+          hd = H[r]; H[r] = h;
+          const uint32_t u = imad(h, one_p, ngoe32);
+          E[r] = __vimax3_s16x2(imad(E[r], one_p, nge32), u, 0x40004000u);
+          F = __vimax3_s16x2(imad(F, one_p, nge32), u, 0x40004000u);
+        } else if (VAR == HAINT || VAR == HAINT_T || VAR == HMIX2 || VAR == HMIX3) {
           h = __vimax3_s16x2(imad(hd, one_p, sub), E[r], F);
           hd = H[r]; H[r] = h;
           const uint32_t hg = __viaddmax_s16x2(h, ngoe, 0x40004000u);
@@ -269,6 +278,9 @@ void run_all(int nsm, uint32_t *d_in, uint32_t *d_out, long long *d_cyc, int bps
     run<HAINT, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
     run<HAINT_T, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
     run<HA_I_T, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
+    run<HC, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
+    run<HMIX2, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
+    run<HMIX3, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
   }
 }
 

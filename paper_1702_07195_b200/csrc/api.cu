@@ -377,6 +377,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     q.stride = g.scratch_stride;
     q.scores = k ? d_scores2 : d_scores;
     q.cells = g.cells32.p;
+    q.one = 1u;
     CUDA_TRY(launch_sw32(g.sw32_grid, q, st));
   }
   CUDA_TRY(cudaEventRecord(g.ev[3], st));

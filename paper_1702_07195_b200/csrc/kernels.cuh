@@ -57,6 +57,7 @@ struct SW32Params {
   int64_t stride;           // >= max_len + 64
   int32_t *scores;
   int64_t *cells;           // re-scored cells (statistics), may be null
+  uint32_t one;             // 1 (keeps the diagonal add on the FMA pipe)
 };
 
 struct TileInfo {
