@@ -32,8 +32,6 @@ if os.environ.get("SW_ARITH"):    # cell arithmetic (kernels.cuh): 1 biased (def
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ARITH=" + os.environ["SW_ARITH"]]
 if os.environ.get("SW_NTMODE"):   # threads per CTA by tile (experiment, kernels.cu)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_NTMODE=" + os.environ["SW_NTMODE"]]
-if os.environ.get("SW_PENSHFL"):  # penalty words by shuffle (1, default) or IMAD (0)
-    NVCC_FLAGS = NVCC_FLAGS + ["-DSW_PENSHFL=" + os.environ["SW_PENSHFL"]]
 if os.environ.get("SW_ROWAHEAD"):  # row order of the biased cell loop (experiment)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ROWAHEAD=" + os.environ["SW_ROWAHEAD"]]
 if os.environ.get("SW_UNROLL"):    # columns per unrolled block (experiment)

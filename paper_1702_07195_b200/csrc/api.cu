@@ -291,7 +291,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(cudaEventRecord(g.ev[0], st));
   CUDA_TRY(launch_qp_build(g.query.p, m, pair ? g.query2.p : nullptr, m2, g.matrix.p, T.G, T.R, P, g.qp.p,
                            g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr,
-                           (uint32_t)(32767 - std::min(goe, 32767)), (uint32_t)(32767 - std::min(ge, 32767)), st));
+                           goe, ge, st));
 
   const int grid = g.num_sms * std::max(1, tile_ctas_per_sm(ti));
   // resident database: one "chunk" (the whole image); streamed database: the
@@ -343,8 +343,6 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       p.thresh = thresh;
       p.zero = 0u;
       p.one = 1u;
-      p.dgoe = (uint32_t)(32767 - std::min(goe, 32767));
-      p.dge = (uint32_t)(32767 - std::min(ge, 32767));
       CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
       if (strm) {
         const State::Chunk &c = g.chunks[k];

@@ -31,12 +31,6 @@
 #include <climits>
 #include <cstdio>
 
-// SW_PENSHFL: 1 = the per-column gap penalties and S-reset words come from the
-// descriptor table (built per query) and travel lane to lane by shuffle; 0 =
-// each lane computes them from the separator bits with three IMADs.
-#ifndef SW_PENSHFL
-#define SW_PENSHFL 1
-#endif
 // SW_ROWAHEAD: 1 = biased rows form the next row's diagonal add before the
 // current row's H is overwritten (see the pass kernel); 0 = plain row order.
 #ifndef SW_ROWAHEAD
@@ -169,8 +163,6 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   const uint32_t zero = p.zero;
   const uint32_t s_desc = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t s_qp = s_desc + DESC_U4 * 16 + t * 16;
-  const uint32_t pen_base = 0x80018001u;      // -32767 in both halves
-  const uint32_t dgoe = p.dgoe, dge = p.dge;  // 32767 - Goe, 32767 - Ge (clamped)
   const bool bout = last && p.bnd_out != nullptr;
   const uint4 nul = lds128(s_desc + kNulWord);
 
@@ -179,11 +171,9 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
   for (int r = 0; r < R; ++r) { H[r] = kB2; E[r] = kB2; }
   uint32_t S = 0u, hout = kB2, fout = kB2, sc = 0u, hprev = kB2;
-  uint32_t w0 = nul.x, ns = nul.y;               // column chain (NUL)
+  uint32_t w0 = nul.x;                           // column chain (NUL)
   uint32_t kneg = 0u;                            // S-reset value after the previous column
-#if SW_PENSHFL
   uint32_t ngoe = nul.y, nge = nul.z, knext = nul.w;   // descriptor penalty words of the column chain
-#endif
 
   // Lane G-1 prefetches the stream and the previous pass's boundary 4 columns
   // ahead, and stores per column the score chain value (sc_out) and the
@@ -228,12 +218,9 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           }
           const uint4 d = lds128(s_desc + __ldg(sptr));   // lane 0's first column
           w0 = d.x;
-          ns = d.y;
-#if SW_PENSHFL
           ngoe = d.y;
           nge = d.z;
           knext = d.w;
-#endif
           const uint2 b0 = BIN ? __ldg(bptr) : make_uint2(kB2, kB2);   // ncols >= 4
           hout = b0.x;
           fout = b0.y;
@@ -252,12 +239,9 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
           for (int u = 0; u < U; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(kB2, kB2); }
           w0 = nul.x;
-          ns = nul.y;
-#if SW_PENSHFL
           ngoe = nul.y;
           nge = nul.z;
           knext = nul.w;
-#endif
           hout = kB2;
           fout = kB2;
           sc = 0u;
@@ -270,44 +254,27 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
     for (int u = 0; u < U; ++u) {
       // ---- this column's inputs from lane t-1 (lane 0: from lane G-1)
       w0 = __shfl_sync(0xffffffffu, w0, src);
-#if SW_PENSHFL
       ngoe = __shfl_sync(0xffffffffu, ngoe, src);
       nge = __shfl_sync(0xffffffffu, nge, src);
       knext = __shfl_sync(0xffffffffu, knext, src);
-#else
-      ns = __shfl_sync(0xffffffffu, ns, src);
-#endif
       const uint32_t hu = __shfl_sync(0xffffffffu, hout, src);
       uint32_t F = __shfl_sync(0xffffffffu, fout, src);
       const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
-      // ---- profile addresses and per-column gap penalties (FMA pipe)
+      // ---- profile addresses (FMA pipe)
       const uint32_t offB = umulhi(w0, 65536u);           // profile offsets / 16
       const uint32_t offA = imad(offB, 0xffff0000u, w0);
-#if !SW_PENSHFL
-      const uint32_t ngoe = imad(ns, dgoe, pen_base);   // -Goe, or -32767 in a separator half
-      const uint32_t nge = imad(ns, dge, pen_base);     // -Ge,  or -32767 in a separator half
-#endif
       const uint32_t aA = imad(offA, 16u, s_qp);
       const uint32_t aB = imad(offB, 16u, s_qp);
       // S is reset after every separator column (END: the score was just read
       // from the chain; NUL: S is already 0): -32768 in each separator half.
       const uint32_t kneg_prev = kneg;
-#if SW_PENSHFL
       kneg = knext;
-#else
-      kneg = imad(ns, 0xffff8000u, 0x80008000u);
-#endif
       // ---- lane G-1: lane 0's next column (s+u+1) descriptor; refill its ring slot
       uint2 bnext = make_uint2(bdef, bdef);   // added to the outgoing (H, F): 0 for lanes t < G-1
-      // descriptor of lane 0's next column: loaded after the rows with
-      // SW_PENSHFL (lane G-1 still needs its own column's penalty words)
+      // descriptor of lane 0's next column: loaded after the rows (lane G-1
+      // still needs its own column's penalty words)
       const uint32_t dnext = sring[(u + 1) % U];
       if (last) {
-#if !SW_PENSHFL
-        const uint2 d = lds64(s_desc + dnext);
-        w0 = d.x;
-        ns = d.y;
-#endif
         SW_CHECK(sptr == p.nul_stream ? (u + 1 + U < 16)
                                       : (sptr + u + 1 + U - p.stream >= p.col_lo &&
                                          sptr + u + 1 + U - p.stream < p.col_hi));
@@ -416,7 +383,6 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       SW_CHECK(!last || scp == reinterpret_cast<uint32_t *>(dummy) ||
                (scp + u - p.sc_out >= p.col_lo && scp + u - p.sc_out < p.col_hi));
       SW_CHECK(!bout || bop == dummy || (bop + u - p.bnd_out >= p.col_lo && bop + u - p.bnd_out < p.col_hi));
-#if SW_PENSHFL
       if (last) {
         const uint4 d = lds128(s_desc + dnext);
         w0 = d.x;
@@ -424,7 +390,6 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         nge = d.z;
         knext = d.w;
       }
-#endif
       if (last) st_global_u32(scp + u, so);
       if (bout) st_global_v2(bop + u, H[R - 1], F);
       // outgoing registers; lane G-1 hands over lane 0's next-column inputs
@@ -593,7 +558,7 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
 // ---------------------------------------------------------------------------
 __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint8_t *__restrict__ q2, int m2,
                                 const int8_t *__restrict__ M, int G, int R, int P, uint32_t *qp, uint4 *desc,
-                                int32_t *qp32, int32_t *qp32b, uint32_t dgoe, uint32_t dge) {
+                                int32_t *qp32, int32_t *qp32b, int goe, int ge) {
   // q2 == nullptr: one query; profile word = zero-extended int16 (QPM 0).
   // q2 != nullptr: query pair; profile word = (SM[q_r][c], SM[q2_r][c]) (QPM 3).
   const int KC = (R + 3) / 4;
@@ -629,15 +594,15 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
       const int k = (int)(i - nq);
       const int cA = k / kNL, cB = k % kNL;
       const uint32_t offA = (uint32_t)(cA * LS / 16), offB = (uint32_t)(cB * LS / 16);
-      const uint32_t ns = (cA < kAlpha ? 1u : 0u) + (cB < kAlpha ? 65536u : 0u);
-#if SW_PENSHFL
-      // per half: -Goe / -Ge, or -32767 in a separator half (zeroes E and F); S
-      // reset -32768 after a separator half
-      desc[k] = make_uint4(offA | (offB << 16), ns * dgoe + 0x80018001u, ns * dge + 0x80018001u,
-                           ns * 0xffff8000u + 0x80008000u);
-#else
-      desc[k] = make_uint4(offA | (offB << 16), ns, 0u, 0u);   // separator bits (1 per non-separator half)
-#endif
+      // Per half, built explicitly (a packed add of the two halves would carry
+      // when a penalty is 0): -Goe / -Ge, or -32767 in a separator half (zeroes
+      // E and F at the column); the S-reset word -32768 after a separator half.
+      const bool sA = cA >= kAlpha, sB = cB >= kAlpha;
+      const uint32_t pgoe = (uint32_t)(uint16_t)(-(int)min(goe, 32767));
+      const uint32_t pge = (uint32_t)(uint16_t)(-(int)min(ge, 32767));
+      desc[k] = make_uint4(offA | (offB << 16), (sA ? 0x8001u : pgoe) | ((sB ? 0x8001u : pgoe) << 16),
+                           (sA ? 0x8001u : pge) | ((sB ? 0x8001u : pge) << 16),
+                           (sA ? 0x8000u : 0u) | ((sB ? 0x8000u : 0u) << 16));
     } else {
       // s32 profile(s), pass-slice layout [pass][letter][4-row chunk][lane][4]
       const int64_t j = i - nq - ndesc;
@@ -922,13 +887,13 @@ size_t qp_bytes(int G, int R, int P, int qpm) {
 
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,
                             int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
-                            uint32_t dgoe, uint32_t dge, cudaStream_t st) {
+                            int goe, int ge, cudaStream_t st) {
   const int mm = d_query2 ? (m > m2 ? m : m2) : m;
   const int P32 = (mm + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
   const int64_t total = (int64_t)P * kNL * ((R + 3) / 4) * G * 4 + kNL * kNL + (int64_t)kNL * P32 * 32 * kSW32Rows;
   qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_query2, m2, d_matrix, G, R, P,
                                                          reinterpret_cast<uint32_t *>(d_qp), d_desc, d_qp32,
-                                                         d_qp32b, dgoe, dge);
+                                                         d_qp32b, goe, ge);
   return cudaGetLastError();
 }
 

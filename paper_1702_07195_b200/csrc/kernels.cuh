@@ -41,7 +41,6 @@ struct SW16Params {
   int thresh;               // 32768 - max(1, smax)
   uint32_t zero;            // 0 (passed in so ptxas keeps it in a register)
   uint32_t one;             // 1 (passed in: keeps 32-bit adds on the FMA pipe as IMAD)
-  uint32_t dgoe, dge;       // 32767 - min(Goe, 32767), 32767 - min(Ge, 32767)
 };
 
 struct SW32Params {
@@ -84,8 +83,8 @@ int tile_threads(int i);
 // d_query2 != nullptr: query-pair profile (QPM 3) and a second s32 profile.
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,
                             int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
-                            uint32_t dgoe, uint32_t dge, cudaStream_t st);
-// dgoe, dge = 32767 - min(Goe, 32767), 32767 - min(Ge, 32767) (descriptor penalty words)
+                            int goe, int ge, cudaStream_t st);
+// goe = gap open + extend, ge = gap extend (>= 0; the descriptor penalty words clamp at 32767)
 cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cudaStream_t st);
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,

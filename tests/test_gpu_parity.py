@@ -69,6 +69,34 @@ def test_random_small_databases_random_scoring():
         _check_db(_db(seqs), q, M, go, ge, label=f"trial {trial} m={m} go={go} ge={ge}")
 
 
+def test_extreme_scoring_parameters():
+    """The biased 16-bit arithmetic (stored = score + 16384, DESIGN.md 4.2 / R7)
+    at the edges of its argument range: int8 matrices spanning [-128, 127] (the
+    32-bit diagonal add must not carry between halves), gap penalties around and
+    above 16384 and 32767 (clamped in 16 bit), zero penalties, and scores above
+    the 16-bit flag threshold (re-scored in 32 bit)."""
+    rng = np.random.default_rng(4242)
+    seqs = [rng.integers(0, 24, int(L)).astype(np.uint8) for L in rng.integers(0, 400, 150)]
+    seqs += [np.full(600, 3, np.uint8), np.full(300, 7, np.uint8)]   # long runs: large scores
+    db = _db(seqs)
+    wide = rng.integers(-128, 128, (24, 24)).astype(np.int8)
+    wide[np.arange(24), np.arange(24)] = 127
+    low = rng.integers(-128, -60, (24, 24)).astype(np.int8)          # every entry negative
+    low[3, 3] = 1
+    q = np.concatenate([rng.integers(0, 24, 250).astype(np.uint8), np.full(200, 3, np.uint8)])
+    for M in (BLOSUM62, wide, low):
+        for go, ge in ((0, 0), (10, 2), (16383, 1), (16384, 0), (16385, 0), (30000, 5), (5, 30000),
+                       (40000, 40000), (1 << 20, 1 << 20)):
+            _check_db(db, q, M, go, ge, label=f"go={go} ge={ge} smax={int(M.max())}")
+    # query pairs (QPM 3) with the wide matrix
+    qs = [q, rng.integers(0, 24, 333).astype(np.uint8)]
+    sw.sw_db_load(db.residues, db.offsets)
+    got = sw.sw_search_batch(qs, wide, 7, 3)
+    for k, qq in enumerate(qs):
+        exp = oracle.batch(qq, db.residues, db.offsets, wide, 7, 3)
+        assert (got[k] == exp).all(), k
+
+
 def test_every_tile_is_exact():
     rng = np.random.default_rng(7)
     seqs = [si.rr_residues(rng, int(L)) for L in rng.integers(1, 500, 300)]
