@@ -34,9 +34,9 @@
   fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
 
 constexpr int ITERS = 1024;
-enum Var { DPX, HA, HB, HBF, MIX, HB_I, HBF_I, MIX_I, HA_I, HAINT, HAINT_T, HA_I_T, HC, HMIX2, HMIX3, NUM_VARS };
+enum Var { DPX, HA, HB, HBF, MIX, HB_I, HBF_I, MIX_I, HA_I, HAINT, HAINT_T, HA_I_T, HC, HMIX2, HMIX3, SPV, NUM_VARS };
 static const char *kNames[] = {"dpx", "hybA_biased", "hybB_fp16", "hybB_fp16_fmarelu", "mix_AB_biased",
-                               "hybB_fp16_imm", "hybB_fp16_fmarelu_imm", "mix_AB_biased_imm", "hybA_biased_imm", "hybA_int_imad", "hybA_int_imad_Stree", "hybA_biased_imm_Stree", "hybC_int_fmaroute", "hybAC_mix_1to1", "hybAC_mix_2to1"};
+                               "hybB_fp16_imm", "hybB_fp16_fmarelu_imm", "mix_AB_biased_imm", "hybA_biased_imm", "hybA_int_imad", "hybA_int_imad_Stree", "hybA_biased_imm_Stree", "hybC_int_fmaroute", "hybAC_mix_1to1", "hybAC_mix_2to1", "score_profile_SP"};
 
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -59,6 +59,11 @@ __device__ __forceinline__ uint32_t hfma2_relu_m12(uint32_t a) {  // relu(a*1 - 
   return u32(__hfma2_relu(h2(a), __float2half2_rn(1.0f), __float2half2_rn(-12.0f)));
 }
 
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -68,8 +73,8 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 
 template <int VAR, int R, bool LDS>
 __global__ void __launch_bounds__(256, (R <= 8 ? 4 : 2)) bench(const uint32_t *__restrict__ in, uint32_t *out, long long *cycles, uint32_t one_p) {
-  __shared__ uint4 prof[8 * (R / 4) * 32];
-  for (int i = threadIdx.x; i < 8 * (R / 4) * 32; i += blockDim.x)
+  __shared__ uint4 prof[VAR == SPV ? 1 : 8 * (R / 4) * 32];
+  for (int i = threadIdx.x; i < (VAR == SPV ? 1 : 8 * (R / 4) * 32); i += blockDim.x)
     prof[i] = make_uint4(in[i & 15], in[(i + 1) & 15], in[(i + 2) & 15], in[(i + 3) & 15]);
   const uint32_t ngoe = in[12], nge = in[13], bias = in[4], one = in[5];
   const uint32_t ngoe32 = in[8] * 0xfff4fff4u, nge32 = in[8] * 0xfffefffeu;
@@ -79,12 +84,40 @@ __global__ void __launch_bounds__(256, (R <= 8 ? 4 : 2)) bench(const uint32_t *_
   for (int r = 0; r < R; ++r) { H[r] = in[r & 15] + threadIdx.x; E[r] = in[(r + 3) & 15]; }
   uint32_t S = 0, A0 = in[14], B0 = in[15], b = in[0], c = in[1];
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(prof) + (threadIdx.x & 31) * 16;
+  __shared__ uint32_t sptab[VAR == SPV ? 400 * 26 : 1];
+  if (VAR == SPV)
+    for (int i = threadIdx.x; i < 400 * 26; i += blockDim.x) sptab[i] = in[i & 15] * 0x10001u;
+  const uint32_t spbase = (uint32_t)__cvta_generic_to_shared(sptab);
+  uint32_t qoff[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) qoff[r] = ((threadIdx.x * 7 + r * 11) % 26) * 4;
   __syncthreads();
   long long t0 = clock64();
   for (int it = 0; it < ITERS; ++it) {
     uint32_t F = b, hd = c;
     A0 += it;
     B0 ^= it;
+    if constexpr (VAR == SPV) {
+      // NEXT-1 score profile: the column's letter pair selects a
+      // 26-word vector SP[c] = SM(c, dB) * 65536 + SM(c, dA) (built once per
+      // matrix: a 26 x 26 x 26 table, no packing per cell); each row reads
+      // SP[q_r] with its own query letter -> one LDS.32 per row, random banks.
+      const uint32_t pairbase = spbase + (((it * 7) ^ (threadIdx.x * 13)) % 400) * 104;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t sub = lds32(pairbase + qoff[r]);
+        uint32_t h = __vimax3_s16x2(imad(hd, one_p, sub), E[r], F);
+        hd = H[r]; H[r] = h;
+        const uint32_t hg = __viaddmax_s16x2(h, ngoe, 0x40004000u);
+        E[r] = __viaddmax_s16x2(E[r], nge, hg);
+        F = __viaddmax_s16x2(F, nge, hg);
+      }
+#pragma unroll
+      for (int r = 0; r < R; r += 2) S = __vimax3_s16x2(S, H[r], H[r + 1]);
+      b ^= F;
+      c += S;
+      continue;
+    }
     const uint32_t la = sbase + ((it * 7) & 7) * (R / 4) * 512;
     const uint32_t lb = sbase + ((it * 13) & 7) * (R / 4) * 512;
 #pragma unroll
@@ -281,6 +314,7 @@ void run_all(int nsm, uint32_t *d_in, uint32_t *d_out, long long *d_cyc, int bps
     run<HC, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
     run<HMIX2, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
     run<HMIX3, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
+    run<SPV, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
   }
 }
 
