@@ -36,6 +36,9 @@ if os.environ.get("SW_ROWAHEAD"):  # row order of the biased cell loop (experime
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ROWAHEAD=" + os.environ["SW_ROWAHEAD"]]
 if os.environ.get("SW_UNROLL"):    # columns per unrolled block (experiment)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_UNROLL=" + os.environ["SW_UNROLL"]]
+for _flag in ("SW_DESC32", "SW_SCSEP"):   # kernel experiments (kernels.cu / swdb_internal.h)
+    if os.environ.get(_flag):
+        NVCC_FLAGS = NVCC_FLAGS + [f"-D{_flag}=" + os.environ[_flag]]
 if os.environ.get("SW_DEBUG"):    # device-side bounds checks (slow; debug builds)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_DEBUG=1"]
 

@@ -31,6 +31,10 @@
 #include <climits>
 #include <cstdio>
 
+// SW_SCSEP: 1 = lane G-1 stores the score chain only at separator columns.
+#ifndef SW_SCSEP
+#define SW_SCSEP 0
+#endif
 // SW_ROWAHEAD: 1 = biased rows form the next row's diagonal add before the
 // current row's H is overwritten (see the pass kernel); 0 = plain row order.
 #ifndef SW_ROWAHEAD
@@ -111,6 +115,17 @@ __device__ __forceinline__ void st_global_u32(uint32_t *p, uint32_t a) {
   asm volatile("st.global.u32 [%0], %1;" :: "l"(p), "r"(a) : "memory");
 }
 
+// Descriptor of a letter pair -> the column-chain words (see qp_build_kernel).
+struct DescWords { uint32_t w0, w1, ngoe, nge, kneg; };
+__device__ __forceinline__ DescWords load_desc(uint32_t addr) {
+  const uint4 d = lds128(addr);
+#if SW_DESC32
+  return DescWords{d.x, d.y, d.z, d.w, lds128(addr + 16).x};
+#else
+  return DescWords{d.x, 0u, d.y, d.z, d.w};
+#endif
+}
+
 template <class T>
 __device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on the FMA pipe
   uint64_t d;
@@ -143,7 +158,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   constexpr int KC = (R + RPC - 1) / RPC;   // chunks per lane
   constexpr int LS = KC * G * 16;           // bytes per letter in the profile slice
   constexpr int QP_U4 = kNL * LS / 16;
-  constexpr int DESC_U4 = kNL * kNL;
+  constexpr int DESC_U4 = kNL * kNL * kDescU4;
   extern __shared__ uint4 smem[];
   {
     const uint4 *gq = p.qp + (size_t)p.pass * QP_U4;
@@ -164,16 +179,16 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   const uint32_t s_desc = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t s_qp = s_desc + DESC_U4 * 16 + t * 16;
   const bool bout = last && p.bnd_out != nullptr;
-  const uint4 nul = lds128(s_desc + kNulWord);
+  const DescWords nul = load_desc(s_desc + kNulWord);
 
   const uint32_t one = p.one;
   uint32_t H[R], E[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) { H[r] = kB2; E[r] = kB2; }
   uint32_t S = 0u, hout = kB2, fout = kB2, sc = 0u, hprev = kB2;
-  uint32_t w0 = nul.x;                           // column chain (NUL)
+  uint32_t w0 = nul.w0, w1 = nul.w1;             // column chain (NUL): profile offsets
   uint32_t kneg = 0u;                            // S-reset value after the previous column
-  uint32_t ngoe = nul.y, nge = nul.z, knext = nul.w;   // descriptor penalty words of the column chain
+  uint32_t ngoe = nul.ngoe, nge = nul.nge, knext = nul.kneg;   // descriptor penalty words of the column chain
 
   // Lane G-1 prefetches the stream and the previous pass's boundary 4 columns
   // ahead, and stores per column the score chain value (sc_out) and the
@@ -216,11 +231,12 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
             sring[u % U] = __ldg(sptr + u);
             if (BIN) bring[u % U] = u < ncols ? __ldg(bptr + u) : make_uint2(kB2, kB2);
           }
-          const uint4 d = lds128(s_desc + __ldg(sptr));   // lane 0's first column
-          w0 = d.x;
-          ngoe = d.y;
-          nge = d.z;
-          knext = d.w;
+          const DescWords d = load_desc(s_desc + __ldg(sptr));   // lane 0's first column
+          w0 = d.w0;
+          w1 = d.w1;
+          ngoe = d.ngoe;
+          nge = d.nge;
+          knext = d.kneg;
           const uint2 b0 = BIN ? __ldg(bptr) : make_uint2(kB2, kB2);   // ncols >= 4
           hout = b0.x;
           fout = b0.y;
@@ -238,10 +254,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         if (last) {
 #pragma unroll
           for (int u = 0; u < U; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(kB2, kB2); }
-          w0 = nul.x;
-          ngoe = nul.y;
-          nge = nul.z;
-          knext = nul.w;
+          w0 = nul.w0;
+          w1 = nul.w1;
+          ngoe = nul.ngoe;
+          nge = nul.nge;
+          knext = nul.kneg;
           hout = kB2;
           fout = kB2;
           sc = 0u;
@@ -254,6 +271,9 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
     for (int u = 0; u < U; ++u) {
       // ---- this column's inputs from lane t-1 (lane 0: from lane G-1)
       w0 = __shfl_sync(0xffffffffu, w0, src);
+#if SW_DESC32
+      w1 = __shfl_sync(0xffffffffu, w1, src);
+#endif
       ngoe = __shfl_sync(0xffffffffu, ngoe, src);
       nge = __shfl_sync(0xffffffffu, nge, src);
       knext = __shfl_sync(0xffffffffu, knext, src);
@@ -261,10 +281,15 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       uint32_t F = __shfl_sync(0xffffffffu, fout, src);
       const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
       // ---- profile addresses (FMA pipe)
+#if SW_DESC32
+      const uint32_t aA = imad(w0, one, s_qp);             // profile byte offsets, pre-split
+      const uint32_t aB = imad(w1, one, s_qp);
+#else
       const uint32_t offB = umulhi(w0, 65536u);           // profile offsets / 16
       const uint32_t offA = imad(offB, 0xffff0000u, w0);
       const uint32_t aA = imad(offA, 16u, s_qp);
       const uint32_t aB = imad(offB, 16u, s_qp);
+#endif
       // S is reset after every separator column (END: the score was just read
       // from the chain; NUL: S is already 0): -32768 in each separator half.
       const uint32_t kneg_prev = kneg;
@@ -384,13 +409,16 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
                (scp + u - p.sc_out >= p.col_lo && scp + u - p.sc_out < p.col_hi));
       SW_CHECK(!bout || bop == dummy || (bop + u - p.bnd_out >= p.col_lo && bop + u - p.bnd_out < p.col_hi));
       if (last) {
-        const uint4 d = lds128(s_desc + dnext);
-        w0 = d.x;
-        ngoe = d.y;
-        nge = d.z;
-        knext = d.w;
+        const DescWords d = load_desc(s_desc + dnext);
+        w0 = d.w0;
+        w1 = d.w1;
+        ngoe = d.ngoe;
+        nge = d.nge;
+        knext = d.kneg;
       }
-      if (last) st_global_u32(scp + u, so);
+      // SW_SCSEP: only separator columns' chain values are ever read (the
+      // gather reads END columns), so only those are stored
+      if (last && (!SW_SCSEP || kneg != 0u)) st_global_u32(scp + u, so);
       if (bout) st_global_v2(bop + u, H[R - 1], F);
       // outgoing registers; lane G-1 hands over lane 0's next-column inputs
       hout = imad(H[R - 1], nlast, bnext.x);
@@ -600,9 +628,15 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
       const bool sA = cA >= kAlpha, sB = cB >= kAlpha;
       const uint32_t pgoe = (uint32_t)(uint16_t)(-(int)min(goe, 32767));
       const uint32_t pge = (uint32_t)(uint16_t)(-(int)min(ge, 32767));
-      desc[k] = make_uint4(offA | (offB << 16), (sA ? 0x8001u : pgoe) | ((sB ? 0x8001u : pgoe) << 16),
-                           (sA ? 0x8001u : pge) | ((sB ? 0x8001u : pge) << 16),
-                           (sA ? 0x8000u : 0u) | ((sB ? 0x8000u : 0u) << 16));
+      const uint32_t wgoe = (sA ? 0x8001u : pgoe) | ((sB ? 0x8001u : pgoe) << 16);
+      const uint32_t wge = (sA ? 0x8001u : pge) | ((sB ? 0x8001u : pge) << 16);
+      const uint32_t wk = (sA ? 0x8000u : 0u) | ((sB ? 0x8000u : 0u) << 16);
+#if SW_DESC32
+      desc[2 * k] = make_uint4(offA * 16u, offB * 16u, wgoe, wge);
+      desc[2 * k + 1] = make_uint4(wk, 0u, 0u, 0u);
+#else
+      desc[k] = make_uint4(offA | (offB << 16), wgoe, wge, wk);
+#endif
     } else {
       // s32 profile(s), pass-slice layout [pass][letter][4-row chunk][lane][4]
       const int64_t j = i - nq - ndesc;
@@ -749,7 +783,7 @@ using PassFn = void (*)(const SW16Params);
 
 template <int R, int G, int QPM>
 constexpr int smem_of() {
-  return (kNL * kNL + kNL * ((R + 3) / 4) * G) * 16;
+  return (kNL * kNL * kDescU4 + kNL * ((R + 3) / 4) * G) * 16;
 }
 
 struct TileEntry {
