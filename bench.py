@@ -127,6 +127,18 @@ def measured_peaks():
     return {"sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md nominal clocks)"
 
 
+def ncu_pipes():
+    """ALU-pipe thread instructions per cell of the pass kernel, measured by ncu
+    on the bench launch (profiles/r01b_ncu_pipes.json), for the roofline with
+    the kernel's measured I_pipe."""
+    p = os.path.join(ROOT, "profiles", "r01b_ncu_pipes.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("alu_thread_inst_per_cell")
+    except Exception:
+        return None
+
+
 def ncu_traffic():
     """DRAM bytes per launch of the pass kernel from the committed ncu summary."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -371,6 +383,14 @@ def run_ours(args):
             "peak_basis": f"{nsm} SMs x {f_max:.0f} MHz (sm_max_mhz, {peaks_src}) x "
                           f"{ALU_LANE_OPS_PER_CLK_PER_SM} ALU lane-ops/clk/SM / {alu_per_cell} ALU instructions per cell",
             "frac_at_observed_clock": (round(achieved / (peak * f_obs / f_max), 4) if f_obs else None)}
+    # SURVEY.md 8(d) D5's two other fractions: against the bound with the
+    # kernel's measured ALU instructions per cell (ncu), and against the relu
+    # form's 5.5 DPX per pair of cells (2.75 per cell)
+    ipipe = ncu_pipes()
+    if ipipe:
+        roof["frac_measured_ipipe"] = round(achieved / (nsm * f_max * 1e6 * ALU_LANE_OPS_PER_CLK_PER_SM / ipipe / 1e9), 4)
+        roof["ipipe_alu_per_cell"] = ipipe
+    roof["frac_vs_2.75_dpx_per_cell"] = round(achieved / (nsm * f_max * 1e6 * ALU_LANE_OPS_PER_CLK_PER_SM / 2.75 / 1e9), 4)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
