@@ -30,15 +30,10 @@ if os.environ.get("SW_ABLATE"):   # performance experiments only (wrong results)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ABLATE=" + os.environ["SW_ABLATE"]]
 if os.environ.get("SW_ARITH"):    # cell arithmetic (kernels.cuh): 1 biased (default), 0 relu DPX
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ARITH=" + os.environ["SW_ARITH"]]
-if os.environ.get("SW_NTMODE"):   # threads per CTA by tile (experiment, kernels.cu)
-    NVCC_FLAGS = NVCC_FLAGS + ["-DSW_NTMODE=" + os.environ["SW_NTMODE"]]
 if os.environ.get("SW_ROWAHEAD"):  # row order of the biased cell loop (experiment)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ROWAHEAD=" + os.environ["SW_ROWAHEAD"]]
 if os.environ.get("SW_UNROLL"):    # columns per unrolled block (experiment)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_UNROLL=" + os.environ["SW_UNROLL"]]
-for _flag in ("SW_DESC32", "SW_SCSEP"):   # kernel experiments (kernels.cu / swdb_internal.h)
-    if os.environ.get(_flag):
-        NVCC_FLAGS = NVCC_FLAGS + [f"-D{_flag}=" + os.environ[_flag]]
 if os.environ.get("SW_DEBUG"):    # device-side bounds checks (slow; debug builds)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_DEBUG=1"]
 

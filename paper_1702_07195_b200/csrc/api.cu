@@ -275,7 +275,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   if (pair) CUDA_TRY(g.query2.ensure((size_t)m2));
   CUDA_TRY(g.matrix.ensure(kAlpha * kAlpha));
   CUDA_TRY(g.qp.ensure(qp_bytes(T.G, T.R, P, T.qpm)));
-  CUDA_TRY(g.desc.ensure((size_t)kNL * kNL * kDescU4));
+  CUDA_TRY(g.desc.ensure((size_t)kNL * kNL));
   CUDA_TRY(g.qp32.ensure((size_t)kNL * P32max * 32 * kSW32Rows));
   if (pair) CUDA_TRY(g.qp32b.ensure((size_t)kNL * P32max * 32 * kSW32Rows));
 

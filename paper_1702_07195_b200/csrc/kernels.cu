@@ -31,10 +31,6 @@
 #include <climits>
 #include <cstdio>
 
-// SW_SCSEP: 1 = lane G-1 stores the score chain only at separator columns.
-#ifndef SW_SCSEP
-#define SW_SCSEP 0
-#endif
 // SW_ROWAHEAD: 1 = biased rows form the next row's diagonal add before the
 // current row's H is overwritten (see the pass kernel); 0 = plain row order.
 #ifndef SW_ROWAHEAD
@@ -116,14 +112,10 @@ __device__ __forceinline__ void st_global_u32(uint32_t *p, uint32_t a) {
 }
 
 // Descriptor of a letter pair -> the column-chain words (see qp_build_kernel).
-struct DescWords { uint32_t w0, w1, ngoe, nge, kneg; };
+struct DescWords { uint32_t w0, ngoe, nge, kneg; };
 __device__ __forceinline__ DescWords load_desc(uint32_t addr) {
   const uint4 d = lds128(addr);
-#if SW_DESC32
-  return DescWords{d.x, d.y, d.z, d.w, lds128(addr + 16).x};
-#else
-  return DescWords{d.x, 0u, d.y, d.z, d.w};
-#endif
+  return DescWords{d.x, d.y, d.z, d.w};
 }
 
 template <class T>
@@ -158,7 +150,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   constexpr int KC = (R + RPC - 1) / RPC;   // chunks per lane
   constexpr int LS = KC * G * 16;           // bytes per letter in the profile slice
   constexpr int QP_U4 = kNL * LS / 16;
-  constexpr int DESC_U4 = kNL * kNL * kDescU4;
+  constexpr int DESC_U4 = kNL * kNL;
   extern __shared__ uint4 smem[];
   {
     const uint4 *gq = p.qp + (size_t)p.pass * QP_U4;
@@ -186,7 +178,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
   for (int r = 0; r < R; ++r) { H[r] = kB2; E[r] = kB2; }
   uint32_t S = 0u, hout = kB2, fout = kB2, sc = 0u, hprev = kB2;
-  uint32_t w0 = nul.w0, w1 = nul.w1;             // column chain (NUL): profile offsets
+  uint32_t w0 = nul.w0;                          // column chain (NUL): profile offsets
   uint32_t kneg = 0u;                            // S-reset value after the previous column
   uint32_t ngoe = nul.ngoe, nge = nul.nge, knext = nul.kneg;   // descriptor penalty words of the column chain
 
@@ -233,7 +225,6 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           }
           const DescWords d = load_desc(s_desc + __ldg(sptr));   // lane 0's first column
           w0 = d.w0;
-          w1 = d.w1;
           ngoe = d.ngoe;
           nge = d.nge;
           knext = d.kneg;
@@ -255,7 +246,6 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
           for (int u = 0; u < U; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(kB2, kB2); }
           w0 = nul.w0;
-          w1 = nul.w1;
           ngoe = nul.ngoe;
           nge = nul.nge;
           knext = nul.kneg;
@@ -271,9 +261,6 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
     for (int u = 0; u < U; ++u) {
       // ---- this column's inputs from lane t-1 (lane 0: from lane G-1)
       w0 = __shfl_sync(0xffffffffu, w0, src);
-#if SW_DESC32
-      w1 = __shfl_sync(0xffffffffu, w1, src);
-#endif
       ngoe = __shfl_sync(0xffffffffu, ngoe, src);
       nge = __shfl_sync(0xffffffffu, nge, src);
       knext = __shfl_sync(0xffffffffu, knext, src);
@@ -281,15 +268,10 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       uint32_t F = __shfl_sync(0xffffffffu, fout, src);
       const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
       // ---- profile addresses (FMA pipe)
-#if SW_DESC32
-      const uint32_t aA = imad(w0, one, s_qp);             // profile byte offsets, pre-split
-      const uint32_t aB = imad(w1, one, s_qp);
-#else
       const uint32_t offB = umulhi(w0, 65536u);           // profile offsets / 16
       const uint32_t offA = imad(offB, 0xffff0000u, w0);
       const uint32_t aA = imad(offA, 16u, s_qp);
       const uint32_t aB = imad(offB, 16u, s_qp);
-#endif
       // S is reset after every separator column (END: the score was just read
       // from the chain; NUL: S is already 0): -32768 in each separator half.
       const uint32_t kneg_prev = kneg;
@@ -411,14 +393,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       if (last) {
         const DescWords d = load_desc(s_desc + dnext);
         w0 = d.w0;
-        w1 = d.w1;
         ngoe = d.ngoe;
         nge = d.nge;
         knext = d.kneg;
       }
-      // SW_SCSEP: only separator columns' chain values are ever read (the
-      // gather reads END columns), so only those are stored
-      if (last && (!SW_SCSEP || kneg != 0u)) st_global_u32(scp + u, so);
+      if (last) st_global_u32(scp + u, so);
       if (bout) st_global_v2(bop + u, H[R - 1], F);
       // outgoing registers; lane G-1 hands over lane 0's next-column inputs
       hout = imad(H[R - 1], nlast, bnext.x);
@@ -631,12 +610,7 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
       const uint32_t wgoe = (sA ? 0x8001u : pgoe) | ((sB ? 0x8001u : pgoe) << 16);
       const uint32_t wge = (sA ? 0x8001u : pge) | ((sB ? 0x8001u : pge) << 16);
       const uint32_t wk = (sA ? 0x8000u : 0u) | ((sB ? 0x8000u : 0u) << 16);
-#if SW_DESC32
-      desc[2 * k] = make_uint4(offA * 16u, offB * 16u, wgoe, wge);
-      desc[2 * k + 1] = make_uint4(wk, 0u, 0u, 0u);
-#else
       desc[k] = make_uint4(offA | (offB << 16), wgoe, wge, wk);
-#endif
     } else {
       // s32 profile(s), pass-slice layout [pass][letter][4-row chunk][lane][4]
       const int64_t j = i - nq - ndesc;
@@ -783,7 +757,7 @@ using PassFn = void (*)(const SW16Params);
 
 template <int R, int G, int QPM>
 constexpr int smem_of() {
-  return (kNL * kNL * kDescU4 + kNL * ((R + 3) / 4) * G) * 16;
+  return (kNL * kNL + kNL * ((R + 3) / 4) * G) * 16;
 }
 
 struct TileEntry {
@@ -799,13 +773,7 @@ struct TileEntry {
 #define SW_UNROLL 4   // columns per unrolled block = lane G-1's prefetch distance
 #endif
 #define SW_TILE_NT(G_, R_, M_, NT_) SW_TILE_NTU(G_, R_, M_, NT_, SW_UNROLL)
-// SW_NTMODE (experiment): 0 = 512 threads (16 warps) for every tile; 1 = more
-// warps for the smaller R (768 threads up to R = 18, 640 up to R = 24).
-#ifndef SW_NTMODE
-#define SW_NTMODE 0
-#endif
-#define SW_NT_OF(R_) (SW_NTMODE == 1 ? ((R_) <= 18 ? 768 : (R_) <= 24 ? 640 : 512) : 512)
-#define SW_TILE(G_, R_, M_) SW_TILE_NT(G_, R_, M_, SW_NT_OF(R_))
+#define SW_TILE(G_, R_, M_) SW_TILE_NT(G_, R_, M_, 512)
 #define SW_TILES(M_)                                                                          \
   SW_TILE(8, 8, M_), SW_TILE(8, 12, M_), SW_TILE(8, 16, M_), SW_TILE(8, 18, M_),              \
   SW_TILE(8, 20, M_), SW_TILE(8, 22, M_), SW_TILE(8, 24, M_), SW_TILE(8, 26, M_),             \

@@ -20,13 +20,7 @@ constexpr int kAlpha = 24;
 constexpr int kEnd = 24;
 constexpr int kNul = 25;
 constexpr int kNL = 26;             // letters in the query profile / descriptor table
-// SW_DESC32 (experiment): 32-byte descriptors holding both profile byte
-// offsets pre-split (two words) instead of one packed word.
-#ifndef SW_DESC32
-#define SW_DESC32 0
-#endif
-constexpr int kDescBytes = SW_DESC32 ? 32 : 16;   // bytes per descriptor table entry
-constexpr int kDescU4 = kDescBytes / 16;          // uint4 per descriptor table entry
+constexpr int kDescBytes = 16;      // bytes per descriptor table entry
 constexpr int kColAlign = 4;        // item column counts are multiples of this
 // Columns of NUL padding after every item in the stream image (and before the
 // first): lets lane 0 prefetch past an item's end and lane G-1 store its
