@@ -305,8 +305,9 @@ def run_ours(args):
         step()
     stream.synchronize()
     st = sw.sw_last_stats()
-    # qp build, P x (pass kernel + score gather), flag compact, s32 re-score, top-k (2 + decode)
-    per_step_kernels = 1 + 2 * st["passes"] + 2 + 3
+    # qp build, P x (pass kernel + score gather + flag compaction + s32 re-scoring
+    # of that pass's newly flagged sequences), top-k (2 + decode)
+    per_step_kernels = 1 + 4 * st["passes"] + 3
     if dist:
         dist.barrier()
     torch.cuda.synchronize()

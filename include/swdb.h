@@ -193,7 +193,7 @@ int sw_last_stats(int64_t *stats, int n);
 /*
  * Device timing of the last search, from CUDA events recorded on the search
  * stream (synchronises with it):
- *   ms[0] = s16x2 pass kernels (start of the first pass .. end of the last),
+ *   ms[0] = s16x2 pass kernels (sum of the pass-kernel launches),
  *   ms[1] = whole search on the device (query-profile build .. end of the
  *           32-bit re-scoring kernel).
  * Returns the number of entries written (<= n) or a negative status.

@@ -97,7 +97,7 @@ struct State {
   DevBuf<int32_t> bscores;  // internal scores (sw_search_batch)
   DevBuf<uint8_t> flagged, flagged2;
   DevBuf<int32_t> flag_list, flag_list2;
-  DevBuf<int> counters;     // [kMaxPass..+3] flag counts / cursors
+  DevBuf<int> fcounters;    // 32-bit re-scoring: (count, cursor) per (pass, query of a pair)
   DevBuf<int> pcounters;    // per (chunk, pass) item cursors
   const uint8_t *res_dev = nullptr;  // residues for s32 re-scoring (device or mapped host)
   DevBuf<int64_t> cells32;
@@ -127,6 +127,8 @@ struct State {
   int force_G = 0, force_R = 0;
   // timing events of the last search
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> pev;   // (start, end) of every pass-kernel launch of the last search
+  int npev = 0;                   // pairs recorded by the last search
   // ---- streamed (out-of-core) database, SURVEY 8(f) NEXT-3
   struct Chunk {
     int item_begin, item_end;   // items [begin, end)
@@ -166,7 +168,7 @@ struct State {
     img[0].release(); img[1].release();
     sc_out.release(); res.release(); offs.release();
     scores.release(); bscores.release(); flagged.release(); flagged2.release(); flag_list.release();
-    flag_list2.release(); counters.release(); pcounters.release(); cells32.release();
+    flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release();
     query.release(); query2.release(); matrix.release(); qp.release(); desc.release(); qp32.release();
     qp32b.release(); bnd.release();
     scratch32.release(); dummy.release(); nulcols.release(); zerocols.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
@@ -264,7 +266,6 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int rows = T.G * T.R;
   const int P = (mm + rows - 1) / rows;
   if (P > kMaxPass) return fail(SW_EINVAL, "query too long");
-  const int P32max = (mm + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
   int smax = 1;
   for (int i = 0; i < kAlpha * kAlpha; ++i) smax = std::max(smax, (int)matrix[i]);
   const int thresh = 32768 - smax;   // stored 16-bit units (R7)
@@ -276,13 +277,16 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(g.matrix.ensure(kAlpha * kAlpha));
   CUDA_TRY(g.qp.ensure(qp_bytes(T.G, T.R, P, T.qpm)));
   CUDA_TRY(g.desc.ensure((size_t)kNL * kNL));
-  CUDA_TRY(g.qp32.ensure((size_t)kNL * P32max * 32 * kSW32Rows));
-  if (pair) CUDA_TRY(g.qp32b.ensure((size_t)kNL * P32max * 32 * kSW32Rows));
+  CUDA_TRY(g.qp32.ensure((size_t)kNL * mm));
+  if (pair) CUDA_TRY(g.qp32b.ensure((size_t)kNL * mm));
 
   CUDA_TRY(cudaMemcpyAsync(g.query.p, q, (size_t)m, cudaMemcpyHostToDevice, st));
   if (pair) CUDA_TRY(cudaMemcpyAsync(g.query2.p, q2, (size_t)m2, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(g.matrix.p, matrix, kAlpha * kAlpha, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemsetAsync(g.counters.p, 0, sizeof(int) * (kMaxPass + 4), st));
+  // 32-bit re-scoring counters: (count, cursor) per (pass, query of the pair),
+  // plus one set for the end-of-search launch
+  CUDA_TRY(g.fcounters.ensure((size_t)4 * (P + 1)));
+  CUDA_TRY(cudaMemsetAsync(g.fcounters.p, 0, sizeof(int) * 4 * (P + 1), st));
   CUDA_TRY(cudaMemsetAsync(g.flagged.p, 0, (size_t)g.count, st));
   if (pair) CUDA_TRY(cudaMemsetAsync(g.flagged2.p, 0, (size_t)g.count, st));
   CUDA_TRY(cudaMemsetAsync(g.cells32.p, 0, sizeof(int64_t), st));
@@ -294,6 +298,46 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
                            goe, ge, st));
 
   const int grid = g.num_sms * std::max(1, tile_ctas_per_sm(ti));
+  // Exact s32 re-scoring ("recalculated using the next wider
+  // integer range").  Resident database: right after the gather of pass p, the
+  // sequences first flagged in pass p are re-scored from row p*rows on, seeded
+  // with that pass's input boundary (exact: no earlier pass flagged them) and
+  // with the exact maximum of the earlier passes.  Streamed database: once at
+  // the end, from row 0.
+  // The flag byte is min(pass + 1, 255): passes >= 254 share the value 255 and
+  // are re-scored at the end, from row 0.
+  auto rescore = [&](int k, int pass, const uint2 *bnd16) -> cudaError_t {
+    const bool early = pass >= 0 && pass + 1 < 255;
+    const int slot = early ? pass : P;
+    int *cnt = g.fcounters.p + 4 * slot + 2 * k;
+    const int row0 = early ? pass * rows : 0;
+    const int want = pass < 0 ? 0 : (early ? pass + 1 : 255);
+    const int len = k ? m2 : m;
+    cudaError_t e = launch_flag_compact(k ? g.flagged2.p : g.flagged.p, g.count, k ? g.flag_list2.p : g.flag_list.p,
+                                        cnt, want, st);
+    if (e != cudaSuccess || row0 >= len) return e;
+    SW32Params q;
+    q.flag_list = k ? g.flag_list2.p : g.flag_list.p;
+    q.flag_count = cnt;
+    q.cursor = cnt + 1;
+    q.res = g.res_dev;
+    q.offs = g.offs.p;
+    q.qp32 = k ? g.qp32b.p : g.qp32.p;
+    q.m = mm;
+    q.row0 = row0;
+    q.passes = (len - row0 + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
+    q.neg_goe = -goe;
+    q.neg_ge = -ge;
+    q.bnd16 = row0 > 0 ? bnd16 : nullptr;
+    q.endcol = I.endcol.p;
+    q.half = pair ? k : -1;
+    q.scratch = g.scratch32.p;
+    q.stride = g.scratch_stride;
+    q.scores = k ? d_scores2 : d_scores;
+    q.cells = g.cells32.p;
+    q.one = 1u;
+    return launch_sw32(g.sw32_grid, q, st);
+  };
   // resident database: one "chunk" (the whole image); streamed database: the
   // image's chunks are copied host->device on copy_st into two buffers,
   // overlapping the passes of the previous chunk
@@ -343,7 +387,16 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       p.thresh = thresh;
       p.zero = 0u;
       p.one = 1u;
+      const size_t pe = 2 * (size_t)(k * P + pass);
+      while (g.pev.size() < pe + 2) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        g.pev.push_back(e);
+      }
+      CUDA_TRY(cudaEventRecord(g.pev[pe], st));
       CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
+      CUDA_TRY(cudaEventRecord(g.pev[pe + 1], st));
+      g.npev = (int)(pe / 2) + 1;
       if (strm) {
         const State::Chunk &c = g.chunks[k];
         CUDA_TRY(launch_sw16_gather(g.cseq_endcol.p + c.seq_begin, c.seq_end - c.seq_begin, g.sc_out.p - base,
@@ -352,32 +405,15 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       } else {
         CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p,
                                     pair ? d_scores2 : nullptr, pair ? g.flagged2.p : nullptr, pass, thresh, st));
+        if (pass + 1 < 255)
+          for (int k = 0; k < (pair ? 2 : 1); ++k) CUDA_TRY(rescore(k, pass, p.bnd_in));
       }
     }
     if (strm) CUDA_TRY(cudaEventRecord(g.ev_free[b], st));
   }
   CUDA_TRY(cudaEventRecord(g.ev[2], st));
-  // exact s32 re-scoring of every sequence whose 16-bit score saturated
-  for (int k = 0; k < (pair ? 2 : 1); ++k) {
-    CUDA_TRY(launch_flag_compact(k ? g.flagged2.p : g.flagged.p, g.count, k ? g.flag_list2.p : g.flag_list.p,
-                                 g.counters.p + kMaxPass + 2 * k, st));
-    SW32Params q;
-    q.flag_list = k ? g.flag_list2.p : g.flag_list.p;
-    q.flag_count = g.counters.p + kMaxPass + 2 * k;
-    q.cursor = g.counters.p + kMaxPass + 2 * k + 1;
-    q.res = g.res_dev;
-    q.offs = g.offs.p;
-    q.qp32 = k ? g.qp32b.p : g.qp32.p;
-    q.passes = ((k ? m2 : m) + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
-    q.neg_goe = -goe;
-    q.neg_ge = -ge;
-    q.scratch = g.scratch32.p;
-    q.stride = g.scratch_stride;
-    q.scores = k ? d_scores2 : d_scores;
-    q.cells = g.cells32.p;
-    q.one = 1u;
-    CUDA_TRY(launch_sw32(g.sw32_grid, q, st));
-  }
+  if (strm || P >= 255)
+    for (int k = 0; k < (pair ? 2 : 1); ++k) CUDA_TRY(rescore(k, strm ? -1 : 254, nullptr));
   CUDA_TRY(cudaEventRecord(g.ev[3], st));
 
   g.has_search = true;
@@ -590,7 +626,6 @@ int load_impl(const uint8_t *residues, const int64_t *offsets, int64_t count, in
   CUDA_TRY(g.flagged2.ensure((size_t)count));
   CUDA_TRY(g.flag_list.ensure((size_t)count));
   CUDA_TRY(g.flag_list2.ensure((size_t)count));
-  CUDA_TRY(g.counters.ensure(kMaxPass + 4));
   CUDA_TRY(g.cells32.ensure(1));
   CUDA_TRY(g.dummy.ensure((size_t)nsm * 4 * 1024));   // one 16-B slot per resident thread
   {
@@ -708,10 +743,9 @@ int sw_last_stats(int64_t *stats, int n) {
     int fc = 0;
     int64_t cells = 0;
     CUDA_TRY(cudaStreamSynchronize(g.last_stream));
-    int fc2 = 0;
-    CUDA_TRY(cudaMemcpy(&fc, g.counters.p + kMaxPass, sizeof(int), cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(&fc2, g.counters.p + kMaxPass + 2, sizeof(int), cudaMemcpyDeviceToHost));
-    fc += fc2;
+    std::vector<int> fcs((size_t)4 * (g.last_P + 1));
+    CUDA_TRY(cudaMemcpy(fcs.data(), g.fcounters.p, fcs.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < fcs.size(); i += 2) fc += fcs[i];
     CUDA_TRY(cudaMemcpy(&cells, g.cells32.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
     g.last_flags = fc;
     g.last_cells32 = cells;
@@ -730,7 +764,11 @@ int sw_last_timing(float *ms, int n) {
   if (!g.has_search || !g.ev[0]) return fail(SW_ESTATE, "no completed search");
   CUDA_TRY(cudaEventSynchronize(g.ev[3]));
   float a = 0.f, b = 0.f;
-  CUDA_TRY(cudaEventElapsedTime(&a, g.ev[1], g.ev[2]));
+  for (int i = 0; i < g.npev; ++i) {   // sum of the pass-kernel launches only
+    float x = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&x, g.pev[2 * i], g.pev[2 * i + 1]));
+    a += x;
+  }
   CUDA_TRY(cudaEventElapsedTime(&b, g.ev[0], g.ev[3]));
   const float v[2] = {a, b};
   const int m = std::min(n, 2);

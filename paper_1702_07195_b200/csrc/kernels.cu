@@ -430,13 +430,17 @@ __global__ void sw16_gather_kernel(const int64_t *__restrict__ endcol, int64_t c
     const int64_t o = seq_idx ? (int64_t)seq_idx[i] : i;
     const int64_t e = endcol[i];
     const uint32_t w = sc_out[e >> 1];
-    const int v = (int)((!scores2 && (e & 1)) ? (w >> 16) : (w & 0xffffu));
-    scores[o] = max(pass == 0 ? 0 : scores[o], v - kBias16);
-    if (v >= thresh) flagged[o] = 1;
-    if (scores2) {
+    // once flagged, the 32-bit kernel owns the score (started from the last
+    // exact pass boundary, or from row 0)
+    if (flagged[o] == 0) {
+      const int v = (int)((!scores2 && (e & 1)) ? (w >> 16) : (w & 0xffffu));
+      if (v >= thresh) flagged[o] = (uint8_t)min(pass + 1, 255);
+      else scores[o] = max(pass == 0 ? 0 : scores[o], v - kBias16);
+    }
+    if (scores2 && flagged2[o] == 0) {
       const int v2 = (int)(w >> 16);
-      scores2[o] = max(pass == 0 ? 0 : scores2[o], v2 - kBias16);
-      if (v2 >= thresh) flagged2[o] = 1;
+      if (v2 >= thresh) flagged2[o] = (uint8_t)min(pass + 1, 255);
+      else scores2[o] = max(pass == 0 ? 0 : scores2[o], v2 - kBias16);
     }
   }
 }
@@ -483,14 +487,31 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
       n = (int)(p.offs[orig + 1] - b);
       res = p.res + b;
     }
+    // rows < row0 were exact in 16 bit: their maximum is already in scores,
+    // and the 16-bit pass boundary of row row0-1 seeds the first pass below
     int best = 0;
+    int64_t col0 = 0;
+    int half = 0;
+    if (active && p.row0 > 0) {
+      best = p.scores[orig];
+      const int64_t e = p.endcol[orig];
+      col0 = (e >> 1) - n;                   // the sequence's first stream column
+      half = p.half >= 0 ? p.half : (int)(e & 1);
+    }
     for (int pass = 0; pass < p.passes; ++pass) {
       __syncthreads();
-      const uint4 *g = reinterpret_cast<const uint4 *>(p.qp32) + (size_t)pass * SLICE_U4;
-      for (int i = threadIdx.x; i < SLICE_U4; i += blockDim.x) sq[i] = g[i];
+      // stage this pass's profile slice [letter][4-row chunk][lane][4] from the
+      // plain [letter][m] profile, rows row0 + pass*32*R ...
+      for (int i = threadIdx.x; i < SLICE_U4 * 4; i += blockDim.x) {
+        const int e4 = i & 3, ln = (i >> 2) & 31, rest = i >> 7;
+        const int kk = rest % K4, c = rest / K4;
+        const int row = p.row0 + pass * 32 * R + ln * R + kk * 4 + e4;
+        reinterpret_cast<int32_t *>(sq)[i] = row < p.m ? p.qp32[(int64_t)c * p.m + row] : -(1 << 30);
+      }
       __syncthreads();
       if (!active) continue;
       const uint2 *bin = pass == 0 ? nullptr : ((pass & 1) ? buf0 : buf1);
+      const uint2 *b16 = (pass == 0 && p.row0 > 0) ? p.bnd16 + col0 : nullptr;
       uint2 *bout = pass == p.passes - 1 ? nullptr : ((pass & 1) ? buf1 : buf0);
       int H[R], E[R];
 #pragma unroll
@@ -512,6 +533,11 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
             const uint2 b = bin[c];
             bh = (int)b.x;
             bf = (int)b.y;
+          }
+          if (first && b16 && c < n) {       // exact 16-bit boundary, unbiased
+            const uint2 b = b16[c];
+            bh = (int)((b.x >> (16 * half)) & 0xffffu) - kBias16;
+            bf = (int)((b.y >> (16 * half)) & 0xffffu) - kBias16;
           }
           code = first ? cring[u] : code_up;
           if (first) cring[u] = (c + 4 < n) ? (int)res[c + 4] : kNul;
@@ -566,15 +592,14 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
 __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint8_t *__restrict__ q2, int m2,
                                 const int8_t *__restrict__ M, int G, int R, int P, uint32_t *qp, uint4 *desc,
                                 int32_t *qp32, int32_t *qp32b, int goe, int ge) {
-  // q2 == nullptr: one query; profile word = zero-extended int16 (QPM 0).
-  // q2 != nullptr: query pair; profile word = (SM[q_r][c], SM[q2_r][c]) (QPM 3).
+  // q2 == nullptr: one query (QPM 0); q2 != nullptr: query pair (QPM 3).  See
+  // the profile-mode notes above the pass kernel for the word formats.
   const int KC = (R + 3) / 4;
   const int LS = KC * G * 16;
   const int mm = q2 ? max(m, m2) : m;
-  const int P32 = (mm + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
   const int64_t nq = (int64_t)P * kNL * KC * G * 4;
   const int64_t ndesc = kNL * kNL;
-  const int64_t n32 = (int64_t)kNL * P32 * 32 * kSW32Rows;
+  const int64_t n32 = (int64_t)kNL * mm;   // plain s32 profile(s)
   const int64_t total = nq + ndesc + n32;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -612,15 +637,9 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
       const uint32_t wk = (sA ? 0x8000u : 0u) | ((sB ? 0x8000u : 0u) << 16);
       desc[k] = make_uint4(offA | (offB << 16), wgoe, wge, wk);
     } else {
-      // s32 profile(s), pass-slice layout [pass][letter][4-row chunk][lane][4]
+      // s32 profile(s), plain [letter][m] (the 32-bit kernel stages its slices)
       const int64_t j = i - nq - ndesc;
-      int64_t rest = j;
-      const int e = (int)(rest & 3); rest >>= 2;
-      const int ln = (int)(rest & 31); rest >>= 5;
-      const int kk = (int)(rest % (kSW32Rows / 4)); rest /= (kSW32Rows / 4);
-      const int c = (int)(rest % kNL);
-      const int pass = (int)(rest / kNL);
-      const int row = pass * 32 * kSW32Rows + ln * kSW32Rows + kk * 4 + e;
+      const int c = (int)(j / mm), row = (int)(j % mm);
       qp32[j] = (row < m && c < kAlpha) ? (int32_t)M[q[row] * kAlpha + c] : -(1 << 30);
       if (q2) qp32b[j] = (row < m2 && c < kAlpha) ? (int32_t)M[q2[row] * kAlpha + c] : -(1 << 30);
     }
@@ -628,11 +647,11 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
 }
 
 __global__ void flag_compact_kernel(const uint8_t *__restrict__ flagged, int64_t count, int32_t *list,
-                                    int *n) {
+                                    int *n, int want) {
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < count;
        base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
-    const bool f = i < count && flagged[i];
+    const bool f = i < count && (want ? flagged[i] == want : flagged[i] != 0);
     const unsigned bal = __ballot_sync(0xffffffffu, f);
     if (bal) {
       const int lane = threadIdx.x & 31;
@@ -891,8 +910,7 @@ cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_quer
                             int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
                             int goe, int ge, cudaStream_t st) {
   const int mm = d_query2 ? (m > m2 ? m : m2) : m;
-  const int P32 = (mm + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
-  const int64_t total = (int64_t)P * kNL * ((R + 3) / 4) * G * 4 + kNL * kNL + (int64_t)kNL * P32 * 32 * kSW32Rows;
+  const int64_t total = (int64_t)P * kNL * ((R + 3) / 4) * G * 4 + kNL * kNL + (int64_t)kNL * mm;
   qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_query2, m2, d_matrix, G, R, P,
                                                          reinterpret_cast<uint32_t *>(d_qp), d_desc, d_qp32,
                                                          d_qp32b, goe, ge);
@@ -914,8 +932,9 @@ cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint3
   return cudaGetLastError();
 }
 
-cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n, cudaStream_t st) {
-  flag_compact_kernel<<<grid_for(count, 256), 256, 0, st>>>(flagged, count, list, n);
+cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n, int want,
+                                cudaStream_t st) {
+  flag_compact_kernel<<<grid_for(count, 256), 256, 0, st>>>(flagged, count, list, n, want);
   return cudaGetLastError();
 }
 

@@ -49,12 +49,20 @@ struct SW32Params {
   int *cursor;
   const uint8_t *res;       // plain database, original order
   const int64_t *offs;
-  const int32_t *qp32;      // [pass][kNL][kSW32Rows/4][32 lanes][4] int32
-  int passes;
+  const int32_t *qp32;      // plain int32 profile [kNL][m] (-2^30 for separator letters)
+  int m;                    // query length (rows of qp32)
+  int row0;                 // first query row to compute (rows < row0 were exact in 16 bit)
+  int passes;               // ceil((m - row0) / (32 * R))
   int neg_goe, neg_ge;      // -(open+extend), -extend  (>= -2^30)
+  // row0 > 0: the exact 16-bit boundary (H, F) of row row0-1, per stream column
+  // (pass output of the 16-bit kernel, stored + kBias16 per half), located by
+  // endcol (2 * END column + half) and read from half `half` (< 0: endcol's own)
+  const uint2 *bnd16;
+  const int64_t *endcol;
+  int half;
   uint2 *scratch;           // per warp: 2 * stride
   int64_t stride;           // >= max_len + 64
-  int32_t *scores;
+  int32_t *scores;          // row0 > 0: holds the exact max over rows < row0 on entry
   int64_t *cells;           // re-scored cells (statistics), may be null
   uint32_t one;             // 1 (keeps the diagonal add on the FMA pipe)
 };
@@ -90,7 +98,11 @@ cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint3
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
                                cudaStream_t st, const int32_t *seq_idx = nullptr);
 // thresh: in stored 16-bit units (32768 - smax); scores are stored - kBias16.
-cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n,
+// A sequence already flagged is skipped; one flagged in this pass gets
+// flagged = pass + 1 and keeps in scores the exact maximum of the earlier passes
+// (pass 0: not written) -- the 32-bit kernel owns its score from then on.
+// Compacts the indices i with flagged[i] == want (want == 0: any non-zero).
+cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n, int want,
                                 cudaStream_t st);
 constexpr int kSW32Rows = 16;         // rows per lane of the 32-bit kernel
 constexpr int kSW32Threads = 256;
