@@ -104,7 +104,10 @@ cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint3
 // Compacts the indices i with flagged[i] == want (want == 0: any non-zero).
 cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n, int want,
                                 cudaStream_t st);
-constexpr int kSW32Rows = 16;         // rows per lane of the 32-bit kernel
+#ifndef SW_S32ROWS
+#define SW_S32ROWS 24
+#endif
+constexpr int kSW32Rows = SW_S32ROWS;  // rows per lane of the 32-bit kernel
 constexpr int kSW32Threads = 256;
 cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st);
 
