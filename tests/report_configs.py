@@ -1,7 +1,7 @@
 """Run BASELINE.json configurations on one GPU: device GCUPS per query, flag
 statistics and a sampled oracle parity check (dev / report tool).
 
-    python tools/run_configs.py 0 1 2 3 4 [--scale S] [--sample N] [--reps K]
+    python tests/report_configs.py 0 1 2 3 4 [--scale S] [--sample N] [--reps K]
 
 Prints one JSON line per (config, query).
 """

@@ -3,7 +3,7 @@ CUDA path (through the C-ABI, default tile choice = the bench's launch
 configuration) against the CPU oracle on the whole database, plus the top-10
 (report tool; the pytest suite samples instead because this takes minutes).
 
-    python tools/exhaustive_parity.py [--configs 0,1,2,4] [--cfg3-queries 0,1] [--streamed]
+    python tests/report_exhaustive_parity.py [--configs 0,1,2,4] [--cfg3-queries 0,1] [--streamed]
 
 Prints one JSON line per (config, query, path) with the mismatch count and the
 oracle's own full-database time and GCUPS on this host.

@@ -12,4 +12,4 @@ timeout 300 $CMD > gpurun_out/fm_plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/fm_launches.csv $CMD > gpurun_out/fm_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sw16_pass -s 4 -c 1 -o gpurun_out/fm_prof_bench $CMD > gpurun_out/fm_ncu_full.log 2>&1
 tail -2 gpurun_out/fm_ncu_full.log
-timeout 1500 python tools/run_configs.py 0 1 2 4 > gpurun_out/fm_configs.jsonl 2> gpurun_out/fm_configs.err; cat gpurun_out/fm_configs.jsonl; tail -3 gpurun_out/fm_configs.err
+timeout 1500 python tests/report_configs.py 0 1 2 4 > gpurun_out/fm_configs.jsonl 2> gpurun_out/fm_configs.err; cat gpurun_out/fm_configs.jsonl; tail -3 gpurun_out/fm_configs.err
