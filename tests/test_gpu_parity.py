@@ -138,6 +138,32 @@ def test_saturation_boundary_and_rescoring():
     assert st["flagged"] == sum(1 for n in ns if 11 * n >= T)
 
 
+def test_rescoring_seeded_from_pass_boundaries():
+    """Sequences flagged in a later 16-bit pass are re-scored in 32 bit from that
+    pass's first row, seeded with its exact input boundary.  A
+    prefix of A rows before W^3000 moves the flagging pass; small tiles (64 rows
+    per pass) make the 16-bit pass boundaries cut the 32-bit kernel's slices at
+    many different offsets."""
+    rng = np.random.default_rng(31)
+    seqs = [encode("W" * n) for n in (1400, 1489, 1600, 2500, 3000)]
+    seqs += [np.concatenate([si.rr_residues(rng, 300), encode("W" * 2000), si.rr_residues(rng, 200)])]
+    seqs += [si.rr_residues(rng, int(L)) for L in rng.integers(1, 800, 40)]
+    db = _db(seqs)
+    sw.sw_db_load(db.residues, db.offsets)
+    try:
+        for x in (0, 37, 700, 1501):
+            q = encode("A" * x + "W" * 3000)
+            exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
+            for G, R in ((0, 0), (8, 8), (16, 12), (32, 29)):
+                sw.sw_set_tile(G, R)
+                got = sw.sw_search(q, BLOSUM62, 10, 2)
+                st = sw.sw_last_stats()
+                assert (got == exp).all(), (x, G, R, np.nonzero(got != exp)[0][:5])
+                assert st["flagged"] == int((exp >= st["flag_threshold"]).sum())
+    finally:
+        sw.sw_set_tile(0)
+
+
 def test_adversarial_mixed_with_planted_copies():
     w = si.config4(scale=0.002)   # 400 sequences incl. long ones and 8 planted copies
     got = _check_db(w.db, w.queries[0], label="cfg4 small")
