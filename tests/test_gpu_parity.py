@@ -97,6 +97,34 @@ def test_extreme_scoring_parameters():
         assert (got[k] == exp).all(), k
 
 
+def test_degenerate_databases_and_queries():
+    """Edge cases of the method: only empty sequences, a single residue, a query of
+    length 1, many one-residue sequences, identical sequences (ties in the sorting
+    stage), and a database whose total length is odd (an empty B half)."""
+    rng = np.random.default_rng(77)
+    cases = [
+        [np.zeros(0, np.uint8)],
+        [np.zeros(0, np.uint8)] * 5,
+        [encode("W")],
+        [encode("W"), np.zeros(0, np.uint8), encode("A")],
+        [si.rr_residues(rng, 1) for _ in range(257)],
+        [encode("MKVLAAGW")] * 33,
+        [si.rr_residues(rng, int(L)) for L in (1, 2, 3, 5000, 7)],
+    ]
+    queries = [encode("W"), encode("A"), si.rr_residues(rng, 2), si.rr_residues(rng, 700)]
+    for ci, seqs in enumerate(cases):
+        db = _db(seqs)
+        sw.sw_db_load(db.residues, db.offsets)
+        for q in queries:
+            got = sw.sw_search(q, BLOSUM62, 10, 2)
+            exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
+            assert (got == exp).all(), (ci, len(q), got[:8], exp[:8])
+            k = min(10, len(seqs))
+            idx, sc = sw.sw_topk(k)
+            eidx, esc = oracle.topk(exp, k)
+            assert (idx == eidx).all() and (sc == esc).all(), (ci, len(q))
+
+
 def test_every_tile_is_exact():
     rng = np.random.default_rng(7)
     seqs = [si.rr_residues(rng, int(L)) for L in rng.integers(1, 500, 300)]
