@@ -34,9 +34,9 @@
   fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
 
 constexpr int ITERS = 1024;
-enum Var { DPX, HA, HB, HBF, MIX, HB_I, HBF_I, MIX_I, HA_I, HAINT, HAINT_T, HA_I_T, HC, HMIX2, HMIX3, SPV, NUM_VARS };
+enum Var { DPX, HA, HB, HBF, MIX, HB_I, HBF_I, MIX_I, HA_I, HAINT, HAINT_T, HA_I_T, HC, HMIX2, HMIX3, SPV, HAI16, NUM_VARS };
 static const char *kNames[] = {"dpx", "hybA_biased", "hybB_fp16", "hybB_fp16_fmarelu", "mix_AB_biased",
-                               "hybB_fp16_imm", "hybB_fp16_fmarelu_imm", "mix_AB_biased_imm", "hybA_biased_imm", "hybA_int_imad", "hybA_int_imad_Stree", "hybA_biased_imm_Stree", "hybC_int_fmaroute", "hybAC_mix_1to1", "hybAC_mix_2to1", "score_profile_SP"};
+                               "hybB_fp16_imm", "hybB_fp16_fmarelu_imm", "mix_AB_biased_imm", "hybA_biased_imm", "hybA_int_imad", "hybA_int_imad_Stree", "hybA_biased_imm_Stree", "hybC_int_fmaroute", "hybAC_mix_1to1", "hybAC_mix_2to1", "score_profile_SP", "hybA_int_profile16"};
 
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -111,6 +111,39 @@ __global__ void __launch_bounds__(256, (R <= 8 ? 4 : 2)) bench(const uint32_t *_
         const uint32_t hg = __viaddmax_s16x2(h, ngoe, 0x40004000u);
         E[r] = __viaddmax_s16x2(E[r], nge, hg);
         F = __viaddmax_s16x2(F, nge, hg);
+      }
+#pragma unroll
+      for (int r = 0; r < R; r += 2) S = __vimax3_s16x2(S, H[r], H[r + 1]);
+      b ^= F;
+      c += S;
+      continue;
+    }
+    if constexpr (VAR == HAI16) {
+      // int16 query profile: one LDS.128 holds 8 rows of a letter (half the
+      // shared-memory bytes of the 32-bit-word profile); the packed words are
+      // rebuilt on the FMA pipe: 5 IMAD per 2 rows (+ the 2 diagonal adds)
+      const uint32_t la16 = sbase + ((it * 7) & 7) * (R / 8) * 512;
+      const uint32_t lb16 = sbase + ((it * 13) & 7) * (R / 8) * 512;
+#pragma unroll
+      for (int k = 0; k < R / 8; ++k) {
+        const uint4 a4 = lds128(la16 + k * 512), b4 = lds128(lb16 + k * 512);
+        const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w}, bw[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t hiA = (uint32_t)__mulhi((int)aw[j], 65536);          // sext(a[r+1])
+          const uint32_t loA = imad(hiA, 0xffff0000u, aw[j]);                 // sext(a[r])
+          const uint32_t hiB = (uint32_t)__mulhi((int)bw[j], 65536);
+          const uint32_t P0 = imad(bw[j], 65536u, loA), P1 = imad(hiB, 65536u, hiA);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = k * 8 + j * 2 + e;
+            uint32_t h = __vimax3_s16x2(imad(hd, one_p, e ? P1 : P0), E[r], F);
+            hd = H[r]; H[r] = h;
+            const uint32_t hg = __viaddmax_s16x2(h, ngoe, 0x40004000u);
+            E[r] = __viaddmax_s16x2(E[r], nge, hg);
+            F = __viaddmax_s16x2(F, nge, hg);
+          }
+        }
       }
 #pragma unroll
       for (int r = 0; r < R; r += 2) S = __vimax3_s16x2(S, H[r], H[r + 1]);
@@ -315,6 +348,7 @@ void run_all(int nsm, uint32_t *d_in, uint32_t *d_out, long long *d_cyc, int bps
     run<HMIX2, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
     run<HMIX3, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
     run<SPV, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
+    if constexpr (R % 8 == 0) run<HAI16, R, LDS>(nsm, bps, d_in, d_out, d_cyc);
   }
 }
 
