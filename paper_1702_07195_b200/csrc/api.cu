@@ -18,6 +18,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kernels.cuh"
@@ -515,13 +516,27 @@ int load_impl(const uint8_t *residues, const int64_t *offsets, int64_t count, in
   const int64_t target_groups = (int64_t)nsm * 16 * 2;
   HostImage himg[2];
   const int nimg = strm ? 1 : 2;
-  try {
+  // the two images are independent: build them on two host threads
+  {
+    std::string errs[2];
+    int rcs[2] = {0, 0};
+    auto build_one = [&](int k) {
+      try {
+        rcs[k] = build_image(residues, offsets, count, target_groups, k == 1, himg[k], errs[k]) ? SW_EINVAL : 0;
+      } catch (const std::bad_alloc &) {
+        rcs[k] = SW_ENOMEM;
+        errs[k] = "host allocation failed in the pre-processor";
+      } catch (const std::exception &e) {
+        rcs[k] = SW_EINVAL;
+        errs[k] = e.what();
+      }
+    };
+    std::thread second;
+    if (nimg == 2) second = std::thread(build_one, 1);
+    build_one(0);
+    if (second.joinable()) second.join();
     for (int k = 0; k < nimg; ++k)
-      if (build_image(residues, offsets, count, target_groups, k == 1, himg[k], err)) return fail(SW_EINVAL, err);
-  } catch (const std::bad_alloc &) {
-    return fail(SW_ENOMEM, "host allocation failed in the pre-processor");
-  } catch (const std::exception &e) {
-    return fail(SW_EINVAL, e.what());
+      if (rcs[k]) return fail(rcs[k], errs[k]);
   }
   for (int k = 0; k < nimg; ++k)
     if (himg[k].items.size() >= (size_t)INT_MAX) return fail(SW_EINVAL, "too many work items");

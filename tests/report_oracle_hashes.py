@@ -27,7 +27,8 @@ import numpy as np  # noqa: E402
 import oracle  # noqa: E402
 import sw_inputs as si  # noqa: E402
 
-OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "oracle_full_scores.jsonl")
+GOLDEN_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "oracle_full_scores.jsonl")
+OUT = GOLDEN_PATH
 
 
 def fingerprint(w) -> str:
@@ -60,9 +61,11 @@ def main():
     args = ap.parse_args()
     out = args.out
     qsel = None
-    if args.queries:
-        a, b = (int(x) for x in args.queries.split("-"))
-        qsel = set(range(a, b + 1))
+    if args.queries:   # e.g. "17-19,7-9"
+        qsel = set()
+        for part in args.queries.split(","):
+            a, _, b = part.partition("-")
+            qsel.update(range(int(a), int(b or a) + 1))
     done = set()
     if os.path.exists(out):
         for ln in open(out):

@@ -365,3 +365,41 @@ def test_streamed_database_matches_resident_and_oracle():
     assert sw.sw_db_chunks() == 0
     assert (sw.sw_search(queries[1], BLOSUM62, 10, 2) ==
             oracle.batch(queries[1], db.residues, db.offsets, BLOSUM62, 10, 2)).all()
+
+
+def test_shard_count_invariance_sequential_shards():
+    """Multi-GPU without a multi-GPU box (SPEC.md:409 analogue): the
+    database is residue-balanced into G shards (parallel.shard_database), each
+    shard is loaded and searched in turn on this GPU with the real kernels, the
+    per-shard scores are scattered back to original order and the per-shard
+    top-10 candidates merged with sw_topk_dev -- the exact host logic of the
+    NCCL path.  Scores and top-10 must be identical for G = 1, 2, 4, 8."""
+    import torch
+    from paper_1702_07195_b200.parallel import assemble_scores, shard_arrays, shard_database
+    w = si.config4(scale=0.002)            # long tail + planted (flagged) copies
+    q = w.queries[0]
+    exp = oracle.batch(q, w.db.residues, w.db.offsets, BLOSUM62, 10, 2)
+    eidx, esc = oracle.topk(exp, 10)
+    for G in (1, 2, 4, 8):
+        shards = shard_database(w.db.lengths(), G)
+        parts, cand_i, cand_s = [], [], []
+        for idx in shards:
+            res, offs = shard_arrays(w.db.residues, w.db.offsets, idx)
+            sw.sw_db_load(res, offs)
+            sc = sw.sw_search(q, BLOSUM62, 10, 2)
+            parts.append(sc)
+            d_sc = torch.from_numpy(sc).cuda()
+            d_gi = torch.from_numpy(idx.astype(np.int64)).cuda()
+            ti = torch.empty(10, dtype=torch.int64, device="cuda")
+            ts = torch.empty(10, dtype=torch.int32, device="cuda")
+            n = sw.sw_topk_dev(d_sc, d_gi, sc.size, 10, ti, ts)
+            cand_i.append(ti[:n])
+            cand_s.append(ts[:n])
+        got = assemble_scores(parts, shards, w.db.count)
+        assert (got == exp).all(), G
+        ci, cs = torch.cat(cand_i), torch.cat(cand_s)
+        mi = torch.empty(10, dtype=torch.int64, device="cuda")
+        ms = torch.empty(10, dtype=torch.int32, device="cuda")
+        sw.sw_topk_dev(cs, ci, cs.numel(), 10, mi, ms)
+        assert mi.tolist() == eidx.tolist() and ms.tolist() == esc.tolist(), G
+
