@@ -1,31 +1,33 @@
 // sm_100a kernels of the inter-task Smith-Waterman database search.
 //
 // The recurrence (Eqs. 1-3), per cell (i = query row, j =
-// database column), in the equivalent relu form (readings R2, R6):
+// database column), in the equivalent relu form (readings R2, R3):
 //   H_ij = max{0, H_{i-1,j-1} + SM(q_i, d_j), E_ij, F_ij}
 //   E_{i,j+1} = max{E_ij - Ge, max(H_ij - Goe, 0)}
 //   F_{i+1,j} = max{F_ij - Ge, max(H_ij - Goe, 0)}
 //   S = max over all H_ij
 // is evaluated on packed s16x2 registers: each 32-bit value holds the same
 // cell of two different database sequences ("halves" A and B, inter-task
-// parallelism), with the Blackwell DPX instructions
-// VIADDMNMX.S16x2(.RELU) / VIMNMX.S16x2 / VIMNMX3.S16x2 -- 5.5 DPX per pair of
-// cells.  DPX adds wrap instead of saturating (R7): a sequence whose
-// 16-bit score reaches T = 32768 - smax is flagged and re-scored exactly by
-// the s32 kernel ("recalculated using the next wider integer
-// range").
+// parallelism), or of two queries (query pairs).  Default
+// arithmetic (SW_ARITH=1, kernels.cuh): every value is stored
+// + 16384 per half, so H_diag + SM is one 32-bit IMAD on the FMA pipe and
+// Eq. 1 one VIMNMX3 -- 4.5 Blackwell DPX instructions (VIMNMX3.S16x2 +
+// 3 VIADDMNMX.S16x2 + 1/2 VIMNMX3 for S) and 2 IMADs per pair of cells.  DPX
+// adds wrap instead of saturating (R7): a sequence whose stored
+// 16-bit score reaches 32768 - smax is flagged and re-scored exactly by the
+// s32 kernel ("recalculated using the next wider integer range"),
+// starting from the last exact 16-bit pass boundary.
 //
-// Mapping: a *group* of G lanes (G in 8/16/32)
-// is a systolic array over the query: lane t owns R consecutive query rows
-// of the current pass, keeps H and E of its rows in registers, and passes the
-// bottom-row (H, F), the column word and the running score chain to lane t+1
-// with one SHFL each per column.  A group streams one work item (two lane
+// Mapping: a *group* of G lanes (G in 8/16/32) is a systolic
+// array over the query: lane t owns R consecutive query rows of the current
+// pass, keeps H and E of its rows in registers, and passes the bottom-row
+// (H, F), the column's descriptor words and the running score chain to lane
+// t+1 with one SHFL each per column.  A group streams one work item (two lane
 // streams of whole sequences separated by END/NUL columns) at a time, claimed
 // longest-first from an atomic counter (PAPER.md:119 dynamic distribution).
 // The substitution scores come from a query profile in shared
-// memory, one zero-extended int16 per (letter, row) word, so that packing the
-// two halves is one IMAD on the FMA pipe instead of a PRMT on the ALU pipe
-// (the ALU pipe is the bound: 64 lane-ops/clk/SM for DPX, measured).
+// memory, one score per (letter, row) 32-bit word, read with conflict-free
+// LDS.128 (4 rows per load).
 #include "kernels.cuh"
 
 #include <climits>
