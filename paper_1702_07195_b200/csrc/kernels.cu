@@ -128,22 +128,23 @@ __device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on
 }
 
 // Profile modes (what the two 16-bit halves of a register hold):
-//   QPM 0: two database sequences, one query.  Profile: one zero-extended
-//          int16 per (letter,row) 32-bit word, 4 rows per 16-B chunk; the two
-//          halves' scores are packed with one IMAD(B, 65536, A) (FMA pipe).
-//          (int16-pair profiles packed with PRMT or IMAD.HI were measured
-//          slower: profiles/r01_tile_calibration.jsonl.)
+//   QPM 0: two database sequences, one query.  Profile: one score per
+//          (letter,row) 32-bit word (sign-extended; zero-extended in the relu
+//          form), 4 rows per 16-B chunk; the two halves' scores are packed into
+//          SM_B * 65536 + SM_A with one IMAD(B, 65536, A) (FMA pipe).
+//          (int16-pair profiles were measured slower: DESIGN.md 3 and 4.2.)
 //   QPM 3: one database sequence, two queries (multi-query packing, SURVEY
-//          8(f) NEXT-2).  Profile word = (SM[q1_r][c], SM[q2_r][c]): no
-//          packing at all; the stream holds one sequence per column (column
-//          word of the letter pair (c, c)).
+//          8(f) NEXT-2).  Profile word = SM(q2_r, c) * 65536 + SM(q1_r, c)
+//          (relu form: the two halves): no packing at all; the stream holds one
+//          sequence per column (column word of the letter pair (c, c)).
 //
 // Lane roles inside a group (shuffles rotate: lane 0 receives from lane G-1):
 //   lane G-1 after computing its column: stores the column's score chain value
-//   (and the pass boundary), then overwrites its outgoing registers with the
-//   inputs of lane 0's next column -- the stream descriptor (loaded from smem
-//   early in the step, once its own copy is consumed) and the boundary of the
-//   previous pass (prefetched 4 columns ahead).  No per-lane selects at lane 0.
+//   (and the pass boundary), loads the descriptor of lane 0's next column from
+//   smem (its stream word was prefetched U columns ahead) and overwrites its
+//   outgoing registers with lane 0's next-column inputs, including the
+//   previous pass's boundary (prefetched U columns ahead).  No per-lane
+//   selects at lane 0.
 template <int R, int G, bool BIN, int QPM, int NT, int U>
 __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   static_assert(U == 1 || U == 2 || U == 4, "U: columns per unrolled block / prefetch distance");
