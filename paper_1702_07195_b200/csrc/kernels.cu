@@ -821,43 +821,43 @@ constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
 // The tile choice predicts time ~ G*R * (1/eff0 + (P-1)/eff1).
 struct TileEff { int G, R; float eff0, eff1; };
 const TileEff kTileEff[] = {
-    {8, 8, 4389.5f, 3408.8f},
-    {8, 12, 4966.9f, 4168.2f},
-    {8, 16, 5259.9f, 4805.2f},
-    {8, 18, 5379.2f, 4889.6f},
-    {8, 20, 5477.4f, 5138.6f},
-    {8, 22, 5518.4f, 5159.2f},
-    {8, 24, 5631.3f, 5374.1f},
-    {8, 26, 5625.2f, 5339.2f},
-    {8, 28, 5671.0f, 5441.1f},
-    {8, 29, 5690.3f, 5437.5f},
-    {8, 30, 5784.8f, 5422.8f},
-    {8, 32, 5709.8f, 5463.9f},
-    {16, 8, 4452.6f, 3497.9f},
-    {16, 12, 5025.1f, 4259.5f},
-    {16, 16, 5324.0f, 4893.3f},
-    {16, 18, 5435.9f, 4959.8f},
-    {16, 20, 5517.0f, 5195.7f},
-    {16, 22, 5550.3f, 5241.6f},
-    {16, 24, 5668.9f, 5434.2f},
-    {16, 26, 5666.7f, 5381.2f},
-    {16, 28, 5721.0f, 5493.5f},
-    {16, 29, 5729.9f, 5508.8f},
-    {16, 30, 5831.6f, 5466.7f},
-    {16, 32, 5746.5f, 5496.7f},
-    {32, 8, 4404.6f, 3668.1f},
-    {32, 12, 5053.5f, 4357.2f},
-    {32, 15, 5220.7f, 4809.7f},
-    {32, 16, 5174.7f, 4845.5f},
-    {32, 18, 5431.1f, 5056.3f},
-    {32, 20, 5525.3f, 5180.1f},
-    {32, 22, 5579.1f, 5151.0f},
-    {32, 24, 5544.8f, 5248.8f},
-    {32, 26, 5583.6f, 5233.2f},
-    {32, 28, 5631.5f, 5415.7f},
-    {32, 29, 5418.3f, 5407.7f},
-    {32, 30, 5539.0f, 5324.0f},
-    {32, 32, 5570.3f, 5446.3f}};
+    {8, 8, 4234.8f, 3414.0f},
+    {8, 12, 4899.9f, 4200.3f},
+    {8, 16, 5157.3f, 4594.1f},
+    {8, 18, 5399.9f, 4767.3f},
+    {8, 20, 5480.0f, 5097.9f},
+    {8, 22, 5513.1f, 5137.2f},
+    {8, 24, 5577.7f, 5263.6f},
+    {8, 26, 5657.6f, 5260.6f},
+    {8, 28, 5733.4f, 5262.6f},
+    {8, 29, 5734.4f, 5325.3f},
+    {8, 30, 5748.1f, 5307.2f},
+    {8, 32, 5808.6f, 5370.7f},
+    {16, 8, 4333.4f, 3601.8f},
+    {16, 12, 4959.5f, 4343.8f},
+    {16, 16, 5219.7f, 4719.4f},
+    {16, 18, 5430.5f, 4867.5f},
+    {16, 20, 5514.0f, 5109.5f},
+    {16, 22, 5565.4f, 5176.6f},
+    {16, 24, 5610.8f, 5316.2f},
+    {16, 26, 5690.3f, 5307.1f},
+    {16, 28, 5761.7f, 5320.6f},
+    {16, 29, 5765.1f, 5399.8f},
+    {16, 30, 5792.9f, 5369.6f},
+    {16, 32, 5845.3f, 5443.5f},
+    {32, 8, 4287.5f, 3595.9f},
+    {32, 12, 4992.9f, 4392.8f},
+    {32, 15, 5103.7f, 4624.2f},
+    {32, 16, 5189.7f, 4820.9f},
+    {32, 18, 5383.7f, 5021.3f},
+    {32, 20, 5479.9f, 5096.2f},
+    {32, 22, 5467.9f, 5102.7f},
+    {32, 24, 5465.8f, 5249.9f},
+    {32, 26, 5607.0f, 5278.3f},
+    {32, 28, 5573.6f, 5404.2f},
+    {32, 29, 5543.5f, 5350.3f},
+    {32, 30, 5509.7f, 5307.7f},
+    {32, 32, 5702.6f, 5281.3f}};
 
 TileEff tile_eff(int G, int R) {
   for (const TileEff &e : kTileEff)
