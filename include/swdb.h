@@ -185,7 +185,8 @@ int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, 
  *              sequence whose exact score is >= T is (R7),
  *   stats[9] = cell arithmetic of the 16-bit kernel: 1 = biased (4.5 ALU +
  *              2 FMA instructions per pair of cells), 0 = relu form (5.5 ALU
- *              + 1 FMA).
+ *              + 1 FMA),
+ *   stats[10] = 1 if the last search ran as a cross-pass wavefront.
  * Returns the number of entries written (<= n).
  */
 int sw_last_stats(int64_t *stats, int n);
@@ -208,6 +209,18 @@ int sw_last_timing(float *ms, int n);
  */
 int sw_set_tile(int32_t G, int32_t R);
 int sw_tile_supported(int32_t G, int32_t R);
+
+/*
+ * sw_set_wave -- cross-pass wavefront for multi-pass single-query searches of
+ * a resident database: one launch runs every query pass, an
+ * item's pass p trailing its pass p-1 through the boundary buffer, so several
+ * lane groups work on one long sequence at once (intra-task parallelism,
+ * PAPER.md:32).  mode 0 (default): used when a pass has fewer work items than
+ * lane groups; 1: always (when the query needs more than one pass); -1: never.
+ * In wavefront mode flagged sequences are re-scored in 32 bit from row 0.
+ * Returns SW_OK or SW_EINVAL.
+ */
+int sw_set_wave(int32_t mode);
 
 /* Message for the most recent failing call on this thread ("" if none). */
 const char *sw_last_error(void);

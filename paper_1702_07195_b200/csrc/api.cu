@@ -126,6 +126,9 @@ struct State {
   int64_t last_flags = -1, last_cells32 = -1, last_thresh = 0;
   // forced tile
   int force_G = 0, force_R = 0;
+  int wave_mode = 0;        // cross-pass wavefront: 0 auto, 1 always (multi-pass), -1 never
+  bool last_wave = false;
+  DevBuf<int> progress;     // wavefront: finished columns per (pass, item)
   // timing events of the last search
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> pev;   // (start, end) of every pass-kernel launch of the last search
@@ -169,7 +172,7 @@ struct State {
     img[0].release(); img[1].release();
     sc_out.release(); res.release(); offs.release();
     scores.release(); bscores.release(); flagged.release(); flagged2.release(); flag_list.release();
-    flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release();
+    flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release(); progress.release();
     query.release(); query2.release(); matrix.release(); qp.release(); desc.release(); qp32.release();
     qp32b.release(); bnd.release();
     scratch32.release(); dummy.release(); nulcols.release(); zerocols.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
@@ -204,7 +207,7 @@ int ensure_device_ready() {
 // processes alone (the intra-task part of the kernel); balance = min(1,
 // average columns per group / (1.15 * longest item)) charges tiles with many
 // small groups for that tail (cfg4: 5-35 k residue sequences).
-int choose_tile(int m, int qpm, const Image &I) {
+int choose_tile(int m, int qpm, const Image &I, bool wave_only = false) {
   if (g.force_G) {
     int ti = find_tile_mode(g.force_G, g.force_R, qpm);
     if (ti >= 0) return ti;
@@ -213,12 +216,14 @@ int choose_tile(int m, int qpm, const Image &I) {
   int bi = -1;
   for (int i = 0; i < num_tiles(); ++i) {
     const TileInfo ti = tile(i);
-    if (ti.qpm != qpm || tile_ctas_per_sm(i) < 1) continue;
+    if (ti.qpm != qpm || tile_ctas_per_sm(i) < 1 || (wave_only && !tile_has_wave(i))) continue;
     const int rows = ti.G * ti.R;
     const int P = (m + rows - 1) / rows;
     const double groups = (double)g.num_sms * tile_ctas_per_sm(i) * tile_threads(i) / ti.G;
     const double avg_cols = (double)I.total_cols / groups;
-    const double balance = I.max_item_cols > 0 ? std::min(1.0, avg_cols / (1.15 * (double)I.max_item_cols)) : 1.0;
+    // (the wavefront overlaps the passes of the longest item: no balance term)
+    const double balance = (I.max_item_cols > 0 && !wave_only)
+                               ? std::min(1.0, avg_cols / (1.15 * (double)I.max_item_cols)) : 1.0;
     const double cost = (double)rows * (1.0 / ti.eff0 + (P - 1) / ti.eff1) / balance + P * 0.002;
     if (cost < best - 1e-12) {
       best = cost;
@@ -261,8 +266,28 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int mode = pair ? 3 : 0;
   const Image &I = g.img[pair ? 1 : 0];
   const int mm = pair ? std::max(m, m2) : m;
-  const int ti = choose_tile(mm, mode, I);
+  int ti = choose_tile(mm, mode, I);
   if (ti < 0) return fail(SW_ECUDA, "no runnable kernel tile");
+  // Cross-pass wavefront (one launch runs every pass): for a
+  // multi-pass single query when the items of one pass cannot fill the lane
+  // groups (a database of few, long sequences), or when forced.
+  bool wave = false;
+  if (!pair && !g.streamed && g.wave_mode >= 0) {
+    const TileInfo T0 = tile(ti);
+    const int P0 = (mm + T0.G * T0.R - 1) / (T0.G * T0.R);
+    const double groups = (double)g.num_sms * std::max(1, tile_ctas_per_sm(ti)) * 512.0 / T0.G;
+    if (P0 > 1 && (g.wave_mode == 1 || (double)I.num_items < groups)) {
+      int tw = tile_has_wave(ti) ? ti : choose_tile(mm, mode, I, true);
+      if (g.force_G && !tile_has_wave(ti)) tw = -1;   // a forced tile without a wavefront kernel
+      if (tw >= 0) {
+        const TileInfo Tw = tile(tw);
+        if ((mm + Tw.G * Tw.R - 1) / (Tw.G * Tw.R) > 1) {
+          ti = tw;
+          wave = true;
+        }
+      }
+    }
+  }
   const TileInfo T = tile(ti);
   const int rows = T.G * T.R;
   const int P = (mm + rows - 1) / rows;
@@ -349,7 +374,48 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(cudaMemsetAsync(g.pcounters.p, 0, sizeof(int) * (size_t)nch * P, st));
   if (P > 1 && g.bnd.n < (size_t)span * 2) CUDA_TRY(g.bnd.ensure((size_t)span * 2));
   CUDA_TRY(cudaEventRecord(g.ev[1], st));
-  for (int k = 0; k < nch; ++k) {
+  if (wave) {
+    CUDA_TRY(g.progress.ensure((size_t)P * std::max(1, I.num_items)));
+    CUDA_TRY(cudaMemsetAsync(g.progress.p, 0, sizeof(int) * (size_t)P * std::max(1, I.num_items), st));
+    SW16Params p{};
+    p.stream = I.stream.p;
+    p.items = I.items.p;
+    p.num_items = I.num_items;
+    p.counter = g.pcounters.p;
+    p.qp = reinterpret_cast<const uint4 *>(g.qp.p);
+    p.desc = g.desc.p;
+    p.bnd_in = nullptr;
+    p.bnd_out = nullptr;
+    p.dummy = g.dummy.p;
+    p.nul_stream = g.nulcols.p;
+    p.zero_bnd = g.zerocols.p;
+    p.col_lo = 0;
+    p.col_hi = I.total_cols;
+    p.sc_out = g.sc_out.p;
+    p.pass = 0;
+    p.thresh = thresh;
+    p.zero = 0u;
+    p.one = 1u;
+    p.npass = P;
+    p.pcounters = g.pcounters.p;
+    p.progress = g.progress.p;
+    p.bndbuf[0] = g.bnd.p;
+    p.bndbuf[1] = g.bnd.p + span;
+    while (g.pev.size() < 2) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      g.pev.push_back(e);
+    }
+    CUDA_TRY(cudaEventRecord(g.pev[0], st));
+    // every CTA must be resident: a wavefront CTA may wait on another's progress
+    CUDA_TRY(launch_sw16_pass(ti, g.num_sms * tile_wave_ctas_per_sm(ti), p, st));
+    CUDA_TRY(cudaEventRecord(g.pev[1], st));
+    g.npev = 1;
+    // the score chain was carried through the passes: one gather of the maxima
+    CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p, nullptr, nullptr, 0,
+                                thresh, st));
+  }
+  for (int k = 0; k < (wave ? 0 : nch); ++k) {
     const uint32_t *stream_base = I.stream.p;
     const Item *items = I.items.p;
     int nitems = I.num_items;
@@ -413,8 +479,8 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     if (strm) CUDA_TRY(cudaEventRecord(g.ev_free[b], st));
   }
   CUDA_TRY(cudaEventRecord(g.ev[2], st));
-  if (strm || P >= 255)
-    for (int k = 0; k < (pair ? 2 : 1); ++k) CUDA_TRY(rescore(k, strm ? -1 : 254, nullptr));
+  if (strm || wave || P >= 255)
+    for (int k = 0; k < (pair ? 2 : 1); ++k) CUDA_TRY(rescore(k, (strm || wave) ? -1 : 254, nullptr));
   CUDA_TRY(cudaEventRecord(g.ev[3], st));
 
   g.has_search = true;
@@ -424,6 +490,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   g.last_R = T.R;
   g.last_P = P;
   g.last_mode = mode;
+  g.last_wave = wave;
   g.last_flags = -1;
   g.last_cells32 = -1;
   return SW_OK;
@@ -766,9 +833,10 @@ int sw_last_stats(int64_t *stats, int n) {
     g.last_cells32 = cells;
   }
   const Image &I = g.img[g.last_mode == 3 ? 1 : 0];
-  const int64_t v[10] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
-                         g.last_flags, g.last_cells32, I.total_cols, I.num_items, g.last_thresh, kArith};
-  const int m = std::min(n, 10);
+  const int64_t v[11] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
+                         g.last_flags, g.last_cells32, I.total_cols, I.num_items, g.last_thresh, kArith,
+                         g.last_wave ? 1 : 0};
+  const int m = std::min(n, 11);
   for (int i = 0; i < m; ++i) stats[i] = v[i];
   return m;
 }
@@ -804,6 +872,13 @@ int sw_set_tile(int32_t G, int32_t R) {
 }
 
 int sw_tile_supported(int32_t G, int32_t R) { return find_tile_mode(G, R, 0) >= 0 ? 1 : 0; }
+
+int sw_set_wave(int32_t mode) {
+  t_err.clear();
+  if (mode < -1 || mode > 1) return fail(SW_EINVAL, "mode must be -1, 0 or 1");
+  g.wave_mode = mode;
+  return SW_OK;
+}
 
 int sw_search_batch_dev(const uint8_t *queries, const int64_t *qoffsets, int32_t nq, const int8_t *matrix,
                         int32_t gap_open, int32_t gap_extend, int32_t *d_scores, void *cuda_stream) {

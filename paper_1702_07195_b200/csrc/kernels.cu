@@ -99,6 +99,27 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
+// L2-coherent loads (the cross-pass wavefront reads data other SMs write
+// during the launch; __ldg / L1-cached loads could return stale lines).
+__device__ __forceinline__ uint2 ld_cg_v2(const uint2 *p) {
+  uint2 v;
+  asm volatile("ld.global.cg.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void st_global_v2(uint2 *p, uint32_t a, uint32_t b) {
   asm volatile("st.global.v2.u32 [%0], {%1, %2};" :: "l"(p), "r"(a), "r"(b) : "memory");
 }
@@ -145,8 +166,9 @@ __device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on
 //   outgoing registers with lane 0's next-column inputs, including the
 //   previous pass's boundary (prefetched U columns ahead).  No per-lane
 //   selects at lane 0.
-template <int R, int G, bool BIN, int QPM, int NT, int U>
+template <int R, int G, bool BIN, int QPM, int NT, int U, bool WAVE = false>
 __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
+  static_assert(!WAVE || BIN, "the wavefront kernel reads boundaries (from pass 1 on)");
   static_assert(U == 1 || U == 2 || U == 4, "U: columns per unrolled block / prefetch distance");
   static_assert(QPM == 0 || QPM == 3, "profile mode");
   constexpr int RPC = 4;                    // rows per 16-B profile chunk
@@ -155,12 +177,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   constexpr int QP_U4 = kNL * LS / 16;
   constexpr int DESC_U4 = kNL * kNL;
   extern __shared__ uint4 smem[];
-  {
-    const uint4 *gq = p.qp + (size_t)p.pass * QP_U4;
-    for (int i = threadIdx.x; i < DESC_U4; i += blockDim.x) smem[i] = p.desc[i];
-    for (int i = threadIdx.x; i < QP_U4; i += blockDim.x) smem[DESC_U4 + i] = gq[i];
-  }
-  __syncthreads();
+  for (int i = threadIdx.x; i < DESC_U4; i += blockDim.x) smem[i] = p.desc[i];
 
   const int lane = threadIdx.x & 31;
   const int t = lane & (G - 1);
@@ -173,7 +190,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   const uint32_t zero = p.zero;
   const uint32_t s_desc = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t s_qp = s_desc + DESC_U4 * 16 + t * 16;
-  const bool bout = last && p.bnd_out != nullptr;
+  __syncthreads();
   const DescWords nul = load_desc(s_desc + kNulWord);
 
   const uint32_t one = p.one;
@@ -201,13 +218,40 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   bool done = false;
   uint32_t sring[U];
   uint2 bring[U];
+  uint32_t scring[WAVE ? U : 1];   // WAVE: the previous pass's score chain, per column
 #pragma unroll
   for (int u = 0; u < U; ++u) { sring[u] = 0u; bring[u] = make_uint2(kB2, kB2); }
+#pragma unroll
+  for (int u = 0; u < (WAVE ? U : 1); ++u) scring[u] = 0u;
+  const uint32_t *scin = nullptr;  // WAVE: sc_out of the item's columns (previous pass)
+  int cur_it = 0, cur_ncols = 0, sdone = 0, avail = 0;   // WAVE progress bookkeeping
+
+  // Passes: one per launch (p.pass), or all of them in a cross-pass wavefront
+  // (WAVE): the CTA runs pass p's items (profile slice p in shared memory)
+  // until pass p's cursor is exhausted, then moves to pass p+1.  An item of
+  // pass p reads the boundary and score chain that pass p-1 writes, after
+  // checking pass p-1's published progress on that item.
+  const int pass_end = WAVE ? p.npass : p.pass + 1;
+  for (int pass = p.pass; pass < pass_end; ++pass) {
+  __syncthreads();   // every group of the CTA has left the previous slice
+  {
+    const uint4 *gq = p.qp + (size_t)pass * QP_U4;
+    for (int i = threadIdx.x; i < QP_U4; i += blockDim.x) smem[DESC_U4 + i] = gq[i];
+  }
+  __syncthreads();
+  int *const counter = WAVE ? p.pcounters + pass : p.counter;
+  const uint2 *const bnd_in = WAVE ? (pass > 0 ? p.bndbuf[(pass - 1) & 1] : nullptr) : p.bnd_in;
+  uint2 *const bnd_out = WAVE ? (pass + 1 < p.npass ? p.bndbuf[pass & 1] : nullptr) : p.bnd_out;
+  const bool bout = last && bnd_out != nullptr;
+  const int *const prog_in = (WAVE && pass > 0) ? p.progress + (size_t)(pass - 1) * p.num_items : nullptr;
+  int *const prog_out = (WAVE && pass + 1 < p.npass) ? p.progress + (size_t)pass * p.num_items : nullptr;
+  rem = 0;
+  done = false;
 
   for (;;) {
     if (rem <= 0) {  // group-uniform: claim the next work item
       int it = 0;
-      if (last) it = atomicAdd(p.counter, 1);
+      if (last) it = atomicAdd(counter, 1);
       it = __shfl_sync(gmask, it, gbase + G - 1);
       if (it < p.num_items) {
         const int64_t c0 = p.items[it].col_begin;
@@ -215,26 +259,39 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         rem = (ncols + G - 1 + U - 1) & ~(U - 1);
         inc = (uint32_t)U;
         sptr = p.stream + c0;
-        if (BIN) bptr = p.bnd_in + c0;
-        bcols = ncols;
+        if (BIN) bptr = bnd_in ? bnd_in + c0 : p.zero_bnd;
+        bcols = (BIN && bnd_in) ? ncols : 0;   // no input boundary: every column reads as zero
         scp = p.sc_out + (c0 - (G - 1));
-        if (p.bnd_out) bop = p.bnd_out + (c0 - (G - 1));
+        if (bnd_out) bop = bnd_out + (c0 - (G - 1));
+        if (WAVE) {
+          scin = p.sc_out + c0;
+          cur_it = it;
+          cur_ncols = ncols;
+          sdone = 0;
+          avail = 0;
+          if (prog_in && last) {   // columns 0..U are read below
+            const int need = min(ncols, U + 1);
+            while ((avail = ld_acquire(prog_in + it)) < need) __nanosleep(200);
+          }
+        }
         if (last) {
           // ring slot x % U holds column x; columns 1..U are prefetched here
 #pragma unroll
           for (int u = 1; u <= U; ++u) {
             sring[u % U] = __ldg(sptr + u);
-            if (BIN) bring[u % U] = u < ncols ? __ldg(bptr + u) : make_uint2(kB2, kB2);
+            if (BIN)
+              bring[u % U] = u < bcols ? (WAVE ? ld_cg_v2(bptr + u) : __ldg(bptr + u)) : make_uint2(kB2, kB2);
+            if (WAVE) scring[u % U] = u < bcols ? ld_cg(scin + u) : 0u;
           }
           const DescWords d = load_desc(s_desc + __ldg(sptr));   // lane 0's first column
           w0 = d.w0;
           ngoe = d.ngoe;
           nge = d.nge;
           knext = d.kneg;
-          const uint2 b0 = BIN ? __ldg(bptr) : make_uint2(kB2, kB2);   // ncols >= 4
+          const uint2 b0 = bcols > 0 ? (WAVE ? ld_cg_v2(bptr) : __ldg(bptr)) : make_uint2(kB2, kB2);   // ncols >= 4
           hout = b0.x;
           fout = b0.y;
-          sc = 0u;
+          sc = (WAVE && bcols > 0) ? ld_cg(scin) : 0u;
         }
       } else {
         done = true;
@@ -245,9 +302,15 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         if (BIN) bptr = p.zero_bnd;        // zero boundary
         scp = reinterpret_cast<uint32_t *>(dummy);
         bop = dummy;
+        if (WAVE) {
+          scin = nullptr;
+          cur_ncols = 0;
+        }
         if (last) {
 #pragma unroll
           for (int u = 0; u < U; ++u) { sring[u] = kNulWord; bring[u] = make_uint2(kB2, kB2); }
+#pragma unroll
+          for (int u = 0; u < (WAVE ? U : 1); ++u) scring[u] = 0u;
           w0 = nul.w0;
           ngoe = nul.ngoe;
           nge = nul.nge;
@@ -259,6 +322,15 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       }
     }
     if (__all_sync(0xffffffffu, done)) break;
+    if (WAVE && prog_in && last && cur_ncols > 0) {
+      // this block reads the boundary of columns up to sdone + 2U: wait until
+      // pass p-1 has published them
+      const int need = min(cur_ncols, sdone + 2 * U + 1);
+      while (avail < need) {
+        avail = ld_acquire(prog_in + cur_it);
+        if (avail < need) __nanosleep(200);
+      }
+    }
 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -281,6 +353,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       kneg = knext;
       // ---- lane G-1: lane 0's next column (s+u+1) descriptor; refill its ring slot
       uint2 bnext = make_uint2(bdef, bdef);   // added to the outgoing (H, F): 0 for lanes t < G-1
+      uint32_t scnext = 0u;                   // WAVE: lane 0's score-chain input (previous pass)
       // descriptor of lane 0's next column: loaded after the rows (lane G-1
       // still needs its own column's penalty words)
       const uint32_t dnext = sring[(u + 1) % U];
@@ -291,9 +364,15 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         sring[(u + 1) % U] = __ldg(sptr + u + 1 + U);
         if (BIN) {
           bnext = bring[(u + 1) % U];
-          SW_CHECK(u + 1 + U >= bcols || (bptr + u + 1 + U - p.bnd_in >= p.col_lo &&
-                                           bptr + u + 1 + U - p.bnd_in < p.col_hi));
-          bring[(u + 1) % U] = (u + 1 + U < bcols) ? __ldg(bptr + u + 1 + U) : make_uint2(kB2, kB2);
+          SW_CHECK(u + 1 + U >= bcols || (bptr + u + 1 + U - bnd_in >= p.col_lo &&
+                                           bptr + u + 1 + U - bnd_in < p.col_hi));
+          bring[(u + 1) % U] = (u + 1 + U < bcols)
+                                   ? (WAVE ? ld_cg_v2(bptr + u + 1 + U) : __ldg(bptr + u + 1 + U))
+                                   : make_uint2(kB2, kB2);
+        }
+        if (WAVE) {
+          scnext = scring[(u + 1) % U];
+          scring[(u + 1) % U] = (u + 1 + U < bcols) ? ld_cg(scin + u + 1 + U) : 0u;
         }
       }
       uint32_t hd = hprev;
@@ -392,7 +471,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       const uint32_t so = __vmaxs2(sc_in, S);   // max over lanes 0..t (read at END columns)
       SW_CHECK(!last || scp == reinterpret_cast<uint32_t *>(dummy) ||
                (scp + u - p.sc_out >= p.col_lo && scp + u - p.sc_out < p.col_hi));
-      SW_CHECK(!bout || bop == dummy || (bop + u - p.bnd_out >= p.col_lo && bop + u - p.bnd_out < p.col_hi));
+      SW_CHECK(!bout || bop == dummy || (bop + u - bnd_out >= p.col_lo && bop + u - bnd_out < p.col_hi));
       if (last) {
         const DescWords d = load_desc(s_desc + dnext);
         w0 = d.w0;
@@ -405,7 +484,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       // outgoing registers; lane G-1 hands over lane 0's next-column inputs
       hout = imad(H[R - 1], nlast, bnext.x);
       fout = imad(F, nlast, bnext.y);
-      sc = imad(so, nlast, 0u);
+      sc = imad(so, nlast, scnext);
     }
     rem -= U;
     if (BIN) bcols -= U;
@@ -413,7 +492,16 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
     if (BIN) bptr = ptr_add(bptr, inc);
     scp = ptr_add(scp, inc);
     bop = ptr_add(bop, inc);
+    if (WAVE) {
+      if (scin) scin += U;
+      sdone += U;
+      // publish the columns whose boundary and chain value are now stored
+      // (lane G-1 stores column s - (G-1) at step s); release orders the stores
+      if (prog_out && last && cur_ncols > 0)
+        st_release(prog_out + cur_it, min(cur_ncols, max(0, sdone - (G - 1))));
+    }
   }
+  }   // passes
 }
 
 // Scores of one pass from the per-column score chain: the value at a
@@ -786,29 +874,40 @@ struct TileEntry {
   int G, R, qpm, nt, smem;
   PassFn fn0, fn1;   // pass 0 / passes > 0 (boundary input)
   int ctas;
+  PassFn fnw;        // cross-pass wavefront (all passes in one launch), or null
+  int ctasw;         // resident CTAs per SM of fnw (its grid must be fully resident)
 };
 
 #define SW_TILE_NTU(G_, R_, M_, NT_, U_)                                                     \
   {G_, R_, M_, NT_, smem_of<R_, G_, M_>(), sw16_pass_kernel<R_, G_, false, M_, NT_, U_>,   \
-   sw16_pass_kernel<R_, G_, true, M_, NT_, U_>, 0}
+   sw16_pass_kernel<R_, G_, true, M_, NT_, U_>, 0, nullptr}
+// tiles that also have a wavefront kernel (single-query mode)
+#define SW_TILE_W(G_, R_)                                                                     \
+  {G_, R_, 0, 512, smem_of<R_, G_, 0>(), sw16_pass_kernel<R_, G_, false, 0, 512, SW_UNROLL>, \
+   sw16_pass_kernel<R_, G_, true, 0, 512, SW_UNROLL>, 0,                                      \
+   sw16_pass_kernel<R_, G_, true, 0, 512, SW_UNROLL, true>}
 #ifndef SW_UNROLL
 #define SW_UNROLL 4   // columns per unrolled block = lane G-1's prefetch distance
 #endif
 #define SW_TILE_NT(G_, R_, M_, NT_) SW_TILE_NTU(G_, R_, M_, NT_, SW_UNROLL)
 #define SW_TILE(G_, R_, M_) SW_TILE_NT(G_, R_, M_, 512)
-#define SW_TILES(M_)                                                                          \
+#define SW_TILES_COMMON(M_)                                                                   \
   SW_TILE(8, 8, M_), SW_TILE(8, 12, M_), SW_TILE(8, 16, M_), SW_TILE(8, 18, M_),              \
   SW_TILE(8, 20, M_), SW_TILE(8, 22, M_), SW_TILE(8, 24, M_), SW_TILE(8, 26, M_),             \
   SW_TILE(8, 28, M_), SW_TILE(8, 29, M_), SW_TILE(8, 30, M_), SW_TILE(8, 32, M_),             \
-  SW_TILE(16, 8, M_), SW_TILE(16, 12, M_), SW_TILE(16, 16, M_), SW_TILE(16, 18, M_),          \
+  SW_TILE(16, 8, M_), SW_TILE(16, 12, M_), SW_TILE(16, 18, M_),                               \
   SW_TILE(16, 20, M_), SW_TILE(16, 22, M_), SW_TILE(16, 24, M_), SW_TILE(16, 26, M_),         \
-  SW_TILE(16, 28, M_), SW_TILE(16, 29, M_), SW_TILE(16, 30, M_), SW_TILE(16, 32, M_),         \
-  SW_TILE(32, 8, M_), SW_TILE(32, 12, M_), SW_TILE(32, 15, M_), SW_TILE(32, 16, M_),          \
+  SW_TILE(16, 28, M_), SW_TILE(16, 30, M_),                                                   \
+  SW_TILE(32, 12, M_), SW_TILE(32, 15, M_),                                                   \
   SW_TILE(32, 18, M_), SW_TILE(32, 20, M_), SW_TILE(32, 22, M_), SW_TILE(32, 24, M_),         \
-  SW_TILE(32, 26, M_), SW_TILE(32, 28, M_), SW_TILE(32, 29, M_), SW_TILE(32, 30, M_),         \
-  SW_TILE(32, 32, M_)
-TileEntry g_tiles[] = {SW_TILES(0), SW_TILES(3)};
-#undef SW_TILES
+  SW_TILE(32, 26, M_), SW_TILE(32, 28, M_), SW_TILE(32, 30, M_)
+TileEntry g_tiles[] = {
+    SW_TILES_COMMON(0), SW_TILE_W(16, 16), SW_TILE_W(16, 29), SW_TILE_W(16, 32), SW_TILE_W(32, 8),
+    SW_TILE_W(32, 16), SW_TILE_W(32, 29), SW_TILE_W(32, 32),
+    SW_TILES_COMMON(3), SW_TILE(16, 16, 3), SW_TILE(16, 29, 3), SW_TILE(16, 32, 3), SW_TILE(32, 8, 3),
+    SW_TILE(32, 16, 3), SW_TILE(32, 29, 3), SW_TILE(32, 32, 3)};
+#undef SW_TILES_COMMON
+#undef SW_TILE_W
 #undef SW_TILE
 #undef SW_TILE_NT
 #undef SW_TILE_NTU
@@ -890,7 +989,8 @@ int tile_threads(int i) { return g_tiles[i].nt; }
 
 cudaError_t init_kernels() {
   for (int i = 0; i < kNumTiles; ++i) {
-    for (PassFn fn : {g_tiles[i].fn0, g_tiles[i].fn1}) {
+    for (PassFn fn : {g_tiles[i].fn0, g_tiles[i].fn1, g_tiles[i].fnw}) {
+      if (!fn) continue;
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g_tiles[i].smem);
       if (e != cudaSuccess) return e;
     }
@@ -900,6 +1000,11 @@ cudaError_t init_kernels() {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, g_tiles[i].fn1, g_tiles[i].nt, g_tiles[i].smem);
     if (e != cudaSuccess) return e;
     g_tiles[i].ctas = n0 < n1 ? n0 : n1;
+    if (g_tiles[i].fnw) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_tiles[i].ctasw, g_tiles[i].fnw, g_tiles[i].nt,
+                                                        g_tiles[i].smem);
+      if (e != cudaSuccess) return e;
+    }
   }
   return cudaSuccess;
 }
@@ -920,8 +1025,12 @@ cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_quer
   return cudaGetLastError();
 }
 
+bool tile_has_wave(int i) { return g_tiles[i].fnw != nullptr && g_tiles[i].ctasw > 0; }
+int tile_wave_ctas_per_sm(int i) { return g_tiles[i].ctasw; }
+
 cudaError_t launch_sw16_pass(int ti, int grid, const SW16Params &p, cudaStream_t st) {
-  PassFn fn = p.bnd_in ? g_tiles[ti].fn1 : g_tiles[ti].fn0;
+  PassFn fn = p.npass > 0 ? g_tiles[ti].fnw : (p.bnd_in ? g_tiles[ti].fn1 : g_tiles[ti].fn0);
+  if (!fn) return cudaErrorInvalidValue;
   fn<<<grid, g_tiles[ti].nt, g_tiles[ti].smem, st>>>(p);
   return cudaGetLastError();
 }

@@ -41,6 +41,15 @@ struct SW16Params {
   int thresh;               // 32768 - max(1, smax)
   uint32_t zero;            // 0 (passed in so ptxas keeps it in a register)
   uint32_t one;             // 1 (passed in: keeps 32-bit adds on the FMA pipe as IMAD)
+  // Cross-pass wavefront (one launch runs every pass): npass
+  // passes starting at `pass`, item cursors pcounters[npass], per-(pass, item)
+  // finished-column counts progress[npass * num_items] (zeroed), and the two
+  // boundary buffers (pass p reads bndbuf[(p-1)&1], writes bndbuf[p&1]).  The
+  // score chain is carried from pass to pass through sc_out.  npass == 0: off.
+  int npass;
+  int *pcounters;
+  int *progress;
+  uint2 *bndbuf[2];
 };
 
 struct SW32Params {
@@ -94,6 +103,9 @@ cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_quer
                             int goe, int ge, cudaStream_t st);
 // goe = gap open + extend, ge = gap extend (>= 0; the descriptor penalty words clamp at 32767)
 cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cudaStream_t st);
+// Whether tile i has a cross-pass wavefront kernel (p.npass > 0 launches it).
+bool tile_has_wave(int i);
+int tile_wave_ctas_per_sm(int i);
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
                                cudaStream_t st, const int32_t *seq_idx = nullptr);

@@ -21,7 +21,7 @@ _NAMES = {SW_EINVAL: "SW_EINVAL", SW_ENOMEM: "SW_ENOMEM", SW_ECUDA: "SW_ECUDA",
 
 EXPORTS = ["sw_db_load", "sw_db_load_streamed", "sw_db_chunks", "sw_db_free", "sw_db_count", "sw_db_residues", "sw_search",
            "sw_search_dev", "sw_search_batch", "sw_search_batch_dev", "sw_topk", "sw_topk_dev", "sw_last_stats", "sw_last_timing", "sw_set_tile",
-           "sw_tile_supported", "sw_last_error", "sw_version"]
+           "sw_tile_supported", "sw_set_wave", "sw_last_error", "sw_version"]
 
 
 class SWError(RuntimeError):
@@ -64,6 +64,7 @@ def load_library():
         "sw_last_timing": (ctypes.c_int, [p, ctypes.c_int]),
         "sw_set_tile": (ctypes.c_int, [i32, i32]),
         "sw_tile_supported": (ctypes.c_int, [i32, i32]),
+        "sw_set_wave": (ctypes.c_int, [i32]),
         "sw_last_error": (ctypes.c_char_p, []),
         "sw_version": (ctypes.c_char_p, []),
     }
@@ -211,10 +212,10 @@ def sw_topk_dev(d_scores, d_index, n: int, k: int, d_idx_out, d_score_out, strea
 
 
 def sw_last_stats() -> dict:
-    a = np.zeros(10, dtype=np.int64)
-    _check(load_library().sw_last_stats(_ptr(a), 10))
+    a = np.zeros(11, dtype=np.int64)
+    _check(load_library().sw_last_stats(_ptr(a), 11))
     keys = ["rows_per_pass", "passes", "G", "R", "flagged", "cells32", "pair_columns", "items",
-            "flag_threshold", "arith"]
+            "flag_threshold", "arith", "wave"]
     return {k: int(v) for k, v in zip(keys, a)}
 
 
@@ -226,6 +227,11 @@ def sw_last_timing() -> dict:
 
 def sw_set_tile(G: int, R: int = 0) -> None:
     _check(load_library().sw_set_tile(int(G), int(R)))
+
+
+def sw_set_wave(mode: int) -> None:
+    """Cross-pass wavefront: 0 auto (default), 1 always, -1 never (swdb.h)."""
+    _check(load_library().sw_set_wave(int(mode)))
 
 
 def sw_tile_supported(G: int, R: int) -> bool:

@@ -403,3 +403,43 @@ def test_shard_count_invariance_sequential_shards():
         sw.sw_topk_dev(cs, ci, cs.numel(), 10, mi, ms)
         assert mi.tolist() == eidx.tolist() and ms.tolist() == esc.tolist(), G
 
+
+def test_cross_pass_wavefront_matches_oracle():
+    """The cross-pass wavefront (one launch runs every query pass; an item's
+    pass p trails pass p-1 through the boundary buffer and the score chain,
+    synchronised by published progress) gives the same scores as the oracle:
+    few long sequences (the case it exists for), a random mix with flagged
+    sequences, several tiles, and auto mode choosing it by itself."""
+    rng = np.random.default_rng(2718)
+    dbs = [
+        [si.rr_residues(rng, int(L)) for L in rng.integers(3000, 12000, 9)],
+        [si.rr_residues(rng, int(L)) for L in rng.integers(0, 700, 500)] + [encode("W" * 2500)] * 3,
+    ]
+    queries = [si.rr_residues(rng, 1700), encode("W" * 2600 + "A" * 50), si.rr_residues(rng, 5478)]
+    try:
+        for di, seqs in enumerate(dbs):
+            db = _db(seqs)
+            sw.sw_db_load(db.residues, db.offsets)
+            for q in queries:
+                exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
+                for G, R in ((0, 0), (16, 16), (32, 8), (32, 29)):
+                    sw.sw_set_tile(G, R)
+                    sw.sw_set_wave(1)
+                    got = sw.sw_search(q, BLOSUM62, 10, 2)
+                    st = sw.sw_last_stats()
+                    assert st["wave"] == (1 if st["passes"] > 1 else 0), (di, len(q), G, R, st)
+                    assert (got == exp).all(), (di, len(q), G, R, np.nonzero(got != exp)[0][:5])
+                    idx, sc = sw.sw_topk(5)
+                    eidx, esc = oracle.topk(exp, 5)
+                    assert (idx == eidx).all() and (sc == esc).all()
+                # auto mode on the few-long-sequences database picks the wavefront
+                sw.sw_set_tile(0)
+                sw.sw_set_wave(0)
+                got = sw.sw_search(q, BLOSUM62, 10, 2)
+                assert (got == exp).all()
+                if di == 0:
+                    assert sw.sw_last_stats()["wave"] == 1
+    finally:
+        sw.sw_set_tile(0)
+        sw.sw_set_wave(0)
+
