@@ -268,24 +268,36 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int mm = pair ? std::max(m, m2) : m;
   int ti = choose_tile(mm, mode, I);
   if (ti < 0) return fail(SW_ECUDA, "no runnable kernel tile");
-  // Cross-pass wavefront (one launch runs every pass): for a
-  // multi-pass single query when the items of one pass cannot fill the lane
-  // groups (a database of few, long sequences), or when forced.
+  // Cross-pass wavefront (one launch runs every pass).  A pass
+  // of the per-pass path keeps at most one lane group per work item busy; with
+  // far fewer items than groups (a database of few, long sequences) the
+  // wavefront runs the query passes of an item on several groups at once.
+  // Auto rule, from a tile sweep on databases of 10-4,000 items of 1-35 k
+  // residues (profiles/r01b_wavefront_tiles.jsonl): below half as many items
+  // as 32-lane groups, 32x8 tiles when the query makes >= 8 passes of them and
+  // the units (items x passes) do not overfill the groups 1.5 times, else 32x16
+  // tiles when their units exceed half the groups.  Forced mode (1) uses the
+  // forced or chosen tile when it has a wavefront kernel, else 32x16 / 32x8.
   bool wave = false;
   if (!pair && !g.streamed && g.wave_mode >= 0) {
-    const TileInfo T0 = tile(ti);
-    const int P0 = (mm + T0.G * T0.R - 1) / (T0.G * T0.R);
-    const double groups = (double)g.num_sms * std::max(1, tile_ctas_per_sm(ti)) * 512.0 / T0.G;
-    if (P0 > 1 && (g.wave_mode == 1 || (double)I.num_items < groups)) {
-      int tw = tile_has_wave(ti) ? ti : choose_tile(mm, mode, I, true);
-      if (g.force_G && !tile_has_wave(ti)) tw = -1;   // a forced tile without a wavefront kernel
-      if (tw >= 0) {
-        const TileInfo Tw = tile(tw);
-        if ((mm + Tw.G * Tw.R - 1) / (Tw.G * Tw.R) > 1) {
-          ti = tw;
-          wave = true;
-        }
+    auto passes_of = [&](int i) { return (mm + tile(i).G * tile(i).R - 1) / (tile(i).G * tile(i).R); };
+    const int t8 = find_tile_mode(32, 8, 0), t16 = find_tile_mode(32, 16, 0);
+    const double items = (double)std::max(1, I.num_items);
+    int tw = -1;
+    if (g.wave_mode == 1) {
+      if (tile_has_wave(ti) && passes_of(ti) > 1) tw = ti;
+      else if (!g.force_G && t16 >= 0 && tile_has_wave(t16) && passes_of(t16) > 1) tw = t16;
+      else if (!g.force_G && t8 >= 0 && tile_has_wave(t8) && passes_of(t8) > 1) tw = t8;
+    } else if (!g.force_G && t8 >= 0 && t16 >= 0 && tile_has_wave(t8) && tile_has_wave(t16)) {
+      const double groups32 = (double)g.num_sms * std::max(1, tile_ctas_per_sm(t8)) * 512.0 / 32.0;
+      if (items < 0.5 * groups32) {
+        if (passes_of(t8) >= 8 && items * passes_of(t8) <= 1.5 * groups32) tw = t8;
+        else if (passes_of(t16) >= 2 && items * passes_of(t16) > 0.5 * groups32) tw = t16;
       }
+    }
+    if (tw >= 0) {
+      ti = tw;
+      wave = true;
     }
   }
   const TileInfo T = tile(ti);
@@ -342,7 +354,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     cudaError_t e = launch_flag_compact(k ? g.flagged2.p : g.flagged.p, g.count, k ? g.flag_list2.p : g.flag_list.p,
                                         cnt, want, st);
     if (e != cudaSuccess || row0 >= len) return e;
-    SW32Params q;
+    SW32Params q{};
     q.flag_list = k ? g.flag_list2.p : g.flag_list.p;
     q.flag_count = cnt;
     q.cursor = cnt + 1;
@@ -435,7 +447,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       nitems = c.item_end - c.item_begin;
     }
     for (int pass = 0; pass < P; ++pass) {
-      SW16Params p;
+      SW16Params p{};   // npass = 0: one pass per launch
       p.stream = stream_base;
       p.items = items;
       p.num_items = nitems;

@@ -60,6 +60,7 @@ namespace swdb {
 namespace {
 
 constexpr int kThreads = 512;
+constexpr int kWavePublish = 64;   // wavefront: columns between progress publications
 constexpr uint32_t kB2 = (uint32_t)kBias16 * 0x10001u;   // the stored zero, both halves
 constexpr uint32_t kNulWord = (uint32_t)((kNul * kNL + kNul) * kDescBytes);
 
@@ -496,8 +497,10 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       if (scin) scin += U;
       sdone += U;
       // publish the columns whose boundary and chain value are now stored
-      // (lane G-1 stores column s - (G-1) at step s); release orders the stores
-      if (prog_out && last && cur_ncols > 0)
+      // (lane G-1 stores column s - (G-1) at step s); release orders the
+      // stores.  A release store waits for the earlier stores to complete, so
+      // it is issued every kWavePublish columns and when the item ends.
+      if (prog_out && last && cur_ncols > 0 && ((sdone & (kWavePublish - 1)) == 0 || rem <= 0))
         st_release(prog_out + cur_it, min(cur_ncols, max(0, sdone - (G - 1))));
     }
   }

@@ -437,7 +437,7 @@ def test_cross_pass_wavefront_matches_oracle():
                 sw.sw_set_wave(0)
                 got = sw.sw_search(q, BLOSUM62, 10, 2)
                 assert (got == exp).all()
-                if di == 0:
+                if di == 0 and len(q) >= 8 * 256:   # >= 8 passes of 32x8 tiles (api.cu auto rule)
                     assert sw.sw_last_stats()["wave"] == 1
     finally:
         sw.sw_set_tile(0)
