@@ -4,8 +4,9 @@
 Each trial draws a database (count, length mix, alphabet use), a query or a
 query pair, a scoring matrix (BLOSUM62, random symmetric, random asymmetric,
 extreme int8), gap penalties (including 0 and very large), a tile (default or
-any compiled one) and a path (resident single, resident query pair, streamed),
-then compares every score and the top-k with the oracle.
+any compiled one), the cross-pass wavefront (off / auto / forced) and a path
+(resident single, resident query pair, streamed), then compares every score and
+the top-k with the oracle.
 
     python tests/report_stress.py [--seconds 600] [--seed 1]
 
@@ -93,6 +94,8 @@ def main():
         path = ["single", "single", "pair", "streamed"][int(rng.integers(0, 4))]
         tile = (0, 0) if rng.random() < 0.5 else tiles[int(rng.integers(0, len(tiles)))]
         sw.sw_set_tile(*tile)
+        wave = int(rng.choice([-1, 0, 1, 1]))   # cross-pass wavefront off / auto / forced
+        sw.sw_set_wave(wave)
         try:
             if path == "streamed":
                 sw.sw_db_load_streamed(db.residues, db.offsets, int(rng.integers(1, 64)) * 4096)
@@ -111,7 +114,7 @@ def main():
                 bad = np.nonzero(g != exp)[0]
                 if bad.size:
                     ok = False
-                    print(json.dumps({"trial": trials, "path": path, "tile": tile, "matrix": mname, "gaps": [go, ge],
+                    print(json.dumps({"trial": trials, "path": path, "tile": tile, "wave": wave, "matrix": mname, "gaps": [go, ge],
                                       "m": len(qq), "count": db.count, "mismatches": int(bad.size),
                                       "first": bad[:5].tolist(), "got": g[bad[:5]].tolist(),
                                       "exp": exp[bad[:5]].tolist()}), flush=True)
@@ -127,6 +130,7 @@ def main():
             fails += 1
             print(json.dumps({"trial": trials, "path": path, "error": str(e)}), flush=True)
     sw.sw_set_tile(0)
+    sw.sw_set_wave(0)
     print(json.dumps({"trials": trials, "failures": fails, "cells": cells, "seconds": args.seconds}), flush=True)
     sys.exit(1 if fails else 0)
 
