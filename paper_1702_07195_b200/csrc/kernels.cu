@@ -178,7 +178,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   constexpr int QP_U4 = kNL * LS / 16;
   constexpr int DESC_U4 = kNL * kNL;
   extern __shared__ uint4 smem[];
-  for (int i = threadIdx.x; i < DESC_U4; i += blockDim.x) smem[i] = p.desc[i];
+  {
+    const uint4 *gq = p.qp + (size_t)p.pass * QP_U4;
+    for (int i = threadIdx.x; i < DESC_U4; i += blockDim.x) smem[i] = p.desc[i];
+    for (int i = threadIdx.x; i < QP_U4; i += blockDim.x) smem[DESC_U4 + i] = gq[i];
+  }
 
   const int lane = threadIdx.x & 31;
   const int t = lane & (G - 1);
@@ -232,14 +236,10 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   // until pass p's cursor is exhausted, then moves to pass p+1.  An item of
   // pass p reads the boundary and score chain that pass p-1 writes, after
   // checking pass p-1's published progress on that item.
-  const int pass_end = WAVE ? p.npass : p.pass + 1;
-  for (int pass = p.pass; pass < pass_end; ++pass) {
-  __syncthreads();   // every group of the CTA has left the previous slice
-  {
-    const uint4 *gq = p.qp + (size_t)pass * QP_U4;
-    for (int i = threadIdx.x; i < QP_U4; i += blockDim.x) smem[DESC_U4 + i] = gq[i];
-  }
-  __syncthreads();
+  // (Without WAVE the do-while runs once; the profile slice of p.pass was
+  // loaded in the prologue.)
+  int pass = p.pass;
+  do {
   int *const counter = WAVE ? p.pcounters + pass : p.counter;
   const uint2 *const bnd_in = WAVE ? (pass > 0 ? p.bndbuf[(pass - 1) & 1] : nullptr) : p.bnd_in;
   uint2 *const bnd_out = WAVE ? (pass + 1 < p.npass ? p.bndbuf[pass & 1] : nullptr) : p.bnd_out;
@@ -504,7 +504,14 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         st_release(prog_out + cur_it, min(cur_ncols, max(0, sdone - (G - 1))));
     }
   }
-  }   // passes
+  if (WAVE) {   // next pass: every group of the CTA has left this slice
+    if (++pass >= p.npass) break;
+    __syncthreads();
+    const uint4 *gq = p.qp + (size_t)pass * QP_U4;
+    for (int i = threadIdx.x; i < QP_U4; i += blockDim.x) smem[DESC_U4 + i] = gq[i];
+    __syncthreads();
+  }
+  } while (WAVE);
 }
 
 // Scores of one pass from the per-column score chain: the value at a
