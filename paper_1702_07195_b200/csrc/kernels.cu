@@ -93,6 +93,26 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   return v;
 }
 
+// 1-D bulk copy global -> shared (TMA engine, cp.async.bulk) completing on an
+// mbarrier: one thread arms the barrier with the byte count and issues the
+// copies; every thread waits on the barrier's phase.
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(mbar), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  asm volatile("{\n\t.reg .pred P;\n"
+               "WAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+               "\t@!P bra WAIT_%=;\n}" :: "r"(mbar), "r"(phase) : "memory");
+}
+
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -178,10 +198,20 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   constexpr int QP_U4 = kNL * LS / 16;
   constexpr int DESC_U4 = kNL * kNL;
   extern __shared__ uint4 smem[];
+  __shared__ uint64_t s_mbar;
   {
-    const uint4 *gq = p.qp + (size_t)p.pass * QP_U4;
-    for (int i = threadIdx.x; i < DESC_U4; i += blockDim.x) smem[i] = p.desc[i];
-    for (int i = threadIdx.x; i < QP_U4; i += blockDim.x) smem[DESC_U4 + i] = gq[i];
+    // the descriptor table and this pass's profile slice arrive by two 1-D
+    // bulk copies (TMA) on one mbarrier
+    const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    if (threadIdx.x == 0) {
+      mbar_init(mbar, 1);
+      mbar_arm(mbar, (DESC_U4 + QP_U4) * 16);
+      bulk_g2s(sbase, p.desc, DESC_U4 * 16, mbar);
+      bulk_g2s(sbase + DESC_U4 * 16, p.qp + (size_t)p.pass * QP_U4, QP_U4 * 16, mbar);
+    }
+    __syncthreads();   // the barrier is initialised before anyone waits on it
+    mbar_wait(mbar, 0);
   }
 
   const int lane = threadIdx.x & 31;
