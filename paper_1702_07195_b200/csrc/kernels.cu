@@ -648,30 +648,50 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
 #pragma unroll
       for (int r = 0; r < R; ++r) { H[r] = 0; E[r] = 0; }
       int S = 0, hout = 0, fout = 0, hprev = 0, code = kNul;
-      int cring[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) cring[u] = (first && u < n) ? (int)res[u] : kNul;
+      // Lane 0's column inputs (letter, boundary H and F of the row above) are
+      // fetched 32 columns at a time, one column per lane, coalesced and one
+      // 32-column block ahead, and handed to lane 0 by shuffle: no dependent
+      // global load per column.  Columns >= n read as NUL with a zero boundary.
+      auto fetch = [&](int cb, int &r, int &bh, int &bf) {
+        const int c = cb + lane;
+        r = kNul;
+        bh = 0;
+        bf = 0;
+        if (c < n) {
+          r = (int)res[c];
+          if (bin) {
+            const uint2 b = bin[c];
+            bh = (int)b.x;
+            bf = (int)b.y;
+          } else if (b16) {                 // exact 16-bit boundary, unbiased
+            const uint2 b = b16[c];
+            bh = (int)((b.x >> (16 * half)) & 0xffffu) - kBias16;
+            bf = (int)((b.y >> (16 * half)) & 0xffffu) - kBias16;
+          }
+        }
+      };
+      int rcur, hcur, fcur, rnxt, hnxt, fnxt;
+      fetch(0, rcur, hcur, fcur);
+      fetch(32, rnxt, hnxt, fnxt);
       const int nsteps = (n + 31 + 3) & ~3;
       for (int c0 = 0; c0 < nsteps; c0 += 4) {
+        if (c0 > 0 && (c0 & 31) == 0) {    // warp-uniform
+          rcur = rnxt;
+          hcur = hnxt;
+          fcur = fnxt;
+          fetch(c0 + 32, rnxt, hnxt, fnxt);
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int c = c0 + u;
           const int code_up = __shfl_up_sync(0xffffffffu, code, 1);
           const int hu_up = __shfl_up_sync(0xffffffffu, hout, 1);
           const int fu_up = __shfl_up_sync(0xffffffffu, fout, 1);
-          int bh = 0, bf = 0;
-          if (first && bin && c < n) {
-            const uint2 b = bin[c];
-            bh = (int)b.x;
-            bf = (int)b.y;
-          }
-          if (first && b16 && c < n) {       // exact 16-bit boundary, unbiased
-            const uint2 b = b16[c];
-            bh = (int)((b.x >> (16 * half)) & 0xffffu) - kBias16;
-            bf = (int)((b.y >> (16 * half)) & 0xffffu) - kBias16;
-          }
-          code = first ? cring[u] : code_up;
-          if (first) cring[u] = (c + 4 < n) ? (int)res[c + 4] : kNul;
+          const int sel = c & 31;
+          const int rc = __shfl_sync(0xffffffffu, rcur, sel);
+          const int bh = (int)imad((uint32_t)__shfl_sync(0xffffffffu, hcur, sel), 1u - nfirst, 0u);
+          const int bf = (int)imad((uint32_t)__shfl_sync(0xffffffffu, fcur, sel), 1u - nfirst, 0u);
+          code = first ? rc : code_up;
           const int hu = hu_up * nfirst + bh;
           int F = fu_up * nfirst + bf;
           const uint32_t qa = sbase + (uint32_t)code * (K4 * 32 * 16);
