@@ -192,6 +192,35 @@ def test_rescoring_seeded_from_pass_boundaries():
         sw.sw_set_tile(0)
 
 
+def test_rescoring_short_sequences_at_fetch_block_edges():
+    """The 32-bit kernel fetches lane 0's column inputs in blocks of 32 columns
+    (DESIGN.md 4.3).  With every substitution +127 and prohibitive gaps, the
+    score is the closed form 127 * min(n, m) (an ungapped diagonal run), so
+    sequences from 129 residues on are flagged; lengths around the multiples of
+    32 put the sequence end at every position of a fetch block, for flagging in
+    the first pass (row 0) and in a later one (64-row passes)."""
+    M = np.full((24, 24), 127, np.int8)
+    lens = [0, 1, 31, 32, 33, 63, 64, 65, 127, 128, 129, 130, 159, 160, 161, 191, 192, 193,
+            223, 224, 225, 255, 256, 257, 300, 319, 320, 321, 511, 512, 513, 1000]
+    rng = np.random.default_rng(77)
+    db = _db([rng.integers(0, 24, n).astype(np.uint8) for n in lens])
+    sw.sw_db_load(db.residues, db.offsets)
+    try:
+        for m in (150, 300, 700):
+            q = rng.integers(0, 24, m).astype(np.uint8)
+            closed = np.array([127 * min(n, m) for n in lens], np.int32)
+            exp = oracle.batch(q, db.residues, db.offsets, M, 30000, 30000)
+            assert (exp == closed).all()
+            for G, R in ((0, 0), (8, 8), (32, 29)):
+                sw.sw_set_tile(G, R)
+                got = sw.sw_search(q, M, 30000, 30000)
+                st = sw.sw_last_stats()
+                assert (got == closed).all(), (m, G, R, [(lens[i], int(got[i])) for i in np.nonzero(got != closed)[0][:5]])
+                assert st["flagged"] == int((closed >= st["flag_threshold"]).sum()) > 0
+    finally:
+        sw.sw_set_tile(0)
+
+
 def test_adversarial_mixed_with_planted_copies():
     w = si.config4(scale=0.002)   # 400 sequences incl. long ones and 8 planted copies
     got = _check_db(w.db, w.queries[0], label="cfg4 small")
