@@ -35,6 +35,9 @@
 
 // SW_ROWAHEAD: 1 = biased rows form the next row's diagonal add before the
 // current row's H is overwritten (see the pass kernel); 0 = plain row order.
+#ifndef SW_BRING
+#define SW_BRING 0   // 1: boundary prefetch ring in every boundary-reading kernel (experiment)
+#endif
 #ifndef SW_ROWAHEAD
 #define SW_ROWAHEAD 1
 #endif
@@ -197,6 +200,12 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   constexpr int LS = KC * G * 16;           // bytes per letter in the profile slice
   constexpr int QP_U4 = kNL * LS / 16;
   constexpr int DESC_U4 = kNL * kNL;
+  // Lane G-1 prefetches the previous pass's boundary U columns ahead through a
+  // register ring only in the wavefront kernel; the per-pass boundary-reading
+  // kernel loads it at the start of the column (the rows hide the latency):
+  // the ring's 8 registers push that variant past the register cap (spills,
+  // register shuffles at the loop back-edge).
+  constexpr bool BRING = WAVE || SW_BRING;
   extern __shared__ uint4 smem[];
   __shared__ uint64_t s_mbar;
   {
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
           for (int u = 1; u <= U; ++u) {
             sring[u % U] = __ldg(sptr + u);
-            if (BIN)
+            if (BIN && BRING)
               bring[u % U] = u < bcols ? (WAVE ? ld_cg_v2(bptr + u) : __ldg(bptr + u)) : make_uint2(kB2, kB2);
             if (WAVE) scring[u % U] = u < bcols ? ld_cg(scin + u) : 0u;
           }
@@ -393,13 +402,17 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
                                       : (sptr + u + 1 + U - p.stream >= p.col_lo &&
                                          sptr + u + 1 + U - p.stream < p.col_hi));
         sring[(u + 1) % U] = __ldg(sptr + u + 1 + U);
-        if (BIN) {
+        if (BIN && BRING) {
           bnext = bring[(u + 1) % U];
           SW_CHECK(u + 1 + U >= bcols || (bptr + u + 1 + U - bnd_in >= p.col_lo &&
                                            bptr + u + 1 + U - bnd_in < p.col_hi));
           bring[(u + 1) % U] = (u + 1 + U < bcols)
                                    ? (WAVE ? ld_cg_v2(bptr + u + 1 + U) : __ldg(bptr + u + 1 + U))
                                    : make_uint2(kB2, kB2);
+        } else if (BIN) {
+          // no ring: the boundary is loaded here and first used after the rows
+          SW_CHECK(u + 1 >= bcols || (bptr + u + 1 - bnd_in >= p.col_lo && bptr + u + 1 - bnd_in < p.col_hi));
+          bnext = (u + 1 < bcols) ? __ldg(bptr + u + 1) : make_uint2(kB2, kB2);
         }
         if (WAVE) {
           scnext = scring[(u + 1) % U];
@@ -975,48 +988,49 @@ constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
 
 // Measured full-row throughput (GCUPS) of each tile's pass kernel on one
 // B200, biased arithmetic (configs[1] at 0.3 scale; tools/calibrate_tiles.py,
-// profiles/r01_tile_calibration_biased.jsonl): eff0 = first pass (query of G*R),
-// eff1 = a pass reading the previous pass's boundary (2*G*R minus G*R).
+// profiles/r01_tile_calibration_biased.jsonl): eff0 = first pass (query of G*R;
+// mean of two runs), eff1 = a pass reading the previous pass's boundary (2*G*R
+// minus G*R; measured after the boundary ring was dropped from that variant).
 // The tile choice predicts time ~ G*R * (1/eff0 + (P-1)/eff1).
 struct TileEff { int G, R; float eff0, eff1; };
 const TileEff kTileEff[] = {
-    {8, 8, 4234.8f, 3414.0f},
-    {8, 12, 4899.9f, 4200.3f},
-    {8, 16, 5157.3f, 4594.1f},
-    {8, 18, 5399.9f, 4767.3f},
-    {8, 20, 5480.0f, 5097.9f},
-    {8, 22, 5513.1f, 5137.2f},
-    {8, 24, 5577.7f, 5263.6f},
-    {8, 26, 5657.6f, 5260.6f},
-    {8, 28, 5733.4f, 5262.6f},
-    {8, 29, 5734.4f, 5325.3f},
-    {8, 30, 5748.1f, 5307.2f},
-    {8, 32, 5808.6f, 5370.7f},
-    {16, 8, 4333.4f, 3601.8f},
-    {16, 12, 4959.5f, 4343.8f},
-    {16, 16, 5219.7f, 4719.4f},
-    {16, 18, 5430.5f, 4867.5f},
-    {16, 20, 5514.0f, 5109.5f},
-    {16, 22, 5565.4f, 5176.6f},
-    {16, 24, 5610.8f, 5316.2f},
-    {16, 26, 5690.3f, 5307.1f},
-    {16, 28, 5761.7f, 5320.6f},
-    {16, 29, 5765.1f, 5399.8f},
-    {16, 30, 5792.9f, 5369.6f},
-    {16, 32, 5845.3f, 5443.5f},
-    {32, 8, 4287.5f, 3595.9f},
-    {32, 12, 4992.9f, 4392.8f},
-    {32, 15, 5103.7f, 4624.2f},
-    {32, 16, 5189.7f, 4820.9f},
-    {32, 18, 5383.7f, 5021.3f},
-    {32, 20, 5479.9f, 5096.2f},
-    {32, 22, 5467.9f, 5102.7f},
-    {32, 24, 5465.8f, 5249.9f},
-    {32, 26, 5607.0f, 5278.3f},
-    {32, 28, 5573.6f, 5404.2f},
-    {32, 29, 5543.5f, 5350.3f},
-    {32, 30, 5509.7f, 5307.7f},
-    {32, 32, 5702.6f, 5281.3f}};
+    {8, 8, 4220.0f, 3476.3f},
+    {8, 12, 4904.7f, 4338.7f},
+    {8, 16, 5189.6f, 4876.9f},
+    {8, 18, 5389.9f, 4978.0f},
+    {8, 20, 5486.9f, 5131.1f},
+    {8, 22, 5527.5f, 5230.0f},
+    {8, 24, 5580.8f, 5323.5f},
+    {8, 26, 5643.8f, 5434.3f},
+    {8, 28, 5677.0f, 5468.9f},
+    {8, 29, 5748.0f, 5488.7f},
+    {8, 30, 5748.6f, 5465.4f},
+    {8, 32, 5789.5f, 5431.1f},
+    {16, 8, 4316.1f, 3671.4f},
+    {16, 12, 4962.9f, 4472.8f},
+    {16, 16, 5249.9f, 4964.5f},
+    {16, 18, 5428.1f, 5047.1f},
+    {16, 20, 5525.2f, 5188.2f},
+    {16, 22, 5564.0f, 5299.8f},
+    {16, 24, 5612.9f, 5354.9f},
+    {16, 26, 5678.6f, 5478.5f},
+    {16, 28, 5709.1f, 5491.1f},
+    {16, 29, 5787.8f, 5524.9f},
+    {16, 30, 5779.9f, 5492.1f},
+    {16, 32, 5826.2f, 5454.0f},
+    {32, 8, 4274.6f, 3776.3f},
+    {32, 12, 4914.3f, 4575.2f},
+    {32, 15, 5127.2f, 4816.1f},
+    {32, 16, 5177.9f, 4822.6f},
+    {32, 18, 5394.9f, 5005.7f},
+    {32, 20, 5450.8f, 5187.7f},
+    {32, 22, 5460.6f, 5261.3f},
+    {32, 24, 5479.5f, 5377.5f},
+    {32, 26, 5574.1f, 5332.9f},
+    {32, 28, 5517.0f, 5410.3f},
+    {32, 29, 5564.6f, 5387.9f},
+    {32, 30, 5568.9f, 5423.8f},
+    {32, 32, 5717.9f, 5473.8f}};
 
 TileEff tile_eff(int G, int R) {
   for (const TileEff &e : kTileEff)
