@@ -34,6 +34,8 @@ if os.environ.get("SW_ROWAHEAD"):  # row order of the biased cell loop (experime
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ROWAHEAD=" + os.environ["SW_ROWAHEAD"]]
 if os.environ.get("SW_UNROLL"):    # columns per unrolled block (experiment)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_UNROLL=" + os.environ["SW_UNROLL"]]
+if os.environ.get("SW_BRING"):    # boundary prefetch ring in every boundary-reading kernel (experiment)
+    NVCC_FLAGS = NVCC_FLAGS + ["-DSW_BRING=" + os.environ["SW_BRING"]]
 if os.environ.get("SW_S32ROWS"):  # rows per lane of the 32-bit kernel (experiment)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_S32ROWS=" + os.environ["SW_S32ROWS"]]
 if os.environ.get("SW_DEBUG"):    # device-side bounds checks (slow; debug builds)
