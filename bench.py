@@ -306,8 +306,9 @@ def run_ours(args):
     stream.synchronize()
     st = sw.sw_last_stats()
     # qp build, P x (pass kernel + score gather + flag compaction + s32 re-scoring
-    # of that pass's newly flagged sequences), top-k (2 + decode)
-    per_step_kernels = 1 + 4 * st["passes"] + 3
+    # of that pass's newly flagged sequences), P-1 item-skip launches (between
+    # passes), top-k (2 + decode)
+    per_step_kernels = 1 + 4 * st["passes"] + max(0, st["passes"] - 1) + 3
     if dist:
         dist.barrier()
     torch.cuda.synchronize()

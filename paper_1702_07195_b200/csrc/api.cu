@@ -69,11 +69,12 @@ struct Image {
   DevBuf<uint32_t> stream;  // column words
   DevBuf<Item> items;
   DevBuf<int64_t> endcol;   // per sequence: 2 * END column + half
+  DevBuf<int32_t> slots;    // slot -> original sequence (items' sequences in column order)
   int64_t total_cols = 0;
   int64_t max_item_cols = 0;  // longest work item (columns)
   int num_items = 0;
   void release() {
-    stream.release(); items.release(); endcol.release();
+    stream.release(); items.release(); endcol.release(); slots.release();
     total_cols = 0;
     max_item_cols = 0;
     num_items = 0;
@@ -108,6 +109,7 @@ struct State {
   DevBuf<uint4> desc;
   DevBuf<int32_t> qp32, qp32b;
   DevBuf<uint2> bnd;        // 2 * max_cols
+  DevBuf<int32_t> skip;     // per item: dead leading columns for the next pass
   DevBuf<uint2> dummy;      // scratch for idle-lane stores (16-B slot per thread)
   DevBuf<uint32_t> nulcols; // 16 NUL column words
   DevBuf<uint2> zerocols;   // 16 zero boundary columns
@@ -174,7 +176,7 @@ struct State {
     scores.release(); bscores.release(); flagged.release(); flagged2.release(); flag_list.release();
     flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release(); progress.release();
     query.release(); query2.release(); matrix.release(); qp.release(); desc.release(); qp32.release();
-    qp32b.release(); bnd.release();
+    qp32b.release(); bnd.release(); skip.release();
     scratch32.release(); dummy.release(); nulcols.release(); zerocols.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
     loaded = false;
     has_search = false;
@@ -385,6 +387,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(g.pcounters.ensure((size_t)nch * P));
   CUDA_TRY(cudaMemsetAsync(g.pcounters.p, 0, sizeof(int) * (size_t)nch * P, st));
   if (P > 1 && g.bnd.n < (size_t)span * 2) CUDA_TRY(g.bnd.ensure((size_t)span * 2));
+  if (!strm && !pair && P > 1) CUDA_TRY(g.skip.ensure((size_t)std::max(1, I.num_items)));
   CUDA_TRY(cudaEventRecord(g.ev[1], st));
   if (wave) {
     CUDA_TRY(g.progress.ensure((size_t)P * std::max(1, I.num_items)));
@@ -466,6 +469,10 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       p.thresh = thresh;
       p.zero = 0u;
       p.one = 1u;
+      // resident single-query passes after the first start each item behind
+      // its leading run of flagged sequences (item_skip_kernel below)
+      const bool skipping = !strm && !pair && P > 1;
+      p.skip = (skipping && pass > 0) ? g.skip.p : nullptr;
       const size_t pe = 2 * (size_t)(k * P + pass);
       while (g.pev.size() < pe + 2) {
         cudaEvent_t e;
@@ -486,6 +493,8 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
                                     pair ? d_scores2 : nullptr, pair ? g.flagged2.p : nullptr, pass, thresh, st));
         if (pass + 1 < 255)
           for (int k = 0; k < (pair ? 2 : 1); ++k) CUDA_TRY(rescore(k, pass, p.bnd_in));
+        if (skipping && pass + 1 < P)
+          CUDA_TRY(launch_item_skip(I.items.p, I.num_items, I.slots.p, g.offs.p, g.flagged.p, g.skip.p, st));
       }
     }
     if (strm) CUDA_TRY(cudaEventRecord(g.ev_free[b], st));
@@ -642,6 +651,8 @@ int load_impl(const uint8_t *residues, const int64_t *offsets, int64_t count, in
     CUDA_TRY(I.endcol.ensure(H.endcol.size()));
     CUDA_TRY(cudaMemcpy(I.stream.p, H.stream.data(), H.stream.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(I.endcol.p, H.endcol.data(), H.endcol.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(I.slots.ensure(H.slots.size()));
+    CUDA_TRY(cudaMemcpy(I.slots.p, H.slots.data(), H.slots.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
   if (strm) {
     const HostImage &H = himg[0];

@@ -294,8 +294,9 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       if (last) it = atomicAdd(counter, 1);
       it = __shfl_sync(gmask, it, gbase + G - 1);
       if (it < p.num_items) {
-        const int64_t c0 = p.items[it].col_begin;
-        const int ncols = p.items[it].ncols;
+        const int sk = (!WAVE && p.skip) ? p.skip[it] : 0;   // dead leading columns (flagged)
+        const int64_t c0 = p.items[it].col_begin + sk;
+        const int ncols = p.items[it].ncols - sk;
         rem = (ncols + G - 1 + U - 1) & ~(U - 1);
         inc = (uint32_t)U;
         sptr = p.stream + c0;
@@ -810,6 +811,37 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
   }
 }
 
+// Leading columns of each item that hold only already-flagged sequences in
+// both halves (half A and half B each walk their sequences in column order
+// until the first unflagged one; a half whose sequences are all flagged is
+// dead to the item's end).  Starting a later pass there is exact for every
+// unflagged sequence: the column after a sequence's NUL separator starts from
+// H = E = F = 0, which is what a fresh item start gives, and a half whose dead
+// run is longer only recomputes part of a flagged sequence, whose 16-bit
+// results nobody reads again (the gather skips flagged sequences; their s32
+// re-scoring was seeded in the pass that flagged them).
+__global__ void item_skip_kernel(const Item *__restrict__ items, int nitems, const int32_t *__restrict__ slots,
+                                 const int64_t *__restrict__ offs, const uint8_t *__restrict__ flagged,
+                                 int32_t *skip) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x) {
+    const Item it = items[i];
+    int64_t dead[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int32_t s0 = h ? it.seqB : it.seqA, n = h ? it.nB : it.nA;
+      int64_t d = 0;
+      int k = 0;
+      for (; k < n; ++k) {
+        const int32_t o = slots[s0 + k];
+        if (!flagged[o]) break;
+        d += offs[o + 1] - offs[o] + 2;   // residues, END, NUL
+      }
+      dead[h] = k == n ? (int64_t)it.ncols : d;
+    }
+    skip[i] = (int32_t)min(min(dead[0], dead[1]), (int64_t)it.ncols);
+  }
+}
+
 __global__ void flag_compact_kernel(const uint8_t *__restrict__ flagged, int64_t count, int32_t *list,
                                     int *n, int want) {
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < count;
@@ -1115,6 +1147,13 @@ cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint3
   if (count <= 0) return cudaSuccess;
   sw16_gather_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, scores, flagged, scores2, flagged2,
                                                             pass, thresh, seq_idx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_item_skip(const Item *items, int nitems, const int32_t *slots, const int64_t *offs,
+                             const uint8_t *flagged, int32_t *skip, cudaStream_t st) {
+  if (nitems < 1) return cudaSuccess;
+  item_skip_kernel<<<grid_for(nitems, 256), 256, 0, st>>>(items, nitems, slots, offs, flagged, skip);
   return cudaGetLastError();
 }
 

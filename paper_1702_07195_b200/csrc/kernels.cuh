@@ -50,6 +50,10 @@ struct SW16Params {
   int *pcounters;
   int *progress;
   uint2 *bndbuf[2];
+  // Per item: leading columns to skip in this pass (per-pass launches only),
+  // or null.  They hold only sequences already flagged in both halves
+  // (item_skip_kernel), whose 16-bit results are no longer used.
+  const int32_t *skip;
 };
 
 struct SW32Params {
@@ -116,6 +120,10 @@ cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint3
 // Compacts the indices i with flagged[i] == want (want == 0: any non-zero).
 cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n, int want,
                                 cudaStream_t st);
+// Per item, the leading columns whose sequences are all flagged (both halves);
+// skip[i] = min over the halves.
+cudaError_t launch_item_skip(const Item *items, int nitems, const int32_t *slots, const int64_t *offs,
+                             const uint8_t *flagged, int32_t *skip, cudaStream_t st);
 #ifndef SW_S32ROWS
 #define SW_S32ROWS 24
 #endif

@@ -221,6 +221,42 @@ def test_rescoring_short_sequences_at_fetch_block_edges():
         sw.sw_set_tile(0)
 
 
+def test_later_passes_skip_flagged_leading_sequences():
+    """Passes after the first start each item behind its leading run of
+    flagged sequences (both halves).  Equal-length W-rich
+    copies pair up at the head of items like cfg4's planted copies; some items
+    have a flagged sequence in one half only, or a flagged run longer in one
+    half than in the other, and short unflagged sequences follow them.  Every
+    score must still equal the oracle's, for small tiles (many passes) and the
+    default one."""
+    rng = np.random.default_rng(41)
+    block = encode("W" * 1800)
+    seqs = [block.copy() for _ in range(24)]
+    seqs += [np.concatenate([encode("W" * 1700), si.rr_residues(rng, 100)]) for _ in range(5)]
+    seqs += [si.rr_residues(rng, 1800) for _ in range(7)]                  # same length, unflagged
+    seqs += [si.rr_residues(rng, int(L)) for L in rng.integers(1, 300, 300)]
+    order = rng.permutation(len(seqs))
+    seqs = [seqs[i] for i in order]
+    db = _db(seqs)
+    sw.sw_db_load(db.residues, db.offsets)
+    try:
+        for x in (0, 300):
+            q = encode("A" * x + "W" * 2000)
+            exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
+            for G, R in ((0, 0), (8, 8), (16, 12), (32, 16)):
+                sw.sw_set_tile(G, R)
+                got = sw.sw_search(q, BLOSUM62, 10, 2)
+                st = sw.sw_last_stats()
+                assert st["passes"] > 1 or G == 0
+                assert (got == exp).all(), (x, G, R, np.nonzero(got != exp)[0][:5])
+                assert st["flagged"] == int((exp >= st["flag_threshold"]).sum()) >= 29
+                idx, top = sw.sw_topk(10)
+                eidx, etop = oracle.topk(exp, 10)
+                assert (idx == eidx).all() and (top == etop).all()
+    finally:
+        sw.sw_set_tile(0)
+
+
 def test_adversarial_mixed_with_planted_copies():
     w = si.config4(scale=0.002)   # 400 sequences incl. long ones and 8 planted copies
     got = _check_db(w.db, w.queries[0], label="cfg4 small")
