@@ -16,7 +16,9 @@
 // adds wrap instead of saturating (R7): a sequence whose stored
 // 16-bit score reaches 32768 - smax is flagged and re-scored exactly by the
 // s32 kernel ("recalculated using the next wider integer range"),
-// starting from the last exact 16-bit pass boundary.
+// starting from the last exact 16-bit pass boundary; later
+// 16-bit passes start each work item behind its leading run of flagged
+// sequences (item_skip_kernel).
 //
 // Mapping: a *group* of G lanes (G in 8/16/32) is a systolic
 // array over the query: lane t owns R consecutive query rows of the current
