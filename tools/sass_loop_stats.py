@@ -31,11 +31,12 @@ def main():
     ap.add_argument("--bin", type=int, default=0)
     ap.add_argument("--U", type=int, default=0, help="unroll U of the instantiation (0: SW_UNROLL or 4)")
     ap.add_argument("-D", action="append", default=[])
+    ap.add_argument("--xptxas", action="append", default=[], help="extra ptxas option, e.g. --register-usage-level=8")
     args = ap.parse_args()
     U = args.U or int(next((d.split("=")[1] for d in args.D if d.startswith("SW_UNROLL=")), 4))
     with tempfile.TemporaryDirectory() as td:
         cub = os.path.join(td, "k.cubin")
-        cmd = [B._nvcc()] + B.NVCC_FLAGS + ["-D" + d for d in args.D] + ["-cubin", "-o", cub,
+        cmd = [B._nvcc()] + B.NVCC_FLAGS + ["-D" + d for d in args.D] + [f"-Xptxas={x}" for x in args.xptxas] + ["-cubin", "-o", cub,
                                                                           os.path.join(B.CSRC, "kernels.cu")]
         subprocess.run(cmd, check=True)
         sass = subprocess.run(["cuobjdump", "-sass", cub], check=True, capture_output=True, text=True).stdout
@@ -85,7 +86,7 @@ def main():
         else:
             c["other"] += 1
     n = len(body)
-    print(f"tile {args.G}x{args.R} bin={args.bin} U={U} {' '.join(args.D)}: {n} instructions / {U} columns = "
+    print(f"tile {args.G}x{args.R} bin={args.bin} U={U} {' '.join(args.D + args.xptxas)}: {n} instructions / {U} columns = "
           f"{n / U:.1f} per column; " + ", ".join(f"{k} {v / U:.1f}" for k, v in sorted(c.items())) +
           f"; moves {movs / U:.1f}; ALU-pipe cycles {2 * c['alu'] / U:.1f} vs issue {n / U:.1f} per column")
 
