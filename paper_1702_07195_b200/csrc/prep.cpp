@@ -14,6 +14,7 @@
 // and item capacities shrink geometrically ("guided") so the dynamic
 // longest-first claim ("dynamically distributed ... as soon as
 // the threads become idle") ends with small items.
+#include <cstdlib>
 #include "swdb_internal.h"
 
 #include <algorithm>
@@ -79,6 +80,16 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
                    [&](int32_t a, int32_t b) { return len[a] > len[b]; });
 
   if (target_groups < 1) target_groups = 1;
+  // Guided item sizes: capacity = remaining columns / (item_div * groups),
+  // clipped to [256, item_max].  Measured on one B200: fewer,
+  // longer items pay the group's pipeline fill/drain less often; item_div 1
+  // and item_max 16384 beat 3 / 8192 by 0.4-0.7% on cfg1, cfg2 and cfg4, and
+  // item_div 0.5 loses 7% on cfg1 (tail).  SW_ITEM_DIV / SW_ITEM_MAX override
+  // them for experiments.
+  double item_div = 1.0;
+  if (const char *e = std::getenv("SW_ITEM_DIV")) item_div = std::max(0.25, std::atof(e));
+  int64_t item_max = 16384;
+  if (const char *e = std::getenv("SW_ITEM_MAX")) item_max = std::max<int64_t>(256, std::atoll(e));
   // columns still to place (pair columns: two sequences per column)
   int64_t remaining = single ? total_stream : (total_stream + 1) / 2;
   int64_t lo = 0, hi = count - 1;
@@ -87,8 +98,8 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
   std::vector<Tmp> tmp;
   out.slots.reserve(count);
   while (lo <= hi) {
-    int64_t cap = remaining / (target_groups * 3);
-    cap = std::max<int64_t>(256, std::min<int64_t>(8192, cap));
+    int64_t cap = (int64_t)((double)remaining / ((double)target_groups * item_div));
+    cap = std::max<int64_t>(256, std::min<int64_t>(item_max, cap));
     halfA.clear();
     halfB.clear();
     int64_t lA = 0, lB = 0;
