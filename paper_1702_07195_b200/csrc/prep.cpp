@@ -84,12 +84,13 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
   // clipped to [256, item_max].  Measured on one B200: fewer,
   // longer items pay the group's pipeline fill/drain less often; item_div 1
   // and item_max 16384 beat 3 / 8192 by 0.4-0.7% on cfg1, cfg2 and cfg4, and
-  // item_div 0.5 loses 7% on cfg1 (tail).  SW_ITEM_DIV / SW_ITEM_MAX override
-  // them for experiments.
+  // item_div 0.5 loses 7% on cfg1 (tail); the floor 256 beats 128/512/1024.
+  // SW_ITEM_DIV / SW_ITEM_MAX / SW_ITEM_MIN override them for experiments.
   double item_div = 1.0;
   if (const char *e = std::getenv("SW_ITEM_DIV")) item_div = std::max(0.25, std::atof(e));
-  int64_t item_max = 16384;
+  int64_t item_max = 16384, item_min = 256;
   if (const char *e = std::getenv("SW_ITEM_MAX")) item_max = std::max<int64_t>(256, std::atoll(e));
+  if (const char *e = std::getenv("SW_ITEM_MIN")) item_min = std::max<int64_t>(16, std::atoll(e));
   // columns still to place (pair columns: two sequences per column)
   int64_t remaining = single ? total_stream : (total_stream + 1) / 2;
   int64_t lo = 0, hi = count - 1;
@@ -99,7 +100,7 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
   out.slots.reserve(count);
   while (lo <= hi) {
     int64_t cap = (int64_t)((double)remaining / ((double)target_groups * item_div));
-    cap = std::max<int64_t>(256, std::min<int64_t>(item_max, cap));
+    cap = std::max<int64_t>(item_min, std::min<int64_t>(item_max, cap));
     halfA.clear();
     halfB.clear();
     int64_t lA = 0, lB = 0;
