@@ -82,11 +82,14 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
   if (target_groups < 1) target_groups = 1;
   // Guided item sizes: capacity = remaining columns / (item_div * groups),
   // clipped to [256, item_max].  Measured on one B200: fewer,
-  // longer items pay the group's pipeline fill/drain less often; item_div 1
-  // and item_max 16384 beat 3 / 8192 by 0.4-0.7% on cfg1, cfg2 and cfg4, and
-  // item_div 0.5 loses 7% on cfg1 (tail); the floor 256 beats 128/512/1024.
-  // SW_ITEM_DIV / SW_ITEM_MAX / SW_ITEM_MIN override them for experiments.
-  double item_div = 1.0;
+  // longer items pay the group's pipeline fill/drain less often, but the first
+  // items must stay below one group's share of the work for the 8-lane tiles
+  // (twice as many groups as target_groups): item_div 1 is 0.2-0.3% faster on
+  // cfg1/cfg2/cfg4 than 2 but loses 35% with 8-lane tiles on cfg1; item_div 2
+  // and item_max 16384 beat 3 / 8192 by 0.1-0.5%; the floor 256 beats
+  // 128/512/1024.  SW_ITEM_DIV / SW_ITEM_MAX / SW_ITEM_MIN override them for
+  // experiments.
+  double item_div = 2.0;
   if (const char *e = std::getenv("SW_ITEM_DIV")) item_div = std::max(0.25, std::atof(e));
   int64_t item_max = 16384, item_min = 256;
   if (const char *e = std::getenv("SW_ITEM_MAX")) item_max = std::max<int64_t>(256, std::atoll(e));
