@@ -3,22 +3,34 @@
 against 1,000,000 synthetic sequences (~200 M residues), one B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 0|1|2|3|4]
 
 A *step* is one pass of the whole hot path over the resident database
 (SURVEY.md 8(a) rows a2-a6): query-profile build, the s16x2 pass kernel(s),
 saturation flag compaction + exact s32 re-scoring, and the sorting stage
 (device top-10).  Pre-processing (sw_db_load, row a1) is done once before the
 timed region, as in the paper.  GCUPS = |Q||D| /
-(t 1e9) (Eq. 4).  N > 1 (torchrun): weak scaling -- the database
-is configs[1] x N, residue-balanced over the ranks, each rank searches its
-shard and the per-rank scores and top-10 are gathered to rank 0 over NCCL and
-merged there.  Rank 0 prints one JSON line.
+(t 1e9) (Eq. 4).
+
+Multi-GPU: one process per GPU.  `--gpus N` without a
+torchrun environment re-launches itself under torch.distributed.run with N
+ranks.  Each rank generates and loads only its residue-balanced shard of the
+database; a step is every rank's search of its shard, the NCCL gather of the
+padded score vectors and top-10 candidates to rank 0, and on rank 0 the
+device scatter of all scores to original database order plus the merged
+top-10 (parallel.ShardedSearch).  Time = max over ranks of the device time.
+  --config 0/1 (default 1): weak scaling, database = configs[k] x N.
+  --config 2/3/4: strong scaling, the configuration's fixed database split
+                  over the N ranks (configs[2]: 6.5 M sequences; configs[3]:
+                  its 20 queries as query pairs, all in one step).
+Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -39,9 +51,10 @@ ALU_LANE_OPS_PER_CLK_PER_SM = 64      # measured (profiles/r01_dpx_microbench.js
 # biased arithmetic 4.5 per s16x2 pair of cells (VIMNMX3 + 3 VIADDMNMX + 1/2
 # VIMNMX3; the diagonal add runs on the FMA pipe), relu form 5.5 DPX.
 ALU_PER_CELL = {1: 2.25, 0: 2.75}
+WEAK_CONFIGS = (0, 1)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
@@ -52,7 +65,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist", action="store_true",
                     help="initialise the NCCL process group even at world size 1 (exercises the gather path)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -60,6 +73,24 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(args) -> int:
+    """`--gpus N` outside torchrun: start N ranks (one process per GPU) with
+    torch.distributed.run on this node; rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
 
 
 class ClockSampler:
@@ -119,6 +150,17 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -129,14 +171,16 @@ def measured_peaks():
 
 def ncu_pipes():
     """ALU-pipe thread instructions per cell of the pass kernel, measured by ncu
-    on the bench launch (profiles/r01b_ncu_pipes.json), for the roofline with
+    on the bench launch (profiles/ncu_pipes.json), for the roofline with
     the kernel's measured I_pipe."""
-    p = os.path.join(ROOT, "profiles", "r01b_ncu_pipes.json")
-    try:
-        with open(p) as f:
-            return json.load(f).get("alu_thread_inst_per_cell")
-    except Exception:
-        return None
+    for name in ("ncu_pipes.json", "r01b_ncu_pipes.json"):
+        p = os.path.join(ROOT, "profiles", name)
+        try:
+            with open(p) as f:
+                return json.load(f).get("alu_thread_inst_per_cell")
+        except Exception:
+            continue
+    return None
 
 
 def ncu_traffic():
@@ -152,7 +196,57 @@ def ncu_traffic():
     return None
 
 
-def cpu_baseline(w, target_s: float = 12.0):
+def host_topk(x: np.ndarray, k: int) -> np.ndarray:
+    """Indices of the k largest entries, score descending, index ascending
+    (a host check of the device sorting stage, O(n))."""
+    n = x.size
+    kk = min(k, n)
+    if kk == 0:
+        return np.zeros(0, np.int64)
+    thr = np.partition(x, n - kk)[n - kk]
+    gt = np.nonzero(x > thr)[0]
+    eq = np.nonzero(x == thr)[0][:kk - gt.size]
+    cand = np.concatenate([gt, eq])
+    return cand[np.lexsort((cand, -x[cand].astype(np.int64)))]
+
+
+class Work:
+    """One rank's share of a configuration's workload (see the module doc)."""
+
+    def __init__(self, cfg: int, scale: float, world: int, rank: int, whole: bool = False):
+        from paper_1702_07195_b200.parallel import shard_arrays, shard_database
+        self.cfg = cfg
+        self.weak = cfg in WEAK_CONFIGS
+        gscale = scale * (world if self.weak else 1)
+        if whole:   # the whole (global) database on this process (reference arm)
+            world, rank = 1, 0
+        if cfg == 4:   # built from a shuffled list: generate it whole (200 k sequences), then shard
+            w = si.make_config(4, scale=gscale)
+            lens, self.queries = w.db.lengths(), w.queries
+            self.matrix, self.gap_open, self.gap_extend = w.matrix, w.gap_open, w.gap_extend
+            self.gidx = shard_database(lens, world)[rank] if world > 1 else np.arange(lens.size, dtype=np.int64)
+            res, offs = (shard_arrays(w.db.residues, w.db.offsets, self.gidx) if world > 1
+                         else (w.db.residues, w.db.offsets))
+            self.db = si.Database(res, offs)
+        else:
+            lens = si.config_lengths(cfg, gscale)
+            self.queries = si.config_queries(cfg)
+            self.matrix, self.gap_open, self.gap_extend = si.BLOSUM62, si.GAP_OPEN, si.GAP_EXTEND
+            self.gidx = shard_database(lens, world)[rank] if world > 1 else np.arange(lens.size, dtype=np.int64)
+            self.db = si.config_db_subset(cfg, self.gidx, gscale)
+        self.count_global = int(lens.size)
+        self.residues_global = int(lens.sum())
+        wn = int(round(gscale / scale)) if self.weak else 1
+        self.name = f"cfg{cfg}" + (f" x{wn} (weak)" if wn > 1 else "")
+        if scale != 1.0:
+            self.name += f" scale {scale}"
+        self.qres = int(sum(len(q) for q in self.queries))
+
+    def cells_global(self) -> int:
+        return self.qres * self.residues_global
+
+
+def cpu_baseline(w: Work, target_s: float = 12.0):
     """The oracle (oracle/, plain scalar C, one sequence per task on all host
     cores) timed on a bounded seeded sample of the same workload."""
     import oracle
@@ -175,14 +269,10 @@ def cpu_baseline(w, target_s: float = 12.0):
     oracle.batch(q, w.db.residues, w.db.offsets, w.matrix, w.gap_open, w.gap_extend, idx=idx, threads=cores)
     dt = time.perf_counter() - t0
     cells = len(q) * int(lens[idx].sum())
-    return {"value": round(cells / dt / 1e9, 3), "unit": "GCUPS", "cores": cores, "kind": "oracle",
+    return {"value": round(cells / dt / 1e9, 3), "unit": "GCUPS", "cores": cores, "cpu_model": cpu_model(),
+            "kind": "oracle",
             "sample": f"{nsamp} seeded-random sequences of the workload ({int(lens[idx].sum())} residues) "
-                      f"vs the {len(q)}-residue query, {dt:.1f} s"}
-
-
-def make_workload(args, world):
-    scale = args.scale * (world if world > 1 else 1)
-    return si.make_config(args.config, scale=scale)
+                      f"vs the {len(q)}-residue query 0 of the workload, {dt:.1f} s"}
 
 
 def run_reference(args):
@@ -190,7 +280,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     import oracle
-    w = make_workload(args, world)
+    w = Work(args.config, args.scale, world, 0, whole=True)
     q = w.queries[0]
     cores = os.cpu_count() or 1
     lens = w.db.lengths()
@@ -217,15 +307,16 @@ def run_reference(args):
             cells += len(q) * int(lens[idx].sum())
     total = sum(times)
     val = cells / total / 1e9
-    sample = f"{nsamp} sequences per step (seeded, ~{budget:.0f} s each) of {w.name}, query {len(q)}"
+    sample = f"{nsamp} sequences per step (seeded, ~{budget:.0f} s each) of {w.name}, query 0 ({len(q)})"
     line = {"metric": METRIC, "value": round(val, 3), "unit": "GCUPS", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * total / max(1, len(times)), 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "i64", "data": "synthetic",
-            "config": {"workload": w.name, "query_len": len(q), "db_sequences": w.db.count,
-                       "db_residues": w.db.total_residues},
-            "cpu_baseline": {"value": round(val, 3), "unit": "GCUPS", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+            "scaling": "weak" if args.config in WEAK_CONFIGS else "strong", "vs_baseline": None, "dtype": "i64",
+            "data": "synthetic",
+            "config": {"workload": w.name, "query_len": len(q), "db_sequences": w.count_global,
+                       "db_residues": w.residues_global},
+            "cpu_baseline": {"value": round(val, 3), "unit": "GCUPS", "cores": cores, "cpu_model": cpu_model(),
+                             "kind": "oracle", "sample": sample},
             "e2e": {"value": round(val, 3), "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -235,80 +326,51 @@ def run_ours(args):
     import torch
     import paper_1702_07195_b200 as sw
     from paper_1702_07195_b200 import build as swbuild
-    from paper_1702_07195_b200.parallel import gather_to_root, shard_arrays, shard_database
+    from paper_1702_07195_b200.parallel import LibBackend, ShardedSearch
 
     world, rank, local = dist_env()
     assert torch.cuda.is_available(), "bench needs a CUDA device"
+    if world > torch.cuda.device_count():
+        raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} CUDA devices")
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     dist = None
     if world > 1 or args.dist:
         import torch.distributed as dist
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29531")
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=dev)
+        print(f"[bench] rank {rank}/{world}: NCCL process group up on cuda:{local} "
+              f"({torch.cuda.get_device_name(local)}), NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}",
+              file=sys.stderr, flush=True)
+    if args.gpus != world and rank == 0:
+        print(f"[bench] note: --gpus {args.gpus} but WORLD_SIZE {world}; running {world} ranks",
+              file=sys.stderr, flush=True)
     if rank == 0:
         swbuild.build()
     if dist:
         dist.barrier()
 
-    w = make_workload(args, world)
-    q = w.queries[0]
-    if world > 1:
-        shards = shard_database(w.db.lengths(), world)
-        gidx = shards[rank]
-        res, offs = shard_arrays(w.db.residues, w.db.offsets, gidx)
-    else:
-        gidx = np.arange(w.db.count, dtype=np.int64)
-        res, offs = w.db.residues, w.db.offsets
-    count = int(offs.size - 1)
-    local_res = int(offs[-1])
-    sw.sw_db_load(res, offs)
+    w = Work(args.config, args.scale, world, rank)
+    count = w.db.count
+    local_res = w.db.total_residues
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    nq = len(w.queries)
 
-    dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
-    d_scores = torch.empty(count, dtype=torch.int32, device=dev)
-    d_gidx = torch.from_numpy(gidx.astype(np.int64)).to(dev)
-    d_tk_i = torch.empty(TOPK, dtype=torch.int64, device=dev)
-    d_tk_s = torch.empty(TOPK, dtype=torch.int32, device=dev)
-    nmax = count
-    if dist:
-        t = torch.tensor([count], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        nmax = int(t.item())
-    d_pad = torch.zeros(nmax, dtype=torch.int32, device=dev)
-    m_tk_i = torch.empty(TOPK, dtype=torch.int64, device=dev)
-    m_tk_s = torch.empty(TOPK, dtype=torch.int32, device=dev)
-    launches_per_step = [0]
+    search = ShardedSearch(LibBackend(sw), w.gidx, w.count_global, nq, TOPK, dev, dist=dist, world=world,
+                           rank=rank)
 
     def step():
-        sw.sw_search_dev(q, w.matrix, w.gap_open, w.gap_extend, d_scores, stream)
-        sw.sw_topk_dev(d_scores, d_gidx, count, TOPK, d_tk_i, d_tk_s, stream)
-        n = 0
-        if dist:
-            with torch.cuda.stream(stream):
-                d_pad[:count].copy_(d_scores)
-                all_sc = gather_to_root(d_pad, world, rank, dist)
-                all_ti = gather_to_root(d_tk_i, world, rank, dist)
-                all_ts = gather_to_root(d_tk_s, world, rank, dist)
-                if rank == 0:
-                    cand_i = torch.cat(all_ti)
-                    cand_s = torch.cat(all_ts)
-                    sw.sw_topk_dev(cand_s, cand_i, cand_s.numel(), TOPK, m_tk_i, m_tk_s, stream)
-                    n += 3
-                del all_sc
-        return n
+        return search.step(w.queries, w.matrix, w.gap_open, w.gap_extend, stream)
 
     for _ in range(args.warmup):
         step()
     stream.synchronize()
     st = sw.sw_last_stats()
-    # qp build, P x (pass kernel + score gather + flag compaction + s32 re-scoring
-    # of that pass's newly flagged sequences), P-1 item-skip launches (between
-    # passes), top-k (2 + decode)
-    per_step_kernels = 1 + 4 * st["passes"] + max(0, st["passes"] - 1) + 3
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -318,17 +380,18 @@ def run_ours(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     kernel_ms = []
-    extra = 0
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    l0 = sw.sw_launch_count()
     e0.record(stream)
     for _ in range(args.steps):
-        extra += step()
+        step()
         kernel_ms.append(sw.sw_last_timing()["pass_kernels_ms"])
     e1.record(stream)
     stream.synchronize()
     torch.cuda.synchronize()
+    launches = sw.sw_launch_count() - l0
     if dist:
         dist.barrier()
     clk = clocks.stop()
@@ -337,43 +400,86 @@ def run_ours(args):
         t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
+        tl = torch.tensor([float(launches)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tl, op=dist.ReduceOp.SUM)
+        launches = int(tl.item())
     ms_step = ms_total / args.steps
-    total_res = w.db.total_residues
-    gcups = len(q) * total_res / (ms_step * 1e6)
+    gcups = w.cells_global() / (ms_step * 1e6)
 
-    # ---- end to end through the public C-ABI with host buffers (rank-local)
+    # parity spot check of the assembled result on rank 0 (outside the timed region)
+    checked = None
+    if rank == 0:
+        full, ti, ts = search.result()
+        full_h = full.cpu().numpy()
+        ok = bool(np.all(full_h >= 0))
+        for qi in range(nq):
+            order = host_topk(full_h[qi], search.kk)
+            ok &= bool(np.array_equal(ti[qi].cpu().numpy(), order)
+                       and np.array_equal(ts[qi].cpu().numpy(), full_h[qi][order]))
+        checked = ok
+        assert ok, "assembled scores and merged top-k disagree"
+
+    # ---- end to end through the public C-ABI with host buffers
     e2e_val = None
-    h2d = len(q) + 576
-    d2h = count * 4 + TOPK * 12
-    if True:
-        import torch as _t
-        host_scores = _t.empty(count, dtype=_t.int32, pin_memory=True).numpy()
-        qpin = _t.empty(len(q), dtype=_t.uint8, pin_memory=True).numpy()
-        qpin[:] = q
-        mpin = _t.empty((24, 24), dtype=_t.int8, pin_memory=True).numpy()
+    h2d = w.qres + 576
+    d2h = nq * w.count_global * 4 + nq * TOPK * 12
+    if world == 1 and nq == 1 and dist is None:
+        # sw_search (pinned host scores) + sw_topk, wall clock
+        host_scores = torch.empty(count, dtype=torch.int32, pin_memory=True).numpy()
+        qpin = torch.empty(len(w.queries[0]), dtype=torch.uint8, pin_memory=True).numpy()
+        qpin[:] = w.queries[0]
+        mpin = torch.empty((24, 24), dtype=torch.int8, pin_memory=True).numpy()
         mpin[:] = w.matrix
         for _ in range(2):
             sw.sw_search(qpin, mpin, w.gap_open, w.gap_extend, out=host_scores)
             sw.sw_topk(TOPK)
-        if dist:
-            dist.barrier()
         t0 = time.perf_counter()
         ne = max(3, args.steps // 3)
         for _ in range(ne):
             sw.sw_search(qpin, mpin, w.gap_open, w.gap_extend, out=host_scores)
             sw.sw_topk(TOPK)
         dt = (time.perf_counter() - t0) / ne
+        e2e_how = "sw_search + sw_topk through the C-ABI with pinned host buffers, wall clock"
+    else:
+        # the sharded step with the host query (copied inside sw_search_dev), then
+        # rank 0 reads all assembled scores and the top-k into pinned host memory
+        if rank == 0:
+            h_full = torch.empty(nq * w.count_global, dtype=torch.int32, pin_memory=True)
+            h_ti = torch.empty((nq, TOPK), dtype=torch.int64, pin_memory=True)
+            h_ts = torch.empty((nq, TOPK), dtype=torch.int32, pin_memory=True)
+
+        def e2e_step():
+            step()
+            if rank == 0:
+                with torch.cuda.stream(stream):
+                    h_full.copy_(search.full, non_blocking=True)
+                    h_ti.copy_(search.top_i, non_blocking=True)
+                    h_ts.copy_(search.top_s, non_blocking=True)
+            stream.synchronize()
+
+        e2e_step()
+        ne = max(3, args.steps // 3)
         if dist:
-            t = torch.tensor([dt], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
-        e2e_val = len(q) * total_res / (dt * 1e9)
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ne):
+            e2e_step()
+        if dist:
+            dist.barrier()
+        dt = (time.perf_counter() - t0) / ne
+        e2e_how = ("sharded step through the C-ABI (host query) + NCCL gather + device assembly, then the "
+                   "assembled scores and top-k D2H to pinned host memory on rank 0; wall clock between barriers")
+    if dist:
+        t = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    e2e_val = w.cells_global() / (dt * 1e9)
 
     # ---- roofline of the dominant kernel (s16x2 pass kernel, ALU/DPX bound)
     peaks, peaks_src = measured_peaks()
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     kms = float(np.mean(kernel_ms))
-    achieved = len(q) * local_res / (kms * 1e6)          # GCUPS of the pass kernels, this rank
+    achieved = w.qres * local_res / (kms * 1e6)          # GCUPS of the pass kernels, this rank
     f_max = float(peaks.get("sm_max_mhz", 1965.0))
     alu_per_cell = ALU_PER_CELL[int(sw.sw_last_stats()["arith"])]
     peak = nsm * f_max * 1e6 * ALU_LANE_OPS_PER_CLK_PER_SM / alu_per_cell / 1e9
@@ -394,32 +500,42 @@ def run_ours(args):
         roof["ipipe_alu_per_cell"] = ipipe
     roof["frac_vs_2.75_dpx_per_cell"] = round(achieved / (nsm * f_max * 1e6 * ALU_LANE_OPS_PER_CLK_PER_SM / 2.75 / 1e9), 4)
 
+    clk_all = None
+    if dist:
+        clk_all = [None] * world if rank == 0 else None
+        dist.gather_object(clk, clk_all, dst=0)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w)
 
     if rank == 0:
+        qlens = [len(q) for q in w.queries]
         line = {
             "metric": METRIC, "value": round(gcups, 1), "unit": "GCUPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i16",
-            "data": "synthetic",
-            "config": {"workload": f"{w.name}: query {len(q)} vs {w.db.count} synthetic sequences "
-                                   f"({total_res} residues), BLOSUM62, gaps 10/2",
-                       "query_len": len(q), "db_sequences": w.db.count, "db_residues": total_res,
-                       "per_gpu_db_residues": local_res, "topk": TOPK,
+            "higher_is_better": True, "scaling": "weak" if w.weak else "strong", "vs_baseline": None,
+            "dtype": "i16", "data": "synthetic",
+            "config": {"workload": f"{w.name}: {nq} quer{'y' if nq == 1 else 'ies'} ({w.qres} residues) vs "
+                                   f"{w.count_global} synthetic sequences ({w.residues_global} residues), "
+                                   f"BLOSUM62, gaps 10/2",
+                       "query_len": qlens[0] if nq == 1 else qlens, "db_sequences": w.count_global,
+                       "db_residues": w.residues_global, "per_gpu_db_residues": local_res, "topk": TOPK,
                        "tile_G_R": [st["G"], st["R"]], "passes": st["passes"],
                        "flagged_rescored": st["flagged"],
                        "l2": "inputs larger than L2 (stream image %.0f MB > 126 MB)" % (st["pair_columns"] * 4 / 1e6),
-                       "parallelism": f"dp{world} (database shards)"},
+                       "parallelism": f"dp{world} (database shards, one process per GPU)",
+                       "ranks": world, "assembled_all_scores_on_rank0": True,
+                       "assembly_check": checked},
             "e2e": {"value": round(e2e_val, 1) if e2e_val else None, "unit": "GCUPS",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "how": "sw_search + sw_topk through the C-ABI with pinned host buffers, wall clock"},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "how": e2e_how},
             "roofline": roof,
             "cpu_baseline": cpu,
             "clocks": clk,
-            "gpu_launches": per_step_kernels * args.steps + extra,
+            "gpu_launches": launches,
         }
+        if clk_all:
+            line["clocks_per_rank"] = clk_all
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -431,6 +547,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     return run_ours(args)
 
 

@@ -29,6 +29,10 @@
  *     the calling thread at sw_db_load time.  Multi-GPU = one process per GPU,
  *     each loading its own shard (the Python harness shards and merges).
  *   - The library is not reentrant: calls must be serialised by the caller.
+ *     Searches may be enqueued on different streams: each search's device
+ *     work waits (cudaStreamWaitEvent) for the previous search's work, whose
+ *     per-search scratch buffers it reuses, so no synchronisation is needed
+ *     between them.
  *   - Host pointers are only read during the call (inputs are copied); the
  *     caller keeps ownership of every buffer it passes.
  */
@@ -174,6 +178,25 @@ int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, 
                     int64_t *d_idx_out, int32_t *d_score_out, void *cuda_stream);
 
 /*
+ * sw_scatter_dev -- sorting stage, multi-GPU assembly ("alignment
+ * scores are sorted"): rank 0 puts the score vectors gathered
+ * from every rank's database shard back into the original database order.
+ *   d_src     : device int32[n], the gathered per-rank score vectors (padded).
+ *   d_index   : device int64[n], original database index of each entry, or a
+ *               negative value for a padding slot (skipped).
+ *   n         : >= 0 entries.
+ *   d_dst     : device int32[dst_count]; d_dst[d_index[i]] = d_src[i] for
+ *               every i with 0 <= d_index[i] < dst_count.  Entries not named
+ *               by any index are left unchanged.  Indices must be distinct
+ *               (otherwise which of the duplicates lands is unspecified).
+ *   cuda_stream : stream to enqueue on (NULL = legacy default); asynchronous.
+ * Returns SW_OK, SW_EINVAL (NULL pointer with n > 0, n < 0, dst_count < 0) or
+ * SW_ECUDA.
+ */
+int sw_scatter_dev(const int32_t *d_src, const int64_t *d_index, int64_t n, int32_t *d_dst, int64_t dst_count,
+                   void *cuda_stream);
+
+/*
  * Statistics of the last search (for the benchmark report):
  *   stats[0] = rows per query pass (G*R), stats[1] = passes,
  *   stats[2] = G (lanes per group), stats[3] = R (rows per lane),
@@ -192,8 +215,8 @@ int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, 
 int sw_last_stats(int64_t *stats, int n);
 
 /*
- * Device timing of the last search, from CUDA events recorded on the search
- * stream (synchronises with it):
+ * Device timing of the last search (or of all searches of the last batch),
+ * from CUDA events recorded on the search stream (synchronises with it):
  *   ms[0] = s16x2 pass kernels (sum of the pass-kernel launches),
  *   ms[1] = whole search on the device (query-profile build .. end of the
  *           32-bit re-scoring kernel).
@@ -221,6 +244,10 @@ int sw_tile_supported(int32_t G, int32_t R);
  * Returns SW_OK or SW_EINVAL.
  */
 int sw_set_wave(int32_t mode);
+
+/* Number of CUDA kernels the library has launched since it was loaded (every
+ * entry point counts its own launches; for the benchmark's launch report). */
+int64_t sw_launch_count(void);
 
 /* Message for the most recent failing call on this thread ("" if none). */
 const char *sw_last_error(void);

@@ -134,7 +134,8 @@ struct State {
   // timing events of the last search
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> pev;   // (start, end) of every pass-kernel launch of the last search
-  int npev = 0;                   // pairs recorded by the last search
+  int npev = 0;                   // pairs recorded by the last search (or batch)
+  bool batch_cont = false;        // search_core continues a batch: keep ev[0] and the pass events
   // ---- streamed (out-of-core) database, SURVEY 8(f) NEXT-3
   struct Chunk {
     int item_begin, item_end;   // items [begin, end)
@@ -320,6 +321,10 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(g.qp32.ensure((size_t)kNL * mm));
   if (pair) CUDA_TRY(g.qp32b.ensure((size_t)kNL * mm));
 
+  // The per-search scratch (profile, flags, counters, sc_out, boundaries, ...)
+  // is shared by every search: order this search's device work after the
+  // previous one's, whatever stream that ran on (ev[3] marks its end).
+  if (g.has_search && g.ev[3]) CUDA_TRY(cudaStreamWaitEvent(st, g.ev[3], 0));
   CUDA_TRY(cudaMemcpyAsync(g.query.p, q, (size_t)m, cudaMemcpyHostToDevice, st));
   if (pair) CUDA_TRY(cudaMemcpyAsync(g.query2.p, q2, (size_t)m2, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(g.matrix.p, matrix, kAlpha * kAlpha, cudaMemcpyHostToDevice, st));
@@ -332,7 +337,21 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(cudaMemsetAsync(g.cells32.p, 0, sizeof(int64_t), st));
   if (!g.ev[0])
     for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g.ev[i]));
-  CUDA_TRY(cudaEventRecord(g.ev[0], st));
+  // a batch's timing spans all of its searches (sw_last_timing)
+  if (!g.batch_cont) {
+    CUDA_TRY(cudaEventRecord(g.ev[0], st));
+    g.npev = 0;
+  }
+  auto pass_event = [&](int idx) -> cudaError_t {   // event slot idx of this search's launches
+    while (g.pev.size() < (size_t)idx + 1) {
+      cudaEvent_t e;
+      cudaError_t er = cudaEventCreate(&e);
+      if (er != cudaSuccess) return er;
+      g.pev.push_back(e);
+    }
+    return cudaSuccess;
+  };
+  const int pev0 = 2 * g.npev;
   CUDA_TRY(launch_qp_build(g.query.p, m, pair ? g.query2.p : nullptr, m2, g.matrix.p, T.G, T.R, P, g.qp.p,
                            g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr,
                            goe, ge, st));
@@ -416,16 +435,12 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     p.progress = g.progress.p;
     p.bndbuf[0] = g.bnd.p;
     p.bndbuf[1] = g.bnd.p + span;
-    while (g.pev.size() < 2) {
-      cudaEvent_t e;
-      CUDA_TRY(cudaEventCreate(&e));
-      g.pev.push_back(e);
-    }
-    CUDA_TRY(cudaEventRecord(g.pev[0], st));
+    CUDA_TRY(pass_event(pev0 + 1));
+    CUDA_TRY(cudaEventRecord(g.pev[pev0], st));
     // every CTA must be resident: a wavefront CTA may wait on another's progress
     CUDA_TRY(launch_sw16_pass(ti, g.num_sms * tile_wave_ctas_per_sm(ti), p, st));
-    CUDA_TRY(cudaEventRecord(g.pev[1], st));
-    g.npev = 1;
+    CUDA_TRY(cudaEventRecord(g.pev[pev0 + 1], st));
+    g.npev = pev0 / 2 + 1;
     // the score chain was carried through the passes: one gather of the maxima
     CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p, nullptr, nullptr, 0,
                                 thresh, st));
@@ -473,16 +488,12 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       // its leading run of flagged sequences (item_skip_kernel below)
       const bool skipping = !strm && !pair && P > 1;
       p.skip = (skipping && pass > 0) ? g.skip.p : nullptr;
-      const size_t pe = 2 * (size_t)(k * P + pass);
-      while (g.pev.size() < pe + 2) {
-        cudaEvent_t e;
-        CUDA_TRY(cudaEventCreate(&e));
-        g.pev.push_back(e);
-      }
+      const int pe = pev0 + 2 * (k * P + pass);
+      CUDA_TRY(pass_event(pe + 1));
       CUDA_TRY(cudaEventRecord(g.pev[pe], st));
       CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
       CUDA_TRY(cudaEventRecord(g.pev[pe + 1], st));
-      g.npev = (int)(pe / 2) + 1;
+      g.npev = pe / 2 + 1;
       if (strm) {
         const State::Chunk &c = g.chunks[k];
         CUDA_TRY(launch_sw16_gather(g.cseq_endcol.p + c.seq_begin, c.seq_end - c.seq_begin, g.sc_out.p - base,
@@ -544,7 +555,11 @@ int batch_impl(const uint8_t *queries, const int64_t *qoffsets, int32_t nq, cons
   std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
     return qoffsets[x + 1] - qoffsets[x] > qoffsets[y + 1] - qoffsets[y];
   });
+  struct BatchGuard {   // the batch's searches share one timing window
+    ~BatchGuard() { g.batch_cont = false; }
+  } guard;
   for (int32_t k = 0; k < nq; k += 2) {
+    g.batch_cont = k > 0;
     const int32_t a = order[k];
     const uint8_t *qa = queries + qoffsets[a];
     const int32_t ma = (int32_t)(qoffsets[a + 1] - qoffsets[a]);
@@ -578,6 +593,7 @@ void sw_db_free(void) {
 }
 
 int64_t sw_db_count(void) { return g.loaded ? g.count : 0; }
+int64_t sw_launch_count(void) { return launch_count(); }
 int64_t sw_db_residues(void) { return g.loaded ? g.total_res : 0; }
 
 }  // extern "C"
@@ -823,6 +839,18 @@ int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, 
   }
   CUDA_TRY(cudaStreamSynchronize(st));
   return kk;
+}
+
+int sw_scatter_dev(const int32_t *d_src, const int64_t *d_index, int64_t n, int32_t *d_dst, int64_t dst_count,
+                   void *cuda_stream) {
+  t_err.clear();
+  if (n < 0 || dst_count < 0) return fail(SW_EINVAL, "n and dst_count must be >= 0");
+  if (n == 0) return SW_OK;
+  if (!d_src || !d_index || !d_dst) return fail(SW_EINVAL, "NULL device pointer");
+  int rc = ensure_device_ready();
+  if (rc) return rc;
+  CUDA_TRY(launch_scatter_scores(d_src, d_index, n, d_dst, dst_count, (cudaStream_t)cuda_stream));
+  return SW_OK;
 }
 
 int64_t sw_topk(int64_t k, int64_t *idx_out, int32_t *score_out) {

@@ -959,6 +959,32 @@ __global__ void __launch_bounds__(1024) block_topk_kernel(const int32_t *scores,
   }
 }
 
+// Sorting stage, multi-GPU: scatter the scores gathered
+// from every rank's shard back to the original database order on rank 0,
+// dst[index[i]] = src[i]; index < 0 marks the gather's padding slots.  Four
+// entries per thread with 16-B loads where aligned (the gathered buffer is
+// contiguous and padded per rank); stores are scattered 4-B writes.
+__global__ void scatter_scores_kernel(const int32_t *__restrict__ src, const int64_t *__restrict__ index, int64_t n,
+                                      int32_t *__restrict__ dst, int64_t dst_count) {
+  const int64_t n4 = n >> 2;
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(index)) & 15) == 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (vec ? n4 : 0);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 s = __ldg(reinterpret_cast<const int4 *>(src) + i);
+    const longlong2 a = __ldg(reinterpret_cast<const longlong2 *>(index) + 2 * i);
+    const longlong2 b = __ldg(reinterpret_cast<const longlong2 *>(index) + 2 * i + 1);
+    if (a.x >= 0 && a.x < dst_count) dst[a.x] = s.x;
+    if (a.y >= 0 && a.y < dst_count) dst[a.y] = s.y;
+    if (b.x >= 0 && b.x < dst_count) dst[b.x] = s.z;
+    if (b.y >= 0 && b.y < dst_count) dst[b.y] = s.w;
+  }
+  for (int64_t i = (vec ? 4 * n4 : 0) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = index[i];
+    if (j >= 0 && j < dst_count) dst[j] = src[i];
+  }
+}
+
 __global__ void decode_keys_kernel(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = keys[i];
@@ -1072,6 +1098,8 @@ TileEff tile_eff(int G, int R) {
   return TileEff{G, R, 4000.f, 3500.f};   // uncalibrated tile: pessimistic
 }
 
+int64_t g_launches = 0;   // kernels launched by this library (sw_launch_count)
+
 int grid_for(int64_t total, int threads) {
   int64_t g = (total + threads - 1) / threads;
   if (g > 148 * 32) g = 148 * 32;
@@ -1081,6 +1109,7 @@ int grid_for(int64_t total, int threads) {
 
 }  // namespace
 
+int64_t launch_count() { return g_launches; }
 int num_tiles() { return kNumTiles; }
 TileInfo tile(int i) {
   const TileEff e = tile_eff(g_tiles[i].G, g_tiles[i].R);
@@ -1127,6 +1156,7 @@ cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_quer
                             int goe, int ge, cudaStream_t st) {
   const int mm = d_query2 ? (m > m2 ? m : m2) : m;
   const int64_t total = (int64_t)P * kNL * ((R + 3) / 4) * G * 4 + kNL * kNL + (int64_t)kNL * mm;
+  ++g_launches;
   qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_query2, m2, d_matrix, G, R, P,
                                                          reinterpret_cast<uint32_t *>(d_qp), d_desc, d_qp32,
                                                          d_qp32b, goe, ge);
@@ -1139,6 +1169,7 @@ int tile_wave_ctas_per_sm(int i) { return g_tiles[i].ctasw; }
 cudaError_t launch_sw16_pass(int ti, int grid, const SW16Params &p, cudaStream_t st) {
   PassFn fn = p.npass > 0 ? g_tiles[ti].fnw : (p.bnd_in ? g_tiles[ti].fn1 : g_tiles[ti].fn0);
   if (!fn) return cudaErrorInvalidValue;
+  ++g_launches;
   fn<<<grid, g_tiles[ti].nt, g_tiles[ti].smem, st>>>(p);
   return cudaGetLastError();
 }
@@ -1147,6 +1178,7 @@ cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint3
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
                                cudaStream_t st, const int32_t *seq_idx) {
   if (count <= 0) return cudaSuccess;
+  ++g_launches;
   sw16_gather_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, scores, flagged, scores2, flagged2,
                                                             pass, thresh, seq_idx);
   return cudaGetLastError();
@@ -1155,12 +1187,14 @@ cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint3
 cudaError_t launch_item_skip(const Item *items, int nitems, const int32_t *slots, const int64_t *offs,
                              const uint8_t *flagged, int32_t *skip, cudaStream_t st) {
   if (nitems < 1) return cudaSuccess;
+  ++g_launches;
   item_skip_kernel<<<grid_for(nitems, 256), 256, 0, st>>>(items, nitems, slots, offs, flagged, skip);
   return cudaGetLastError();
 }
 
 cudaError_t launch_flag_compact(const uint8_t *flagged, int64_t count, int32_t *list, int *n, int want,
                                 cudaStream_t st) {
+  ++g_launches;
   flag_compact_kernel<<<grid_for(count, 256), 256, 0, st>>>(flagged, count, list, n, want);
   return cudaGetLastError();
 }
@@ -1173,12 +1207,14 @@ cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  ++g_launches;
   sw32_kernel<kSW32Rows><<<grid, kSW32Threads, smem, st>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_make_keys(const int32_t *scores, const int64_t *index, int64_t n, uint64_t *keys,
                              int64_t npad, cudaStream_t st) {
+  ++g_launches;
   make_keys_kernel<<<grid_for(npad, 256), 256, 0, st>>>(scores, index, n, keys, npad);
   return cudaGetLastError();
 }
@@ -1187,12 +1223,15 @@ cudaError_t launch_bitonic_sort_desc(uint64_t *keys, int64_t npow2, cudaStream_t
   for (int64_t size = 2; size <= npow2; size <<= 1) {
     int64_t stride = size >> 1;
     for (; stride > 1024; stride >>= 1) {
+      ++g_launches;
       bitonic_step_kernel<<<grid_for(npow2 / 2, 256), 256, 0, st>>>(keys, npow2, size, stride);
     }
     if (npow2 >= 2048) {
+      ++g_launches;
       bitonic_local_kernel<<<(unsigned)(npow2 / 2048), 1024, 0, st>>>(keys, size, stride);
     } else {
       for (; stride > 0; stride >>= 1)
+        ++g_launches;
         bitonic_step_kernel<<<grid_for(npow2 / 2, 256), 256, 0, st>>>(keys, npow2, size, stride);
     }
     cudaError_t e = cudaGetLastError();
@@ -1203,11 +1242,21 @@ cudaError_t launch_bitonic_sort_desc(uint64_t *keys, int64_t npow2, cudaStream_t
 
 cudaError_t launch_block_topk(const int32_t *scores, const int64_t *index, const uint64_t *keys_in, int64_t n,
                               int k, uint64_t *out, int blocks, cudaStream_t st) {
+  ++g_launches;
   block_topk_kernel<<<blocks, 1024, 0, st>>>(scores, index, keys_in, n, k, out);
   return cudaGetLastError();
 }
 
+cudaError_t launch_scatter_scores(const int32_t *src, const int64_t *index, int64_t n, int32_t *dst,
+                                  int64_t dst_count, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  scatter_scores_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, st>>>(src, index, n, dst, dst_count);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score, cudaStream_t st) {
+  ++g_launches;
   decode_keys_kernel<<<grid_for(k, 256), 256, 0, st>>>(keys, k, idx, score);
   return cudaGetLastError();
 }

@@ -87,6 +87,9 @@ struct TileInfo {
   float eff0, eff1;         // measured full-row GCUPS: first pass / boundary-reading pass
 };
 
+// Number of kernel launches issued by the library since it was loaded.
+int64_t launch_count();
+
 // Compiled (G, R) tiles of the s16x2 pass kernel.
 int num_tiles();
 TileInfo tile(int i);
@@ -141,5 +144,8 @@ cudaError_t launch_block_topk(const int32_t *scores, const int64_t *index, const
                               int k, uint64_t *out, int blocks, cudaStream_t st);
 cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score,
                                cudaStream_t st);
+// dst[index[i]] = src[i] for i < n, skipping index < 0 or >= dst_count.
+cudaError_t launch_scatter_scores(const int32_t *src, const int64_t *index, int64_t n, int32_t *dst,
+                                  int64_t dst_count, cudaStream_t st);
 
 }  // namespace swdb

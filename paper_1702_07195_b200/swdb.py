@@ -20,8 +20,8 @@ _NAMES = {SW_EINVAL: "SW_EINVAL", SW_ENOMEM: "SW_ENOMEM", SW_ECUDA: "SW_ECUDA",
           SW_ENODB: "SW_ENODB", SW_ESTATE: "SW_ESTATE"}
 
 EXPORTS = ["sw_db_load", "sw_db_load_streamed", "sw_db_chunks", "sw_db_free", "sw_db_count", "sw_db_residues", "sw_search",
-           "sw_search_dev", "sw_search_batch", "sw_search_batch_dev", "sw_topk", "sw_topk_dev", "sw_last_stats", "sw_last_timing", "sw_set_tile",
-           "sw_tile_supported", "sw_set_wave", "sw_last_error", "sw_version"]
+           "sw_search_dev", "sw_search_batch", "sw_search_batch_dev", "sw_topk", "sw_topk_dev", "sw_scatter_dev", "sw_last_stats", "sw_last_timing", "sw_set_tile",
+           "sw_tile_supported", "sw_set_wave", "sw_last_error", "sw_version", "sw_launch_count"]
 
 
 class SWError(RuntimeError):
@@ -60,6 +60,7 @@ def load_library():
         "sw_search_batch_dev": (ctypes.c_int, [p, p, i32, p, i32, i32, p, p]),
         "sw_topk": (i64, [i64, p, p]),
         "sw_topk_dev": (i64, [p, p, i64, i64, p, p, p]),
+        "sw_scatter_dev": (ctypes.c_int, [p, p, i64, p, i64, p]),
         "sw_last_stats": (ctypes.c_int, [p, ctypes.c_int]),
         "sw_last_timing": (ctypes.c_int, [p, ctypes.c_int]),
         "sw_set_tile": (ctypes.c_int, [i32, i32]),
@@ -67,6 +68,7 @@ def load_library():
         "sw_set_wave": (ctypes.c_int, [i32]),
         "sw_last_error": (ctypes.c_char_p, []),
         "sw_version": (ctypes.c_char_p, []),
+        "sw_launch_count": (i64, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -115,6 +117,11 @@ def _stream_ptr(stream) -> int:
 
 def sw_last_error() -> str:
     return load_library().sw_last_error().decode()
+
+
+def sw_launch_count() -> int:
+    """Kernels launched by the library since it was loaded."""
+    return int(load_library().sw_launch_count())
 
 
 def sw_version() -> str:
@@ -209,6 +216,12 @@ def sw_topk_dev(d_scores, d_index, n: int, k: int, d_idx_out, d_score_out, strea
     return int(_check(load_library().sw_topk_dev(_dev_ptr(d_scores), _dev_ptr(d_index), int(n), int(k),
                                                  _dev_ptr(d_idx_out), _dev_ptr(d_score_out),
                                                  _stream_ptr(stream))))
+
+
+def sw_scatter_dev(d_src, d_index, n: int, d_dst, dst_count: int, stream=None) -> None:
+    """d_dst[d_index[i]] = d_src[i] on the device (negative index = padding)."""
+    _check(load_library().sw_scatter_dev(_dev_ptr(d_src), _dev_ptr(d_index), int(n), _dev_ptr(d_dst),
+                                         int(dst_count), _stream_ptr(stream)))
 
 
 def sw_last_stats() -> dict:

@@ -310,6 +310,82 @@ def make_config(k: int, scale: float = 1.0, **kw) -> Workload:
 
 
 # --------------------------------------------------------------------------
+# Per-rank generation for the multi-GPU benchmark: the sequence lengths of a
+# configuration (cheap), its queries, and the residues of any subset of its
+# sequences, generated by streaming the configuration's residue RNG chunk by
+# chunk so that a rank holds only its own shard.  The values are identical to
+# make_config(k, scale).db / .queries (tests/test_inputs.py checks it).
+# Configurations 0-3 only (cfg4 is built from a shuffled list).
+# --------------------------------------------------------------------------
+_RES_CHUNK = 1 << 26   # rr_residues' chunk: the subset stream must draw the same chunks
+
+
+def config_lengths(k: int, scale: float = 1.0) -> np.ndarray:
+    k = int(k)
+    if k == 0:
+        return lognormal_lengths(rng_for(0, 0), _scaled(10_000, scale), 8, 2000)
+    if k == 1:
+        return lognormal_lengths(rng_for(1, 0), _scaled(1_000_000, scale), 8, 2000)
+    if k in (2, 3):
+        count = _scaled(6_500_000, scale)
+        lens = lognormal_lengths(rng_for(2, 0), count, 8, 35_000)
+        lens[int(rng_for(2, 3).integers(0, count))] = 35_000   # as _cfg2_db
+        return lens
+    raise ValueError("config_lengths: configurations 0-3 only")
+
+
+def config_queries(k: int) -> list:
+    k = int(k)
+    if k == 0:
+        return [rr_residues(rng_for(0, 2), 144)]
+    if k == 1:
+        return [rr_residues(rng_for(1, 2), 464)]
+    if k == 2:
+        return [rr_residues(rng_for(2, 2), 1000)]
+    if k == 3:
+        rng = rng_for(3, 2)
+        return [rr_residues(rng, L) for L in CFG3_QUERY_LENGTHS]
+    raise ValueError("config_queries: configurations 0-3 only")
+
+
+def config_db_subset(k: int, idx, scale: float = 1.0) -> Database:
+    """Sub-database of configuration k's sequences idx (strictly ascending),
+    equal to make_config(k, scale).db.subset(idx), generated without holding
+    the whole database."""
+    k = int(k)
+    lens = config_lengths(k, scale)
+    idx = np.asarray(idx, dtype=np.int64)
+    if idx.size and (np.any(np.diff(idx) <= 0) or idx[0] < 0 or idx[-1] >= lens.size):
+        raise ValueError("idx must be strictly ascending sequence indices")
+    if idx.size == lens.size:   # the whole database
+        return database_from_lengths(rng_for(2 if k == 3 else k, 1), lens)
+    offs = np.zeros(lens.size + 1, dtype=np.int64)
+    np.cumsum(lens, out=offs[1:])
+    starts, ends = offs[idx], offs[idx + 1]
+    L = ends - starts
+    noffs = np.zeros(idx.size + 1, dtype=np.int64)
+    np.cumsum(L, out=noffs[1:])
+    out = np.empty(int(noffs[-1]), dtype=np.uint8)
+    rng = rng_for(2 if k == 3 else k, 1)
+    n = int(offs[-1])
+    for s in range(0, n, _RES_CHUNK):
+        e = min(n, s + _RES_CHUNK)
+        codes = _RR_LUT[rng.integers(0, 1 << _LUT_BITS, size=e - s, dtype=np.uint16)]
+        lo = int(np.searchsorted(ends, s, side="right"))
+        hi = int(np.searchsorted(starts, e, side="left"))
+        if hi <= lo:
+            continue
+        seg_s = np.maximum(starts[lo:hi], s)
+        seg_len = np.minimum(ends[lo:hi], e) - seg_s
+        dst0 = noffs[lo:hi] + (seg_s - starts[lo:hi])
+        cum = np.zeros(seg_len.size + 1, dtype=np.int64)
+        np.cumsum(seg_len, out=cum[1:])
+        rel = np.arange(int(cum[-1]), dtype=np.int64) - np.repeat(cum[:-1], seg_len)
+        out[np.repeat(dst0, seg_len) + rel] = codes[np.repeat(seg_s - s, seg_len) + rel]
+    return Database(out, noffs)
+
+
+# --------------------------------------------------------------------------
 # Random small cases for property tests (SPEC.md:492: random symmetric
 # matrices in [-4, 11], gaps in [0, 15]).
 # --------------------------------------------------------------------------

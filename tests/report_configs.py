@@ -1,5 +1,7 @@
 """Run BASELINE.json configurations on one GPU: device GCUPS per query, flag
-statistics and a sampled oracle parity check (dev / report tool).
+statistics and a sampled oracle parity check (dev / report tool).  Every
+timed region is sampled by bench.ClockSampler (nvidia-smi SM clock and
+throttle reasons); each line carries its clocks.
 
     python tests/report_configs.py 0 1 2 3 4 [--scale S] [--sample N] [--reps K]
 
@@ -16,6 +18,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import oracle  # noqa: E402
+from bench import ClockSampler, cpu_model  # noqa: E402
 import paper_1702_07195_b200 as sw  # noqa: E402
 import sw_inputs as si  # noqa: E402
 
@@ -25,7 +28,7 @@ def main():
     ap.add_argument("configs", nargs="*", type=int, default=[0, 1])
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--sample", type=int, default=1500)
-    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--queries", type=str, default="")
     ap.add_argument("--batch", action="store_true", help="also time sw_search_batch over all queries")
     args = ap.parse_args()
@@ -46,15 +49,22 @@ def main():
             q = w.queries[qi]
             sw.sw_search_dev(q, w.matrix, w.gap_open, w.gap_extend, d, st)
             st.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(st)
+            clk = ClockSampler(0)
+            clk.start()
+            time.sleep(0.3)
+            times, pk = [], []
             for _ in range(args.reps):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(st)
                 sw.sw_search_dev(q, w.matrix, w.gap_open, w.gap_extend, d, st)
-            e1.record(st)
-            st.synchronize()
-            ms = e0.elapsed_time(e1) / args.reps
-            tm = sw.sw_last_timing()
+                e1.record(st)
+                st.synchronize()
+                times.append(e0.elapsed_time(e1))
+                pk.append(sw.sw_last_timing()["pass_kernels_ms"])
+            clocks = clk.stop()
+            ms = float(np.median(times))
+            tm = {"pass_kernels_ms": float(np.median(pk))}
             stats = sw.sw_last_stats()
             got = d.cpu().numpy()
             # sampled parity: random sample + the longest sequences + planted copies
@@ -77,19 +87,28 @@ def main():
                 "pass_kernel_gcups": round(cells / (tm["pass_kernels_ms"] * 1e6), 1),
                 "tile": [stats["G"], stats["R"]], "passes": stats["passes"], "flagged": stats["flagged"],
                 "cells32": stats["cells32"], "parity_checked": int(idx.size), "parity_mismatches": bad,
-                "oracle_s": round(tq, 1), "max_score": int(got.max())}), flush=True)
+                "oracle_s": round(tq, 1), "max_score": int(got.max()), "reps": args.reps,
+                "ms_min_max": [round(min(times), 3), round(max(times), 3)], "clocks": clocks,
+                "oracle_cores": cores, "cpu_model": cpu_model()}), flush=True)
             assert bad == 0, f"config {c} query {qi}: {bad} mismatches"
         if args.batch and len(w.queries) > 1:
             dd = torch.empty(len(w.queries) * w.db.count, dtype=torch.int32, device="cuda")
             sw.sw_search_batch_dev(w.queries, w.matrix, w.gap_open, w.gap_extend, dd, st)
             st.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            sw.sw_search_batch_dev(w.queries, w.matrix, w.gap_open, w.gap_extend, dd, st)
-            e1.record(st)
-            st.synchronize()
-            ms = e0.elapsed_time(e1)
+            clk = ClockSampler(0)
+            clk.start()
+            time.sleep(0.3)
+            times = []
+            for _ in range(max(3, args.reps // 2)):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                sw.sw_search_batch_dev(w.queries, w.matrix, w.gap_open, w.gap_extend, dd, st)
+                e1.record(st)
+                st.synchronize()
+                times.append(e0.elapsed_time(e1))
+            clocks = clk.stop()
+            ms = float(np.median(times))
             allsc = dd.view(len(w.queries), w.db.count).cpu().numpy()
             # parity of the batch against the single-query path on every query (exact)
             mism = 0
@@ -99,7 +118,9 @@ def main():
                 mism += int((d.cpu().numpy() != allsc[qi]).sum())
             cells = sum(len(q) for q in w.queries) * w.db.total_residues
             print(json.dumps({"config": c, "batch_queries": len(w.queries), "ms": round(ms, 1),
-                              "gcups": round(cells / (ms * 1e6), 1), "batch_vs_single_mismatches": mism}), flush=True)
+                              "gcups": round(cells / (ms * 1e6), 1), "batch_vs_single_mismatches": mism,
+                              "reps": len(times), "ms_min_max": [round(min(times), 1), round(max(times), 1)],
+                              "clocks": clocks}), flush=True)
             assert mism == 0
 
 

@@ -1,0 +1,176 @@
+"""GPU: the multi-GPU assembly and ordering pieces of the path, on one GPU.
+
+* sw_scatter_dev (rank 0's reassembly of the gathered shard scores in
+  original order) against its documented semantics;
+* parallel.ShardedSearch with the library backend at world size 1 (the same
+  step bench.py times at N ranks), single query and query batch, against the
+  oracle;
+* searches enqueued on different streams without synchronisation (the
+  library orders each search after the previous one);
+* the >= 255-pass path (flag byte saturated at 255, re-scored from row 0);
+* bench.py on BASELINE configs[2] as strong scaling with the NCCL gather at
+  world size 1 (--dist), and the launch counter.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import sw_inputs as si
+from sw_inputs import BLOSUM62, encode
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+sw = pytest.importorskip("paper_1702_07195_b200")
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+    sw.sw_set_tile(0)
+
+
+def test_scatter_dev_semantics():
+    rng = np.random.default_rng(9)
+    for n, dst_count, off in [(1, 1, 0), (7, 20, 0), (4096 + 3, 5000, 0), (100_003, 120_000, 1), (12, 4, 0)]:
+        perm = rng.permutation(dst_count)[:min(n, dst_count)]
+        idx = np.full(n, -1, np.int64)
+        pos = rng.choice(n, perm.size, replace=False)
+        idx[pos] = perm
+        if n > 8:
+            idx[rng.choice(n, 3, replace=False)] = dst_count + 5   # out of range: skipped
+            idx[idx == dst_count + 5] = -7
+        src = rng.integers(-2**31, 2**31 - 1, n).astype(np.int32)
+        exp = np.full(dst_count, 12345, np.int32)
+        keep = (idx >= 0) & (idx < dst_count)
+        exp[idx[keep]] = src[keep]
+        # off = 1: misaligned device pointers (the kernel's scalar path)
+        d_src = torch.from_numpy(np.concatenate([[0] * off, src]).astype(np.int32)).cuda()[off:]
+        d_idx = torch.from_numpy(np.concatenate([[0] * off, idx]).astype(np.int64)).cuda()[off:]
+        d_dst = torch.full((dst_count,), 12345, dtype=torch.int32, device="cuda")
+        sw.sw_scatter_dev(d_src, d_idx, n, d_dst, dst_count)
+        torch.cuda.synchronize()
+        assert np.array_equal(d_dst.cpu().numpy(), exp), (n, dst_count, off)
+    with pytest.raises(sw.SWError):
+        sw.sw_scatter_dev(None, None, 5, None, 5)
+
+
+@pytest.mark.parametrize("nq", [1, 3])
+def test_sharded_search_world1_lib_backend(nq):
+    from paper_1702_07195_b200.parallel import LibBackend, ShardedSearch
+    w = si.config2(scale=0.002)
+    rng = np.random.default_rng(31)
+    qs = [si.rr_residues(rng, L) for L in (464, 1000, 144)[:nq]]
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    st = torch.cuda.Stream()
+    ss = ShardedSearch(LibBackend(sw), np.arange(w.db.count), w.db.count, nq, 10, torch.device("cuda"))
+    ss.step(qs, w.matrix, w.gap_open, w.gap_extend, st)
+    st.synchronize()
+    full, ti, ts = ss.result()
+    for k, q in enumerate(qs):
+        exp = oracle.batch(q, w.db.residues, w.db.offsets, w.matrix, w.gap_open, w.gap_extend)
+        assert np.array_equal(full[k].cpu().numpy(), exp), k
+        ei, es = oracle.topk(exp, 10)
+        assert np.array_equal(ti[k].cpu().numpy(), ei) and np.array_equal(ts[k].cpu().numpy(), es), k
+
+
+def test_searches_on_different_streams_need_no_sync():
+    """sw_search_dev on a side stream followed at once by
+    sw_search / sw_search_dev on other streams must not clobber the shared
+    per-search scratch of the first search."""
+    rng = np.random.default_rng(77)
+    w = si.config1(scale=0.02)
+    qa, qb, qc = si.rr_residues(rng, 1500), si.rr_residues(rng, 300), si.rr_residues(rng, 900)
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    ea = oracle.batch(qa, w.db.residues, w.db.offsets, BLOSUM62, 10, 2)
+    eb = oracle.batch(qb, w.db.residues, w.db.offsets, BLOSUM62, 10, 2)
+    ec = oracle.batch(qc, w.db.residues, w.db.offsets, BLOSUM62, 10, 2)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        da = torch.empty(w.db.count, dtype=torch.int32, device="cuda")
+        dc = torch.empty(w.db.count, dtype=torch.int32, device="cuda")
+        sw.sw_search_dev(qa, BLOSUM62, 10, 2, da, s1)          # multi-pass, side stream
+        gb = sw.sw_search(qb, BLOSUM62, 10, 2)                  # library stream, immediately
+        sw.sw_search_dev(qc, BLOSUM62, 10, 2, dc, s2)          # a third stream
+        sw.sw_search_dev(qa, BLOSUM62, 10, 2, da, None)         # legacy default stream
+        torch.cuda.synchronize()
+        assert np.array_equal(gb, eb)
+        assert np.array_equal(dc.cpu().numpy(), ec)
+        assert np.array_equal(da.cpu().numpy(), ea)
+
+
+def test_255_or_more_query_passes():
+    """queries of >= 255 passes (8x8 tile: 64 rows per pass).  The
+    flag byte saturates at 255; sequences first flagged in pass >= 254 are
+    re-scored from row 0 at the end, earlier ones from their pass boundary."""
+    rng = np.random.default_rng(255)
+    m_rand = 16_320
+    q = np.concatenate([encode("W" * 2000), si.rr_residues(rng, m_rand - 2000), encode("W" * 1600)])
+    seqs = [encode("W" * 1600),                       # flags early (rows < 2000)
+            encode("W" * 1700),
+            si.rr_residues(rng, 900),
+            encode("A" * 5 + "W" * 1550),
+            si.rr_residues(rng, 40)]
+    db = si.database_from_list(seqs)
+    exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
+    assert exp.max() >= 16_373
+    try:
+        sw.sw_set_tile(8, 8)
+        sw.sw_db_load(db.residues, db.offsets)
+        got = sw.sw_search(q, BLOSUM62, 10, 2)
+        st = sw.sw_last_stats()
+        assert st["passes"] >= 255
+        assert np.array_equal(got, exp), (got, exp)
+        # the W runs at the end of the query: a sequence that saturates only there
+        db2 = si.database_from_list([encode("G" * 30 + "W" * 1600), si.rr_residues(rng, 700)])
+        sw.sw_db_load(db2.residues, db2.offsets)
+        q2 = np.concatenate([si.rr_residues(rng, m_rand), encode("W" * 1600)])
+        got2 = sw.sw_search(q2, BLOSUM62, 10, 2)
+        exp2 = oracle.batch(q2, db2.residues, db2.offsets, BLOSUM62, 10, 2)
+        assert sw.sw_last_stats()["flagged"] >= 1
+        assert np.array_equal(got2, exp2), (got2, exp2)
+    finally:
+        sw.sw_set_tile(0)
+
+
+def test_launch_counter_counts_library_kernels():
+    w = si.config0(scale=0.05)
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    n0 = sw.sw_launch_count()
+    sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
+    n1 = sw.sw_launch_count()
+    st = sw.sw_last_stats()
+    assert n1 - n0 >= 1 + 4 * st["passes"]
+    sw.sw_topk(10)
+    assert sw.sw_launch_count() - n1 == 3
+
+
+def _run(args, env=None):
+    r = subprocess.run([sys.executable] + args, cwd=ROOT, capture_output=True, text=True, timeout=900,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_bench_config2_strong_scaling_nccl_world1():
+    d = _run(["bench.py", "--dist", "--config", "2", "--scale", "0.02", "--steps", "3", "--warmup", "3",
+              "--no-cpu-baseline"])
+    assert d["scaling"] == "strong" and d["n_gpus"] == 1 and d["value"] > 0
+    assert d["config"]["assembly_check"] is True and d["gpu_launches"] > 0
+    assert d["config"]["db_sequences"] == 130_000
+
+
+def test_bench_gpus_flag_single_gpu():
+    d = _run(["bench.py", "--gpus", "1", "--steps", "3", "--warmup", "3", "--scale", "0.02", "--no-cpu-baseline"])
+    assert d["n_gpus"] == 1 and d["scaling"] == "weak" and d["config"]["assembly_check"] is True

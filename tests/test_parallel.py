@@ -86,3 +86,84 @@ def test_gloo_gather_merge_matches_single_process(tmp_path, world):
     assert np.array_equal(r["full"], exp)
     ei, es = oracle.topk(exp, k)
     assert np.array_equal(r["mi"], ei) and np.array_equal(r["ms"], es)
+
+
+# ---------------------------------------------------------------------------
+# The bench's own multi-GPU step (bench.Work + parallel.ShardedSearch) on CPU
+# tensors with gloo, world size 2: per-rank shard generation, the gather of
+# padded score vectors and top-k candidates, the rank-0 assembly in original
+# order and the merged top-k.  The library calls are replaced by a stub
+# backend (oracle scores, host top-k and scatter with the kernels' documented
+# semantics); the NCCL/GPU path runs the same ShardedSearch code.
+# ---------------------------------------------------------------------------
+class OracleBackend:
+    def __init__(self, db):
+        self.db = db
+
+    def search(self, queries, M, go, ge, d_out, stream):
+        n = self.db.count
+        for k, q in enumerate(queries):
+            sc = oracle.batch(q, self.db.residues, self.db.offsets, M, go, ge).astype(np.int32)
+            d_out[k * n:(k + 1) * n] = torch.from_numpy(sc)
+        return len(queries)
+
+    def topk(self, d_scores, d_index, n, k, d_idx_out, d_score_out, stream):
+        s = d_scores[:n].numpy().astype(np.int64)
+        idx = d_index[:n].numpy() if d_index is not None else np.arange(n)
+        order = np.lexsort((idx, -s))[:k]
+        d_idx_out[:k] = torch.from_numpy(idx[order].astype(np.int64))
+        d_score_out[:k] = torch.from_numpy(s[order].astype(np.int32))
+        return k
+
+    def scatter(self, d_src, d_index, n, d_dst, dst_count, stream):
+        src, idx = d_src[:n].numpy(), d_index[:n].numpy()
+        keep = (idx >= 0) & (idx < dst_count)
+        d_dst.numpy()[idx[keep]] = src[keep]
+
+
+def _bench_worker(rank, world, port, cfg, scale, nq, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from paper_1702_07195_b200.parallel import ShardedSearch
+    w = bench.Work(cfg, scale, world, rank)
+    queries = w.queries[:nq]
+    ss = ShardedSearch(OracleBackend(w.db), w.gidx, w.count_global, len(queries), 10, torch.device("cpu"),
+                       dist=dist, world=world, rank=rank)
+    ss.step(queries, w.matrix, w.gap_open, w.gap_extend, None)
+    if rank == 0:
+        full, ti, ts = ss.result()
+        np.savez(result_path, full=full.numpy(), ti=ti.numpy(), ts=ts.numpy(),
+                 ng=w.count_global, res=w.residues_global)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,scale,nq", [(0, 0.05, 1), (2, 0.0005, 2)])
+def test_bench_sharded_step_gloo_world2_matches_oracle(tmp_path, cfg, scale, nq):
+    """cfg0 is weak-scaled (database = configs[0] x 2), cfg2 strong (its
+    database split over 2 ranks); cfg2 runs two queries through the batched
+    layout [query][sequence]."""
+    world = 2
+    path = str(tmp_path / "res.npz")
+    mp.spawn(_bench_worker, args=(world, _free_port(), cfg, scale, nq, path), nprocs=world, join=True)
+    r = np.load(path)
+    gscale = scale * (world if cfg in (0, 1) else 1)
+    wfull = si.make_config(cfg, scale=gscale)
+    qs = si.config_queries(cfg)[:nq]
+    assert int(r["ng"]) == wfull.db.count and int(r["res"]) == wfull.db.total_residues
+    for k, q in enumerate(qs):
+        exp = oracle.batch(q, wfull.db.residues, wfull.db.offsets, wfull.matrix, wfull.gap_open, wfull.gap_extend)
+        assert np.array_equal(r["full"][k], exp)
+        ei, es = oracle.topk(exp, 10)
+        assert np.array_equal(r["ti"][k], ei) and np.array_equal(r["ts"][k], es)
+
+
+def test_host_topk_matches_oracle_sort():
+    import bench
+    rng = np.random.default_rng(3)
+    for n, k in [(1, 10), (5, 10), (1000, 10), (1000, 1000), (50_000, 7)]:
+        x = rng.integers(0, 20, n).astype(np.int32)     # many ties
+        ei, _ = oracle.topk(x, k)
+        assert np.array_equal(bench.host_topk(x, k), ei)
