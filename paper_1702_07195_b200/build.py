@@ -38,6 +38,9 @@ if os.environ.get("SW_BRING"):    # boundary prefetch ring in every boundary-rea
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_BRING=" + os.environ["SW_BRING"]]
 if os.environ.get("SW_S32ROWS"):  # rows per lane of the 32-bit kernel (experiment)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_S32ROWS=" + os.environ["SW_S32ROWS"]]
+for _k in ("SW_QPTAIL", "SW_TAILADDR"):   # profile tail layout experiments (kernels.cuh)
+    if os.environ.get(_k):
+        NVCC_FLAGS = NVCC_FLAGS + [f"-D{_k}=" + os.environ[_k]]
 if os.environ.get("SW_DEBUG"):    # device-side bounds checks (slow; debug builds)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_DEBUG=1"]
 
@@ -49,8 +52,22 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+STAMP = LIB + ".flags"
+
+
+def _flags_stamp() -> str:
+    return " ".join(NVCC_FLAGS)
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
+        return True
+    # a library built with another flag set (an experiment variant) is stale
+    try:
+        with open(STAMP) as f:
+            if f.read() != _flags_stamp():
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
@@ -85,6 +102,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(_flags_stamp())
     return LIB
 
 

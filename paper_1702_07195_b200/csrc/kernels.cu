@@ -43,6 +43,9 @@
 #ifndef SW_ROWAHEAD
 #define SW_ROWAHEAD 1
 #endif
+#ifndef SW_TAILADDR
+#define SW_TAILADDR 0   // narrow-tail address: 0 = IMAD from the profile offset, 1 = from the chunk address
+#endif
 // SW_ABLATE (performance experiments only, wrong results): see the pass kernel.
 #ifndef SW_ABLATE
 #define SW_ABLATE 0
@@ -90,6 +93,12 @@ __device__ __forceinline__ uint32_t umulhi(uint32_t a, uint32_t b) {
   uint32_t d;
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
@@ -198,9 +207,12 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   static_assert(U == 1 || U == 2 || U == 4, "U: columns per unrolled block / prefetch distance");
   static_assert(QPM == 0 || QPM == 3, "profile mode");
   constexpr int RPC = 4;                    // rows per 16-B profile chunk
-  constexpr int KC = (R + RPC - 1) / RPC;   // chunks per lane
-  constexpr int LS = KC * G * 16;           // bytes per letter in the profile slice
+  constexpr int KC = (R + RPC - 1) / RPC;   // chunks per lane (the last may be a narrow tail)
+  constexpr int KCF = qp_full_chunks(R);    // chunks read with LDS.128 (kernels.cuh layout)
+  constexpr int TW = qp_tail_w(R) == 16 ? 0 : qp_tail_w(R);   // narrow tail: 4 or 8 B per lane
+  constexpr int LS = qp_letter_bytes(G, R); // bytes per letter in the profile slice
   constexpr int QP_U4 = kNL * LS / 16;
+  static_assert(LS % 128 == 0, "letter slices are 128-B aligned");
   constexpr int DESC_U4 = kNL * kNL;
   // Lane G-1 prefetches the previous pass's boundary U columns ahead through a
   // register ring only in the wavefront kernel; the per-pass boundary-reading
@@ -236,6 +248,10 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   const uint32_t zero = p.zero;
   const uint32_t s_desc = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t s_qp = s_desc + DESC_U4 * 16 + t * 16;
+  // narrow tail block: lane t of group g reads copy g % ncopy at lane stride TW
+  const uint32_t s_qpt = s_desc + DESC_U4 * 16 + KCF * G * 16 +
+                         (uint32_t)(((lane / G) % qp_tail_ncopy(G, R)) * G + t) * (uint32_t)(TW ? TW : 16);
+  const uint32_t s_dqt = s_qpt - s_qp;
   __syncthreads();
   const DescWords nul = load_desc(s_desc + kNulWord);
 
@@ -390,6 +406,20 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       const uint32_t offA = imad(offB, 0xffff0000u, w0);
       const uint32_t aA = imad(offA, 16u, s_qp);
       const uint32_t aB = imad(offB, 16u, s_qp);
+#if SW_TAILADDR == 0
+      const uint32_t aAt = TW ? imad(offA, 16u, s_qpt) : 0u;   // narrow tail chunk
+      const uint32_t aBt = TW ? imad(offB, 16u, s_qpt) : 0u;
+#else
+      const uint32_t aAt = TW ? imad(aA, one, s_dqt) : 0u;   // narrow tail chunk
+      const uint32_t aBt = TW ? imad(aB, one, s_dqt) : 0u;
+#endif
+      // profile chunk kk of the lane's rows (4 rows; the narrow tail: R % 4 rows)
+      auto ldq = [&](uint32_t a, uint32_t at, int kk) -> uint4 {
+        if (kk < KCF) return lds128(a + kk * G * 16);
+        if (TW == 4) return make_uint4(lds32(at), 0u, 0u, 0u);
+        const uint2 v = lds64(at);
+        return make_uint4(v.x, v.y, 0u, 0u);
+      };
       // S is reset after every separator column (END: the score was just read
       // from the chain; NUL: S is already 0): -32768 in each separator half.
       const uint32_t kneg_prev = kneg;
@@ -430,16 +460,18 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         // register (no per-column rotation of the H registers, which otherwise
         // costs a register permutation at every loop back-edge).
         // P(r) = SM(q_r, dB) * 65536 + SM(q_r, dA) (QPM 0) or the profile word (QPM 3).
-        uint4 ca = lds128(aA), cb = QPM == 0 ? lds128(aB) : make_uint4(0u, 0u, 0u, 0u);
+        uint4 ca = ldq(aA, aAt, 0), cb = QPM == 0 ? ldq(aB, aBt, 0) : make_uint4(0u, 0u, 0u, 0u);
         uint32_t tcur = imad(hd, one, QPM == 0 ? imad(cb.x, 65536u, ca.x) : ca.x);
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk) {
-          SW_CHECK(aA + kk * G * 16 + 16 <= s_desc + (DESC_U4 + QP_U4) * 16 &&
-                   aB + kk * G * 16 + 16 <= s_desc + (DESC_U4 + QP_U4) * 16);
+          SW_CHECK(kk >= KCF || (aA + kk * G * 16 + 16 <= s_desc + (DESC_U4 + QP_U4) * 16 &&
+                                 aB + kk * G * 16 + 16 <= s_desc + (DESC_U4 + QP_U4) * 16));
+          SW_CHECK(kk < KCF || (aAt + TW <= s_desc + (DESC_U4 + QP_U4) * 16 &&
+                                aBt + TW <= s_desc + (DESC_U4 + QP_U4) * 16));
           uint4 na = make_uint4(0u, 0u, 0u, 0u), nb = make_uint4(0u, 0u, 0u, 0u);
           if (kk + 1 < KC) {
-            na = lds128(aA + (kk + 1) * G * 16);
-            if (QPM == 0) nb = lds128(aB + (kk + 1) * G * 16);
+            na = ldq(aA, aAt, kk + 1);
+            if (QPM == 0) nb = ldq(aB, aBt, kk + 1);
           }
           const uint32_t av[8] = {ca.x, ca.y, ca.z, ca.w, na.x, na.y, na.z, na.w};
           const uint32_t bv[8] = {cb.x, cb.y, cb.z, cb.w, nb.x, nb.y, nb.z, nb.w};
@@ -464,10 +496,8 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       } else {
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
-        SW_CHECK(aA + kk * G * 16 + 16 <= s_desc + (DESC_U4 + QP_U4) * 16 &&
-                 aB + kk * G * 16 + 16 <= s_desc + (DESC_U4 + QP_U4) * 16);
-        const uint4 a = lds128(aA + kk * G * 16);
-        const uint4 b = (QPM == 0 && SW_ABLATE < 2) ? lds128(aB + kk * G * 16) : make_uint4(0u, 0u, 0u, 0u);
+        const uint4 a = ldq(aA, aAt, kk);
+        const uint4 b = (QPM == 0 && SW_ABLATE < 2) ? ldq(aB, aBt, kk) : make_uint4(0u, 0u, 0u, 0u);
         const uint32_t av[4] = {a.x, a.y, a.z, a.w};
         const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
@@ -761,23 +791,31 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
                                 int32_t *qp32, int32_t *qp32b, int goe, int ge) {
   // q2 == nullptr: one query (QPM 0); q2 != nullptr: query pair (QPM 3).  See
   // the profile-mode notes above the pass kernel for the word formats.
-  const int KC = (R + 3) / 4;
-  const int LS = KC * G * 16;
+  // slice layout: kernels.cuh (qp_letter_bytes): full chunks, then a narrow tail block
+  const int KCF = qp_full_chunks(R);
+  const int TW = qp_tail_w(R) == 16 ? 0 : qp_tail_w(R);
+  const int LS = qp_letter_bytes(G, R);
+  const int LW = LS / 4;                    // 32-bit words per letter
   const int mm = q2 ? max(m, m2) : m;
-  const int64_t nq = (int64_t)P * kNL * KC * G * 4;
+  const int64_t nq = (int64_t)P * kNL * LW;
   const int64_t ndesc = kNL * kNL;
   const int64_t n32 = (int64_t)kNL * mm;   // plain s32 profile(s)
   const int64_t total = nq + ndesc + n32;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (i < nq) {
-      int64_t rest = i;
-      const int e = (int)(rest & 3); rest >>= 2;
-      const int t = (int)(rest % G); rest /= G;
-      const int kk = (int)(rest % KC); rest /= KC;
-      const int c = (int)(rest % kNL);
-      const int pass = (int)(rest / kNL);
-      const int rloc = 4 * kk + e;
+      const int w = (int)(i % LW);
+      const int c = (int)((i / LW) % kNL);
+      const int pass = (int)(i / ((int64_t)LW * kNL));
+      int t, rloc;
+      if (w < KCF * G * 4) {              // full chunk kk: [kk][t][4 rows]
+        t = (w >> 2) % G;
+        rloc = 4 * (w / (G * 4)) + (w & 3);
+      } else {                            // tail block: [copy][t][TW/4 rows]
+        const int u = w - KCF * G * 4, tw = TW / 4;
+        t = (u / tw) % G;
+        rloc = 4 * KCF + u % tw;
+      }
       const int64_t row = (int64_t)pass * G * R + (int64_t)t * R + rloc;
       // kDummy16: separator letters and phantom rows
       int lo = kDummy16, hi = kDummy16;
@@ -1000,7 +1038,7 @@ using PassFn = void (*)(const SW16Params);
 
 template <int R, int G, int QPM>
 constexpr int smem_of() {
-  return (kNL * kNL + kNL * ((R + 3) / 4) * G) * 16;
+  return kNL * kNL * 16 + kNL * qp_letter_bytes(G, R);
 }
 
 struct TileEntry {
@@ -1148,14 +1186,14 @@ cudaError_t init_kernels() {
 
 size_t qp_bytes(int G, int R, int P, int qpm) {
   (void)qpm;
-  return (size_t)P * kNL * ((R + 3) / 4) * G * 16;
+  return (size_t)P * kNL * qp_letter_bytes(G, R);
 }
 
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,
                             int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
                             int goe, int ge, cudaStream_t st) {
   const int mm = d_query2 ? (m > m2 ? m : m2) : m;
-  const int64_t total = (int64_t)P * kNL * ((R + 3) / 4) * G * 4 + kNL * kNL + (int64_t)kNL * mm;
+  const int64_t total = (int64_t)P * kNL * (qp_letter_bytes(G, R) / 4) + kNL * kNL + (int64_t)kNL * mm;
   ++g_launches;
   qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_query2, m2, d_matrix, G, R, P,
                                                          reinterpret_cast<uint32_t *>(d_qp), d_desc, d_qp32,

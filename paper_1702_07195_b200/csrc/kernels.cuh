@@ -23,6 +23,30 @@ constexpr int kArith = SW_ARITH;
 constexpr int kBias16 = kArith == 1 ? 16384 : 0;   // stored = value + kBias16 (per half)
 constexpr int kDummy16 = kArith == 1 ? -16384 : -32768;   // separator / phantom-row score
 
+// Query-profile slice layout of the s16x2 pass kernel (one pass, one letter),
+// for a group of G lanes with R rows each:
+//   R/4 full chunks [chunk][lane t][4 rows x 4 B] (LDS.128, lane t at t*16:
+//   each quarter-warp hits 8 distinct 16-B bank groups), then, when R % 4 is
+//   1 or 2, a tail block of W = 4 or 8 B per lane [copy][lane t][W] read with
+//   LDS.32 / LDS.64 at lane stride W: contiguous, so conflict-free.  The block
+//   holds ncopy copies so that the 32/G groups of a warp read distinct banks
+//   (group g reads copy g % ncopy).  R % 4 == 3: the tail is a full-width
+//   chunk (LDS.128).  Every letter's slice is a multiple of 128 B.
+#ifndef SW_QPTAIL
+#define SW_QPTAIL 0   // 1: narrow conflict-free tail block (measured slower); 0: full-width LDS.128 tail chunk
+#endif
+__host__ __device__ constexpr int qp_tail_w(int R) {
+  return R % 4 == 0 ? 0 : ((R % 4 == 3 || !SW_QPTAIL) ? 16 : (R % 4 == 1 ? 4 : 8));
+}
+__host__ __device__ constexpr int qp_full_chunks(int R) { return qp_tail_w(R) == 16 ? R / 4 + 1 : R / 4; }
+__host__ __device__ constexpr int qp_tail_ncopy(int G, int R) {
+  return (qp_tail_w(R) == 4 || qp_tail_w(R) == 8) ? (G * qp_tail_w(R) >= 128 ? 1 : 128 / (G * qp_tail_w(R))) : 1;
+}
+__host__ __device__ constexpr int qp_tail_bytes(int G, int R) {
+  return (qp_tail_w(R) == 4 || qp_tail_w(R) == 8) ? qp_tail_ncopy(G, R) * G * qp_tail_w(R) : 0;
+}
+__host__ __device__ constexpr int qp_letter_bytes(int G, int R) { return qp_full_chunks(R) * G * 16 + qp_tail_bytes(G, R); }
+
 struct SW16Params {
   const uint32_t *stream;   // column words (descriptor byte offsets)
   const Item *items;

@@ -166,6 +166,16 @@ class ShardedSearch:
             flat[q * self.count:(q + 1) * self.count] = q * self.count_global + gidx
         d_flat = torch.from_numpy(flat).to(device)
         self.kk = min(self.k, self.count_global)
+        # a single process holding the whole database in original order: the
+        # assembly is the identity and the merged top-k is the local one
+        self.identity = (dist is None and world == 1 and self.count == self.count_global
+                         and bool(np.array_equal(gidx, np.arange(self.count, dtype=np.int64))))
+        if self.identity:
+            self.full = self.d_scores[:self.nq * self.count]
+            self.top_i = self.tk_i.view(self.nq, self.k)
+            self.top_s = self.tk_s.view(self.nq, self.k)
+            self.kl = min(self.k, self.count)
+            return
         if rank == 0:
             self.g_scores = torch.empty(world * span, dtype=torch.int32, device=device)
             self.g_tk_i = torch.empty(world * self.nq * self.k, dtype=torch.int64, device=device)
@@ -211,6 +221,8 @@ class ShardedSearch:
                     self.backend.topk(self.d_scores[q * self.count:], self.d_gidx, self.count, self.kl,
                                       self.tk_i[q * k:], self.tk_s[q * k:], stream)
                     launches += 3
+            if self.identity:
+                return launches
             if self.dist is not None:
                 gather_to_root(self.d_scores, self.world, self.rank, self.dist,
                                out=self._views(self.g_scores, self.world, span))
