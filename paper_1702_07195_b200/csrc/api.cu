@@ -129,6 +129,8 @@ struct State {
   // forced tile
   int force_G = 0, force_R = 0;
   int wave_mode = 0;        // cross-pass wavefront: 0 auto, 1 always (multi-pass), -1 never
+  int lat_mode = 0;         // low-latency rows (LAT tiles): 0 auto, 1 always, -1 never
+  bool last_lat = false;
   bool last_wave = false;
   DevBuf<int> progress;     // wavefront: finished columns per (pass, item)
   // timing events of the last search
@@ -212,14 +214,14 @@ int ensure_device_ready() {
 // small groups for that tail (cfg4: 5-35 k residue sequences).
 int choose_tile(int m, int qpm, const Image &I, bool wave_only = false) {
   if (g.force_G) {
-    int ti = find_tile_mode(g.force_G, g.force_R, qpm);
+    int ti = find_tile_mode(g.force_G, g.force_R, qpm, 0);
     if (ti >= 0) return ti;
   }
   double best = 1e300;
   int bi = -1;
   for (int i = 0; i < num_tiles(); ++i) {
     const TileInfo ti = tile(i);
-    if (ti.qpm != qpm || tile_ctas_per_sm(i) < 1 || (wave_only && !tile_has_wave(i))) continue;
+    if (ti.qpm != qpm || ti.lat || tile_ctas_per_sm(i) < 1 || (wave_only && !tile_has_wave(i))) continue;
     const int rows = ti.G * ti.R;
     const int P = (m + rows - 1) / rows;
     const double groups = (double)g.num_sms * tile_ctas_per_sm(i) * tile_threads(i) / ti.G;
@@ -230,6 +232,46 @@ int choose_tile(int m, int qpm, const Image &I, bool wave_only = false) {
     const double cost = (double)rows * (1.0 / ti.eff0 + (P - 1) / ti.eff1) / balance + P * 0.002;
     if (cost < best - 1e-12) {
       best = cost;
+      bi = i;
+    }
+  }
+  return bi;
+}
+
+// Time model of a pass launch (profiles/r02_lat_calibration.jsonl):
+//   bulk  = cells computed (phantom rows included) / the tile's throughput,
+//   chain = (longest item + G) columns x the per-column step latency of one
+//           group running alone, c0 + c1 * R cycles at the SM clock;
+// a pass lasts about max(bulk, chain).  LAT tiles have a short chain (c1 is
+// one dependent instruction per row) and lower throughput.
+struct StepModel { double c0, c1; };
+constexpr StepModel kStepNormal{120.0, 28.0};   // cycles per column: per step + per row
+constexpr StepModel kStepLat{110.0, 10.0};
+constexpr double kLatThroughput = 0.45;         // LAT tile throughput relative to eff0 (one 256-thread CTA/SM)
+
+double pass_time_model(const TileInfo &T, int m, const Image &I, bool lat) {
+  const int rows = T.G * T.R;
+  const int P = (m + rows - 1) / rows;
+  const double f = 1.9e9;   // SM cycles per second (max clock)
+  const double cells = (double)rows * P * 2.0 * (double)I.total_cols;
+  const double bulk = cells / ((lat ? kLatThroughput : 1.0) * T.eff0 * 1e9);
+  const StepModel sm = lat ? kStepLat : kStepNormal;
+  const double chain = (double)P * ((double)I.max_item_cols + T.G) * (sm.c0 + sm.c1 * T.R) / f;
+  return std::max(bulk, chain);
+}
+
+// The LAT tile with the smallest modelled time, if it beats the throughput
+// tile `ti` by 10% (or any LAT tile when forced); -1 if none.
+int choose_lat_tile(int m, const Image &I, int ti, bool forced) {
+  const double base = pass_time_model(tile(ti), m, I, false);
+  double best = forced ? 1e300 : 0.9 * base;
+  int bi = -1;
+  for (int i = 0; i < num_tiles(); ++i) {
+    const TileInfo t = tile(i);
+    if (!t.lat || t.qpm != 0 || tile_ctas_per_sm(i) < 1) continue;
+    const double c = pass_time_model(t, m, I, true);
+    if (c < best) {
+      best = c;
       bi = i;
     }
   }
@@ -303,6 +345,25 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       wave = true;
     }
   }
+  // Low-latency rows (LAT tiles): when one long work item's
+  // critical path, not the total work, bounds the pass (a small database
+  // with a long sequence, e.g. configs[0]), run tiles whose per-row vertical
+  // chain is one instruction, on one 256-thread CTA per SM.
+  bool lat = false;
+  if (!pair && !wave && g.lat_mode >= 0) {
+    int tl = -1;
+    if (g.force_G) {   // a forced LAT tile: used when forced LAT or when it is LAT-only
+      const int tf = find_tile_mode(g.force_G, g.force_R, 0, 1);
+      if (tf >= 0 && (g.lat_mode == 1 || find_tile_mode(g.force_G, g.force_R, 0, 0) < 0)) tl = tf;
+      else if (g.lat_mode == 1) tl = choose_lat_tile(mm, I, ti, true);
+    } else {
+      tl = choose_lat_tile(mm, I, ti, g.lat_mode == 1);
+    }
+    if (tl >= 0) {
+      ti = tl;
+      lat = true;
+    }
+  }
   const TileInfo T = tile(ti);
   const int rows = T.G * T.R;
   const int P = (mm + rows - 1) / rows;
@@ -356,7 +417,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
                            g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr,
                            goe, ge, st));
 
-  const int grid = g.num_sms * std::max(1, tile_ctas_per_sm(ti));
+  const int grid = g.num_sms * (lat ? 1 : std::max(1, tile_ctas_per_sm(ti)));
   // Exact s32 re-scoring ("recalculated using the next wider
   // integer range").  Resident database: right after the gather of pass p, the
   // sequences first flagged in pass p are re-scored from row p*rows on, seeded
@@ -523,6 +584,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   g.last_P = P;
   g.last_mode = mode;
   g.last_wave = wave;
+  g.last_lat = lat;
   g.last_flags = -1;
   g.last_cells32 = -1;
   return SW_OK;
@@ -884,10 +946,10 @@ int sw_last_stats(int64_t *stats, int n) {
     g.last_cells32 = cells;
   }
   const Image &I = g.img[g.last_mode == 3 ? 1 : 0];
-  const int64_t v[11] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
+  const int64_t v[12] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
                          g.last_flags, g.last_cells32, I.total_cols, I.num_items, g.last_thresh, kArith,
-                         g.last_wave ? 1 : 0};
-  const int m = std::min(n, 11);
+                         g.last_wave ? 1 : 0, g.last_lat ? 1 : 0};
+  const int m = std::min(n, 12);
   for (int i = 0; i < m; ++i) stats[i] = v[i];
   return m;
 }
@@ -916,13 +978,23 @@ int sw_set_tile(int32_t G, int32_t R) {
     g.force_G = g.force_R = 0;
     return SW_OK;
   }
-  if (find_tile_mode(G, R, 0) < 0 || find_tile_mode(G, R, 3) < 0) return fail(SW_EINVAL, "tile not compiled");
+  if ((find_tile_mode(G, R, 0) < 0 || find_tile_mode(G, R, 3) < 0) && find_tile_mode(G, R, 0, 1) < 0)
+    return fail(SW_EINVAL, "tile not compiled");
   g.force_G = G;
   g.force_R = R;
   return SW_OK;
 }
 
-int sw_tile_supported(int32_t G, int32_t R) { return find_tile_mode(G, R, 0) >= 0 ? 1 : 0; }
+int sw_tile_supported(int32_t G, int32_t R) {
+  return (find_tile_mode(G, R, 0) >= 0 ? 1 : 0) | (find_tile_mode(G, R, 0, 1) >= 0 ? 2 : 0);
+}
+
+int sw_set_latency_mode(int32_t mode) {
+  t_err.clear();
+  if (mode < -1 || mode > 1) return fail(SW_EINVAL, "mode must be -1, 0 or 1");
+  g.lat_mode = mode;
+  return SW_OK;
+}
 
 int sw_set_wave(int32_t mode) {
   t_err.clear();

@@ -109,6 +109,7 @@ struct TileInfo {
   int smem_bytes;           // dynamic shared memory of the pass kernel
   int qpm;                  // profile mode (see kernels.cu)
   float eff0, eff1;         // measured full-row GCUPS: first pass / boundary-reading pass
+  int lat;                  // low-latency row arithmetic (critical-path-bound launches)
 };
 
 // Number of kernel launches issued by the library since it was loaded.
@@ -118,7 +119,7 @@ int64_t launch_count();
 int num_tiles();
 TileInfo tile(int i);
 int find_tile(int G, int R);                // index or -1 (profile mode 0)
-int find_tile_mode(int G, int R, int qpm);  // index or -1
+int find_tile_mode(int G, int R, int qpm, int lat = 0);  // index or -1
 size_t qp_bytes(int G, int R, int P, int qpm);
 
 // Prepares kernel attributes (max dynamic smem).  Returns cudaError_t.

@@ -508,3 +508,42 @@ def test_cross_pass_wavefront_matches_oracle():
         sw.sw_set_tile(0)
         sw.sw_set_wave(0)
 
+
+
+def test_lat_tiles_are_exact():
+    """Low-latency (LAT) tiles: Eq. 3 as max(F - Ge, max(max(t, E) - Goe, 0))
+    (equal because Goe >= Ge).  Every LAT tile, forced, on random databases
+    with random matrices and gaps (zero open: Goe == Ge), multi-pass queries
+    (boundary-reading launches) and saturating sequences (s32 re-scoring)."""
+    rng = np.random.default_rng(4711)
+    seqs = [rng.integers(0, 24, int(L)).astype(np.uint8) for L in rng.integers(0, 900, 300)]
+    seqs += [si.rr_residues(rng, 4000), encode("W" * 1700), np.full(700, 3, np.uint8)]
+    db = _db(seqs)
+    sw.sw_db_load(db.residues, db.offsets)
+    try:
+        sw.sw_set_latency_mode(1)
+        for G, R in ((32, 4), (32, 5), (32, 6), (32, 8), (16, 9), (32, 12), (32, 16)):
+            assert sw.sw_tile_supported(G, R, lat=True)
+            sw.sw_set_tile(G, R)
+            for trial in range(3):
+                m = int(rng.integers(1, 1800)) if trial else 1700
+                q = rng.integers(0, 24, m).astype(np.uint8) if trial else encode("W" * 1700)
+                M = BLOSUM62 if trial != 1 else si.random_symmetric_matrix(rng)
+                go, ge = (10, 2) if trial != 2 else (0, int(rng.integers(0, 5)))
+                got = sw.sw_search(q, M, go, ge)
+                st = sw.sw_last_stats()
+                assert st["lat"] == 1 and st["G"] == G and st["R"] == R, st
+                exp = oracle.batch(q, db.residues, db.offsets, M, go, ge)
+                bad = np.nonzero(got != exp)[0]
+                assert bad.size == 0, (G, R, trial, m, bad[:5], got[bad[:5]], exp[bad[:5]])
+        # automatic choice on configs[0] (a small database with one long item)
+        sw.sw_set_tile(0)
+        sw.sw_set_latency_mode(0)
+        w = si.config0()
+        sw.sw_db_load(w.db.residues, w.db.offsets)
+        got = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
+        exp = oracle.batch(w.queries[0], w.db.residues, w.db.offsets, BLOSUM62, 10, 2)
+        assert (got == exp).all()
+    finally:
+        sw.sw_set_tile(0)
+        sw.sw_set_latency_mode(0)
