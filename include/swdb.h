@@ -210,7 +210,7 @@ int sw_scatter_dev(const int32_t *d_src, const int64_t *d_index, int64_t n, int3
  *              2 FMA instructions per pair of cells), 0 = relu form (5.5 ALU
  *              + 1 FMA),
  *   stats[10] = 1 if the last search ran as a cross-pass wavefront,
- *   stats[11] = 1 if it ran the low-latency (LAT) tiles.
+ *   stats[11] = 1 if it ran a latency tile (sw_set_latency_mode).
  * Returns the number of entries written (<= n).
  */
 int sw_last_stats(int64_t *stats, int n);
@@ -232,19 +232,18 @@ int sw_last_timing(float *ms, int n);
  * automatic choice.  Returns SW_OK or SW_EINVAL.
  */
 int sw_set_tile(int32_t G, int32_t R);
-/* Bit 0: (G, R) is a compiled throughput tile; bit 1: a compiled LAT tile. */
+/* Bit 0: (G, R) is a compiled throughput tile; bit 1: a compiled latency tile. */
 int sw_tile_supported(int32_t G, int32_t R);
 
 /*
- * sw_set_latency_mode -- low-latency (LAT) pass tiles for searches whose time
- * is one long work item's critical path rather than the total work (small
- * databases with a long sequence): the vertical dependency
- * through a lane's rows is one instruction per row (Eq. 3 rewritten with
- * Goe >= Ge), at 1.5 more ALU instructions per pair of cells.  mode 0
+ * sw_set_latency_mode -- latency tiles for searches whose time is one long
+ * work item's critical path rather than the total work (small databases with
+ * a long sequence): a small number of rows per lane (shorter
+ * per-column step of a lane group) on one 256-thread CTA per SM.  mode 0
  * (default): chosen by the pass time model; 1: always (the forced tile if it
- * is a LAT tile, else the model's best LAT tile); -1: never.  Single-query
- * searches of a resident database without the cross-pass wavefront only.
- * Returns SW_OK or SW_EINVAL.
+ * is a latency tile, else the model's best latency tile); -1: never.
+ * Single-query searches of a resident database without the cross-pass
+ * wavefront only.  Returns SW_OK or SW_EINVAL.
  */
 int sw_set_latency_mode(int32_t mode);
 

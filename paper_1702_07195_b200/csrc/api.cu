@@ -129,7 +129,7 @@ struct State {
   // forced tile
   int force_G = 0, force_R = 0;
   int wave_mode = 0;        // cross-pass wavefront: 0 auto, 1 always (multi-pass), -1 never
-  int lat_mode = 0;         // low-latency rows (LAT tiles): 0 auto, 1 always, -1 never
+  int lat_mode = 0;         // latency tiles: 0 auto, 1 always, -1 never
   bool last_lat = false;
   bool last_wave = false;
   DevBuf<int> progress;     // wavefront: finished columns per (pass, item)
@@ -241,27 +241,27 @@ int choose_tile(int m, int qpm, const Image &I, bool wave_only = false) {
 // Time model of a pass launch (profiles/r02_lat_calibration.jsonl):
 //   bulk  = cells computed (phantom rows included) / the tile's throughput,
 //   chain = (longest item + G) columns x the per-column step latency of one
-//           group running alone, c0 + c1 * R cycles at the SM clock;
-// a pass lasts about max(bulk, chain).  LAT tiles have a short chain (c1 is
-// one dependent instruction per row) and lower throughput.
-struct StepModel { double c0, c1; };
-constexpr StepModel kStepNormal{120.0, 28.0};   // cycles per column: per step + per row
-constexpr StepModel kStepLat{110.0, 10.0};
-constexpr double kLatThroughput = 0.45;         // LAT tile throughput relative to eff0 (one 256-thread CTA/SM)
+//           group, c0 + c1 * R SM cycles (measured on one 12,000-residue
+//           sequence: one warp issues its column's instructions back to back,
+//           ~13.5 cycles per row plus ~150 per column for the lane-to-lane
+//           hand-over, the descriptor -> profile load chain and the stores);
+// a pass lasts about max(bulk, chain).  Latency tiles (small R, one
+// 256-thread CTA per SM) shorten the chain at lower throughput.
+constexpr double kStepC0 = 150.0, kStepC1 = 13.5;
+constexpr double kLatThroughput = 0.6;   // latency-tile throughput relative to a 512-thread tile's eff0
 
 double pass_time_model(const TileInfo &T, int m, const Image &I, bool lat) {
   const int rows = T.G * T.R;
   const int P = (m + rows - 1) / rows;
-  const double f = 1.9e9;   // SM cycles per second (max clock)
+  const double f = 1.9e9;   // SM cycles per second
   const double cells = (double)rows * P * 2.0 * (double)I.total_cols;
   const double bulk = cells / ((lat ? kLatThroughput : 1.0) * T.eff0 * 1e9);
-  const StepModel sm = lat ? kStepLat : kStepNormal;
-  const double chain = (double)P * ((double)I.max_item_cols + T.G) * (sm.c0 + sm.c1 * T.R) / f;
+  const double chain = (double)P * ((double)I.max_item_cols + T.G) * (kStepC0 + kStepC1 * T.R) / f;
   return std::max(bulk, chain);
 }
 
-// The LAT tile with the smallest modelled time, if it beats the throughput
-// tile `ti` by 10% (or any LAT tile when forced); -1 if none.
+// The latency tile with the smallest modelled time, if it beats the throughput
+// tile `ti` by 10% (or the best latency tile when forced); -1 if none.
 int choose_lat_tile(int m, const Image &I, int ti, bool forced) {
   const double base = pass_time_model(tile(ti), m, I, false);
   double best = forced ? 1e300 : 0.9 * base;
@@ -345,14 +345,14 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       wave = true;
     }
   }
-  // Low-latency rows (LAT tiles): when one long work item's
-  // critical path, not the total work, bounds the pass (a small database
-  // with a long sequence, e.g. configs[0]), run tiles whose per-row vertical
-  // chain is one instruction, on one 256-thread CTA per SM.
+  // Latency tiles: when one long work item's critical path,
+  // not the total work, bounds the pass (a small database with a long
+  // sequence, e.g. configs[0]), run a small-R tile on one 256-thread CTA per
+  // SM: the per-column step of a group is shorter.
   bool lat = false;
   if (!pair && !wave && g.lat_mode >= 0) {
     int tl = -1;
-    if (g.force_G) {   // a forced LAT tile: used when forced LAT or when it is LAT-only
+    if (g.force_G) {   // a forced latency tile: used when forced or when it is latency-only
       const int tf = find_tile_mode(g.force_G, g.force_R, 0, 1);
       if (tf >= 0 && (g.lat_mode == 1 || find_tile_mode(g.force_G, g.force_R, 0, 0) < 0)) tl = tf;
       else if (g.lat_mode == 1) tl = choose_lat_tile(mm, I, ti, true);

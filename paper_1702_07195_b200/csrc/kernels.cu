@@ -201,13 +201,7 @@ __device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on
 //   outgoing registers with lane 0's next-column inputs, including the
 //   previous pass's boundary (prefetched U columns ahead).  No per-lane
 //   selects at lane 0.
-// LAT (low-latency rows, for launches whose time is one long item's critical
-// path): Eq. 3 as F' = max(F - Ge, max(max(t, E) - Goe, 0)),
-// equal to max(F - Ge, max(H - Goe, 0)) because Goe >= Ge, so the vertical
-// chain through a lane's R rows is one VIADDMNMX per row instead of three
-// (VIMNMX3 -> VIADDMNMX -> VIADDMNMX), for 1.5 more ALU instructions per pair
-// of cells.
-template <int R, int G, bool BIN, int QPM, int NT, int U, bool WAVE = false, bool LAT = false>
+template <int R, int G, bool BIN, int QPM, int NT, int U, bool WAVE = false>
 __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   static_assert(!WAVE || BIN, "the wavefront kernel reads boundaries (from pass 1 on)");
   static_assert(U == 1 || U == 2 || U == 4, "U: columns per unrolled block / prefetch distance");
@@ -488,20 +482,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
               uint32_t tnext = 0u;
               if (r + 1 < R)
                 tnext = imad(H[r], one, QPM == 0 ? imad(bv[j + 1], 65536u, av[j + 1]) : av[j + 1]);
-              if (LAT) {
-                const uint32_t u = __viaddmax_s16x2(__vmaxs2(tcur, E[r]), ngoe, kB2);   // off the F chain
-                const uint32_t h = __vimax3_s16x2(tcur, E[r], F);     // Eq. 1
-                H[r] = h;
-                const uint32_t hg = __viaddmax_s16x2(h, ngoe, kB2);
-                E[r] = __viaddmax_s16x2(E[r], nge, hg);              // Eq. 2 (next column)
-                F = __viaddmax_s16x2(F, nge, u);                     // Eq. 3 (next row), Goe >= Ge
-              } else {
-                const uint32_t h = __vimax3_s16x2(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
-                H[r] = h;
-                const uint32_t hg = __viaddmax_s16x2(h, ngoe, kB2);  // max(H-Goe, 0)
-                E[r] = __viaddmax_s16x2(E[r], nge, hg);              // Eq. 2 (next column)
-                F = __viaddmax_s16x2(F, nge, hg);                    // Eq. 3 (next row)
-              }
+              const uint32_t h = __vimax3_s16x2(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
+              H[r] = h;
+              const uint32_t hg = __viaddmax_s16x2(h, ngoe, kB2);  // max(H-Goe, 0)
+              E[r] = __viaddmax_s16x2(E[r], nge, hg);              // Eq. 2 (next column)
+              F = __viaddmax_s16x2(F, nge, hg);                    // Eq. 3 (next row)
               tcur = tnext;
             }
           }
@@ -1062,16 +1047,17 @@ struct TileEntry {
   int ctas;
   PassFn fnw;        // cross-pass wavefront (all passes in one launch), or null
   int ctasw;         // resident CTAs per SM of fnw (its grid must be fully resident)
-  int lat;           // 1: low-latency row arithmetic (LAT), for critical-path-bound launches
+  int lat;           // 1: latency tile (256 threads, one CTA per SM), for critical-path-bound launches
 };
 
 #define SW_TILE_NTU(G_, R_, M_, NT_, U_)                                                     \
   {G_, R_, M_, NT_, smem_of<R_, G_, M_>(), sw16_pass_kernel<R_, G_, false, M_, NT_, U_>,   \
    sw16_pass_kernel<R_, G_, true, M_, NT_, U_>, 0, nullptr, 0, 0}
-// low-latency tiles (single query): 256 threads, one CTA per SM when launched
-#define SW_TILE_LAT(G_, R_)                                                                           \
-  {G_, R_, 0, 256, smem_of<R_, G_, 0>(), sw16_pass_kernel<R_, G_, false, 0, 256, SW_UNROLL, false, true>, \
-   sw16_pass_kernel<R_, G_, true, 0, 256, SW_UNROLL, false, true>, 0, nullptr, 0, 1}
+// latency tiles (single query): small R, 256 threads, launched
+// with one CTA per SM, for passes bounded by one long item's critical path
+#define SW_TILE_LAT(G_, R_)                                                                    \
+  {G_, R_, 0, 256, smem_of<R_, G_, 0>(), sw16_pass_kernel<R_, G_, false, 0, 256, SW_UNROLL>, \
+   sw16_pass_kernel<R_, G_, true, 0, 256, SW_UNROLL>, 0, nullptr, 0, 1}
 // tiles that also have a wavefront kernel (single-query mode)
 #define SW_TILE_W(G_, R_)                                                                     \
   {G_, R_, 0, 512, smem_of<R_, G_, 0>(), sw16_pass_kernel<R_, G_, false, 0, 512, SW_UNROLL>, \
@@ -1097,8 +1083,8 @@ TileEntry g_tiles[] = {
     SW_TILE_W(32, 16), SW_TILE_W(32, 29), SW_TILE_W(32, 32),
     SW_TILES_COMMON(3), SW_TILE(16, 16, 3), SW_TILE(16, 29, 3), SW_TILE(16, 32, 3), SW_TILE(32, 8, 3),
     SW_TILE(32, 16, 3), SW_TILE(32, 29, 3), SW_TILE(32, 32, 3),
-    SW_TILE_LAT(32, 4), SW_TILE_LAT(32, 5), SW_TILE_LAT(32, 6), SW_TILE_LAT(32, 8), SW_TILE_LAT(16, 9),
-    SW_TILE_LAT(32, 12), SW_TILE_LAT(32, 16)};
+    SW_TILE_LAT(32, 3), SW_TILE_LAT(32, 4), SW_TILE_LAT(32, 5), SW_TILE_LAT(32, 6), SW_TILE_LAT(32, 8),
+    SW_TILE_LAT(16, 9)};
 #undef SW_TILES_COMMON
 #undef SW_TILE_W
 #undef SW_TILE

@@ -109,7 +109,7 @@ struct TileInfo {
   int smem_bytes;           // dynamic shared memory of the pass kernel
   int qpm;                  // profile mode (see kernels.cu)
   float eff0, eff1;         // measured full-row GCUPS: first pass / boundary-reading pass
-  int lat;                  // low-latency row arithmetic (critical-path-bound launches)
+  int lat;                  // latency tile (critical-path-bound launches)
 };
 
 // Number of kernel launches issued by the library since it was loaded.

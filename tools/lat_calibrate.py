@@ -1,6 +1,6 @@
 """Calibration of the pass time model (api.cu pass_time_model):
 per-column step latency of one group running alone, throughput tiles vs the
-low-latency (LAT) tiles, and configs[0] under each choice (dev tool, 1 GPU).
+latency tiles, and configs[0] under each choice (dev tool, 1 GPU).
 
     python tools/lat_calibrate.py > profiles/r02_lat_calibration.jsonl
 """
@@ -44,7 +44,7 @@ def main():
     sw.sw_db_load(db.residues, db.offsets)
     d = torch.empty(1, dtype=torch.int32, device="cuda")
     tiles = [(32, 8, 0), (32, 12, 0), (32, 16, 0), (16, 16, 0), (16, 29, 0), (32, 29, 0), (8, 18, 0),
-             (32, 4, 1), (32, 5, 1), (32, 6, 1), (32, 8, 1), (16, 9, 1), (32, 12, 1), (32, 16, 1)]
+             (32, 3, 1), (32, 4, 1), (32, 5, 1), (32, 6, 1), (32, 8, 1), (16, 9, 1)]
     for G, R, lat in tiles:
         sw.sw_set_latency_mode(1 if lat else -1)
         sw.sw_set_tile(G, R)
