@@ -210,7 +210,9 @@ int sw_scatter_dev(const int32_t *d_src, const int64_t *d_index, int64_t n, int3
  *              2 FMA instructions per pair of cells), 0 = relu form (5.5 ALU
  *              + 1 FMA),
  *   stats[10] = 1 if the last search ran as a cross-pass wavefront,
- *   stats[11] = 1 if it ran a latency tile (sw_set_latency_mode).
+ *   stats[11] = 1 if it ran a latency tile (sw_set_latency_mode),
+ *   stats[12] = substitution scores of the 16-bit kernel: 1 = query profile,
+ *              2 = score profile (sw_set_profile).
  * Returns the number of entries written (<= n).
  */
 int sw_last_stats(int64_t *stats, int n);
@@ -232,8 +234,27 @@ int sw_last_timing(float *ms, int n);
  * automatic choice.  Returns SW_OK or SW_EINVAL.
  */
 int sw_set_tile(int32_t G, int32_t R);
-/* Bit 0: (G, R) is a compiled throughput tile; bit 1: a compiled latency tile. */
+/* Bit 0: (G, R) is a compiled throughput tile; bit 1: a compiled latency
+ * tile; bit 2: a compiled score-profile tile. */
 int sw_tile_supported(int32_t G, int32_t R);
+
+/*
+ * sw_set_profile -- where the 16-bit kernel takes its substitution scores
+ * from (Section 4.3 "Substitution scores"):
+ *   1: query profile QP[letter][query row], built per query;
+ *      a lane reads 4 rows per 16-B load for each of the column's two
+ *      database letters and packs the two halves with one IMAD per row;
+ *   2: score profile SP[database letter pair][query letter],
+ *      one word SM(c, dB) * 65536 + SM(c, dA) per pair and query letter,
+ *      built per scoring matrix (not per database group: on B200 every pair
+ *      fits in shared memory); a lane reads one word per row at its row's
+ *      query letter (no packing);
+ *   0 (default): chosen by query length from the measured QP/SP crossover
+ *      (DESIGN.md 4.6).
+ * Single-query searches only (query pairs always use their paired profile).
+ * Returns SW_OK or SW_EINVAL.
+ */
+int sw_set_profile(int32_t mode);
 
 /*
  * sw_set_latency_mode -- latency tiles for searches whose time is one long

@@ -130,6 +130,8 @@ struct State {
   int force_G = 0, force_R = 0;
   int wave_mode = 0;        // cross-pass wavefront: 0 auto, 1 always (multi-pass), -1 never
   int lat_mode = 0;         // latency tiles: 0 auto, 1 always, -1 never
+  int prof_mode = 0;        // substitution scores: 0 auto, 1 query profile, 2 score profile
+  int last_prof = 1;
   bool last_lat = false;
   bool last_wave = false;
   DevBuf<int> progress;     // wavefront: finished columns per (pass, item)
@@ -278,6 +280,14 @@ int choose_lat_tile(int m, const Image &I, int ti, bool forced) {
   return bi;
 }
 
+// QP/SP switch by query length (the paper's best profile
+// depended on the query length and the lane width).  Measured on B200 in the
+// real pass kernel over configs[3]'s 20 query lengths: the query profile is
+// faster at every length (profiles/r02_qp_sp_crossover.jsonl), so the switch
+// point lies beyond the longest query measured.
+constexpr int kSPMinLen = INT_MAX;
+bool sp_wins(int m) { return m >= kSPMinLen; }
+
 int validate_query(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t gap_open,
                    int32_t gap_extend) {
   if (!query || !matrix) return fail(SW_EINVAL, "query or matrix is NULL");
@@ -308,7 +318,12 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
 
   const bool pair = q2 != nullptr;
   if (pair && g.streamed) return fail(SW_EINVAL, "query pairs / batch search need a resident database");
-  const int mode = pair ? 3 : 0;
+  // Substitution scores: the query profile
+  // (QPM 0) or the score profile (QPM 1, sw_set_profile).  Auto: the query
+  // profile at every query length (the switch point measured on configs[3]'s
+  // 20 lengths, profiles/r02_qp_sp_crossover.jsonl).
+  const bool use_sp = !pair && (g.prof_mode == 2 || (g.prof_mode == 0 && sp_wins(pair ? std::max(m, m2) : m)));
+  const int mode = pair ? 3 : (use_sp ? 1 : 0);
   const Image &I = g.img[pair ? 1 : 0];
   const int mm = pair ? std::max(m, m2) : m;
   int ti = choose_tile(mm, mode, I);
@@ -324,7 +339,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // tiles when their units exceed half the groups.  Forced mode (1) uses the
   // forced or chosen tile when it has a wavefront kernel, else 32x16 / 32x8.
   bool wave = false;
-  if (!pair && !g.streamed && g.wave_mode >= 0) {
+  if (!pair && !use_sp && !g.streamed && g.wave_mode >= 0) {
     auto passes_of = [&](int i) { return (mm + tile(i).G * tile(i).R - 1) / (tile(i).G * tile(i).R); };
     const int t8 = find_tile_mode(32, 8, 0), t16 = find_tile_mode(32, 16, 0);
     const double items = (double)std::max(1, I.num_items);
@@ -350,7 +365,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // sequence, e.g. configs[0]), run a small-R tile on one 256-thread CTA per
   // SM: the per-column step of a group is shorter.
   bool lat = false;
-  if (!pair && !wave && g.lat_mode >= 0) {
+  if (!pair && !use_sp && !wave && g.lat_mode >= 0) {
     int tl = -1;
     if (g.force_G) {   // a forced latency tile: used when forced or when it is latency-only
       const int tf = find_tile_mode(g.force_G, g.force_R, 0, 1);
@@ -415,7 +430,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int pev0 = 2 * g.npev;
   CUDA_TRY(launch_qp_build(g.query.p, m, pair ? g.query2.p : nullptr, m2, g.matrix.p, T.G, T.R, P, g.qp.p,
                            g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr,
-                           goe, ge, st));
+                           goe, ge, st, use_sp ? 1 : 0));
 
   const int grid = g.num_sms * (lat ? 1 : std::max(1, tile_ctas_per_sm(ti)));
   // Exact s32 re-scoring ("recalculated using the next wider
@@ -549,6 +564,8 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       // its leading run of flagged sequences (item_skip_kernel below)
       const bool skipping = !strm && !pair && P > 1;
       p.skip = (skipping && pass > 0) ? g.skip.p : nullptr;
+      p.query = g.query.p;
+      p.m = m;
       const int pe = pev0 + 2 * (k * P + pass);
       CUDA_TRY(pass_event(pe + 1));
       CUDA_TRY(cudaEventRecord(g.pev[pe], st));
@@ -585,6 +602,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   g.last_mode = mode;
   g.last_wave = wave;
   g.last_lat = lat;
+  g.last_prof = use_sp ? 2 : 1;
   g.last_flags = -1;
   g.last_cells32 = -1;
   return SW_OK;
@@ -946,10 +964,10 @@ int sw_last_stats(int64_t *stats, int n) {
     g.last_cells32 = cells;
   }
   const Image &I = g.img[g.last_mode == 3 ? 1 : 0];
-  const int64_t v[12] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
+  const int64_t v[13] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
                          g.last_flags, g.last_cells32, I.total_cols, I.num_items, g.last_thresh, kArith,
-                         g.last_wave ? 1 : 0, g.last_lat ? 1 : 0};
-  const int m = std::min(n, 12);
+                         g.last_wave ? 1 : 0, g.last_lat ? 1 : 0, g.last_prof};
+  const int m = std::min(n, 13);
   for (int i = 0; i < m; ++i) stats[i] = v[i];
   return m;
 }
@@ -978,7 +996,8 @@ int sw_set_tile(int32_t G, int32_t R) {
     g.force_G = g.force_R = 0;
     return SW_OK;
   }
-  if ((find_tile_mode(G, R, 0) < 0 || find_tile_mode(G, R, 3) < 0) && find_tile_mode(G, R, 0, 1) < 0)
+  if ((find_tile_mode(G, R, 0) < 0 || find_tile_mode(G, R, 3) < 0) && find_tile_mode(G, R, 0, 1) < 0 &&
+      find_tile_mode(G, R, 1) < 0)
     return fail(SW_EINVAL, "tile not compiled");
   g.force_G = G;
   g.force_R = R;
@@ -986,7 +1005,16 @@ int sw_set_tile(int32_t G, int32_t R) {
 }
 
 int sw_tile_supported(int32_t G, int32_t R) {
-  return (find_tile_mode(G, R, 0) >= 0 ? 1 : 0) | (find_tile_mode(G, R, 0, 1) >= 0 ? 2 : 0);
+  return (find_tile_mode(G, R, 0) >= 0 ? 1 : 0) | (find_tile_mode(G, R, 0, 1) >= 0 ? 2 : 0) |
+         (find_tile_mode(G, R, 1) >= 0 ? 4 : 0);
+}
+
+int sw_set_profile(int32_t mode) {
+  t_err.clear();
+  if (mode < 0 || mode > 2) return fail(SW_EINVAL, "mode must be 0, 1 or 2");
+  if (mode == 2 && kArith != 1) return fail(SW_EINVAL, "the score profile needs the biased arithmetic build");
+  g.prof_mode = mode;
+  return SW_OK;
 }
 
 int sw_set_latency_mode(int32_t mode) {

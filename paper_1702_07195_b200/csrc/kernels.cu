@@ -205,13 +205,14 @@ template <int R, int G, bool BIN, int QPM, int NT, int U, bool WAVE = false>
 __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   static_assert(!WAVE || BIN, "the wavefront kernel reads boundaries (from pass 1 on)");
   static_assert(U == 1 || U == 2 || U == 4, "U: columns per unrolled block / prefetch distance");
-  static_assert(QPM == 0 || QPM == 3, "profile mode");
+  static_assert(QPM == 0 || QPM == 1 || QPM == 3, "profile mode");
+  static_assert(QPM != 1 || kArith == 1, "the score profile is built for the biased arithmetic");
   constexpr int RPC = 4;                    // rows per 16-B profile chunk
   constexpr int KC = (R + RPC - 1) / RPC;   // chunks per lane (the last may be a narrow tail)
   constexpr int KCF = qp_full_chunks(R);    // chunks read with LDS.128 (kernels.cuh layout)
   constexpr int TW = qp_tail_w(R) == 16 ? 0 : qp_tail_w(R);   // narrow tail: 4 or 8 B per lane
   constexpr int LS = qp_letter_bytes(G, R); // bytes per letter in the profile slice
-  constexpr int QP_U4 = kNL * LS / 16;
+  constexpr int QP_U4 = QPM == 1 ? kSPBytes / 16 : kNL * LS / 16;   // profile words in shared memory
   static_assert(LS % 128 == 0, "letter slices are 128-B aligned");
   constexpr int DESC_U4 = kNL * kNL;
   // Lane G-1 prefetches the previous pass's boundary U columns ahead through a
@@ -231,7 +232,8 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       mbar_init(mbar, 1);
       mbar_arm(mbar, (DESC_U4 + QP_U4) * 16);
       bulk_g2s(sbase, p.desc, DESC_U4 * 16, mbar);
-      bulk_g2s(sbase + DESC_U4 * 16, p.qp + (size_t)p.pass * QP_U4, QP_U4 * 16, mbar);
+      // QPM 1: the score profile does not depend on the pass
+      bulk_g2s(sbase + DESC_U4 * 16, p.qp + (QPM == 1 ? (size_t)0 : (size_t)p.pass * QP_U4), QP_U4 * 16, mbar);
     }
     __syncthreads();   // the barrier is initialised before anyone waits on it
     mbar_wait(mbar, 0);
@@ -252,6 +254,17 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   const uint32_t s_qpt = s_desc + DESC_U4 * 16 + KCF * G * 16 +
                          (uint32_t)(((lane / G) % qp_tail_ncopy(G, R)) * G + t) * (uint32_t)(TW ? TW : 16);
   const uint32_t s_dqt = s_qpt - s_qp;
+  // QPM 1 (score profile): the byte address in SP of each of the lane's query
+  // rows' letter (24 = phantom row); the column's pair offset is added per row
+  uint32_t qoff[QPM == 1 ? R : 1];
+  if (QPM == 1) {
+    const uint32_t s_sp = s_desc + DESC_U4 * 16;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int row = p.pass * G * R + t * R + r;
+      qoff[r] = s_sp + 4u * (row < p.m ? (uint32_t)__ldg(p.query + row) : (uint32_t)kAlpha);
+    }
+  }
   __syncthreads();
   const DescWords nul = load_desc(s_desc + kNulWord);
 
@@ -454,7 +467,24 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       }
       uint32_t hd = hprev;
       hprev = hu;
-      if (kArith == 1 && SW_ROWAHEAD && SW_ABLATE == 0) {
+      if (QPM == 1) {
+        // Score profile: P(r) = SP[pair][q_r], one
+        // 32-bit word SM(q_r, dB) * 65536 + SM(q_r, dA) per (letter pair, query
+        // letter), read with one LDS.32 per row at the lane's own query letter;
+        // no packing IMAD.  w0 is the column pair's byte offset in SP.
+        uint32_t tcur = imad(hd, one, lds32(imad(w0, one, qoff[0])));
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          uint32_t tnext = 0u;
+          if (r + 1 < R) tnext = imad(H[r], one, lds32(imad(w0, one, qoff[r + 1 < R ? r + 1 : 0])));
+          const uint32_t h = __vimax3_s16x2(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
+          H[r] = h;
+          const uint32_t hg = __viaddmax_s16x2(h, ngoe, kB2);  // max(H-Goe, 0)
+          E[r] = __viaddmax_s16x2(E[r], nge, hg);              // Eq. 2 (next column)
+          F = __viaddmax_s16x2(F, nge, hg);                    // Eq. 3 (next row)
+          tcur = tnext;
+        }
+      } else if (kArith == 1 && SW_ROWAHEAD && SW_ABLATE == 0) {
         // Biased rows with the diagonal add one row ahead: t(r+1) = H_old[r] + P(r+1)
         // is formed before H[r] is overwritten, so the new H can take the old H's
         // register (no per-column rotation of the H registers, which otherwise
@@ -788,7 +818,7 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
 // ---------------------------------------------------------------------------
 __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint8_t *__restrict__ q2, int m2,
                                 const int8_t *__restrict__ M, int G, int R, int P, uint32_t *qp, uint4 *desc,
-                                int32_t *qp32, int32_t *qp32b, int goe, int ge) {
+                                int32_t *qp32, int32_t *qp32b, int goe, int ge, int sp) {
   // q2 == nullptr: one query (QPM 0); q2 != nullptr: query pair (QPM 3).  See
   // the profile-mode notes above the pass kernel for the word formats.
   // slice layout: kernels.cuh (qp_letter_bytes): full chunks, then a narrow tail block
@@ -797,13 +827,20 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
   const int LS = qp_letter_bytes(G, R);
   const int LW = LS / 4;                    // 32-bit words per letter
   const int mm = q2 ? max(m, m2) : m;
-  const int64_t nq = (int64_t)P * kNL * LW;
+  // sp: the score profile SP[pair (cA, cB)][query letter c < kSPL] instead
+  const int64_t nq = sp ? (int64_t)kSPBytes / 4 : (int64_t)P * kNL * LW;
   const int64_t ndesc = kNL * kNL;
   const int64_t n32 = (int64_t)kNL * mm;   // plain s32 profile(s)
   const int64_t total = nq + ndesc + n32;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < nq) {
+    if (i < nq && sp) {
+      const int pr = (int)(i / kSPL), c = (int)(i % kSPL);
+      const int cA = pr / kNL, cB = pr % kNL;
+      const int lo = (c < kAlpha && cA < kAlpha) ? M[c * kAlpha + cA] : kDummy16;
+      const int hi = (c < kAlpha && cB < kAlpha) ? M[c * kAlpha + cB] : kDummy16;
+      qp[i] = (uint32_t)(hi * 65536 + lo);
+    } else if (i < nq) {
       const int w = (int)(i % LW);
       const int c = (int)((i / LW) % kNL);
       const int pass = (int)(i / ((int64_t)LW * kNL));
@@ -840,7 +877,7 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
       const uint32_t wgoe = (sA ? 0x8001u : pgoe) | ((sB ? 0x8001u : pgoe) << 16);
       const uint32_t wge = (sA ? 0x8001u : pge) | ((sB ? 0x8001u : pge) << 16);
       const uint32_t wk = (sA ? 0x8000u : 0u) | ((sB ? 0x8000u : 0u) << 16);
-      desc[k] = make_uint4(offA | (offB << 16), wgoe, wge, wk);
+      desc[k] = make_uint4(sp ? (uint32_t)(k * kSPL * 4) : (offA | (offB << 16)), wgoe, wge, wk);
     } else {
       // s32 profile(s), plain [letter][m] (the 32-bit kernel stages its slices)
       const int64_t j = i - nq - ndesc;
@@ -1038,7 +1075,7 @@ using PassFn = void (*)(const SW16Params);
 
 template <int R, int G, int QPM>
 constexpr int smem_of() {
-  return kNL * kNL * 16 + kNL * qp_letter_bytes(G, R);
+  return kNL * kNL * 16 + (QPM == 1 ? kSPBytes : kNL * qp_letter_bytes(G, R));
 }
 
 struct TileEntry {
@@ -1084,7 +1121,14 @@ TileEntry g_tiles[] = {
     SW_TILES_COMMON(3), SW_TILE(16, 16, 3), SW_TILE(16, 29, 3), SW_TILE(16, 32, 3), SW_TILE(32, 8, 3),
     SW_TILE(32, 16, 3), SW_TILE(32, 29, 3), SW_TILE(32, 32, 3),
     SW_TILE_LAT(32, 3), SW_TILE_LAT(32, 4), SW_TILE_LAT(32, 5), SW_TILE_LAT(32, 6), SW_TILE_LAT(32, 8),
-    SW_TILE_LAT(16, 9)};
+    SW_TILE_LAT(16, 9)
+#if SW_ARITH == 1
+    // score-profile tiles (NEXT-1): R registers of row-letter offsets cap R
+    , SW_TILE(8, 8, 1), SW_TILE(8, 12, 1), SW_TILE(8, 16, 1), SW_TILE(8, 20, 1),
+    SW_TILE(16, 8, 1), SW_TILE(16, 12, 1), SW_TILE(16, 16, 1), SW_TILE(16, 20, 1),
+    SW_TILE(32, 8, 1), SW_TILE(32, 12, 1), SW_TILE(32, 16, 1), SW_TILE(32, 20, 1)
+#endif
+};
 #undef SW_TILES_COMMON
 #undef SW_TILE_W
 #undef SW_TILE
@@ -1194,19 +1238,19 @@ cudaError_t init_kernels() {
 }
 
 size_t qp_bytes(int G, int R, int P, int qpm) {
-  (void)qpm;
-  return (size_t)P * kNL * qp_letter_bytes(G, R);
+  return qpm == 1 ? (size_t)kSPBytes : (size_t)P * kNL * qp_letter_bytes(G, R);
 }
 
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,
                             int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
-                            int goe, int ge, cudaStream_t st) {
+                            int goe, int ge, cudaStream_t st, int sp) {
   const int mm = d_query2 ? (m > m2 ? m : m2) : m;
-  const int64_t total = (int64_t)P * kNL * (qp_letter_bytes(G, R) / 4) + kNL * kNL + (int64_t)kNL * mm;
+  const int64_t total = (sp ? (int64_t)kSPBytes / 4 : (int64_t)P * kNL * (qp_letter_bytes(G, R) / 4)) +
+                        kNL * kNL + (int64_t)kNL * mm;
   ++g_launches;
   qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_query2, m2, d_matrix, G, R, P,
                                                          reinterpret_cast<uint32_t *>(d_qp), d_desc, d_qp32,
-                                                         d_qp32b, goe, ge);
+                                                         d_qp32b, goe, ge, sp);
   return cudaGetLastError();
 }
 

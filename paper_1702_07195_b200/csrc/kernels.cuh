@@ -47,6 +47,13 @@ __host__ __device__ constexpr int qp_tail_bytes(int G, int R) {
 }
 __host__ __device__ constexpr int qp_letter_bytes(int G, int R) { return qp_full_chunks(R) * G * 16 + qp_tail_bytes(G, R); }
 
+// Score profile (QPM 1): per letter pair (cA, cB) of the stream alphabet, a
+// vector over the query letters c < kSPL (24 residue codes + one phantom-row
+// letter) of SM(c, cB) * 65536 + SM(c, cA): 676 x 25 words.
+constexpr int kSPL = 25;
+constexpr int kSPBytes = 26 * 26 * kSPL * 4;
+static_assert(kSPBytes % 16 == 0, "bulk copy size");
+
 struct SW16Params {
   const uint32_t *stream;   // column words (descriptor byte offsets)
   const Item *items;
@@ -78,6 +85,9 @@ struct SW16Params {
   // or null.  They hold only sequences already flagged in both halves
   // (item_skip_kernel), whose 16-bit results are no longer used.
   const int32_t *skip;
+  // QPM 1 (score profile): the query and its length (each lane's row letters)
+  const uint8_t *query;
+  int m;
 };
 
 struct SW32Params {
@@ -132,7 +142,8 @@ int tile_threads(int i);
 // d_query2 != nullptr: query-pair profile (QPM 3) and a second s32 profile.
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,
                             int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
-                            int goe, int ge, cudaStream_t st);
+                            int goe, int ge, cudaStream_t st, int sp = 0);
+// sp = 1: d_qp receives the score profile (QPM 1) and the descriptors its pair offsets.
 // goe = gap open + extend, ge = gap extend (>= 0; the descriptor penalty words clamp at 32767)
 cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cudaStream_t st);
 // Whether tile i has a cross-pass wavefront kernel (p.npass > 0 launches it).

@@ -547,3 +547,44 @@ def test_lat_tiles_are_exact():
     finally:
         sw.sw_set_tile(0)
         sw.sw_set_latency_mode(0)
+
+
+def test_score_profile_tiles_are_exact():
+    """Score profile (sw_set_profile(2)): P(r) = SP[pair][q_r]
+    read per row at the lane's query letter.  Every score-profile tile, forced,
+    on random databases with random (also asymmetric) matrices, random gaps,
+    multi-pass queries and saturating sequences; then the automatic switch."""
+    rng = np.random.default_rng(1650)
+    seqs = [rng.integers(0, 24, int(L)).astype(np.uint8) for L in rng.integers(0, 700, 400)]
+    seqs += [si.rr_residues(rng, 3000), encode("W" * 1700), np.full(500, 7, np.uint8)]
+    db = _db(seqs)
+    sw.sw_db_load(db.residues, db.offsets)
+    try:
+        sw.sw_set_profile(2)
+        for G in (8, 16, 32):
+            for R in (8, 12, 16, 20):
+                assert sw.sw_tile_supported(G, R, sp=True)
+                sw.sw_set_tile(G, R)
+                for trial in range(2):
+                    m = [1700, int(rng.integers(1, 2500))][trial]
+                    q = encode("W" * 1700) if trial == 0 else rng.integers(0, 24, m).astype(np.uint8)
+                    M = BLOSUM62 if trial == 0 else (si.random_symmetric_matrix(rng) if G != 16
+                                                     else rng.integers(-8, 12, (24, 24)).astype(np.int8))
+                    go, ge = (10, 2) if trial == 0 else (int(rng.integers(0, 16)), int(rng.integers(0, 6)))
+                    got = sw.sw_search(q, M, go, ge)
+                    st = sw.sw_last_stats()
+                    assert st["profile"] == 2 and st["G"] == G and st["R"] == R, st
+                    exp = oracle.batch(q, db.residues, db.offsets, M, go, ge)
+                    bad = np.nonzero(got != exp)[0]
+                    assert bad.size == 0, (G, R, trial, m, bad[:5], got[bad[:5]], exp[bad[:5]])
+        sw.sw_set_tile(0)
+        q = si.rr_residues(rng, 464)
+        got = sw.sw_search(q, BLOSUM62, 10, 2)       # automatic SP tile
+        assert sw.sw_last_stats()["profile"] == 2
+        assert (got == oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)).all()
+        sw.sw_set_profile(0)
+        sw.sw_search(q, BLOSUM62, 10, 2)
+        assert sw.sw_last_stats()["profile"] == 1   # the measured switch picks QP
+    finally:
+        sw.sw_set_tile(0)
+        sw.sw_set_profile(0)
