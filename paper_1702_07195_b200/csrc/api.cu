@@ -245,11 +245,11 @@ int choose_tile(int m, int qpm, const Image &I, bool wave_only = false) {
 //   chain = (longest item + G) columns x the per-column step latency of one
 //           group, c0 + c1 * R SM cycles (measured on one 12,000-residue
 //           sequence: one warp issues its column's instructions back to back,
-//           ~13.5 cycles per row plus ~150 per column for the lane-to-lane
+//           ~14 cycles per row plus ~145 per column for the lane-to-lane
 //           hand-over, the descriptor -> profile load chain and the stores);
 // a pass lasts about max(bulk, chain).  Latency tiles (small R, one
 // 256-thread CTA per SM) shorten the chain at lower throughput.
-constexpr double kStepC0 = 150.0, kStepC1 = 13.5;
+constexpr double kStepC0 = 145.0, kStepC1 = 14.0;
 constexpr double kLatThroughput = 0.6;   // latency-tile throughput relative to a 512-thread tile's eff0
 
 double pass_time_model(const TileInfo &T, int m, const Image &I, bool lat) {
