@@ -908,6 +908,20 @@ int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, 
     CUDA_TRY(launch_block_topk(d_scores, d_index, nullptr, n, (int)kk, g.keys.p, nb, st));
     CUDA_TRY(launch_block_topk(nullptr, nullptr, g.keys.p, (int64_t)nb * kk, (int)kk, g.keys2.p, 1, st));
     CUDA_TRY(launch_decode_keys(g.keys2.p, kk, d_idx_out, d_score_out, st));
+  } else if (kk * 4 <= n) {
+    // radix select of the kk-th largest key, then a sort of the kk keys only
+    // (DESIGN.md 4.4); the full sort below when kk is a large part of n
+    int64_t np2 = 1;
+    while (np2 < kk) np2 <<= 1;
+    if (np2 < 2) np2 = 2;
+    CUDA_TRY(g.keys.ensure((size_t)np2));
+    CUDA_TRY(g.keys2.ensure((radix_topk_scratch_bytes() + 7) / 8));
+    CUDA_TRY(launch_radix_topk(d_scores, d_index, n, kk, g.keys.p, g.keys2.p, st));
+    if (kk > 4096) {
+      CUDA_TRY(cudaMemsetAsync(g.keys.p + kk, 0, (size_t)(np2 - kk) * sizeof(uint64_t), st));
+      CUDA_TRY(launch_bitonic_sort_desc(g.keys.p, np2, st));
+    }
+    CUDA_TRY(launch_decode_keys(g.keys.p, kk, d_idx_out, d_score_out, st));
   } else {
     int64_t np2 = 1;
     while (np2 < n) np2 <<= 1;

@@ -32,6 +32,7 @@
 // LDS.128 (4 rows per load).
 #include "kernels.cuh"
 
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 
@@ -1034,6 +1035,103 @@ __global__ void __launch_bounds__(1024) block_topk_kernel(const int32_t *scores,
   }
 }
 
+// Sorting stage for k > 32: radix select of the k-th largest
+// 64-bit key (score, -index), 8 passes of 8 bits from the most significant
+// digit, then compaction of the k keys >= it and a sort of those k only.
+// State in device memory, no host round trip: each pass histograms the digit
+// of the keys that match the selected prefix so far, and a one-block kernel
+// picks the digit where the count from the top reaches the keys still
+// needed.  When every key with the new prefix is needed the selection is
+// complete (done) and the remaining passes return at once.
+struct SelState {
+  uint64_t prefix, mask;
+  long long need;
+  int done;
+};
+
+__global__ void __launch_bounds__(512) radix_hist_kernel(const int32_t *__restrict__ scores,
+                                                         const int64_t *__restrict__ index, int64_t n,
+                                                         const SelState *__restrict__ st, int shift,
+                                                         unsigned *hist) {
+  __shared__ unsigned sh[256];
+  if (st->done) return;
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) sh[b] = 0u;
+  __syncthreads();
+  const uint64_t prefix = st->prefix, mask = st->mask;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = make_key(scores[i], index ? (uint64_t)index[i] : (uint64_t)i);
+    if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += blockDim.x)
+    if (sh[b]) atomicAdd(&hist[b], sh[b]);
+}
+
+__global__ void radix_select_kernel(SelState *st, unsigned *hist, int shift) {
+  __shared__ unsigned sh[256];
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) sh[b] = hist[b];
+  __syncthreads();
+  if (threadIdx.x == 0 && !st->done) {
+    long long cum = 0;
+    const long long need = st->need;
+    for (int d = 255; d >= 0; --d) {
+      if (cum + (long long)sh[d] >= need) {
+        st->need = need - cum;
+        st->prefix |= (uint64_t)d << shift;
+        st->mask |= (uint64_t)255u << shift;
+        if ((long long)sh[d] == need - cum) st->done = 1;   // every key with this prefix is needed
+        break;
+      }
+      cum += sh[d];
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0u;   // for the next pass
+}
+
+// The k selected keys ((key & mask) >= prefix), in any order.
+__global__ void radix_gather_kernel(const int32_t *__restrict__ scores, const int64_t *__restrict__ index,
+                                    int64_t n, const SelState *__restrict__ st, uint64_t *out, unsigned *cnt) {
+  const uint64_t prefix = st->prefix, mask = st->mask;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    uint64_t key = 0;
+    bool take = false;
+    if (i < n) {
+      key = make_key(scores[i], index ? (uint64_t)index[i] : (uint64_t)i);
+      take = (key & mask) >= prefix;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    if (bal) {
+      const int lane = threadIdx.x & 31;
+      unsigned pos = 0;
+      if (lane == 0) pos = atomicAdd(cnt, (unsigned)__popc(bal));
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      if (take) out[pos + __popc(bal & ((1u << lane) - 1u))] = key;
+    }
+  }
+}
+
+// One-block descending bitonic sort of n <= 4096 keys (padded with 0).
+__global__ void __launch_bounds__(1024) block_sort_desc_kernel(uint64_t *keys, int n, int npow2) {
+  __shared__ uint64_t sk[4096];
+  for (int i = threadIdx.x; i < npow2; i += blockDim.x) sk[i] = i < n ? keys[i] : 0ull;
+  __syncthreads();
+  for (int size = 2; size <= npow2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < npow2 / 2; i += blockDim.x) {
+        const int lo = (i / stride) * stride * 2 + (i % stride);
+        const int hi = lo + stride;
+        const bool desc = (lo & size) == 0;
+        const uint64_t a = sk[lo], b = sk[hi];
+        if ((a < b) == desc) { sk[lo] = b; sk[hi] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) keys[i] = sk[i];
+}
+
 // Sorting stage, multi-GPU: scatter the scores gathered
 // from every rank's shard back to the original database order on rank 0,
 // dst[index[i]] = src[i]; index < 0 marks the gather's padding slots.  Four
@@ -1344,6 +1442,40 @@ cudaError_t launch_scatter_scores(const int32_t *src, const int64_t *index, int6
   ++g_launches;
   scatter_scores_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, st>>>(src, index, n, dst, dst_count);
   return cudaGetLastError();
+}
+
+size_t radix_topk_scratch_bytes() { return sizeof(SelState) + 256 * sizeof(unsigned) + 16; }
+
+cudaError_t launch_radix_topk(const int32_t *scores, const int64_t *index, int64_t n, int64_t k, uint64_t *out,
+                              void *scratch, cudaStream_t st) {
+  SelState *ss = reinterpret_cast<SelState *>(scratch);
+  unsigned *hist = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(scratch) + sizeof(SelState));
+  unsigned *cnt = hist + 256;
+  SelState init{0ull, 0ull, (long long)k, 0};
+  cudaError_t e = cudaMemcpyAsync(ss, &init, sizeof(SelState), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(hist, 0, 257 * sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  const int hg = (int)std::min<int64_t>((n + 511) / 512, 148 * 4);
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    ++g_launches;
+    radix_hist_kernel<<<hg, 512, 0, st>>>(scores, index, n, ss, shift, hist);
+    ++g_launches;
+    radix_select_kernel<<<1, 256, 0, st>>>(ss, hist, shift);
+  }
+  ++g_launches;
+  radix_gather_kernel<<<grid_for(n, 256), 256, 0, st>>>(scores, index, n, ss, out, cnt);
+  if (k <= 4096) {
+    int np2 = 1;
+    while (np2 < k) np2 <<= 1;
+    ++g_launches;
+    block_sort_desc_kernel<<<1, 1024, 0, st>>>(out, (int)k, np2);
+    return cudaGetLastError();
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // k > 4096: the caller sorts out[0, k) padded to a power of two
+  return cudaSuccess;
 }
 
 cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score, cudaStream_t st) {

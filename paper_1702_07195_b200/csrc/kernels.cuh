@@ -180,6 +180,12 @@ cudaError_t launch_block_topk(const int32_t *scores, const int64_t *index, const
                               int k, uint64_t *out, int blocks, cudaStream_t st);
 cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score,
                                cudaStream_t st);
+// k > 32: radix select (8 digit passes of the 64-bit key) + compaction of the
+// k largest keys into out[0, k); sorted descending when k <= 4096 (otherwise
+// unsorted: the caller sorts them).  scratch: radix_topk_scratch_bytes().
+size_t radix_topk_scratch_bytes();
+cudaError_t launch_radix_topk(const int32_t *scores, const int64_t *index, int64_t n, int64_t k, uint64_t *out,
+                              void *scratch, cudaStream_t st);
 // dst[index[i]] = src[i] for i < n, skipping index < 0 or >= dst_count.
 cudaError_t launch_scatter_scores(const int32_t *src, const int64_t *index, int64_t n, int32_t *dst,
                                   int64_t dst_count, cudaStream_t st);

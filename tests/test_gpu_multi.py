@@ -174,3 +174,34 @@ def test_bench_config2_strong_scaling_nccl_world1():
 def test_bench_gpus_flag_single_gpu():
     d = _run(["bench.py", "--gpus", "1", "--steps", "3", "--warmup", "3", "--scale", "0.02", "--no-cpu-baseline"])
     assert d["n_gpus"] == 1 and d["scaling"] == "weak" and d["config"]["assembly_check"] is True
+
+
+@pytest.mark.parametrize("k", [33, 100, 1000, 4096, 4097, 10_000])
+def test_topk_radix_select_matches_oracle(k):
+    """Sorting stage for k > 32 (radix select of the k-th key + sort of k):
+    scores with many ties, positions as indices and a sparse index map."""
+    rng = np.random.default_rng(k)
+    n = 600_000
+    x = rng.integers(0, 60, n).astype(np.int32)            # heavy ties
+    x[rng.choice(n, 50, replace=False)] = rng.integers(-5, 3000, 50)
+    d = torch.from_numpy(x).cuda()
+    ti = torch.empty(k, dtype=torch.int64, device="cuda")
+    ts = torch.empty(k, dtype=torch.int32, device="cuda")
+    assert sw.sw_topk_dev(d, None, n, k, ti, ts) == k
+    ei, es = oracle.topk(x, k)
+    assert np.array_equal(ti.cpu().numpy(), ei) and np.array_equal(ts.cpu().numpy(), es)
+    # with an index map (global indices of a shard, as the multi-GPU merge uses)
+    gidx = np.sort(rng.choice(8 * n, n, replace=False)).astype(np.int64)
+    sw.sw_topk_dev(d, torch.from_numpy(gidx).cuda(), n, k, ti, ts)
+    order = np.lexsort((gidx, -x.astype(np.int64)))[:k]
+    assert np.array_equal(ti.cpu().numpy(), gidx[order]) and np.array_equal(ts.cpu().numpy(), x[order])
+
+
+def test_topk_on_config2_scores():
+    w = si.config2(scale=0.05)
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    got = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
+    for k in (10, 33, 100, 10_000):
+        idx, sc = sw.sw_topk(k)
+        ei, es = oracle.topk(got, k)
+        assert np.array_equal(idx, ei) and np.array_equal(sc, es), k
