@@ -48,9 +48,9 @@ CONFIG_INDEX = 1
 TOPK = 10
 ALU_LANE_OPS_PER_CLK_PER_SM = 64      # measured (profiles/r01_dpx_microbench.jsonl); guide: rt_SMSP=2
 # ALU-pipe instructions per cell of the 16-bit pass kernel:
-# biased arithmetic 4.5 per s16x2 pair of cells (VIMNMX3 + 3 VIADDMNMX + 1/2
+# biased arithmetic (unsigned or signed halves) 4.5 per 16x2 pair of cells (VIMNMX3 + 3 VIADDMNMX + 1/2
 # VIMNMX3; the diagonal add runs on the FMA pipe), relu form 5.5 DPX.
-ALU_PER_CELL = {1: 2.25, 0: 2.75}
+ALU_PER_CELL = {2: 2.25, 1: 2.25, 0: 2.75}
 WEAK_CONFIGS = (0, 1)
 
 

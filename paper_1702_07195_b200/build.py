@@ -28,7 +28,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3"
                      "-I" + os.path.join(ROOT, "include")]
 if os.environ.get("SW_ABLATE"):   # performance experiments only (wrong results)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ABLATE=" + os.environ["SW_ABLATE"]]
-if os.environ.get("SW_ARITH"):    # cell arithmetic (kernels.cuh): 1 biased (default), 0 relu DPX
+if os.environ.get("SW_ARITH"):    # cell arithmetic (kernels.cuh): 2 biased unsigned (default), 1 biased signed, 0 relu
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ARITH=" + os.environ["SW_ARITH"]]
 if os.environ.get("SW_ROWAHEAD"):  # row order of the biased cell loop (experiment)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_ROWAHEAD=" + os.environ["SW_ROWAHEAD"]]

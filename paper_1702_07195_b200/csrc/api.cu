@@ -385,7 +385,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   if (P > kMaxPass) return fail(SW_EINVAL, "query too long");
   int smax = 1;
   for (int i = 0; i < kAlpha * kAlpha; ++i) smax = std::max(smax, (int)matrix[i]);
-  const int thresh = 32768 - smax;   // stored 16-bit units (R7)
+  const int thresh = kHalfTop - smax;   // stored 16-bit units (R7)
   g.last_thresh = thresh - kBias16;  // in score units
   const int goe = gap_open + gap_extend, ge = gap_extend;
 
@@ -1026,7 +1026,7 @@ int sw_tile_supported(int32_t G, int32_t R) {
 int sw_set_profile(int32_t mode) {
   t_err.clear();
   if (mode < 0 || mode > 2) return fail(SW_EINVAL, "mode must be 0, 1 or 2");
-  if (mode == 2 && kArith != 1) return fail(SW_EINVAL, "the score profile needs the biased arithmetic build");
+  if (mode == 2 && !kBiased) return fail(SW_EINVAL, "the score profile needs the biased arithmetic build");
   g.prof_mode = mode;
   return SW_OK;
 }

@@ -73,6 +73,18 @@ constexpr int kWavePublish = 64;   // wavefront: columns between progress public
 constexpr uint32_t kB2 = (uint32_t)kBias16 * 0x10001u;   // the stored zero, both halves
 constexpr uint32_t kNulWord = (uint32_t)((kNul * kNL + kNul) * kDescBytes);
 
+// 16x2 max operations of the cell: unsigned halves in the biased-unsigned
+// form (SW_ARITH 2), signed otherwise (kernels.cuh).
+__device__ __forceinline__ uint32_t hmax3(uint32_t a, uint32_t b, uint32_t c) {
+  return kArith == 2 ? __vimax3_u16x2(a, b, c) : __vimax3_s16x2(a, b, c);
+}
+__device__ __forceinline__ uint32_t haddmax(uint32_t a, uint32_t b, uint32_t c) {   // max(a + b, c)
+  return kArith == 2 ? __viaddmax_u16x2(a, b, c) : __viaddmax_s16x2(a, b, c);
+}
+__device__ __forceinline__ uint32_t hmax(uint32_t a, uint32_t b) {
+  return kArith == 2 ? __vmaxu2(a, b) : __vmaxs2(a, b);
+}
+
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
@@ -207,7 +219,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   static_assert(!WAVE || BIN, "the wavefront kernel reads boundaries (from pass 1 on)");
   static_assert(U == 1 || U == 2 || U == 4, "U: columns per unrolled block / prefetch distance");
   static_assert(QPM == 0 || QPM == 1 || QPM == 3, "profile mode");
-  static_assert(QPM != 1 || kArith == 1, "the score profile is built for the biased arithmetic");
+  static_assert(QPM != 1 || kBiased, "the score profile is built for the biased arithmetic");
   constexpr int RPC = 4;                    // rows per 16-B profile chunk
   constexpr int KC = (R + RPC - 1) / RPC;   // chunks per lane (the last may be a narrow tail)
   constexpr int KCF = qp_full_chunks(R);    // chunks read with LDS.128 (kernels.cuh layout)
@@ -478,14 +490,14 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         for (int r = 0; r < R; ++r) {
           uint32_t tnext = 0u;
           if (r + 1 < R) tnext = imad(H[r], one, lds32(imad(w0, one, qoff[r + 1 < R ? r + 1 : 0])));
-          const uint32_t h = __vimax3_s16x2(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
+          const uint32_t h = hmax3(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
           H[r] = h;
-          const uint32_t hg = __viaddmax_s16x2(h, ngoe, kB2);  // max(H-Goe, 0)
-          E[r] = __viaddmax_s16x2(E[r], nge, hg);              // Eq. 2 (next column)
-          F = __viaddmax_s16x2(F, nge, hg);                    // Eq. 3 (next row)
+          const uint32_t hg = haddmax(h, ngoe, kB2);  // max(H-Goe, 0)
+          E[r] = haddmax(E[r], nge, hg);              // Eq. 2 (next column)
+          F = haddmax(F, nge, hg);                    // Eq. 3 (next row)
           tcur = tnext;
         }
-      } else if (kArith == 1 && SW_ROWAHEAD && SW_ABLATE == 0) {
+      } else if (kBiased && SW_ROWAHEAD && SW_ABLATE == 0) {
         // Biased rows with the diagonal add one row ahead: t(r+1) = H_old[r] + P(r+1)
         // is formed before H[r] is overwritten, so the new H can take the old H's
         // register (no per-column rotation of the H registers, which otherwise
@@ -513,11 +525,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
               uint32_t tnext = 0u;
               if (r + 1 < R)
                 tnext = imad(H[r], one, QPM == 0 ? imad(bv[j + 1], 65536u, av[j + 1]) : av[j + 1]);
-              const uint32_t h = __vimax3_s16x2(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
+              const uint32_t h = hmax3(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
               H[r] = h;
-              const uint32_t hg = __viaddmax_s16x2(h, ngoe, kB2);  // max(H-Goe, 0)
-              E[r] = __viaddmax_s16x2(E[r], nge, hg);              // Eq. 2 (next column)
-              F = __viaddmax_s16x2(F, nge, hg);                    // Eq. 3 (next row)
+              const uint32_t hg = haddmax(h, ngoe, kB2);  // max(H-Goe, 0)
+              E[r] = haddmax(E[r], nge, hg);              // Eq. 2 (next column)
+              F = haddmax(F, nge, hg);                    // Eq. 3 (next row)
               tcur = tnext;
             }
           }
@@ -545,16 +557,16 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
               if (r < R) {
                 const uint32_t sub = sub0;
                 uint32_t h;
-                if (kArith == 1) {
+                if (kBiased) {
                   // biased: H, E, F >= kB2 halfwise, so Hdiag + SM never crosses a
                   // half boundary and is one 32-bit add (FMA pipe); E >= kB2
                   // makes the 0 of Eq. 1 implicit
-                  h = __vimax3_s16x2(imad(hd, one, sub), E[r], F);     // Eq. 1
+                  h = hmax3(imad(hd, one, sub), E[r], F);     // Eq. 1
                   hd = H[r];
                   H[r] = h;
-                  const uint32_t hg = __viaddmax_s16x2(h, ngoe, kB2);  // max(H-Goe, 0)
-                  E[r] = __viaddmax_s16x2(E[r], nge, hg);              // Eq. 2 (next column)
-                  F = __viaddmax_s16x2(F, nge, hg);                    // Eq. 3 (next row)
+                  const uint32_t hg = haddmax(h, ngoe, kB2);  // max(H-Goe, 0)
+                  E[r] = haddmax(E[r], nge, hg);              // Eq. 2 (next column)
+                  F = haddmax(F, nge, hg);                    // Eq. 3 (next row)
                 } else {
                   h = __viaddmax_s16x2_relu(hd, sub, E[r]);  // max(Hdiag+SM, E, 0)
                   h = __vmaxs2(h, F);                        // Eq. 1
@@ -572,11 +584,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       }
       // S = max(S reset at the previous END, H_0 .. H_{R-1}); the reset adds
       // -32768 to a half in [0, 32767] (no wrap), folded into the first max.
-      S = __viaddmax_s16x2(S, kneg_prev, H[0]);
+      S = haddmax(S, kneg_prev, H[0]);
 #pragma unroll
-      for (int r = 1; r + 1 < R; r += 2) S = __vimax3_s16x2(S, H[r], H[r + 1]);
-      if ((R & 1) == 0) S = __vmaxs2(S, H[R - 1]);
-      const uint32_t so = __vmaxs2(sc_in, S);   // max over lanes 0..t (read at END columns)
+      for (int r = 1; r + 1 < R; r += 2) S = hmax3(S, H[r], H[r + 1]);
+      if ((R & 1) == 0) S = hmax(S, H[R - 1]);
+      const uint32_t so = hmax(sc_in, S);   // max over lanes 0..t (read at END columns)
       SW_CHECK(!last || scp == reinterpret_cast<uint32_t *>(dummy) ||
                (scp + u - p.sc_out >= p.col_lo && scp + u - p.sc_out < p.col_hi));
       SW_CHECK(!bout || bop == dummy || (bop + u - bnd_out >= p.col_lo && bop + u - bnd_out < p.col_hi));
@@ -861,7 +873,7 @@ __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint
         if (row < m) lo = M[q[row] * kAlpha + c];
         if (q2 && row < m2) hi = M[q2[row] * kAlpha + c];
       }
-      if (kArith == 1)   // the 32-bit integer hi * 65536 + lo (added to H_diag as one 32-bit add)
+      if (kBiased)   // the 32-bit integer hi * 65536 + lo (added to H_diag as one 32-bit add)
         qp[i] = q2 ? (uint32_t)(hi * 65536 + lo) : (uint32_t)lo;
       else               // zero-extended halves
         qp[i] = q2 ? ((uint32_t)(uint16_t)lo | ((uint32_t)(uint16_t)hi << 16)) : (uint32_t)(uint16_t)lo;
@@ -1220,7 +1232,7 @@ TileEntry g_tiles[] = {
     SW_TILE(32, 16, 3), SW_TILE(32, 29, 3), SW_TILE(32, 32, 3),
     SW_TILE_LAT(32, 3), SW_TILE_LAT(32, 4), SW_TILE_LAT(32, 5), SW_TILE_LAT(32, 6), SW_TILE_LAT(32, 8),
     SW_TILE_LAT(16, 9)
-#if SW_ARITH == 1
+#if SW_ARITH >= 1
     // score-profile tiles (NEXT-1): R registers of row-letter offsets cap R
     , SW_TILE(8, 8, 1), SW_TILE(8, 12, 1), SW_TILE(8, 16, 1), SW_TILE(8, 20, 1),
     SW_TILE(16, 8, 1), SW_TILE(16, 12, 1), SW_TILE(16, 16, 1), SW_TILE(16, 20, 1),

@@ -5,23 +5,28 @@
 
 #include "swdb_internal.h"
 
-// SW_ARITH selects the s16x2 cell arithmetic of the pass kernel:
-//   1 (default): "biased" form.  Every 16-bit value is stored as x + kBias16
-//     (kBias16 = 16384), so the diagonal add H_diag + SM can run as a plain
-//     32-bit add on the FMA pipe (no carry between the halves is possible) and
-//     Eq. 1 becomes one VIMNMX3 on the ALU pipe: 4.5 ALU + 2 FMA instructions
-//     per pair of cells instead of 5.5 ALU + 1 FMA.  Exact below
-//     32768 - smax - kBias16 (= 16373 for BLOSUM62); above, flagged.
+// SW_ARITH selects the 16x2 cell arithmetic of the pass kernel:
+//   2 (default): "biased unsigned" form.  Every 16-bit value is stored as
+//     x + kBias16 with kBias16 = 32768 in UNSIGNED halves [32768, 65535], so
+//     the diagonal add H_diag + SM runs as one 32-bit add on the FMA pipe (no
+//     carry between the halves while exact) and Eq. 1 is one VIMNMX3.U16x2 on
+//     the ALU pipe: 4.5 ALU + 2 FMA instructions per pair of cells, exact
+//     below 65536 - smax - kBias16 (= 32757 for BLOSUM62), the same range as
+//     the relu form; above, flagged for 32-bit re-scoring.
+//   1: the same with SIGNED halves and kBias16 = 16384 (round 1): exact only
+//     below 32768 - smax - 16384 (= 16373).
 //   0: the plain relu form, 5.5 DPX per pair of cells, exact below 32768 - smax.
 #ifndef SW_ARITH
-#define SW_ARITH 1
+#define SW_ARITH 2
 #endif
 
 namespace swdb {
 
 constexpr int kArith = SW_ARITH;
-constexpr int kBias16 = kArith == 1 ? 16384 : 0;   // stored = value + kBias16 (per half)
-constexpr int kDummy16 = kArith == 1 ? -16384 : -32768;   // separator / phantom-row score
+constexpr bool kBiased = kArith >= 1;               // the diagonal add on the FMA pipe, Eq. 1 one VIMNMX3
+constexpr int kBias16 = kArith == 2 ? 32768 : (kArith == 1 ? 16384 : 0);   // stored = value + kBias16 (per half)
+constexpr int kDummy16 = kArith == 1 ? -16384 : -32768;   // separator / phantom-row score (-kBias16 when biased)
+constexpr int kHalfTop = kArith == 2 ? 65536 : 32768;     // stored halves are < kHalfTop
 
 // Query-profile slice layout of the s16x2 pass kernel (one pass, one letter),
 // for a group of G lanes with R rows each:

@@ -113,27 +113,27 @@ def test_255_or_more_query_passes():
     flag byte saturates at 255; sequences first flagged in pass >= 254 are
     re-scored from row 0 at the end, earlier ones from their pass boundary."""
     rng = np.random.default_rng(255)
-    m_rand = 16_320
-    q = np.concatenate([encode("W" * 2000), si.rr_residues(rng, m_rand - 2000), encode("W" * 1600)])
-    seqs = [encode("W" * 1600),                       # flags early (rows < 2000)
-            encode("W" * 1700),
+    m_rand = 13_300
+    q = np.concatenate([encode("W" * 3100), si.rr_residues(rng, m_rand), encode("W" * 3000)])   # 302 passes
+    seqs = [encode("W" * 3000),                       # flags early (rows < 3100)
+            encode("W" * 3050),
             si.rr_residues(rng, 900),
-            encode("A" * 5 + "W" * 1550),
+            encode("A" * 5 + "W" * 2990),
             si.rr_residues(rng, 40)]
     db = si.database_from_list(seqs)
     exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
-    assert exp.max() >= 16_373
+    assert exp.max() >= 32_757
     try:
         sw.sw_set_tile(8, 8)
         sw.sw_db_load(db.residues, db.offsets)
         got = sw.sw_search(q, BLOSUM62, 10, 2)
         st = sw.sw_last_stats()
-        assert st["passes"] >= 255
+        assert st["passes"] >= 255 and st["flagged"] >= 3
         assert np.array_equal(got, exp), (got, exp)
-        # the W runs at the end of the query: a sequence that saturates only there
-        db2 = si.database_from_list([encode("G" * 30 + "W" * 1600), si.rr_residues(rng, 700)])
+        # the W run at the end of the query: a sequence that saturates only in pass >= 254
+        db2 = si.database_from_list([encode("G" * 30 + "W" * 2990), si.rr_residues(rng, 700)])
         sw.sw_db_load(db2.residues, db2.offsets)
-        q2 = np.concatenate([si.rr_residues(rng, m_rand), encode("W" * 1600)])
+        q2 = np.concatenate([si.rr_residues(rng, 16_320), encode("W" * 3000)])
         got2 = sw.sw_search(q2, BLOSUM62, 10, 2)
         exp2 = oracle.batch(q2, db2.residues, db2.offsets, BLOSUM62, 10, 2)
         assert sw.sw_last_stats()["flagged"] >= 1

@@ -153,8 +153,8 @@ def test_config0_full_parity():
 
 def test_saturation_boundary_and_rescoring():
     # W^n vs W^n scores 11n: below, at and above the flag threshold T
-    # (T = 32768 - 11 - bias in score units: 16373 biased, 32757 relu form;
-    # DESIGN.md R7), and far above the 16-bit range
+    # (T = 32757 in the default biased-unsigned and the relu form, 16373 in
+    # the biased-signed form; R7), and far above the 16-bit range
     ns = [1487, 1488, 1489, 1490, 2977, 2978, 2979, 2980, 3000, 4000]
     seqs = [encode("W" * n) for n in ns] + [encode("A" * 50)]
     q = encode("W" * 4000)
@@ -163,6 +163,7 @@ def test_saturation_boundary_and_rescoring():
     st = sw.sw_last_stats()
     T = st["flag_threshold"]
     assert T in (32757, 16373)
+    assert T == (16373 if sw.sw_last_stats()["arith"] == 1 else 32757)
     assert st["flagged"] == sum(1 for n in ns if 11 * n >= T)
 
 
@@ -173,14 +174,14 @@ def test_rescoring_seeded_from_pass_boundaries():
     per pass) make the 16-bit pass boundaries cut the 32-bit kernel's slices at
     many different offsets."""
     rng = np.random.default_rng(31)
-    seqs = [encode("W" * n) for n in (1400, 1489, 1600, 2500, 3000)]
-    seqs += [np.concatenate([si.rr_residues(rng, 300), encode("W" * 2000), si.rr_residues(rng, 200)])]
+    seqs = [encode("W" * n) for n in (1400, 1489, 1600, 2500, 2979, 3000, 3300)]
+    seqs += [np.concatenate([si.rr_residues(rng, 300), encode("W" * 3100), si.rr_residues(rng, 200)])]
     seqs += [si.rr_residues(rng, int(L)) for L in rng.integers(1, 800, 40)]
     db = _db(seqs)
     sw.sw_db_load(db.residues, db.offsets)
     try:
         for x in (0, 37, 700, 1501):
-            q = encode("A" * x + "W" * 3000)
+            q = encode("A" * x + "W" * 3400)
             exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
             for G, R in ((0, 0), (8, 8), (16, 12), (32, 29)):
                 sw.sw_set_tile(G, R)
@@ -196,17 +197,19 @@ def test_rescoring_short_sequences_at_fetch_block_edges():
     """The 32-bit kernel fetches lane 0's column inputs in blocks of 32 columns
     (DESIGN.md 4.3).  With every substitution +127 and prohibitive gaps, the
     score is the closed form 127 * min(n, m) (an ungapped diagonal run), so
-    sequences from 129 residues on are flagged; lengths around the multiples of
-    32 put the sequence end at every position of a fetch block, for flagging in
-    the first pass (row 0) and in a later one (64-row passes)."""
+    sequences from 258 residues on are flagged (129 in the biased-signed
+    form); lengths around the multiples of 32 put the sequence end at every
+    position of a fetch block, for flagging in the first pass (row 0) and in a
+    later one (64-row passes)."""
     M = np.full((24, 24), 127, np.int8)
     lens = [0, 1, 31, 32, 33, 63, 64, 65, 127, 128, 129, 130, 159, 160, 161, 191, 192, 193,
-            223, 224, 225, 255, 256, 257, 300, 319, 320, 321, 511, 512, 513, 1000]
+            223, 224, 225, 255, 256, 257, 258, 259, 287, 288, 289, 300, 319, 320, 321, 351, 352, 353,
+            383, 384, 385, 415, 416, 417, 447, 448, 449, 479, 480, 481, 511, 512, 513, 1000]
     rng = np.random.default_rng(77)
     db = _db([rng.integers(0, 24, n).astype(np.uint8) for n in lens])
     sw.sw_db_load(db.residues, db.offsets)
     try:
-        for m in (150, 300, 700):
+        for m in (300, 700, 1100):
             q = rng.integers(0, 24, m).astype(np.uint8)
             closed = np.array([127 * min(n, m) for n in lens], np.int32)
             exp = oracle.batch(q, db.residues, db.offsets, M, 30000, 30000)
@@ -230,10 +233,10 @@ def test_later_passes_skip_flagged_leading_sequences():
     score must still equal the oracle's, for small tiles (many passes) and the
     default one."""
     rng = np.random.default_rng(41)
-    block = encode("W" * 1800)
+    block = encode("W" * 3000)
     seqs = [block.copy() for _ in range(24)]
-    seqs += [np.concatenate([encode("W" * 1700), si.rr_residues(rng, 100)]) for _ in range(5)]
-    seqs += [si.rr_residues(rng, 1800) for _ in range(7)]                  # same length, unflagged
+    seqs += [np.concatenate([encode("W" * 2990), si.rr_residues(rng, 10)]) for _ in range(5)]
+    seqs += [si.rr_residues(rng, 3000) for _ in range(7)]                  # same length, unflagged
     seqs += [si.rr_residues(rng, int(L)) for L in rng.integers(1, 300, 300)]
     order = rng.permutation(len(seqs))
     seqs = [seqs[i] for i in order]
@@ -241,7 +244,7 @@ def test_later_passes_skip_flagged_leading_sequences():
     sw.sw_db_load(db.residues, db.offsets)
     try:
         for x in (0, 300):
-            q = encode("A" * x + "W" * 2000)
+            q = encode("A" * x + "W" * 3100)
             exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
             for G, R in ((0, 0), (8, 8), (16, 12), (32, 16)):
                 sw.sw_set_tile(G, R)
@@ -478,9 +481,9 @@ def test_cross_pass_wavefront_matches_oracle():
     rng = np.random.default_rng(2718)
     dbs = [
         [si.rr_residues(rng, int(L)) for L in rng.integers(3000, 12000, 9)],
-        [si.rr_residues(rng, int(L)) for L in rng.integers(0, 700, 500)] + [encode("W" * 2500)] * 3,
+        [si.rr_residues(rng, int(L)) for L in rng.integers(0, 700, 500)] + [encode("W" * 3100)] * 3,
     ]
-    queries = [si.rr_residues(rng, 1700), encode("W" * 2600 + "A" * 50), si.rr_residues(rng, 5478)]
+    queries = [si.rr_residues(rng, 1700), encode("W" * 3200 + "A" * 50), si.rr_residues(rng, 5478)]
     try:
         for di, seqs in enumerate(dbs):
             db = _db(seqs)
@@ -517,7 +520,7 @@ def test_lat_tiles_are_exact():
     (boundary-reading launches) and saturating sequences (s32 re-scoring)."""
     rng = np.random.default_rng(4711)
     seqs = [rng.integers(0, 24, int(L)).astype(np.uint8) for L in rng.integers(0, 900, 300)]
-    seqs += [si.rr_residues(rng, 4000), encode("W" * 1700), np.full(700, 3, np.uint8)]
+    seqs += [si.rr_residues(rng, 4000), encode("W" * 3100), np.full(700, 3, np.uint8)]
     db = _db(seqs)
     sw.sw_db_load(db.residues, db.offsets)
     try:
@@ -526,8 +529,8 @@ def test_lat_tiles_are_exact():
             assert sw.sw_tile_supported(G, R, lat=True)
             sw.sw_set_tile(G, R)
             for trial in range(3):
-                m = int(rng.integers(1, 1800)) if trial else 1700
-                q = rng.integers(0, 24, m).astype(np.uint8) if trial else encode("W" * 1700)
+                m = int(rng.integers(1, 1800)) if trial else 3100
+                q = rng.integers(0, 24, m).astype(np.uint8) if trial else encode("W" * 3100)
                 M = BLOSUM62 if trial != 1 else si.random_symmetric_matrix(rng)
                 go, ge = (10, 2) if trial != 2 else (0, int(rng.integers(0, 5)))
                 got = sw.sw_search(q, M, go, ge)
@@ -556,7 +559,7 @@ def test_score_profile_tiles_are_exact():
     multi-pass queries and saturating sequences; then the automatic switch."""
     rng = np.random.default_rng(1650)
     seqs = [rng.integers(0, 24, int(L)).astype(np.uint8) for L in rng.integers(0, 700, 400)]
-    seqs += [si.rr_residues(rng, 3000), encode("W" * 1700), np.full(500, 7, np.uint8)]
+    seqs += [si.rr_residues(rng, 3000), encode("W" * 3100), np.full(500, 7, np.uint8)]
     db = _db(seqs)
     sw.sw_db_load(db.residues, db.offsets)
     try:
@@ -566,8 +569,8 @@ def test_score_profile_tiles_are_exact():
                 assert sw.sw_tile_supported(G, R, sp=True)
                 sw.sw_set_tile(G, R)
                 for trial in range(2):
-                    m = [1700, int(rng.integers(1, 2500))][trial]
-                    q = encode("W" * 1700) if trial == 0 else rng.integers(0, 24, m).astype(np.uint8)
+                    m = [3100, int(rng.integers(1, 2500))][trial]
+                    q = encode("W" * 3100) if trial == 0 else rng.integers(0, 24, m).astype(np.uint8)
                     M = BLOSUM62 if trial == 0 else (si.random_symmetric_matrix(rng) if G != 16
                                                      else rng.integers(-8, 12, (24, 24)).astype(np.int8))
                     go, ge = (10, 2) if trial == 0 else (int(rng.integers(0, 16)), int(rng.integers(0, 6)))
