@@ -65,7 +65,15 @@ enum {
  *   count    : number of sequences, >= 1, < 2^31.
  * Builds the device-resident, length-balanced, residue-interleaved stream
  * image on the current CUDA device.  Replaces any
- * previously loaded database; on error the previous database is kept.
+ * previously loaded database.  On SW_EINVAL (validation, before any device
+ * work) the previous database is kept; the previous database's device memory
+ * is released before the new one is uploaded (so a database of nearly the
+ * device's size can replace another), hence after SW_ENOMEM / SW_ECUDA no
+ * database is loaded (sw_db_count() == 0).
+ * Device memory: about 4 B per residue for the two stream images, 1 B per
+ * residue for the plain copy, 4 B per image column for the score chain, and
+ * for 32-bit re-scoring 2 x 8 B x (longest sequence + 64) per re-scoring
+ * warp, capped at 4 GiB (fewer re-scoring warps for very long sequences).
  * Not part of the timed search.
  * Errors: SW_EINVAL (NULL, count < 1, bad offsets, code >= 24),
  *         SW_ENOMEM, SW_ECUDA.

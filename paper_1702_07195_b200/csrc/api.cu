@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -70,11 +71,12 @@ struct Image {
   DevBuf<Item> items;
   DevBuf<int64_t> endcol;   // per sequence: 2 * END column + half
   DevBuf<int32_t> slots;    // slot -> original sequence (items' sequences in column order)
+  DevBuf<int32_t> item_of;  // original sequence -> work item (sequence-pair image)
   int64_t total_cols = 0;
   int64_t max_item_cols = 0;  // longest work item (columns)
   int num_items = 0;
   void release() {
-    stream.release(); items.release(); endcol.release(); slots.release();
+    stream.release(); items.release(); endcol.release(); slots.release(); item_of.release();
     total_cols = 0;
     max_item_cols = 0;
     num_items = 0;
@@ -110,6 +112,7 @@ struct State {
   DevBuf<int32_t> qp32, qp32b;
   DevBuf<uint2> bnd;        // 2 * max_cols
   DevBuf<int32_t> skip;     // per item: dead leading columns for the next pass
+  DevBuf<uint8_t> item_hot; // per item: a low-half sequence flagged (carry propagation, R7)
   DevBuf<uint2> dummy;      // scratch for idle-lane stores (16-B slot per thread)
   DevBuf<uint32_t> nulcols; // 16 NUL column words
   DevBuf<uint2> zerocols;   // 16 zero boundary columns
@@ -149,9 +152,10 @@ struct State {
   bool streamed = false;
   std::vector<Chunk> chunks;
   int64_t chunk_span = 0;       // max columns of a chunk
-  uint32_t *h_stream = nullptr; // pinned host image
+  uint16_t *h_stream = nullptr; // pinned host image, compact: letter-pair index per column (2 B)
   uint8_t *h_res = nullptr;     // pinned, mapped host copy of the residues (s32 re-scoring)
-  DevBuf<uint32_t> cbuf[2];     // device chunk buffers (double-buffered)
+  DevBuf<uint32_t> cbuf[2];     // device chunk buffers (double-buffered), column words
+  DevBuf<uint16_t> cbuf16[2];   // their compact copies as they arrive over the host link
   DevBuf<int32_t> cseq_idx;     // sequences grouped by chunk
   DevBuf<int64_t> cseq_endcol;  // their END columns (global image columns)
   cudaStream_t copy_st = nullptr;
@@ -162,7 +166,8 @@ struct State {
     if (h_res) cudaFreeHost(h_res);
     h_stream = nullptr;
     h_res = nullptr;
-    cbuf[0].release(); cbuf[1].release(); cseq_idx.release(); cseq_endcol.release();
+    cbuf[0].release(); cbuf[1].release(); cbuf16[0].release(); cbuf16[1].release();
+    cseq_idx.release(); cseq_endcol.release();
     for (int k = 0; k < 2; ++k) {
       if (ev_copied[k]) cudaEventDestroy(ev_copied[k]);
       if (ev_free[k]) cudaEventDestroy(ev_free[k]);
@@ -181,7 +186,7 @@ struct State {
     scores.release(); bscores.release(); flagged.release(); flagged2.release(); flag_list.release();
     flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release(); progress.release();
     query.release(); query2.release(); matrix.release(); qp.release(); desc.release(); qp32.release();
-    qp32b.release(); bnd.release(); skip.release();
+    qp32b.release(); bnd.release(); skip.release(); item_hot.release();
     scratch32.release(); dummy.release(); nulcols.release(); zerocols.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
     loaded = false;
     has_search = false;
@@ -411,6 +416,11 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(cudaMemsetAsync(g.flagged.p, 0, (size_t)g.count, st));
   if (pair) CUDA_TRY(cudaMemsetAsync(g.flagged2.p, 0, (size_t)g.count, st));
   CUDA_TRY(cudaMemsetAsync(g.cells32.p, 0, sizeof(int64_t), st));
+  const int32_t *item_of = pair ? nullptr : g.img[0].item_of.p;
+  if (!pair) {
+    CUDA_TRY(g.item_hot.ensure((size_t)std::max(1, g.img[0].num_items)));
+    CUDA_TRY(cudaMemsetAsync(g.item_hot.p, 0, (size_t)std::max(1, g.img[0].num_items), st));
+  }
   if (!g.ev[0])
     for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g.ev[i]));
   // a batch's timing spans all of its searches (sw_last_timing)
@@ -519,7 +529,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     g.npev = pev0 / 2 + 1;
     // the score chain was carried through the passes: one gather of the maxima
     CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p, nullptr, nullptr, 0,
-                                thresh, st));
+                                thresh, st, nullptr, item_of, g.item_hot.p));
   }
   for (int k = 0; k < (wave ? 0 : nch); ++k) {
     const uint32_t *stream_base = I.stream.p;
@@ -531,10 +541,13 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       const State::Chunk &c = g.chunks[k];
       // the buffer is free once the passes of the chunk that used it last are done
       CUDA_TRY(cudaStreamWaitEvent(g.copy_st, g.ev_free[b], 0));
-      CUDA_TRY(cudaMemcpyAsync(g.cbuf[b].p, g.h_stream + c.col_begin, (size_t)(c.col_end - c.col_begin) * 4,
+      // the compact image crosses the host link (2 B per column, 1 B per
+      // residue) and is expanded to column words on the device
+      CUDA_TRY(cudaMemcpyAsync(g.cbuf16[b].p, g.h_stream + c.col_begin, (size_t)(c.col_end - c.col_begin) * 2,
                                cudaMemcpyHostToDevice, g.copy_st));
       CUDA_TRY(cudaEventRecord(g.ev_copied[b], g.copy_st));
       CUDA_TRY(cudaStreamWaitEvent(st, g.ev_copied[b], 0));
+      CUDA_TRY(launch_expand_columns(g.cbuf16[b].p, c.col_end - c.col_begin, g.cbuf[b].p, st));
       base = c.col_begin;
       stream_base = g.cbuf[b].p - base;     // so that item.col_begin indexes the buffer
       items = I.items.p + c.item_begin;
@@ -576,10 +589,11 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
         const State::Chunk &c = g.chunks[k];
         CUDA_TRY(launch_sw16_gather(g.cseq_endcol.p + c.seq_begin, c.seq_end - c.seq_begin, g.sc_out.p - base,
                                     d_scores, g.flagged.p, nullptr, nullptr, pass, thresh, st,
-                                    g.cseq_idx.p + c.seq_begin));
+                                    g.cseq_idx.p + c.seq_begin, item_of, g.item_hot.p));
       } else {
         CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p,
-                                    pair ? d_scores2 : nullptr, pair ? g.flagged2.p : nullptr, pass, thresh, st));
+                                    pair ? d_scores2 : nullptr, pair ? g.flagged2.p : nullptr, pass, thresh, st,
+                                    nullptr, item_of, pair ? nullptr : g.item_hot.p));
         if (pass + 1 < 255)
           for (int k = 0; k < (pair ? 2 : 1); ++k) CUDA_TRY(rescore(k, pass, p.bnd_in));
         if (skipping && pass + 1 < P)
@@ -684,7 +698,7 @@ namespace {
 // chunk_bytes  > 0: streamed database: the sequence-pair image stays in
 // pinned host memory, split into chunks of at most chunk_bytes of stream,
 // copied to the device during every search.
-int load_impl(const uint8_t *residues, const int64_t *offsets, int64_t count, int64_t chunk_bytes) {
+int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t count, int64_t chunk_bytes) {
   t_err.clear();
   std::string err;
   if (validate_db(residues, offsets, count, err)) return fail(SW_EINVAL, err);
@@ -742,6 +756,11 @@ int load_impl(const uint8_t *residues, const int64_t *offsets, int64_t count, in
     for (const Item &it : H.items) I.max_item_cols = std::max<int64_t>(I.max_item_cols, it.ncols);
     CUDA_TRY(I.items.ensure(H.items.size()));
     CUDA_TRY(cudaMemcpy(I.items.p, H.items.data(), H.items.size() * sizeof(Item), cudaMemcpyHostToDevice));
+    if (k == 0) {
+      CUDA_TRY(I.item_of.ensure(H.item_of.size()));
+      CUDA_TRY(cudaMemcpy(I.item_of.p, H.item_of.data(), H.item_of.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice));
+    }
     if (strm) continue;
     CUDA_TRY(I.stream.ensure(H.stream.size()));
     CUDA_TRY(I.endcol.ensure(H.endcol.size()));
@@ -798,10 +817,11 @@ int load_impl(const uint8_t *residues, const int64_t *offsets, int64_t count, in
     CUDA_TRY(g.cseq_endcol.ensure((size_t)count));
     CUDA_TRY(cudaMemcpy(g.cseq_idx.p, idx.data(), idx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(g.cseq_endcol.p, ecol.data(), ecol.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaHostAlloc(&g.h_stream, H.stream.size() * sizeof(uint32_t), cudaHostAllocDefault));
-    std::memcpy(g.h_stream, H.stream.data(), H.stream.size() * sizeof(uint32_t));
+    CUDA_TRY(cudaHostAlloc(&g.h_stream, H.stream.size() * sizeof(uint16_t), cudaHostAllocDefault));
+    for (size_t i = 0; i < H.stream.size(); ++i) g.h_stream[i] = (uint16_t)(H.stream[i] / kDescBytes);
     for (int k = 0; k < 2; ++k) {
       CUDA_TRY(g.cbuf[k].ensure((size_t)span));
+      CUDA_TRY(g.cbuf16[k].ensure((size_t)span + 8));
       CUDA_TRY(cudaEventCreateWithFlags(&g.ev_copied[k], cudaEventDisableTiming));
       CUDA_TRY(cudaEventCreateWithFlags(&g.ev_free[k], cudaEventDisableTiming));
     }
@@ -840,14 +860,37 @@ int load_impl(const uint8_t *residues, const int64_t *offsets, int64_t count, in
     }
   }
   CUDA_TRY(cudaMemcpy(g.offs.p, offsets, ((size_t)count + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
-  // s32 re-scoring scratch: one warp per 8 per SM, 2 boundary rows each
-  g.sw32_grid = nsm * 2;  // 2 CTAs x 8 warps per SM
+  // s32 re-scoring scratch: 2 boundary rows of the longest sequence per warp,
+  // 2 CTAs x 8 warps per SM -- capped at 4 GiB (or an eighth of the free
+  // device memory): with a very long sequence the 32-bit kernel runs on fewer
+  // CTAs instead of failing the load (it claims flagged sequences in a loop)
   g.scratch_stride = g.max_len + 64;
+  {
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    const double budget = std::min<double>(4.0 * (1ull << 30), (double)free_b / 8.0);
+    const double per_cta = (double)(kSW32Threads / 32) * 2.0 * (double)g.scratch_stride * sizeof(uint2);
+    g.sw32_grid = (int)std::max<double>(1.0, std::min<double>(nsm * 2.0, std::floor(budget / per_cta)));
+  }
   const int64_t nwarps32 = (int64_t)g.sw32_grid * (kSW32Threads / 32);
   CUDA_TRY(g.scratch32.ensure((size_t)(nwarps32 * 2 * g.scratch_stride)));
   CUDA_TRY(cudaDeviceSynchronize());
   g.loaded = true;
   return SW_OK;
+}
+
+// No C++ exception crosses the ABI: host allocation failures (pre-processor
+// vectors, pinned buffers) and thread-creation errors become status codes.
+int load_impl(const uint8_t *residues, const int64_t *offsets, int64_t count, int64_t chunk_bytes) {
+  try {
+    return load_impl_body(residues, offsets, count, chunk_bytes);
+  } catch (const std::bad_alloc &) {
+    return fail(SW_ENOMEM, "host allocation failed while loading the database");
+  } catch (const std::exception &e) {
+    return fail(SW_ECUDA, std::string("sw_db_load: ") + e.what());
+  } catch (...) {
+    return fail(SW_ECUDA, "sw_db_load: unknown exception");
+  }
 }
 
 }  // namespace

@@ -635,14 +635,21 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 
 // Scores of one pass from the per-column score chain: the value at a
 // sequence's END column.  Max over passes;
-// flag the 16-bit saturation test.
-__global__ void sw16_gather_kernel(const int64_t *__restrict__ endcol, int64_t count,
-                                   const uint32_t *__restrict__ sc_out, int32_t *scores, uint8_t *flagged,
-                                   int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
-                                   const int32_t *__restrict__ seq_idx) {
-  // scores2 == nullptr: two sequences per column, the END column's half is the
-  // sequence's.  scores2 != nullptr (query pair): both halves belong to the
-  // sequence, low half = query 1, high half = query 2.
+// flag the 16-bit saturation test.  Two launches per pass:
+//   detect: a sequence whose stored 16-bit score reaches thresh is flagged
+//           (flag byte = first flagging pass + 1); with the biased-unsigned
+//           arithmetic a flagged LOW half (half A, or query 1 of a pair) marks
+//           its work item "hot": once its H passes 65536 - SM the 32-bit
+//           diagonal add carries into the high half (R7);
+//   update: every HIGH-half sequence of a hot item (every query-2 half of a
+//           sequence whose query-1 half flagged) is flagged in the same pass
+//           -- its 16-bit values may carry that +1 from this pass on, and its
+//           32-bit re-scoring starts from this pass's exact input boundary --
+//           the other unflagged sequences take max(score, this pass's value).
+__global__ void sw16_detect_kernel(const int64_t *__restrict__ endcol, int64_t count,
+                                   const uint32_t *__restrict__ sc_out, uint8_t *flagged, uint8_t *flagged2,
+                                   bool pairq, int pass, int thresh, const int32_t *__restrict__ seq_idx,
+                                   const int32_t *__restrict__ item_of, uint8_t *item_hot) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
     // seq_idx (streamed databases): entry i describes original sequence seq_idx[i]
@@ -650,18 +657,45 @@ __global__ void sw16_gather_kernel(const int64_t *__restrict__ endcol, int64_t c
     const int64_t o = seq_idx ? (int64_t)seq_idx[i] : i;
     const int64_t e = endcol[i];
     const uint32_t w = sc_out[e >> 1];
+    const int flag = min(pass + 1, 255);
+    if (flagged[o] == 0) {
+      const int v = (int)((!pairq && (e & 1)) ? (w >> 16) : (w & 0xffffu));
+      if (v >= thresh) {
+        flagged[o] = (uint8_t)flag;
+        if (kArith == 2) {   // a flagged low half may carry into the high half
+          if (pairq) {
+            if (flagged2[o] == 0) flagged2[o] = (uint8_t)flag;
+          } else if ((e & 1) == 0 && item_of) {
+            item_hot[item_of[o]] = 1;
+          }
+        }
+      }
+    }
+    if (pairq && flagged2[o] == 0 && (int)(w >> 16) >= thresh) flagged2[o] = (uint8_t)flag;
+  }
+}
+
+__global__ void sw16_update_kernel(const int64_t *__restrict__ endcol, int64_t count,
+                                   const uint32_t *__restrict__ sc_out, int32_t *scores, uint8_t *flagged,
+                                   int32_t *scores2, const uint8_t *__restrict__ flagged2, int pass,
+                                   const int32_t *__restrict__ seq_idx, const int32_t *__restrict__ item_of,
+                                   const uint8_t *__restrict__ item_hot) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = seq_idx ? (int64_t)seq_idx[i] : i;
+    const int64_t e = endcol[i];
+    const uint32_t w = sc_out[e >> 1];
     // once flagged, the 32-bit kernel owns the score (started from the last
     // exact pass boundary, or from row 0)
     if (flagged[o] == 0) {
-      const int v = (int)((!scores2 && (e & 1)) ? (w >> 16) : (w & 0xffffu));
-      if (v >= thresh) flagged[o] = (uint8_t)min(pass + 1, 255);
-      else scores[o] = max(pass == 0 ? 0 : scores[o], v - kBias16);
+      if (kArith == 2 && !scores2 && (e & 1) && item_of && item_hot[item_of[o]]) {
+        flagged[o] = (uint8_t)min(pass + 1, 255);
+      } else {
+        const int v = (int)((!scores2 && (e & 1)) ? (w >> 16) : (w & 0xffffu));
+        scores[o] = max(pass == 0 ? 0 : scores[o], v - kBias16);
+      }
     }
-    if (scores2 && flagged2[o] == 0) {
-      const int v2 = (int)(w >> 16);
-      if (v2 >= thresh) flagged2[o] = (uint8_t)min(pass + 1, 255);
-      else scores2[o] = max(pass == 0 ? 0 : scores2[o], v2 - kBias16);
-    }
+    if (scores2 && flagged2[o] == 0) scores2[o] = max(pass == 0 ? 0 : scores2[o], (int)(w >> 16) - kBias16);
   }
 }
 
@@ -1047,6 +1081,23 @@ __global__ void __launch_bounds__(1024) block_topk_kernel(const int32_t *scores,
   }
 }
 
+// Out-of-core database: a chunk arrives over the host
+// link as one 16-bit letter-pair index per column (1 B per residue) and is
+// expanded here to the pass kernel's column words (descriptor byte offsets).
+__global__ void expand_columns_kernel(const uint16_t *__restrict__ in, int64_t n, uint32_t *__restrict__ out) {
+  const int64_t n4 = n >> 2;
+  const bool vec = ((reinterpret_cast<uintptr_t>(in) & 7) | (reinterpret_cast<uintptr_t>(out) & 15)) == 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (vec ? n4 : 0);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(in) + i);
+    reinterpret_cast<uint4 *>(out)[i] = make_uint4((v.x & 0xffffu) * kDescBytes, (v.x >> 16) * kDescBytes,
+                                                   (v.y & 0xffffu) * kDescBytes, (v.y >> 16) * kDescBytes);
+  }
+  for (int64_t i = (vec ? 4 * n4 : 0) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)in[i] * kDescBytes;
+}
+
 // Sorting stage for k > 32: radix select of the k-th largest
 // 64-bit key (score, -index), 8 passes of 8 bits from the most significant
 // digit, then compaction of the k keys >= it and a sort of those k only.
@@ -1377,11 +1428,16 @@ cudaError_t launch_sw16_pass(int ti, int grid, const SW16Params &p, cudaStream_t
 
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
-                               cudaStream_t st, const int32_t *seq_idx) {
+                               cudaStream_t st, const int32_t *seq_idx, const int32_t *item_of,
+                               uint8_t *item_hot) {
   if (count <= 0) return cudaSuccess;
   ++g_launches;
-  sw16_gather_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, scores, flagged, scores2, flagged2,
-                                                            pass, thresh, seq_idx);
+  sw16_detect_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, flagged, flagged2,
+                                                            scores2 != nullptr, pass, thresh, seq_idx, item_of,
+                                                            item_hot);
+  ++g_launches;
+  sw16_update_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, scores, flagged, scores2,
+                                                            flagged2, pass, seq_idx, item_of, item_hot);
   return cudaGetLastError();
 }
 
@@ -1453,6 +1509,13 @@ cudaError_t launch_scatter_scores(const int32_t *src, const int64_t *index, int6
   if (n <= 0) return cudaSuccess;
   ++g_launches;
   scatter_scores_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, st>>>(src, index, n, dst, dst_count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand_columns(const uint16_t *in, int64_t n, uint32_t *out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  expand_columns_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, st>>>(in, n, out);
   return cudaGetLastError();
 }
 

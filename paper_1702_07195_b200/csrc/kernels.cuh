@@ -154,9 +154,13 @@ cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cuda
 // Whether tile i has a cross-pass wavefront kernel (p.npass > 0 launches it).
 bool tile_has_wave(int i);
 int tile_wave_ctas_per_sm(int i);
+// item_of: per original sequence its work item (sequence-pair image), with
+// item_hot[items] zeroed per search: the carry propagation of SW_ARITH 2
+// (kernels.cu, R7); null for the query-pair image.
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
-                               cudaStream_t st, const int32_t *seq_idx = nullptr);
+                               cudaStream_t st, const int32_t *seq_idx, const int32_t *item_of,
+                               uint8_t *item_hot);
 // thresh: in stored 16-bit units (32768 - smax); scores are stored - kBias16.
 // A sequence already flagged is skipped; one flagged in this pass gets
 // flagged = pass + 1 and keeps in scores the exact maximum of the earlier passes
@@ -185,6 +189,9 @@ cudaError_t launch_block_topk(const int32_t *scores, const int64_t *index, const
                               int k, uint64_t *out, int blocks, cudaStream_t st);
 cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score,
                                cudaStream_t st);
+// Streamed database: out[i] = in[i] * kDescBytes (compact letter-pair index ->
+// column word) for i < n.
+cudaError_t launch_expand_columns(const uint16_t *in, int64_t n, uint32_t *out, cudaStream_t st);
 // k > 32: radix select (8 digit passes of the 64-bit key) + compaction of the
 // k largest keys into out[0, k); sorted descending when k <= 4096 (otherwise
 // unsorted: the caller sorts them).  scratch: radix_topk_scratch_bytes().

@@ -161,8 +161,9 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
   // Write the stream: column word per pair column.
   out.stream.assign((size_t)col, column_word(kNul, kNul));
   out.endcol.assign((size_t)count, -1);
+  out.item_of.assign((size_t)count, -1);
   // half: 0 = A (low 16 bits), 1 = B (high), 2 = both (single-sequence image)
-  auto write_half = [&](const Item &it, int32_t slot0, int32_t n, int half) {
+  auto write_half = [&](const Item &it, int32_t item, int32_t slot0, int32_t n, int half) {
     int64_t c = it.col_begin;
     auto put = [&](int64_t col, int letter) {
       uint32_t w = out.stream[col];
@@ -176,6 +177,7 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
       const uint8_t *r = residues + offsets[s];
       for (int64_t j = 0; j < len[s]; ++j, ++c) put(c, r[j]);
       out.endcol[s] = 2 * c + (half == 1 ? 1 : 0);   // the END column of sequence s
+      out.item_of[s] = item;
       put(c++, kEnd);
       put(c++, kNul);
     }
@@ -189,10 +191,10 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
         for (size_t i = k; i < ni; i += nth) {
           const Item &it = out.items[i];
           if (single) {
-            write_half(it, it.seqA, it.nA, 2);
+            write_half(it, (int32_t)i, it.seqA, it.nA, 2);
           } else {
-            write_half(it, it.seqA, it.nA, 0);
-            write_half(it, it.seqB, it.nB, 1);
+            write_half(it, (int32_t)i, it.seqA, it.nA, 0);
+            write_half(it, (int32_t)i, it.seqB, it.nB, 1);
           }
         }
       });

@@ -51,6 +51,7 @@ struct HostImage {
   std::vector<Item> items;        // sorted by ncols descending (claim order)
   std::vector<int32_t> slots;     // slot -> original sequence index
   std::vector<int64_t> endcol;    // per original sequence: 2 * (END column) + half (0 = A, 1 = B)
+  std::vector<int32_t> item_of;   // per original sequence: its work item
   int64_t total_cols = 0;
   int64_t max_len = 0;
 };
