@@ -35,4 +35,6 @@ for budget in [0] + budgets:
         print(json.dumps({"config": cfg, "m": len(q), "chunk_MiB": budget / 2**20, "chunks": sw.sw_db_chunks(),
                           "ms": round(ms, 2), "gcups": round(len(q) * w.db.total_residues / (ms * 1e6), 1),
                           "image_GB": round(sw.sw_last_stats()["pair_columns"] * 4 / 1e9, 3),
+                          "pass_kernels_ms": round(sw.sw_last_timing()["pass_kernels_ms"], 2),
+                          "search_ms": round(sw.sw_last_timing()["search_ms"], 2),
                           "identical_to_resident": same}), flush=True)
