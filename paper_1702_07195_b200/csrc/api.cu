@@ -720,7 +720,10 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
     int rcs[2] = {0, 0};
     auto build_one = [&](int k) {
       try {
-        rcs[k] = build_image(residues, offsets, count, target_groups, k == 1, himg[k], errs[k]) ? SW_EINVAL : 0;
+        // streamed: items of at most a quarter of a chunk's share per group,
+        // so each chunk's launch keeps the 8-lane tiles' 2 x target_groups busy
+        const int64_t cap = strm ? std::max<int64_t>(256, (chunk_bytes / 4) / (4 * target_groups)) : 0;
+        rcs[k] = build_image(residues, offsets, count, target_groups, k == 1, himg[k], errs[k], cap) ? SW_EINVAL : 0;
       } catch (const std::bad_alloc &) {
         rcs[k] = SW_ENOMEM;
         errs[k] = "host allocation failed in the pre-processor";

@@ -62,7 +62,7 @@ inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 }  // namespace
 
 int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
-                int64_t target_groups, bool single, HostImage &out, std::string &err) {
+                int64_t target_groups, bool single, HostImage &out, std::string &err, int64_t item_cap) {
   out = HostImage();
   std::vector<int64_t> len(count);
   int64_t total_stream = 0;
@@ -94,6 +94,9 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
   int64_t item_max = 16384, item_min = 256;
   if (const char *e = std::getenv("SW_ITEM_MAX")) item_max = std::max<int64_t>(256, std::atoll(e));
   if (const char *e = std::getenv("SW_ITEM_MIN")) item_min = std::max<int64_t>(16, std::atoll(e));
+  // a streamed database processes one chunk per launch: its items must stay
+  // small enough that every chunk keeps every group busy (item_cap)
+  if (item_cap > 0) item_max = std::max(item_min, std::min(item_max, item_cap));
   // columns still to place (pair columns: two sequences per column)
   int64_t remaining = single ? total_stream : (total_stream + 1) / 2;
   int64_t lo = 0, hi = count - 1;

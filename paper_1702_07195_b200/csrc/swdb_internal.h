@@ -61,8 +61,10 @@ struct HostImage {
 // Returns 0 or -1 (err set).
 // single = false: two sequences per column (halves A/B, one query);
 // single = true: one sequence per column in both halves (query pairs).
+// item_cap > 0: upper bound on the columns of a work item (streamed databases:
+// a chunk is processed per launch and must hold several items per group).
 int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
-                int64_t target_groups, bool single, HostImage &out, std::string &err);
+                int64_t target_groups, bool single, HostImage &out, std::string &err, int64_t item_cap = 0);
 
 // Validation of the raw database (codes < 24, offsets monotone).
 int validate_db(const uint8_t *residues, const int64_t *offsets, int64_t count, std::string &err);
