@@ -4,9 +4,11 @@
 Each trial draws a database (count, length mix, alphabet use), a query or a
 query pair, a scoring matrix (BLOSUM62, random symmetric, random asymmetric,
 extreme int8), gap penalties (including 0 and very large), a tile (default or
-any compiled one), the cross-pass wavefront (off / auto / forced) and a path
-(resident single, resident query pair, streamed), then compares every score and
-the top-k with the oracle.
+any compiled one: throughput, latency or score-profile tiles), the cross-pass
+wavefront (off / auto / forced), the latency-tile mode and the substitution
+profile (query / score profile), and a path (resident single, resident query
+pair, streamed), then compares every score and the top-k (k up to 200: both
+sorting paths) with the oracle.
 
     python tests/report_stress.py [--seconds 600] [--seed 1]
 
@@ -79,7 +81,8 @@ def main():
     import torch
     torch.cuda.set_device(0)
     rng = np.random.default_rng(args.seed)
-    tiles = [(G, R) for G in (8, 16, 32) for R in range(1, 33) if sw.sw_tile_supported(G, R)]
+    tiles = [(G, R) for G in (8, 16, 32) for R in range(1, 33)
+             if sw.sw_tile_supported(G, R) or sw.sw_tile_supported(G, R, lat=True) or sw.sw_tile_supported(G, R, sp=True)]
     t_end = time.time() + args.seconds
     trials = fails = cells = 0
     while time.time() < t_end:
@@ -96,6 +99,10 @@ def main():
         sw.sw_set_tile(*tile)
         wave = int(rng.choice([-1, 0, 1, 1]))   # cross-pass wavefront off / auto / forced
         sw.sw_set_wave(wave)
+        lat = int(rng.choice([-1, 0, 1]))       # latency tiles never / auto / always
+        sw.sw_set_latency_mode(lat)
+        prof = int(rng.choice([0, 1, 2]))       # substitution scores: auto / query profile / score profile
+        sw.sw_set_profile(prof)
         try:
             if path == "streamed":
                 sw.sw_db_load_streamed(db.residues, db.offsets, int(rng.integers(1, 64)) * 4096)
@@ -114,12 +121,13 @@ def main():
                 bad = np.nonzero(g != exp)[0]
                 if bad.size:
                     ok = False
-                    print(json.dumps({"trial": trials, "path": path, "tile": tile, "wave": wave, "matrix": mname, "gaps": [go, ge],
+                    print(json.dumps({"trial": trials, "path": path, "tile": tile, "wave": wave, "lat": lat,
+                                      "profile": prof, "matrix": mname, "gaps": [go, ge],
                                       "m": len(qq), "count": db.count, "mismatches": int(bad.size),
                                       "first": bad[:5].tolist(), "got": g[bad[:5]].tolist(),
                                       "exp": exp[bad[:5]].tolist()}), flush=True)
             if ok and path != "pair":
-                k = int(min(db.count, rng.integers(1, 40)))
+                k = int(min(db.count, rng.integers(1, 40) if rng.random() < 0.7 else rng.integers(33, 200)))
                 idx, sc = sw.sw_topk(k)
                 eidx, esc = oracle.topk(outs[0][1], k)
                 if not ((idx == eidx).all() and (sc == esc).all()):
@@ -131,6 +139,8 @@ def main():
             print(json.dumps({"trial": trials, "path": path, "error": str(e)}), flush=True)
     sw.sw_set_tile(0)
     sw.sw_set_wave(0)
+    sw.sw_set_latency_mode(0)
+    sw.sw_set_profile(0)
     print(json.dumps({"trials": trials, "failures": fails, "cells": cells, "seconds": args.seconds}), flush=True)
     sys.exit(1 if fails else 0)
 

@@ -105,3 +105,25 @@ def test_config4_structure():
         frac = (w.db.seq(int(i)) != q).mean()
         assert 0.03 < frac < 0.23
     assert ((L >= 5000) & (L != 5478)).sum() >= 100
+
+
+def test_config_db_subset_equals_full_generation():
+    """bench.py's per-rank generation (sw_inputs.config_db_subset streams the
+    residue generator and keeps only the shard) equals the full configuration's
+    sub-database, across residue chunk boundaries (2^26)."""
+    rng = np.random.default_rng(5)
+    for k, sc in [(0, 1.0), (1, 0.4), (2, 0.005), (3, 0.005)]:
+        w = si.make_config(k, scale=sc)
+        assert np.array_equal(si.config_lengths(k, sc), w.db.lengths())
+        assert all(np.array_equal(a, b) for a, b in zip(si.config_queries(k), w.queries))
+        for frac in (0.5, 0.02):
+            idx = np.sort(rng.choice(w.db.count, max(1, int(w.db.count * frac)), replace=False))
+            sub = si.config_db_subset(k, idx, sc)
+            ref = w.db.subset(idx)
+            assert np.array_equal(sub.offsets, ref.offsets) and np.array_equal(sub.residues, ref.residues)
+    # a sequence straddling the first 2^26-residue chunk boundary
+    w = si.config1(scale=0.4)
+    b = int(np.searchsorted(w.db.offsets, 1 << 26, side="right") - 1)
+    sub = si.config_db_subset(1, np.array([b - 1, b, b + 1]), 0.4)
+    for j, i in enumerate((b - 1, b, b + 1)):
+        assert np.array_equal(sub.seq(j), w.db.seq(i))
