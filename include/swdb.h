@@ -220,7 +220,8 @@ int sw_scatter_dev(const int32_t *d_src, const int64_t *d_index, int64_t n, int3
  *   stats[10] = 1 if the last search ran as a cross-pass wavefront,
  *   stats[11] = 1 if it ran a latency tile (sw_set_latency_mode),
  *   stats[12] = substitution scores of the 16-bit kernel: 1 = query profile,
- *              2 = score profile (sw_set_profile).
+ *              2 = score profile (sw_set_profile),
+ *   stats[13] = long-sequence pairs scored in rows mode (sw_set_rows_mode).
  * Returns the number of entries written (<= n).
  */
 int sw_last_stats(int64_t *stats, int n);
@@ -263,6 +264,23 @@ int sw_tile_supported(int32_t G, int32_t R);
  * Returns SW_OK or SW_EINVAL.
  */
 int sw_set_profile(int32_t mode);
+
+/*
+ * sw_set_rows_mode -- rows mode for the long sequences of a database
+ * (intra-task parallelism for long alignments).
+ * sw_db_load gives every sequence longer than 4x the average columns per
+ * lane group (at least 512 residues) a work item of its own, paired with the
+ * next long one.  In rows mode those pairs are scored with the database
+ * sequence along the rows and the query as the column stream (the same
+ * recurrence on the transposed matrix; scores are identical): the passes over
+ * the sequence run as a wavefront on many lane groups at once, so the
+ * critical path is about m + (n / 256) x 40 steps instead of n.  mode 0
+ * (default): used when the query is at most half as long as the shortest long
+ * sequence; 1: whenever possible; -1: never.  Resident single-query searches
+ * whose pass kernel makes one pass, without the cross-pass wavefront.
+ * Returns SW_OK or SW_EINVAL.
+ */
+int sw_set_rows_mode(int32_t mode);
 
 /*
  * sw_set_latency_mode -- latency tiles for searches whose time is one long

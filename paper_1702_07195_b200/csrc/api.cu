@@ -75,11 +75,22 @@ struct Image {
   int64_t total_cols = 0;
   int64_t max_item_cols = 0;  // longest work item (columns)
   int num_items = 0;
+  // rows mode (sequence-pair image): the leading n_long items hold one long
+  // sequence per half; units (item, pass) of the rows kernel
+  int n_long = 0;
+  int64_t long_min_len = 0;       // shortest long sequence
+  int64_t long_cols = 0;          // pair-columns of the long items
+  int64_t max_item_cols_rest = 0; // longest item after them
+  DevBuf<int2> units;
+  int n_units = 0;
   void release() {
-    stream.release(); items.release(); endcol.release(); slots.release(); item_of.release();
+    stream.release(); items.release(); endcol.release(); slots.release(); item_of.release(); units.release();
     total_cols = 0;
     max_item_cols = 0;
     num_items = 0;
+    n_long = 0;
+    n_units = 0;
+    long_min_len = long_cols = max_item_cols_rest = 0;
   }
 };
 
@@ -133,6 +144,11 @@ struct State {
   int force_G = 0, force_R = 0;
   int wave_mode = 0;        // cross-pass wavefront: 0 auto, 1 always (multi-pass), -1 never
   int lat_mode = 0;         // latency tiles: 0 auto, 1 always, -1 never
+  int rows_mode = 0;        // rows mode for the long items: 0 auto, 1 whenever possible, -1 never
+  int64_t last_rows = 0;    // long pairs scored in rows mode by the last search
+  DevBuf<uint2> rows_bnd;   // rows mode: per long item 2 x ncq boundary
+  DevBuf<uint32_t> rows_sc; // rows mode: per long item ncq chain values
+  DevBuf<int> rows_prog;    // rows mode: per unit progress, + 1 counter
   int prof_mode = 0;        // substitution scores: 0 auto, 1 query profile, 2 score profile
   int last_prof = 1;
   bool last_lat = false;
@@ -187,6 +203,7 @@ struct State {
     flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release(); progress.release();
     query.release(); query2.release(); matrix.release(); qp.release(); desc.release(); qp32.release();
     qp32b.release(); bnd.release(); skip.release(); item_hot.release();
+    rows_bnd.release(); rows_sc.release(); rows_prog.release();
     scratch32.release(); dummy.release(); nulcols.release(); zerocols.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
     loaded = false;
     has_search = false;
@@ -329,10 +346,32 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // 20 lengths, profiles/r02_qp_sp_crossover.jsonl).
   const bool use_sp = !pair && (g.prof_mode == 2 || (g.prof_mode == 0 && sp_wins(pair ? std::max(m, m2) : m)));
   const int mode = pair ? 3 : (use_sp ? 1 : 0);
-  const Image &I = g.img[pair ? 1 : 0];
+  const Image &I0 = g.img[pair ? 1 : 0];
   const int mm = pair ? std::max(m, m2) : m;
-  int ti = choose_tile(mm, mode, I);
+  // Rows mode: the long pairs (the image's leading items) are
+  // scored with the sequence along the rows by sw16_rows_kernel, the pass
+  // kernel claims the other items only.  Auto: when the query is at most half
+  // as long as the shortest long sequence (the rows kernel's chain is about
+  // m + passes x 40 steps instead of n).  Single-pass resident single-query
+  // searches without the wavefront.
+  const bool rows_cand = !pair && !g.streamed && I0.n_long > 0 && I0.n_units > 0 && g.rows_mode >= 0 &&
+                         (g.rows_mode == 1 || (int64_t)mm * 2 <= I0.long_min_len);
+  const Image &I = I0;
+  // the tile model's view of the items the pass kernel runs (rows mode: all
+  // but the long pairs); device buffers are shared, only these sizes differ
+  Image Iv = I0;
+  if (rows_cand) {
+    Iv.max_item_cols = I0.max_item_cols_rest;
+    Iv.total_cols = std::max<int64_t>(1, I0.total_cols - I0.long_cols);
+    Iv.num_items = std::max(1, I0.num_items - I0.n_long);
+  }
+  auto passes_of = [&](int i) { return (mm + tile(i).G * tile(i).R - 1) / (tile(i).G * tile(i).R); };
+  int ti = choose_tile(mm, mode, rows_cand ? Iv : I);
   if (ti < 0) return fail(SW_ECUDA, "no runnable kernel tile");
+  // rows mode needs a single pass of the pass kernel; otherwise the ordinary choice
+  const bool rowsm = rows_cand && passes_of(ti) == 1;
+  if (rows_cand && !rowsm) ti = choose_tile(mm, mode, I);
+  const Image &Im = rowsm ? Iv : I;   // what the latency model sees
   // Cross-pass wavefront (one launch runs every pass).  A pass
   // of the per-pass path keeps at most one lane group per work item busy; with
   // far fewer items than groups (a database of few, long sequences) the
@@ -344,8 +383,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // tiles when their units exceed half the groups.  Forced mode (1) uses the
   // forced or chosen tile when it has a wavefront kernel, else 32x16 / 32x8.
   bool wave = false;
-  if (!pair && !use_sp && !g.streamed && g.wave_mode >= 0) {
-    auto passes_of = [&](int i) { return (mm + tile(i).G * tile(i).R - 1) / (tile(i).G * tile(i).R); };
+  if (!pair && !use_sp && !g.streamed && !rowsm && g.wave_mode >= 0) {
     const int t8 = find_tile_mode(32, 8, 0), t16 = find_tile_mode(32, 16, 0);
     const double items = (double)std::max(1, I.num_items);
     int tw = -1;
@@ -375,10 +413,11 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     if (g.force_G) {   // a forced latency tile: used when forced or when it is latency-only
       const int tf = find_tile_mode(g.force_G, g.force_R, 0, 1);
       if (tf >= 0 && (g.lat_mode == 1 || find_tile_mode(g.force_G, g.force_R, 0, 0) < 0)) tl = tf;
-      else if (g.lat_mode == 1) tl = choose_lat_tile(mm, I, ti, true);
+      else if (g.lat_mode == 1) tl = choose_lat_tile(mm, Im, ti, true);
     } else {
-      tl = choose_lat_tile(mm, I, ti, g.lat_mode == 1);
+      tl = choose_lat_tile(mm, Im, ti, g.lat_mode == 1);
     }
+    if (tl >= 0 && rowsm && passes_of(tl) != 1) tl = -1;   // rows mode keeps a single pass
     if (tl >= 0) {
       ti = tl;
       lat = true;
@@ -491,6 +530,16 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int64_t span = strm ? g.chunk_span : I.total_cols;
   CUDA_TRY(g.pcounters.ensure((size_t)nch * P));
   CUDA_TRY(cudaMemsetAsync(g.pcounters.p, 0, sizeof(int) * (size_t)nch * P, st));
+  const int ncq = (m + 2 + 3) & ~3;   // rows mode: the query stream (m letters, END, NUL, padding)
+  if (rowsm) {
+    // the pass kernel starts claiming after the long items
+    const int first = I0.n_long;
+    CUDA_TRY(cudaMemcpyAsync(g.pcounters.p, &first, sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(g.rows_bnd.ensure((size_t)I0.n_long * 2 * ncq));
+    CUDA_TRY(g.rows_sc.ensure((size_t)I0.n_long * ncq));
+    CUDA_TRY(g.rows_prog.ensure((size_t)I0.n_units + 1));
+    CUDA_TRY(cudaMemsetAsync(g.rows_prog.p, 0, sizeof(int) * ((size_t)I0.n_units + 1), st));
+  }
   if (P > 1 && g.bnd.n < (size_t)span * 2) CUDA_TRY(g.bnd.ensure((size_t)span * 2));
   if (!strm && !pair && P > 1) CUDA_TRY(g.skip.ensure((size_t)std::max(1, I.num_items)));
   CUDA_TRY(cudaEventRecord(g.ev[1], st));
@@ -583,6 +632,29 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       CUDA_TRY(pass_event(pe + 1));
       CUDA_TRY(cudaEventRecord(g.pev[pe], st));
       CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
+      if (rowsm) {   // the long pairs, rows along the database sequence (before the gather reads sc_out)
+        RowsParams r{};
+        r.query = g.query.p;
+        r.m = m;
+        r.ncq = ncq;
+        r.matrix = g.matrix.p;
+        r.res = g.res.p;
+        r.offs = g.offs.p;
+        r.items = I0.items.p;
+        r.slots = I0.slots.p;
+        r.units = I0.units.p;
+        r.n_units = I0.n_units;
+        r.counter = g.rows_prog.p + I0.n_units;
+        r.progress = g.rows_prog.p;
+        r.bnd = g.rows_bnd.p;
+        r.sc = g.rows_sc.p;
+        r.endcol = I0.endcol.p;
+        r.sc_out = g.sc_out.p;
+        r.goe = goe;
+        r.ge = ge;
+        r.one = 1u;
+        CUDA_TRY(launch_sw16_rows(g.num_sms, r, st));
+      }
       CUDA_TRY(cudaEventRecord(g.pev[pe + 1], st));
       g.npev = pe / 2 + 1;
       if (strm) {
@@ -617,6 +689,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   g.last_wave = wave;
   g.last_lat = lat;
   g.last_prof = use_sp ? 2 : 1;
+  g.last_rows = rowsm ? I0.n_long : 0;
   g.last_flags = -1;
   g.last_cells32 = -1;
   return SW_OK;
@@ -723,7 +796,12 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
         // streamed: items of at most a quarter of a chunk's share per group,
         // so each chunk's launch keeps the 8-lane tiles' 2 x target_groups busy
         const int64_t cap = strm ? std::max<int64_t>(256, (chunk_bytes / 4) / (4 * target_groups)) : 0;
-        rcs[k] = build_image(residues, offsets, count, target_groups, k == 1, himg[k], errs[k], cap) ? SW_EINVAL : 0;
+        // rows mode (resident pair image): sequences longer than 4x the
+        // average columns per lane group are the long pairs
+        const int64_t avg = (offsets[count] + 2 * count) / 2 / std::max<int64_t>(1, target_groups);
+        const int64_t long_min = (!strm && k == 0) ? std::max<int64_t>(512, 4 * avg) : 0;
+        rcs[k] = build_image(residues, offsets, count, target_groups, k == 1, himg[k], errs[k], cap, long_min)
+                     ? SW_EINVAL : 0;
       } catch (const std::bad_alloc &) {
         rcs[k] = SW_ENOMEM;
         errs[k] = "host allocation failed in the pre-processor";
@@ -757,6 +835,33 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
     I.num_items = (int)H.items.size();
     I.max_item_cols = 0;
     for (const Item &it : H.items) I.max_item_cols = std::max<int64_t>(I.max_item_cols, it.ncols);
+    I.n_long = H.n_long_items;
+    I.max_item_cols_rest = 0;
+    I.long_cols = 0;
+    I.long_min_len = INT64_MAX;
+    std::vector<int2> units;
+    for (size_t i = 0; i < H.items.size(); ++i) {
+      const Item &it = H.items[i];
+      if ((int)i >= I.n_long) {
+        I.max_item_cols_rest = std::max<int64_t>(I.max_item_cols_rest, it.ncols);
+        continue;
+      }
+      I.long_cols += it.ncols;
+      int64_t nmax = 0;
+      for (int h = 0; h < it.nA + it.nB; ++h) {
+        const int32_t sq = H.slots[it.seqA + h];
+        const int64_t n = offsets[sq + 1] - offsets[sq];
+        I.long_min_len = std::min(I.long_min_len, n);
+        nmax = std::max(nmax, n);
+      }
+      for (int64_t ps = 0; ps < (nmax + kRowsRows - 1) / kRowsRows; ++ps) units.push_back(make_int2((int)i, (int)ps));
+    }
+    if (I.n_long == 0) I.long_min_len = 0;
+    I.n_units = (int)units.size();
+    if (!units.empty()) {
+      CUDA_TRY(I.units.ensure(units.size()));
+      CUDA_TRY(cudaMemcpy(I.units.p, units.data(), units.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    }
     CUDA_TRY(I.items.ensure(H.items.size()));
     CUDA_TRY(cudaMemcpy(I.items.p, H.items.data(), H.items.size() * sizeof(Item), cudaMemcpyHostToDevice));
     if (k == 0) {
@@ -1024,10 +1129,10 @@ int sw_last_stats(int64_t *stats, int n) {
     g.last_cells32 = cells;
   }
   const Image &I = g.img[g.last_mode == 3 ? 1 : 0];
-  const int64_t v[13] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
+  const int64_t v[14] = {(int64_t)g.last_G * g.last_R, g.last_P, g.last_G, g.last_R,
                          g.last_flags, g.last_cells32, I.total_cols, I.num_items, g.last_thresh, kArith,
-                         g.last_wave ? 1 : 0, g.last_lat ? 1 : 0, g.last_prof};
-  const int m = std::min(n, 13);
+                         g.last_wave ? 1 : 0, g.last_lat ? 1 : 0, g.last_prof, g.last_rows};
+  const int m = std::min(n, 14);
   for (int i = 0; i < m; ++i) stats[i] = v[i];
   return m;
 }
@@ -1067,6 +1172,13 @@ int sw_set_tile(int32_t G, int32_t R) {
 int sw_tile_supported(int32_t G, int32_t R) {
   return (find_tile_mode(G, R, 0) >= 0 ? 1 : 0) | (find_tile_mode(G, R, 0, 1) >= 0 ? 2 : 0) |
          (find_tile_mode(G, R, 1) >= 0 ? 4 : 0);
+}
+
+int sw_set_rows_mode(int32_t mode) {
+  t_err.clear();
+  if (mode < -1 || mode > 1) return fail(SW_EINVAL, "mode must be -1, 0 or 1");
+  g.rows_mode = mode;
+  return SW_OK;
 }
 
 int sw_set_profile(int32_t mode) {

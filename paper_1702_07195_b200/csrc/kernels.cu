@@ -168,6 +168,10 @@ __device__ __forceinline__ void st_release(int *p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 __device__ __forceinline__ void st_global_v2(uint2 *p, uint32_t a, uint32_t b) {
   asm volatile("st.global.v2.u32 [%0], {%1, %2};" :: "l"(p), "r"(a), "r"(b) : "memory");
 }
@@ -631,6 +635,199 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
     __syncthreads();
   }
   } while (WAVE);
+}
+
+// ---------------------------------------------------------------------------
+// Rows mode (row a5): long database sequences laid along the
+// ROWS.  A long pair (one sequence per half of a leading work item) is the
+// "query" of a cross-pass wavefront and the real query is the column stream:
+// the same recurrence on the transposed matrix (E and F swap roles, both use
+// Goe / Ge; the score is the maximum over the matrix, so it is unchanged).  A
+// warp (one 32-lane group, kRowsR rows per lane) claims units (item, pass)
+// item-major from an atomic counter; it builds its own profile slice in
+// shared memory from the two sequences' residues (one pre-packed word
+// SM(c, dB_row) * 65536 + SM(c, dA_row) per query letter c: no packing IMAD)
+// and streams the query; pass p reads the boundary (H, F) and the score chain
+// that pass p-1 of the same item wrote, after an ld.acquire of its published
+// progress.  The chain value at the query's END column after the last pass is
+// the pair's score; it is written into the END columns of the sequences in
+// the stream image, where the ordinary score gather reads it.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const RowsParams p) {
+  constexpr int R = kRowsR, G = 32, KC = R / 4;
+  static_assert(R % 4 == 0, "rows-mode profile chunks");
+  extern __shared__ uint4 rsm[];
+  uint4 *sdesc = rsm;                                          // [kNL] column descriptors
+  int32_t *sM = reinterpret_cast<int32_t *>(rsm + kNL);        // [kNL][kNL]: SM(query letter, db letter)
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(rsm);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = lane;
+  const int src = (t + G - 1) & (G - 1);
+  const bool last = t == G - 1;
+  const uint32_t nlast = last ? 0u : 1u;
+  const uint32_t bdef = last ? kB2 : 0u;
+  const uint32_t one = p.one;
+  const uint32_t s_prof = sbase + kRowsHeadBytes + (uint32_t)warp * (kNL * kRowsLS);
+  const uint32_t s_qp = s_prof + t * 16;
+  for (int i = threadIdx.x; i < kNL; i += blockDim.x) {
+    const bool sep = i >= kAlpha;
+    const uint32_t pgoe = (uint32_t)(uint16_t)(-(int)min(p.goe, 32767));
+    const uint32_t pge = (uint32_t)(uint16_t)(-(int)min(p.ge, 32767));
+    const uint32_t wgoe = sep ? 0x80018001u : (pgoe | (pgoe << 16));
+    const uint32_t wge = sep ? 0x80018001u : (pge | (pge << 16));
+    sdesc[i] = make_uint4((uint32_t)(i * kRowsLS / 16), wgoe, wge, sep ? 0x80008000u : 0u);
+  }
+  for (int i = threadIdx.x; i < kNL * kNL; i += blockDim.x) {
+    const int c = i / kNL, d = i % kNL;
+    sM[i] = (c < kAlpha && d < kAlpha) ? (int32_t)p.matrix[c * kAlpha + d] : kDummy16;
+  }
+  __syncthreads();
+  const DescWords nul = load_desc(sbase + kNul * 16);
+
+  for (;;) {
+    int u = 0;
+    if (last) u = atomicAdd(p.counter, 1);
+    u = __shfl_sync(0xffffffffu, u, G - 1);
+    if (u >= p.n_units) break;
+    const int2 un = p.units[u];
+    const int k = un.x, pass = un.y;
+    const Item it = p.items[k];
+    const int32_t sA = p.slots[it.seqA];
+    const int32_t sB = it.nB ? p.slots[it.seqB] : -1;
+    const int64_t oA = p.offs[sA], nA = p.offs[sA + 1] - oA;
+    const int64_t oB = sB >= 0 ? p.offs[sB] : 0, nB = sB >= 0 ? p.offs[sB + 1] - oB : 0;
+    const int npass = (int)((max(nA, nB) + G * R - 1) / (G * R));
+    // ---- this lane's profile rows: SM(c, dB_row) * 65536 + SM(c, dA_row)
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      int a[4], b[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t row = (int64_t)pass * G * R + t * R + kk * 4 + e;
+        a[e] = row < nA ? (int)__ldg(p.res + oA + row) : -1;
+        b[e] = row < nB ? (int)__ldg(p.res + oB + row) : -1;
+      }
+      for (int c = 0; c < kNL; ++c) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int lo = a[e] >= 0 ? sM[c * kNL + a[e]] : kDummy16;
+          const int hi = b[e] >= 0 ? sM[c * kNL + b[e]] : kDummy16;
+          w[e] = (uint32_t)(hi * 65536 + lo);
+        }
+        st_shared_v4(s_qp + c * kRowsLS + kk * G * 16, w[0], w[1], w[2], w[3]);
+      }
+    }
+    __syncwarp();
+    const uint2 *bnd_in = pass > 0 ? p.bnd + ((size_t)k * 2 + ((pass - 1) & 1)) * p.ncq : nullptr;
+    uint2 *bnd_out = pass + 1 < npass ? p.bnd + ((size_t)k * 2 + (pass & 1)) * p.ncq : nullptr;
+    uint32_t *scc = p.sc + (size_t)k * p.ncq;
+    const int *prog_in = pass > 0 ? p.progress + (u - 1) : nullptr;
+    int avail = 0;
+    uint32_t H[R], E[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) { H[r] = kB2; E[r] = kB2; }
+    uint32_t S = 0u, hprev = kB2, kneg = 0u, final_sc = 0u;
+    uint32_t w0 = nul.w0, ngoe = nul.ngoe, nge = nul.nge, knext = nul.kneg;
+    uint32_t hout = kB2, fout = kB2, sc = 0u;
+    const int ncq = p.ncq, m = p.m;
+    auto letter = [&](int col) -> int { return col < m ? (int)__ldg(p.query + col) : (col == m ? kEnd : kNul); };
+    if (last) {   // lane 0's first column (0), handed over by the first shuffle
+      if (prog_in) {
+        while ((avail = ld_acquire(prog_in)) < 1) __nanosleep(100);
+      }
+      const DescWords d = load_desc(sbase + letter(0) * 16);
+      w0 = d.w0; ngoe = d.ngoe; nge = d.nge; knext = d.kneg;
+      const uint2 b0 = bnd_in ? ld_cg_v2(bnd_in) : make_uint2(kB2, kB2);
+      hout = b0.x;
+      fout = b0.y;
+      sc = pass > 0 ? ld_cg(scc) : 0u;
+    }
+    const int nsteps = ncq + G - 1;
+    for (int s = 0; s < nsteps; ++s) {
+      w0 = __shfl_sync(0xffffffffu, w0, src);
+      ngoe = __shfl_sync(0xffffffffu, ngoe, src);
+      nge = __shfl_sync(0xffffffffu, nge, src);
+      knext = __shfl_sync(0xffffffffu, knext, src);
+      const uint32_t hu = __shfl_sync(0xffffffffu, hout, src);
+      uint32_t F = __shfl_sync(0xffffffffu, fout, src);
+      const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
+      const uint32_t kneg_prev = kneg;
+      kneg = knext;
+      // lane 31: lane 0's next column (s + 1): wait for pass p-1 to have written it
+      uint2 bnext = make_uint2(bdef, bdef);
+      uint32_t scnext = 0u;
+      int cnext = kNul;
+      if (last) {
+        const int cn = s + 1;
+        if (cn < ncq) {
+          cnext = letter(cn);
+          if (prog_in) {
+            const int need = min(ncq, cn + 1);
+            while (avail < need) {
+              avail = ld_acquire(prog_in);
+              if (avail < need) __nanosleep(64);
+            }
+            bnext = ld_cg_v2(bnd_in + cn);
+            scnext = ld_cg(scc + cn);
+          } else {
+            bnext = make_uint2(kB2, kB2);
+          }
+        }
+      }
+      uint32_t hd = hprev;
+      hprev = hu;
+      const uint32_t aA = imad(w0, 16u, s_qp);
+      uint4 ca = lds128(aA);
+      uint32_t tcur = imad(hd, one, ca.x);
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        uint4 na = make_uint4(0u, 0u, 0u, 0u);
+        if (kk + 1 < KC) na = lds128(aA + (kk + 1) * G * 16);
+        const uint32_t av[8] = {ca.x, ca.y, ca.z, ca.w, na.x, na.y, na.z, na.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = kk * 4 + j;
+          uint32_t tnext = 0u;
+          if (r + 1 < R) tnext = imad(H[r], one, av[j + 1]);
+          const uint32_t h = hmax3(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
+          H[r] = h;
+          const uint32_t hg = haddmax(h, ngoe, kB2);  // max(H-Goe, 0)
+          E[r] = haddmax(E[r], nge, hg);              // Eq. 2 (along the query)
+          F = haddmax(F, nge, hg);                    // Eq. 3 (along the database sequence)
+          tcur = tnext;
+        }
+        ca = na;
+      }
+      S = haddmax(S, kneg_prev, H[0]);
+#pragma unroll
+      for (int r = 1; r + 1 < R; r += 2) S = hmax3(S, H[r], H[r + 1]);
+      if ((R & 1) == 0) S = hmax(S, H[R - 1]);
+      const uint32_t so = hmax(sc_in, S);
+      if (last) {
+        const int col = s - (G - 1);
+        if (col >= 0) {
+          st_global_u32(scc + col, so);
+          if (bnd_out) st_global_v2(bnd_out + col, H[R - 1], F);
+          if (col == m) final_sc = so;
+          if (((col + 1) & (kRowsPublish - 1)) == 0 || col + 1 == ncq)
+            st_release(p.progress + u, col + 1);
+        }
+        const DescWords d = load_desc(sbase + cnext * 16);
+        w0 = d.w0; ngoe = d.ngoe; nge = d.nge; knext = d.kneg;
+      }
+      hout = imad(H[R - 1], nlast, bnext.x);
+      fout = imad(F, nlast, bnext.y);
+      sc = imad(so, nlast, scnext);
+    }
+    // the pair's scores (chain at the END column after the last pass) into the
+    // END columns of its sequences in the stream image
+    if (last && pass + 1 == npass) {
+      st_global_u32(p.sc_out + (p.endcol[sA] >> 1), final_sc);
+      if (sB >= 0) st_global_u32(p.sc_out + (p.endcol[sB] >> 1), final_sc);
+    }
+    __syncwarp();
+  }
 }
 
 // Scores of one pass from the per-column score chain: the value at a
@@ -1509,6 +1706,21 @@ cudaError_t launch_scatter_scores(const int32_t *src, const int64_t *index, int6
   if (n <= 0) return cudaSuccess;
   ++g_launches;
   scatter_scores_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, st>>>(src, index, n, dst, dst_count);
+  return cudaGetLastError();
+}
+
+size_t rows_smem_bytes() { return (size_t)kRowsHeadBytes + (size_t)kRowsWarps * kNL * kRowsLS; }
+
+cudaError_t launch_sw16_rows(int grid, const RowsParams &p, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(sw16_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)rows_smem_bytes());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  ++g_launches;
+  sw16_rows_kernel<<<grid, kRowsWarps * 32, rows_smem_bytes(), st>>>(p);
   return cudaGetLastError();
 }
 

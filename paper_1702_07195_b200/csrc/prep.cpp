@@ -62,7 +62,8 @@ inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 }  // namespace
 
 int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
-                int64_t target_groups, bool single, HostImage &out, std::string &err, int64_t item_cap) {
+                int64_t target_groups, bool single, HostImage &out, std::string &err, int64_t item_cap,
+                int64_t long_min) {
   out = HostImage();
   std::vector<int64_t> len(count);
   int64_t total_stream = 0;
@@ -104,6 +105,24 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
   struct Tmp { int64_t ncols; int64_t slot0; int32_t nA, nB; };
   std::vector<Tmp> tmp;
   out.slots.reserve(count);
+  // Long sequences (>= long_min residues, sequence-pair image only): items of
+  // exactly one sequence per half, consecutive in length order, first in the
+  // claim order.  They are the rows-mode pairs: a search may
+  // score them with the sequence along the rows and skip their items.
+  if (!single && long_min > 0) {
+    while (lo <= hi && len[order[lo]] >= long_min) {
+      halfA.assign(1, order[lo++]);
+      halfB.clear();
+      if (lo <= hi && len[order[lo]] >= long_min) halfB.push_back(order[lo++]);
+      const int64_t lA = len[halfA[0]] + 2, lB = halfB.empty() ? 0 : len[halfB[0]] + 2;
+      const int64_t ncols = round_up(std::max(lA, lB), kColAlign);
+      tmp.push_back(Tmp{ncols, (int64_t)out.slots.size(), 1, (int32_t)halfB.size()});
+      for (int32_t s : halfA) out.slots.push_back(s);
+      for (int32_t s : halfB) out.slots.push_back(s);
+      remaining = std::max<int64_t>(0, remaining - (lA + lB + 1) / 2);
+      ++out.n_long_items;
+    }
+  }
   while (lo <= hi) {
     int64_t cap = (int64_t)((double)remaining / ((double)target_groups * item_div));
     cap = std::max<int64_t>(item_min, std::min<int64_t>(item_max, cap));
@@ -143,7 +162,8 @@ int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
   // claim order: longest item first (stable)
   std::vector<int32_t> iorder(tmp.size());
   std::iota(iorder.begin(), iorder.end(), 0);
-  std::stable_sort(iorder.begin(), iorder.end(),
+  // the long items stay first (and in length order); the rest longest first
+  std::stable_sort(iorder.begin() + out.n_long_items, iorder.end(),
                    [&](int32_t a, int32_t b) { return tmp[a].ncols > tmp[b].ncols; });
   int64_t col = kItemPad;
   out.items.resize(tmp.size());

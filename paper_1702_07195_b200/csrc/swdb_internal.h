@@ -54,6 +54,7 @@ struct HostImage {
   std::vector<int32_t> item_of;   // per original sequence: its work item
   int64_t total_cols = 0;
   int64_t max_len = 0;
+  int32_t n_long_items = 0;       // leading items holding one long sequence per half (rows mode)
 };
 
 // Pre-processing stage: validated input -> stream image.
@@ -63,8 +64,11 @@ struct HostImage {
 // single = true: one sequence per column in both halves (query pairs).
 // item_cap > 0: upper bound on the columns of a work item (streamed databases:
 // a chunk is processed per launch and must hold several items per group).
+// long_min > 0 (sequence-pair image): sequences of >= long_min residues get
+// items of one sequence per half, first in the claim order (n_long_items).
 int build_image(const uint8_t *residues, const int64_t *offsets, int64_t count,
-                int64_t target_groups, bool single, HostImage &out, std::string &err, int64_t item_cap = 0);
+                int64_t target_groups, bool single, HostImage &out, std::string &err, int64_t item_cap = 0,
+                int64_t long_min = 0);
 
 // Validation of the raw database (codes < 24, offsets monotone).
 int validate_db(const uint8_t *residues, const int64_t *offsets, int64_t count, std::string &err);

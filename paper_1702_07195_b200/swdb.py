@@ -21,7 +21,7 @@ _NAMES = {SW_EINVAL: "SW_EINVAL", SW_ENOMEM: "SW_ENOMEM", SW_ECUDA: "SW_ECUDA",
 
 EXPORTS = ["sw_db_load", "sw_db_load_streamed", "sw_db_chunks", "sw_db_free", "sw_db_count", "sw_db_residues", "sw_search",
            "sw_search_dev", "sw_search_batch", "sw_search_batch_dev", "sw_topk", "sw_topk_dev", "sw_scatter_dev", "sw_last_stats", "sw_last_timing", "sw_set_tile",
-           "sw_tile_supported", "sw_set_wave", "sw_set_latency_mode", "sw_set_profile", "sw_last_error", "sw_version", "sw_launch_count"]
+           "sw_tile_supported", "sw_set_wave", "sw_set_latency_mode", "sw_set_profile", "sw_set_rows_mode", "sw_last_error", "sw_version", "sw_launch_count"]
 
 
 class SWError(RuntimeError):
@@ -68,6 +68,7 @@ def load_library():
         "sw_set_wave": (ctypes.c_int, [i32]),
         "sw_set_latency_mode": (ctypes.c_int, [i32]),
         "sw_set_profile": (ctypes.c_int, [i32]),
+        "sw_set_rows_mode": (ctypes.c_int, [i32]),
         "sw_last_error": (ctypes.c_char_p, []),
         "sw_version": (ctypes.c_char_p, []),
         "sw_launch_count": (i64, []),
@@ -227,10 +228,10 @@ def sw_scatter_dev(d_src, d_index, n: int, d_dst, dst_count: int, stream=None) -
 
 
 def sw_last_stats() -> dict:
-    a = np.zeros(13, dtype=np.int64)
-    _check(load_library().sw_last_stats(_ptr(a), 13))
+    a = np.zeros(14, dtype=np.int64)
+    _check(load_library().sw_last_stats(_ptr(a), 14))
     keys = ["rows_per_pass", "passes", "G", "R", "flagged", "cells32", "pair_columns", "items",
-            "flag_threshold", "arith", "wave", "lat", "profile"]
+            "flag_threshold", "arith", "wave", "lat", "profile", "rows_pairs"]
     return {k: int(v) for k, v in zip(keys, a)}
 
 
@@ -252,6 +253,11 @@ def sw_set_wave(mode: int) -> None:
 def sw_set_latency_mode(mode: int) -> None:
     """Low-latency (LAT) tiles: 0 auto (default), 1 always, -1 never (swdb.h)."""
     _check(load_library().sw_set_latency_mode(int(mode)))
+
+
+def sw_set_rows_mode(mode: int) -> None:
+    """Rows mode for the long sequences: 0 auto (default), 1 whenever possible, -1 never (swdb.h)."""
+    _check(load_library().sw_set_rows_mode(int(mode)))
 
 
 def sw_set_profile(mode: int) -> None:

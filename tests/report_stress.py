@@ -77,6 +77,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=600)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--trials", type=int, default=0, help="stop after this many trials (0: time only)")
+    ap.add_argument("--verbose", action="store_true", help="print every trial's parameters before running it")
     args = ap.parse_args()
     import torch
     torch.cuda.set_device(0)
@@ -85,7 +87,7 @@ def main():
              if sw.sw_tile_supported(G, R) or sw.sw_tile_supported(G, R, lat=True) or sw.sw_tile_supported(G, R, sp=True)]
     t_end = time.time() + args.seconds
     trials = fails = cells = 0
-    while time.time() < t_end:
+    while time.time() < t_end and (args.trials == 0 or trials < args.trials):
         trials += 1
         db, alpha = draw_db(rng)
         mname, M = draw_matrix(rng)
@@ -103,6 +105,10 @@ def main():
         sw.sw_set_latency_mode(lat)
         prof = int(rng.choice([0, 1, 2]))       # substitution scores: auto / query profile / score profile
         sw.sw_set_profile(prof)
+        if args.verbose:
+            print(json.dumps({"trial": trials, "count": db.count, "max_len": int(db.lengths().max(initial=0)),
+                              "alpha": alpha, "matrix": mname, "gaps": [go, ge], "m": m, "path": path,
+                              "tile": tile, "wave": wave, "lat": lat, "profile": prof}), flush=True)
         try:
             if path == "streamed":
                 sw.sw_db_load_streamed(db.residues, db.offsets, int(rng.integers(1, 64)) * 4096)
@@ -136,7 +142,10 @@ def main():
             fails += 0 if ok else 1
         except sw.SWError as e:
             fails += 1
-            print(json.dumps({"trial": trials, "path": path, "error": str(e)}), flush=True)
+            print(json.dumps({"trial": trials, "path": path, "tile": tile, "wave": wave, "lat": lat, "profile": prof,
+                              "m": m, "count": db.count, "error": str(e)}), flush=True)
+            if e.code == sw.SW_ECUDA:   # a device fault is sticky: stop at the first one
+                break
     sw.sw_set_tile(0)
     sw.sw_set_wave(0)
     sw.sw_set_latency_mode(0)

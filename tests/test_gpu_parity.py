@@ -600,3 +600,50 @@ def test_score_profile_tiles_are_exact():
     finally:
         sw.sw_set_tile(0)
         sw.sw_set_profile(0)
+
+
+def test_rows_mode_matches_oracle():
+    """Rows mode: the long sequences of a database (one per half
+    of the leading items) scored with the sequence along the rows and the query
+    as the column stream, passes as a wavefront.  Forced and automatic, random
+    and asymmetric matrices, zero gap-open, sequences of odd count (an empty
+    half), saturating sequences (flag, carry propagation, 32-bit re-scoring),
+    query lengths around the stream's 4-column rounding."""
+    rng = np.random.default_rng(2048)
+    longs = [si.rr_residues(rng, int(L)) for L in rng.integers(600, 9000, 11)]
+    longs += [encode("W" * 3100), encode("W" * 2990 + "A" * 20)]
+    shorts = [si.rr_residues(rng, int(L)) for L in rng.integers(0, 200, 300)]
+    db = _db(longs + shorts)
+    sw.sw_db_load(db.residues, db.offsets)
+    try:
+        for mode in (1, 0):
+            sw.sw_set_rows_mode(mode)
+            for trial, m in enumerate((1, 2, 3, 4, 5, 37, 144, 299)):
+                q = rng.integers(0, 24, m).astype(np.uint8) if trial % 3 else si.rr_residues(rng, m)
+                M = (BLOSUM62, si.random_symmetric_matrix(rng), rng.integers(-6, 12, (24, 24)).astype(np.int8))[trial % 3]
+                go, ge = ((10, 2), (0, 1), (int(rng.integers(0, 16)), int(rng.integers(0, 6))))[trial % 3]
+                got = sw.sw_search(q, M, go, ge)
+                st = sw.sw_last_stats()
+                exp = oracle.batch(q, db.residues, db.offsets, M, go, ge)
+                bad = np.nonzero(got != exp)[0]
+                assert bad.size == 0, (mode, m, bad[:5], got[bad[:5]], exp[bad[:5]])
+                assert st["rows_pairs"] > 0, (mode, m, st)
+        # saturating: the W runs score 34,100 / 32,890 against a W query
+        sw.sw_set_rows_mode(1)
+        q = encode("W" * 3200)
+        got = sw.sw_search(q, BLOSUM62, 10, 2)
+        st = sw.sw_last_stats()
+        exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
+        assert (got == exp).all() and _flags_ok(st, exp) and st["flagged"] >= 2
+        # configs[0]: the automatic choice uses rows mode for its long sequences
+        sw.sw_set_rows_mode(0)
+        w = si.config0()
+        sw.sw_db_load(w.db.residues, w.db.offsets)
+        got = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
+        assert sw.sw_last_stats()["rows_pairs"] > 0
+        assert (got == oracle.batch(w.queries[0], w.db.residues, w.db.offsets, BLOSUM62, 10, 2)).all()
+        sw.sw_set_rows_mode(-1)
+        got2 = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
+        assert sw.sw_last_stats()["rows_pairs"] == 0 and (got2 == got).all()
+    finally:
+        sw.sw_set_rows_mode(0)
