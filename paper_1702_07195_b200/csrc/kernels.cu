@@ -1684,9 +1684,10 @@ cudaError_t launch_bitonic_sort_desc(uint64_t *keys, int64_t npow2, cudaStream_t
       ++g_launches;
       bitonic_local_kernel<<<(unsigned)(npow2 / 2048), 1024, 0, st>>>(keys, size, stride);
     } else {
-      for (; stride > 0; stride >>= 1)
+      for (; stride > 0; stride >>= 1) {
         ++g_launches;
         bitonic_step_kernel<<<grid_for(npow2 / 2, 256), 256, 0, st>>>(keys, npow2, size, stride);
+      }
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -79,6 +79,9 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--trials", type=int, default=0, help="stop after this many trials (0: time only)")
     ap.add_argument("--verbose", action="store_true", help="print every trial's parameters before running it")
+    ap.add_argument("--only", type=int, default=0, help="draw every trial but run only this one")
+    ap.add_argument("--start", type=int, default=0, help="draw every trial but run only trials >= start")
+    ap.add_argument("--dump", default="", help="with --only: save the trial's inputs to this .npz")
     args = ap.parse_args()
     import torch
     torch.cuda.set_device(0)
@@ -97,6 +100,9 @@ def main():
         if rng.random() < 0.2:
             q[: min(m, 3000)] = 17                       # W-rich query: saturating scores
         path = ["single", "single", "pair", "streamed"][int(rng.integers(0, 4))]
+        chunk = int(rng.integers(1, 64)) * 4096
+        q2 = rng.integers(0, alpha, int(rng.integers(1, 3500))).astype(np.uint8)
+        k = int(min(db.count, rng.integers(1, 40) if rng.random() < 0.7 else rng.integers(33, 200)))
         tile = (0, 0) if rng.random() < 0.5 else tiles[int(rng.integers(0, len(tiles)))]
         sw.sw_set_tile(*tile)
         wave = int(rng.choice([-1, 0, 1, 1]))   # cross-pass wavefront off / auto / forced
@@ -105,17 +111,21 @@ def main():
         sw.sw_set_latency_mode(lat)
         prof = int(rng.choice([0, 1, 2]))       # substitution scores: auto / query profile / score profile
         sw.sw_set_profile(prof)
+        if (args.only and trials != args.only) or trials < args.start:
+            continue
+        if args.dump:
+            np.savez(args.dump, res=db.residues, offs=db.offsets, q=q, q2=q2, M=M, go=go, ge=ge, path=path,
+                     tile=np.array(tile), wave=wave, lat=lat, prof=prof, chunk=chunk, k=k)
         if args.verbose:
             print(json.dumps({"trial": trials, "count": db.count, "max_len": int(db.lengths().max(initial=0)),
                               "alpha": alpha, "matrix": mname, "gaps": [go, ge], "m": m, "path": path,
                               "tile": tile, "wave": wave, "lat": lat, "profile": prof}), flush=True)
         try:
             if path == "streamed":
-                sw.sw_db_load_streamed(db.residues, db.offsets, int(rng.integers(1, 64)) * 4096)
+                sw.sw_db_load_streamed(db.residues, db.offsets, chunk)
             else:
                 sw.sw_db_load(db.residues, db.offsets)
             if path == "pair":
-                q2 = rng.integers(0, alpha, int(rng.integers(1, 3500))).astype(np.uint8)
                 got = sw.sw_search_batch([q, q2], M, go, ge)
                 outs = [(q, got[0]), (q2, got[1])]
             else:
@@ -133,7 +143,6 @@ def main():
                                       "first": bad[:5].tolist(), "got": g[bad[:5]].tolist(),
                                       "exp": exp[bad[:5]].tolist()}), flush=True)
             if ok and path != "pair":
-                k = int(min(db.count, rng.integers(1, 40) if rng.random() < 0.7 else rng.integers(33, 200)))
                 idx, sc = sw.sw_topk(k)
                 eidx, esc = oracle.topk(outs[0][1], k)
                 if not ((idx == eidx).all() and (sc == esc).all()):

@@ -205,3 +205,19 @@ def test_topk_on_config2_scores():
         idx, sc = sw.sw_topk(k)
         ei, es = oracle.topk(got, k)
         assert np.array_equal(idx, ei) and np.array_equal(sc, es), k
+
+
+@pytest.mark.parametrize("n", [2, 5, 100, 195, 1000, 2047, 2048, 5000])
+def test_topk_full_sort_small_n(n):
+    """The sorting stage's full bitonic path (k > n/4) for every size class:
+    n < 2048 runs only global step kernels (a regression of round 2: the
+    launch counter had put a step launch outside its loop)."""
+    rng = np.random.default_rng(n)
+    x = rng.integers(-3, 40, n).astype(np.int32)
+    d = torch.from_numpy(x).cuda()
+    for k in sorted({min(n, 33), n // 2 + 1, n}):
+        ti = torch.empty(k, dtype=torch.int64, device="cuda")
+        ts = torch.empty(k, dtype=torch.int32, device="cuda")
+        assert sw.sw_topk_dev(d, None, n, k, ti, ts) == k
+        ei, es = oracle.topk(x, k)
+        assert np.array_equal(ti.cpu().numpy(), ei) and np.array_equal(ts.cpu().numpy(), es), (n, k)
