@@ -369,9 +369,9 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   int ti = choose_tile(mm, mode, rows_cand ? Iv : I);
   if (ti < 0) return fail(SW_ECUDA, "no runnable kernel tile");
   // rows mode needs a single pass of the pass kernel; otherwise the ordinary choice
-  const bool rowsm = rows_cand && passes_of(ti) == 1;
-  if (rows_cand && !rowsm) ti = choose_tile(mm, mode, I);
-  const Image &Im = rowsm ? Iv : I;   // what the latency model sees
+  const bool rows_ok = rows_cand && passes_of(ti) == 1;
+  if (rows_cand && !rows_ok) ti = choose_tile(mm, mode, I);
+  const Image &Im = rows_ok ? Iv : I;   // what the latency model sees
   // Cross-pass wavefront (one launch runs every pass).  A pass
   // of the per-pass path keeps at most one lane group per work item busy; with
   // far fewer items than groups (a database of few, long sequences) the
@@ -383,7 +383,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // tiles when their units exceed half the groups.  Forced mode (1) uses the
   // forced or chosen tile when it has a wavefront kernel, else 32x16 / 32x8.
   bool wave = false;
-  if (!pair && !use_sp && !g.streamed && !rowsm && g.wave_mode >= 0) {
+  if (!pair && !use_sp && !g.streamed && !rows_ok && g.wave_mode >= 0) {
     const int t8 = find_tile_mode(32, 8, 0), t16 = find_tile_mode(32, 16, 0);
     const double items = (double)std::max(1, I.num_items);
     int tw = -1;
@@ -417,7 +417,6 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     } else {
       tl = choose_lat_tile(mm, Im, ti, g.lat_mode == 1);
     }
-    if (tl >= 0 && rowsm && passes_of(tl) != 1) tl = -1;   // rows mode keeps a single pass
     if (tl >= 0) {
       ti = tl;
       lat = true;
@@ -427,6 +426,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int rows = T.G * T.R;
   const int P = (mm + rows - 1) / rows;
   if (P > kMaxPass) return fail(SW_EINVAL, "query too long");
+  const bool rowsm = rows_ok && !wave && P == 1;   // (a forced multi-pass latency tile turns it off)
   int smax = 1;
   for (int i = 0; i < kAlpha * kAlpha; ++i) smax = std::max(smax, (int)matrix[i]);
   const int thresh = kHalfTop - smax;   // stored 16-bit units (R7)
