@@ -731,20 +731,47 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
     uint32_t w0 = nul.w0, ngoe = nul.ngoe, nge = nul.nge, knext = nul.kneg;
     uint32_t hout = kB2, fout = kB2, sc = 0u;
     const int ncq = p.ncq, m = p.m;
-    auto letter = [&](int col) -> int { return col < m ? (int)__ldg(p.query + col) : (col == m ? kEnd : kNul); };
-    if (last) {   // lane 0's first column (0), handed over by the first shuffle
-      if (prog_in) {
-        while ((avail = ld_acquire(prog_in)) < 1) __nanosleep(100);
+    // Lane 31 feeds lane 0 from a ring of the next kRowsAhead columns (query
+    // letter, previous pass's boundary and chain value), loaded kRowsAhead
+    // steps before use: no global-load latency on the per-column chain.
+    int rl[kRowsAhead];
+    uint2 rb[kRowsAhead];
+    uint32_t rs[kRowsAhead];
+    auto fetch = [&](int col, int &l, uint2 &b, uint32_t &c) {
+      l = kNul;
+      b = make_uint2(kB2, kB2);
+      c = 0u;
+      if (col < ncq) {
+        l = col < m ? (int)__ldg(p.query + col) : (col == m ? kEnd : kNul);
+        if (prog_in) {
+          const int need = col + 1;
+          while (avail < need) {
+            avail = ld_acquire(prog_in);
+            if (avail < need) __nanosleep(32);
+          }
+          b = ld_cg_v2(bnd_in + col);
+          c = ld_cg(scc + col);
+        }
       }
-      const DescWords d = load_desc(sbase + letter(0) * 16);
+    };
+    if (last) {
+#pragma unroll
+      for (int j = 0; j < kRowsAhead; ++j) fetch(j + 1, rl[j], rb[j], rs[j]);   // ring slot j: column s + 1 + j
+      int l0;
+      uint2 b0;
+      uint32_t c0;
+      fetch(0, l0, b0, c0);                 // lane 0's first column, handed over by the first shuffle
+      const DescWords d = load_desc(sbase + l0 * 16);
       w0 = d.w0; ngoe = d.ngoe; nge = d.nge; knext = d.kneg;
-      const uint2 b0 = bnd_in ? ld_cg_v2(bnd_in) : make_uint2(kB2, kB2);
       hout = b0.x;
       fout = b0.y;
-      sc = pass > 0 ? ld_cg(scc) : 0u;
+      sc = c0;
     }
     const int nsteps = ncq + G - 1;
-    for (int s = 0; s < nsteps; ++s) {
+    for (int s0 = 0; s0 < nsteps; s0 += kRowsAhead) {
+#pragma unroll
+    for (int u = 0; u < kRowsAhead; ++u) {
+      const int s = s0 + u;
       w0 = __shfl_sync(0xffffffffu, w0, src);
       ngoe = __shfl_sync(0xffffffffu, ngoe, src);
       nge = __shfl_sync(0xffffffffu, nge, src);
@@ -754,26 +781,15 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
       const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
       const uint32_t kneg_prev = kneg;
       kneg = knext;
-      // lane 31: lane 0's next column (s + 1): wait for pass p-1 to have written it
+      // lane 31: lane 0's next column (s + 1) from the ring; refill the slot with column s + 1 + kRowsAhead
       uint2 bnext = make_uint2(bdef, bdef);
       uint32_t scnext = 0u;
       int cnext = kNul;
-      if (last) {
-        const int cn = s + 1;
-        if (cn < ncq) {
-          cnext = letter(cn);
-          if (prog_in) {
-            const int need = min(ncq, cn + 1);
-            while (avail < need) {
-              avail = ld_acquire(prog_in);
-              if (avail < need) __nanosleep(64);
-            }
-            bnext = ld_cg_v2(bnd_in + cn);
-            scnext = ld_cg(scc + cn);
-          } else {
-            bnext = make_uint2(kB2, kB2);
-          }
-        }
+      if (last) {   // slot u holds column s + 1; refill it with column s + 1 + kRowsAhead
+        cnext = rl[u];
+        bnext = rb[u];
+        scnext = rs[u];
+        fetch(s + 1 + kRowsAhead, rl[u], rb[u], rs[u]);
       }
       uint32_t hd = hprev;
       hprev = hu;
@@ -806,12 +822,12 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
       const uint32_t so = hmax(sc_in, S);
       if (last) {
         const int col = s - (G - 1);
-        if (col >= 0) {
+        if (col >= 0 && col < ncq) {
           st_global_u32(scc + col, so);
           if (bnd_out) st_global_v2(bnd_out + col, H[R - 1], F);
           if (col == m) final_sc = so;
-          if (((col + 1) & (kRowsPublish - 1)) == 0 || col + 1 == ncq)
-            st_release(p.progress + u, col + 1);
+          // a release store waits for the earlier stores: publish every kRowsPublish columns
+          if (((col + 1) & (kRowsPublish - 1)) == 0 || col + 1 == ncq) st_release(p.progress + u, col + 1);
         }
         const DescWords d = load_desc(sbase + cnext * 16);
         w0 = d.w0; ngoe = d.ngoe; nge = d.nge; knext = d.kneg;
@@ -819,6 +835,7 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
       hout = imad(H[R - 1], nlast, bnext.x);
       fout = imad(F, nlast, bnext.y);
       sc = imad(so, nlast, scnext);
+    }
     }
     // the pair's scores (chain at the END column after the last pass) into the
     // END columns of its sequences in the stream image

@@ -98,7 +98,8 @@ struct SW16Params {
 // Rows mode (long database sequences along the rows, kernels.cu).
 constexpr int kRowsR = 8;                           // rows per lane (one 32-lane group per warp)
 constexpr int kRowsWarps = 8;                       // warps per CTA (one CTA per SM)
-constexpr int kRowsPublish = 8;                     // columns between progress publications
+constexpr int kRowsPublish = 16;                    // columns between progress publications
+constexpr int kRowsAhead = 8;                       // lane 31's prefetch distance (columns)
 constexpr int kRowsLS = (kRowsR / 4) * 32 * 16;     // profile bytes per query letter of a warp
 constexpr int kRowsHeadBytes = 26 * 16 + 26 * 26 * 4 + 16;   // descriptors + matrix (+ pad to 16 B)
 constexpr int kRowsRows = 32 * kRowsR;              // database rows per pass
