@@ -745,9 +745,24 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
         l = col < m ? (int)__ldg(p.query + col) : (col == m ? kEnd : kNul);
         if (prog_in) {
           const int need = col + 1;
+#if SW_DEBUG
+          long long spins = 0;
+#endif
           while (avail < need) {
             avail = ld_acquire(prog_in);
             if (avail < need) __nanosleep(32);
+#if SW_DEBUG
+            if (++spins == (1ll << 24)) {
+              printf("rows kernel stuck: unit %d (item %d pass %d) waits for column %d of unit %d, has %d (ncq %d); "
+                     "progress[0..3] %d %d %d %d, counter %d, n_units %d, units[0..2] (%d,%d) (%d,%d) (%d,%d), "
+                     "prev unit (%d,%d)\n",
+                     u, k, pass, need, u - 1, avail, ncq, ld_acquire(p.progress), ld_acquire(p.progress + 1),
+                     ld_acquire(p.progress + 2), ld_acquire(p.progress + 3), ld_acquire(p.counter), p.n_units,
+                     p.units[0].x, p.units[0].y, p.units[1].x, p.units[1].y, p.units[2].x, p.units[2].y,
+                     p.units[u - 1].x, p.units[u - 1].y);
+              __trap();
+            }
+#endif
           }
           b = ld_cg_v2(bnd_in + col);
           c = ld_cg(scc + col);
@@ -770,8 +785,8 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
     const int nsteps = ncq + G - 1;
     for (int s0 = 0; s0 < nsteps; s0 += kRowsAhead) {
 #pragma unroll
-    for (int u = 0; u < kRowsAhead; ++u) {
-      const int s = s0 + u;
+    for (int v = 0; v < kRowsAhead; ++v) {   // (v, not u: u is the unit)
+      const int s = s0 + v;
       w0 = __shfl_sync(0xffffffffu, w0, src);
       ngoe = __shfl_sync(0xffffffffu, ngoe, src);
       nge = __shfl_sync(0xffffffffu, nge, src);
@@ -785,11 +800,11 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
       uint2 bnext = make_uint2(bdef, bdef);
       uint32_t scnext = 0u;
       int cnext = kNul;
-      if (last) {   // slot u holds column s + 1; refill it with column s + 1 + kRowsAhead
-        cnext = rl[u];
-        bnext = rb[u];
-        scnext = rs[u];
-        fetch(s + 1 + kRowsAhead, rl[u], rb[u], rs[u]);
+      if (last) {   // slot v holds column s + 1; refill it with column s + 1 + kRowsAhead
+        cnext = rl[v];
+        bnext = rb[v];
+        scnext = rs[v];
+        fetch(s + 1 + kRowsAhead, rl[v], rb[v], rs[v]);
       }
       uint32_t hd = hprev;
       hprev = hu;
