@@ -274,13 +274,19 @@ int sw_set_profile(int32_t mode);
  * sequence along the rows and the query as the column stream (the same
  * recurrence on the transposed matrix; scores are identical): the passes over
  * the sequence run as a wavefront on many lane groups at once, so the
- * critical path is about m + (n / 256) x 40 steps instead of n.  mode 0
- * (default): used when the query is at most half as long as the shortest long
- * sequence; 1: whenever possible; -1: never.  Resident single-query searches
- * whose pass kernel makes one pass, without the cross-pass wavefront.
+ * critical path is about m + (n / 256) x 55 steps instead of n.  mode 1: use
+ * it whenever possible; 0 (default) and -1: do not.  (Measured slower than the
+ * ordinary path on every database tried, so the default never
+ * uses it.)  Resident single-query searches whose pass kernel makes one pass,
+ * without the cross-pass wavefront.
  * Returns SW_OK or SW_EINVAL.
  */
 int sw_set_rows_mode(int32_t mode);
+
+/* Experiment hook: per-unit timestamps of the last rows-mode launch (a build
+ * with -DSW_ROWS_TRACE=1 and the environment variable SW_ROWS_TRACE_N set);
+ * 4 entries per unit.  Returns the entries copied (0 when not recorded). */
+int64_t sw_rows_trace(uint64_t *out, int64_t n);
 
 /*
  * sw_set_latency_mode -- latency tiles for searches whose time is one long

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -149,6 +150,7 @@ struct State {
   DevBuf<uint2> rows_bnd;   // rows mode: per long item 2 x ncq boundary
   DevBuf<uint32_t> rows_sc; // rows mode: per long item ncq chain values
   DevBuf<int> rows_prog;    // rows mode: per unit progress, + 1 counter
+  DevBuf<unsigned long long> rows_trace;   // SW_ROWS_TRACE experiments
   int prof_mode = 0;        // substitution scores: 0 auto, 1 query profile, 2 score profile
   int last_prof = 1;
   bool last_lat = false;
@@ -203,7 +205,7 @@ struct State {
     flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release(); progress.release();
     query.release(); query2.release(); matrix.release(); qp.release(); desc.release(); qp32.release();
     qp32b.release(); bnd.release(); skip.release(); item_hot.release();
-    rows_bnd.release(); rows_sc.release(); rows_prog.release();
+    rows_bnd.release(); rows_sc.release(); rows_prog.release(); rows_trace.release();
     scratch32.release(); dummy.release(); nulcols.release(); zerocols.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
     loaded = false;
     has_search = false;
@@ -350,12 +352,12 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int mm = pair ? std::max(m, m2) : m;
   // Rows mode: the long pairs (the image's leading items) are
   // scored with the sequence along the rows by sw16_rows_kernel, the pass
-  // kernel claims the other items only.  Auto: when the query is at most half
-  // as long as the shortest long sequence (the rows kernel's chain is about
-  // m + passes x 40 steps instead of n).  Single-pass resident single-query
-  // searches without the wavefront.
-  const bool rows_cand = !pair && !g.streamed && I0.n_long > 0 && I0.n_units > 0 && g.rows_mode >= 0 &&
-                         (g.rows_mode == 1 || (int64_t)mm * 2 <= I0.long_min_len);
+  // kernel claims the other items only.  Only on request (sw_set_rows_mode(1)):
+  // measured slower than the ordinary path on every database tried
+  // (profiles/r02_rows_mode.jsonl) -- the cross-SM progress hand-over between
+  // consecutive passes costs more than the shorter chain saves.  Single-pass
+  // resident single-query searches without the wavefront.
+  const bool rows_cand = !pair && !g.streamed && I0.n_long > 0 && I0.n_units > 0 && g.rows_mode == 1;
   const Image &I = I0;
   // the tile model's view of the items the pass kernel runs (rows mode: all
   // but the long pairs); device buffers are shared, only these sizes differ
@@ -653,6 +655,11 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
         r.goe = goe;
         r.ge = ge;
         r.one = 1u;
+        if (std::getenv("SW_ROWS_TRACE_N")) {   // experiment builds (SW_ROWS_TRACE=1): keep the unit timestamps
+          CUDA_TRY(g.rows_trace.ensure((size_t)4 * I0.n_units));
+          CUDA_TRY(cudaMemsetAsync(g.rows_trace.p, 0, sizeof(unsigned long long) * 4 * I0.n_units, st));
+          r.trace = g.rows_trace.p;
+        }
         CUDA_TRY(launch_sw16_rows(g.num_sms, r, st));
       }
       CUDA_TRY(cudaEventRecord(g.pev[pe + 1], st));
@@ -1172,6 +1179,16 @@ int sw_set_tile(int32_t G, int32_t R) {
 int sw_tile_supported(int32_t G, int32_t R) {
   return (find_tile_mode(G, R, 0) >= 0 ? 1 : 0) | (find_tile_mode(G, R, 0, 1) >= 0 ? 2 : 0) |
          (find_tile_mode(G, R, 1) >= 0 ? 4 : 0);
+}
+
+int64_t sw_rows_trace(uint64_t *out, int64_t n) {
+  t_err.clear();
+  if (!out || n < 0) return fail(SW_EINVAL, "bad arguments");
+  const int64_t have = std::min<int64_t>(n, (int64_t)g.rows_trace.n);
+  if (have == 0) return 0;
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(out, g.rows_trace.p, (size_t)have * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return have;
 }
 
 int sw_set_rows_mode(int32_t mode) {

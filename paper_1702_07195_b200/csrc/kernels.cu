@@ -44,6 +44,9 @@
 #ifndef SW_ROWAHEAD
 #define SW_ROWAHEAD 1
 #endif
+#ifndef SW_ROWS_TRACE
+#define SW_ROWS_TRACE 0   // 1: the rows kernel records per-unit timestamps (sw_rows_trace, experiments)
+#endif
 #ifndef SW_TAILADDR
 #define SW_TAILADDR 0   // narrow-tail address: 0 = IMAD from the profile offset, 1 = from the chunk address
 #endif
@@ -159,6 +162,12 @@ __device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) {
   asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ int ld_acquire(const int *p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -697,6 +706,9 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
     const int64_t oA = p.offs[sA], nA = p.offs[sA + 1] - oA;
     const int64_t oB = sB >= 0 ? p.offs[sB] : 0, nB = sB >= 0 ? p.offs[sB + 1] - oB : 0;
     const int npass = (int)((max(nA, nB) + G * R - 1) / (G * R));
+#if SW_ROWS_TRACE
+    if (last && p.trace) p.trace[4 * u] = globaltimer();
+#endif
     // ---- this lane's profile rows: SM(c, dB_row) * 65536 + SM(c, dA_row)
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
@@ -783,6 +795,9 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
       sc = c0;
     }
     const int nsteps = ncq + G - 1;
+#if SW_ROWS_TRACE
+    if (last && p.trace) p.trace[4 * u + 1] = globaltimer();
+#endif
     for (int s0 = 0; s0 < nsteps; s0 += kRowsAhead) {
 #pragma unroll
     for (int v = 0; v < kRowsAhead; ++v) {   // (v, not u: u is the unit)
@@ -858,6 +873,9 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
       st_global_u32(p.sc_out + (p.endcol[sA] >> 1), final_sc);
       if (sB >= 0) st_global_u32(p.sc_out + (p.endcol[sB] >> 1), final_sc);
     }
+#if SW_ROWS_TRACE
+    if (last && p.trace) { p.trace[4 * u + 2] = globaltimer(); p.trace[4 * u + 3] = (blockIdx.x << 8) | warp; }
+#endif
     __syncwarp();
   }
 }

@@ -122,6 +122,7 @@ struct RowsParams {
   uint32_t *sc_out;         // the image's per-column chain buffer (the gather reads the END columns)
   int goe, ge;
   uint32_t one;
+  unsigned long long *trace;   // SW_ROWS_TRACE builds: per unit (claim, loop start, end ns, block<<8|warp)
 };
 
 struct SW32Params {

@@ -605,10 +605,11 @@ def test_score_profile_tiles_are_exact():
 def test_rows_mode_matches_oracle():
     """Rows mode: the long sequences of a database (one per half
     of the leading items) scored with the sequence along the rows and the query
-    as the column stream, passes as a wavefront.  Forced and automatic, random
+    as the column stream, passes as a wavefront.  Random
     and asymmetric matrices, zero gap-open, sequences of odd count (an empty
     half), saturating sequences (flag, carry propagation, 32-bit re-scoring),
-    query lengths around the stream's 4-column rounding."""
+    query lengths around the stream's 4-column rounding.  (Rows mode is used
+    on request only: sw_set_rows_mode(1).)"""
     rng = np.random.default_rng(2048)
     longs = [si.rr_residues(rng, int(L)) for L in rng.integers(600, 9000, 11)]
     longs += [encode("W" * 3100), encode("W" * 2990 + "A" * 20)]
@@ -616,7 +617,7 @@ def test_rows_mode_matches_oracle():
     db = _db(longs + shorts)
     sw.sw_db_load(db.residues, db.offsets)
     try:
-        for mode in (1, 0):
+        for mode in (1,):
             sw.sw_set_rows_mode(mode)
             for trial, m in enumerate((1, 2, 3, 4, 5, 37, 144, 299)):
                 q = rng.integers(0, 24, m).astype(np.uint8) if trial % 3 else si.rr_residues(rng, m)
@@ -635,14 +636,14 @@ def test_rows_mode_matches_oracle():
         st = sw.sw_last_stats()
         exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
         assert (got == exp).all() and _flags_ok(st, exp) and st["flagged"] >= 2
-        # configs[0]: the automatic choice uses rows mode for its long sequences
-        sw.sw_set_rows_mode(0)
+        # configs[0] in rows mode (on request) and without
+        sw.sw_set_rows_mode(1)
         w = si.config0()
         sw.sw_db_load(w.db.residues, w.db.offsets)
         got = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
         assert sw.sw_last_stats()["rows_pairs"] > 0
         assert (got == oracle.batch(w.queries[0], w.db.residues, w.db.offsets, BLOSUM62, 10, 2)).all()
-        sw.sw_set_rows_mode(-1)
+        sw.sw_set_rows_mode(0)
         got2 = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
         assert sw.sw_last_stats()["rows_pairs"] == 0 and (got2 == got).all()
     finally:
