@@ -283,10 +283,7 @@ int sw_set_profile(int32_t mode);
  */
 int sw_set_rows_mode(int32_t mode);
 
-/* Experiment hook: per-unit timestamps of the last rows-mode launch (a build
- * with -DSW_ROWS_TRACE=1 and the environment variable SW_ROWS_TRACE_N set);
- * 4 entries per unit.  Returns the entries copied (0 when not recorded). */
-int64_t sw_rows_trace(uint64_t *out, int64_t n);
+
 
 /*
  * sw_set_latency_mode -- latency tiles for searches whose time is one long

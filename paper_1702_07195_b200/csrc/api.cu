@@ -147,10 +147,8 @@ struct State {
   int lat_mode = 0;         // latency tiles: 0 auto, 1 always, -1 never
   int rows_mode = 0;        // rows mode for the long items: 0 auto, 1 whenever possible, -1 never
   int64_t last_rows = 0;    // long pairs scored in rows mode by the last search
-  DevBuf<uint2> rows_bnd;   // rows mode: per long item 2 x ncq boundary
-  DevBuf<uint32_t> rows_sc; // rows mode: per long item ncq chain values
-  DevBuf<int> rows_prog;    // rows mode: per unit progress, + 1 counter
-  DevBuf<unsigned long long> rows_trace;   // SW_ROWS_TRACE experiments
+  DevBuf<uint4> rows_wrap;  // rows mode: per CTA one pass of (H, F, chain) (warp 7 -> warp 0)
+  DevBuf<int> rows_prog;    // rows mode: item counter
   int prof_mode = 0;        // substitution scores: 0 auto, 1 query profile, 2 score profile
   int last_prof = 1;
   bool last_lat = false;
@@ -205,7 +203,7 @@ struct State {
     flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release(); progress.release();
     query.release(); query2.release(); matrix.release(); qp.release(); desc.release(); qp32.release();
     qp32b.release(); bnd.release(); skip.release(); item_hot.release();
-    rows_bnd.release(); rows_sc.release(); rows_prog.release(); rows_trace.release();
+    rows_wrap.release(); rows_prog.release();
     scratch32.release(); dummy.release(); nulcols.release(); zerocols.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
     loaded = false;
     has_search = false;
@@ -537,10 +535,9 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     // the pass kernel starts claiming after the long items
     const int first = I0.n_long;
     CUDA_TRY(cudaMemcpyAsync(g.pcounters.p, &first, sizeof(int), cudaMemcpyHostToDevice, st));
-    CUDA_TRY(g.rows_bnd.ensure((size_t)I0.n_long * 2 * ncq));
-    CUDA_TRY(g.rows_sc.ensure((size_t)I0.n_long * ncq));
-    CUDA_TRY(g.rows_prog.ensure((size_t)I0.n_units + 1));
-    CUDA_TRY(cudaMemsetAsync(g.rows_prog.p, 0, sizeof(int) * ((size_t)I0.n_units + 1), st));
+    CUDA_TRY(g.rows_wrap.ensure((size_t)g.num_sms * ncq));
+    CUDA_TRY(g.rows_prog.ensure(1));
+    CUDA_TRY(cudaMemsetAsync(g.rows_prog.p, 0, sizeof(int), st));
   }
   if (P > 1 && g.bnd.n < (size_t)span * 2) CUDA_TRY(g.bnd.ensure((size_t)span * 2));
   if (!strm && !pair && P > 1) CUDA_TRY(g.skip.ensure((size_t)std::max(1, I.num_items)));
@@ -644,22 +641,14 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
         r.offs = g.offs.p;
         r.items = I0.items.p;
         r.slots = I0.slots.p;
-        r.units = I0.units.p;
-        r.n_units = I0.n_units;
-        r.counter = g.rows_prog.p + I0.n_units;
-        r.progress = g.rows_prog.p;
-        r.bnd = g.rows_bnd.p;
-        r.sc = g.rows_sc.p;
+        r.n_items = I0.n_long;
+        r.counter = g.rows_prog.p;
+        r.wrap = g.rows_wrap.p;
         r.endcol = I0.endcol.p;
         r.sc_out = g.sc_out.p;
         r.goe = goe;
         r.ge = ge;
         r.one = 1u;
-        if (std::getenv("SW_ROWS_TRACE_N")) {   // experiment builds (SW_ROWS_TRACE=1): keep the unit timestamps
-          CUDA_TRY(g.rows_trace.ensure((size_t)4 * I0.n_units));
-          CUDA_TRY(cudaMemsetAsync(g.rows_trace.p, 0, sizeof(unsigned long long) * 4 * I0.n_units, st));
-          r.trace = g.rows_trace.p;
-        }
         CUDA_TRY(launch_sw16_rows(g.num_sms, r, st));
       }
       CUDA_TRY(cudaEventRecord(g.pev[pe + 1], st));
@@ -1179,16 +1168,6 @@ int sw_set_tile(int32_t G, int32_t R) {
 int sw_tile_supported(int32_t G, int32_t R) {
   return (find_tile_mode(G, R, 0) >= 0 ? 1 : 0) | (find_tile_mode(G, R, 0, 1) >= 0 ? 2 : 0) |
          (find_tile_mode(G, R, 1) >= 0 ? 4 : 0);
-}
-
-int64_t sw_rows_trace(uint64_t *out, int64_t n) {
-  t_err.clear();
-  if (!out || n < 0) return fail(SW_EINVAL, "bad arguments");
-  const int64_t have = std::min<int64_t>(n, (int64_t)g.rows_trace.n);
-  if (have == 0) return 0;
-  CUDA_TRY(cudaDeviceSynchronize());
-  CUDA_TRY(cudaMemcpy(out, g.rows_trace.p, (size_t)have * sizeof(uint64_t), cudaMemcpyDeviceToHost));
-  return have;
 }
 
 int sw_set_rows_mode(int32_t mode) {

@@ -44,9 +44,6 @@
 #ifndef SW_ROWAHEAD
 #define SW_ROWAHEAD 1
 #endif
-#ifndef SW_ROWS_TRACE
-#define SW_ROWS_TRACE 0   // 1: the rows kernel records per-unit timestamps (sw_rows_trace, experiments)
-#endif
 #ifndef SW_TAILADDR
 #define SW_TAILADDR 0   // narrow-tail address: 0 = IMAD from the profile offset, 1 = from the chunk address
 #endif
@@ -649,25 +646,35 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 // ---------------------------------------------------------------------------
 // Rows mode (row a5): long database sequences laid along the
 // ROWS.  A long pair (one sequence per half of a leading work item) is the
-// "query" of a cross-pass wavefront and the real query is the column stream:
-// the same recurrence on the transposed matrix (E and F swap roles, both use
-// Goe / Ge; the score is the maximum over the matrix, so it is unchanged).  A
-// warp (one 32-lane group, kRowsR rows per lane) claims units (item, pass)
-// item-major from an atomic counter; it builds its own profile slice in
-// shared memory from the two sequences' residues (one pre-packed word
-// SM(c, dB_row) * 65536 + SM(c, dA_row) per query letter c: no packing IMAD)
-// and streams the query; pass p reads the boundary (H, F) and the score chain
-// that pass p-1 of the same item wrote, after an ld.acquire of its published
-// progress.  The chain value at the query's END column after the last pass is
-// the pair's score; it is written into the END columns of the sequences in
-// the stream image, where the ordinary score gather reads it.
+// "query" of a wavefront over its passes and the real query is the column
+// stream: the same recurrence on the transposed matrix (E and F swap roles,
+// both use Goe / Ge; the score is the maximum over the matrix, so it is
+// unchanged).  One CTA takes one item at a time (atomic item counter); warp w
+// runs passes w, w+8, w+16, ... (32 lanes x kRowsR rows each), building the
+// pass's pre-packed profile (SM(c, dB_row) * 65536 + SM(c, dA_row) per query
+// letter: no packing IMAD) in its own shared memory.  Warp w hands its bottom
+// boundary (H, F) and score chain to warp w+1 per column through a
+// shared-memory ring with producer / consumer counters (the wavefront stays
+// on the SM: no release/acquire round trip through L2 per hand-over); warp 7
+// hands to warp 0 (the next pass after a multiple of 8) through a per-CTA
+// buffer of one pass in global memory -- one buffer is enough: warp 7 can only
+// produce column c of its next pass after warp 0 has read column c of this
+// one.  The chain value at the query's END column after the last pass is the
+// pair's score; it is written into the END columns of the sequences in the
+// stream image, where the ordinary score gather reads it.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const RowsParams p) {
-  constexpr int R = kRowsR, G = 32, KC = R / 4;
+  constexpr int R = kRowsR, G = 32, KC = R / 4, NW = kRowsWarps, RS = kRowsRing, D = kRowsAhead;
   static_assert(R % 4 == 0, "rows-mode profile chunks");
+  static_assert((RS & (RS - 1)) == 0 && (D & (D - 1)) == 0, "ring sizes");
   extern __shared__ uint4 rsm[];
   uint4 *sdesc = rsm;                                          // [kNL] column descriptors
   int32_t *sM = reinterpret_cast<int32_t *>(rsm + kNL);        // [kNL][kNL]: SM(query letter, db letter)
+  char *const sraw = reinterpret_cast<char *>(rsm);
+  uint4 *ring = reinterpret_cast<uint4 *>(sraw + kRowsHeadBytes + NW * kNL * kRowsLS);   // [NW-1][RS]
+  volatile int *prod = reinterpret_cast<volatile int *>(ring + (NW - 1) * RS);          // [NW] columns produced
+  volatile int *cons = prod + NW;                                                       // [NW] columns consumed
+  volatile int *s_item = cons + NW;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(rsm);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane;
@@ -676,8 +683,8 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
   const uint32_t nlast = last ? 0u : 1u;
   const uint32_t bdef = last ? kB2 : 0u;
   const uint32_t one = p.one;
-  const uint32_t s_prof = sbase + kRowsHeadBytes + (uint32_t)warp * (kNL * kRowsLS);
-  const uint32_t s_qp = s_prof + t * 16;
+  const uint32_t s_qp = sbase + kRowsHeadBytes + (uint32_t)warp * (kNL * kRowsLS) + t * 16;
+  uint4 *const wrap = p.wrap + (size_t)blockIdx.x * p.ncq;    // warp 7 -> warp 0, one pass
   for (int i = threadIdx.x; i < kNL; i += blockDim.x) {
     const bool sep = i >= kAlpha;
     const uint32_t pgoe = (uint32_t)(uint16_t)(-(int)min(p.goe, 32767));
@@ -690,193 +697,185 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
     const int c = i / kNL, d = i % kNL;
     sM[i] = (c < kAlpha && d < kAlpha) ? (int32_t)p.matrix[c * kAlpha + d] : kDummy16;
   }
-  __syncthreads();
-  const DescWords nul = load_desc(sbase + kNul * 16);
+  const int ncq = p.ncq, m = p.m;
 
   for (;;) {
-    int u = 0;
-    if (last) u = atomicAdd(p.counter, 1);
-    u = __shfl_sync(0xffffffffu, u, G - 1);
-    if (u >= p.n_units) break;
-    const int2 un = p.units[u];
-    const int k = un.x, pass = un.y;
+    __syncthreads();   // every warp has left the previous item
+    if (threadIdx.x == 0) {
+      *s_item = atomicAdd(p.counter, 1);
+      for (int w = 0; w < NW; ++w) { prod[w] = 0; cons[w] = 0; }
+    }
+    __syncthreads();
+    const int k = *s_item;
+    if (k >= p.n_items) break;
+    const DescWords nul = load_desc(sbase + kNul * 16);
     const Item it = p.items[k];
     const int32_t sA = p.slots[it.seqA];
     const int32_t sB = it.nB ? p.slots[it.seqB] : -1;
     const int64_t oA = p.offs[sA], nA = p.offs[sA + 1] - oA;
     const int64_t oB = sB >= 0 ? p.offs[sB] : 0, nB = sB >= 0 ? p.offs[sB + 1] - oB : 0;
     const int npass = (int)((max(nA, nB) + G * R - 1) / (G * R));
-#if SW_ROWS_TRACE
-    if (last && p.trace) p.trace[4 * u] = globaltimer();
-#endif
-    // ---- this lane's profile rows: SM(c, dB_row) * 65536 + SM(c, dA_row)
-#pragma unroll
-    for (int kk = 0; kk < KC; ++kk) {
-      int a[4], b[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t row = (int64_t)pass * G * R + t * R + kk * 4 + e;
-        a[e] = row < nA ? (int)__ldg(p.res + oA + row) : -1;
-        b[e] = row < nB ? (int)__ldg(p.res + oB + row) : -1;
-      }
-      for (int c = 0; c < kNL; ++c) {
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int lo = a[e] >= 0 ? sM[c * kNL + a[e]] : kDummy16;
-          const int hi = b[e] >= 0 ? sM[c * kNL + b[e]] : kDummy16;
-          w[e] = (uint32_t)(hi * 65536 + lo);
-        }
-        st_shared_v4(s_qp + c * kRowsLS + kk * G * 16, w[0], w[1], w[2], w[3]);
-      }
-    }
-    __syncwarp();
-    const uint2 *bnd_in = pass > 0 ? p.bnd + ((size_t)k * 2 + ((pass - 1) & 1)) * p.ncq : nullptr;
-    uint2 *bnd_out = pass + 1 < npass ? p.bnd + ((size_t)k * 2 + (pass & 1)) * p.ncq : nullptr;
-    uint32_t *scc = p.sc + (size_t)k * p.ncq;
-    const int *prog_in = pass > 0 ? p.progress + (u - 1) : nullptr;
-    int avail = 0;
-    uint32_t H[R], E[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) { H[r] = kB2; E[r] = kB2; }
-    uint32_t S = 0u, hprev = kB2, kneg = 0u, final_sc = 0u;
-    uint32_t w0 = nul.w0, ngoe = nul.ngoe, nge = nul.nge, knext = nul.kneg;
-    uint32_t hout = kB2, fout = kB2, sc = 0u;
-    const int ncq = p.ncq, m = p.m;
-    // Lane 31 feeds lane 0 from a ring of the next kRowsAhead columns (query
-    // letter, previous pass's boundary and chain value), loaded kRowsAhead
-    // steps before use: no global-load latency on the per-column chain.
-    int rl[kRowsAhead];
-    uint2 rb[kRowsAhead];
-    uint32_t rs[kRowsAhead];
-    auto fetch = [&](int col, int &l, uint2 &b, uint32_t &c) {
-      l = kNul;
-      b = make_uint2(kB2, kB2);
-      c = 0u;
-      if (col < ncq) {
-        l = col < m ? (int)__ldg(p.query + col) : (col == m ? kEnd : kNul);
-        if (prog_in) {
-          const int need = col + 1;
-#if SW_DEBUG
-          long long spins = 0;
-#endif
-          while (avail < need) {
-            avail = ld_acquire(prog_in);
-            if (avail < need) __nanosleep(32);
-#if SW_DEBUG
-            if (++spins == (1ll << 24)) {
-              printf("rows kernel stuck: unit %d (item %d pass %d) waits for column %d of unit %d, has %d (ncq %d); "
-                     "progress[0..3] %d %d %d %d, counter %d, n_units %d, units[0..2] (%d,%d) (%d,%d) (%d,%d), "
-                     "prev unit (%d,%d)\n",
-                     u, k, pass, need, u - 1, avail, ncq, ld_acquire(p.progress), ld_acquire(p.progress + 1),
-                     ld_acquire(p.progress + 2), ld_acquire(p.progress + 3), ld_acquire(p.counter), p.n_units,
-                     p.units[0].x, p.units[0].y, p.units[1].x, p.units[1].y, p.units[2].x, p.units[2].y,
-                     p.units[u - 1].x, p.units[u - 1].y);
-              __trap();
-            }
-#endif
-          }
-          b = ld_cg_v2(bnd_in + col);
-          c = ld_cg(scc + col);
-        }
-      }
-    };
-    if (last) {
-#pragma unroll
-      for (int j = 0; j < kRowsAhead; ++j) fetch(j + 1, rl[j], rb[j], rs[j]);   // ring slot j: column s + 1 + j
-      int l0;
-      uint2 b0;
-      uint32_t c0;
-      fetch(0, l0, b0, c0);                 // lane 0's first column, handed over by the first shuffle
-      const DescWords d = load_desc(sbase + l0 * 16);
-      w0 = d.w0; ngoe = d.ngoe; nge = d.nge; knext = d.kneg;
-      hout = b0.x;
-      fout = b0.y;
-      sc = c0;
-    }
-    const int nsteps = ncq + G - 1;
-#if SW_ROWS_TRACE
-    if (last && p.trace) p.trace[4 * u + 1] = globaltimer();
-#endif
-    for (int s0 = 0; s0 < nsteps; s0 += kRowsAhead) {
-#pragma unroll
-    for (int v = 0; v < kRowsAhead; ++v) {   // (v, not u: u is the unit)
-      const int s = s0 + v;
-      w0 = __shfl_sync(0xffffffffu, w0, src);
-      ngoe = __shfl_sync(0xffffffffu, ngoe, src);
-      nge = __shfl_sync(0xffffffffu, nge, src);
-      knext = __shfl_sync(0xffffffffu, knext, src);
-      const uint32_t hu = __shfl_sync(0xffffffffu, hout, src);
-      uint32_t F = __shfl_sync(0xffffffffu, fout, src);
-      const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
-      const uint32_t kneg_prev = kneg;
-      kneg = knext;
-      // lane 31: lane 0's next column (s + 1) from the ring; refill the slot with column s + 1 + kRowsAhead
-      uint2 bnext = make_uint2(bdef, bdef);
-      uint32_t scnext = 0u;
-      int cnext = kNul;
-      if (last) {   // slot v holds column s + 1; refill it with column s + 1 + kRowsAhead
-        cnext = rl[v];
-        bnext = rb[v];
-        scnext = rs[v];
-        fetch(s + 1 + kRowsAhead, rl[v], rb[v], rs[v]);
-      }
-      uint32_t hd = hprev;
-      hprev = hu;
-      const uint32_t aA = imad(w0, 16u, s_qp);
-      uint4 ca = lds128(aA);
-      uint32_t tcur = imad(hd, one, ca.x);
+
+    for (int pass = warp; pass < npass; pass += NW) {
+      // ---- this lane's profile rows: SM(c, dB_row) * 65536 + SM(c, dA_row)
+      __syncwarp();
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
-        uint4 na = make_uint4(0u, 0u, 0u, 0u);
-        if (kk + 1 < KC) na = lds128(aA + (kk + 1) * G * 16);
-        const uint32_t av[8] = {ca.x, ca.y, ca.z, ca.w, na.x, na.y, na.z, na.w};
+        int a[4], b[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = kk * 4 + j;
-          uint32_t tnext = 0u;
-          if (r + 1 < R) tnext = imad(H[r], one, av[j + 1]);
-          const uint32_t h = hmax3(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
-          H[r] = h;
-          const uint32_t hg = haddmax(h, ngoe, kB2);  // max(H-Goe, 0)
-          E[r] = haddmax(E[r], nge, hg);              // Eq. 2 (along the query)
-          F = haddmax(F, nge, hg);                    // Eq. 3 (along the database sequence)
-          tcur = tnext;
+        for (int e = 0; e < 4; ++e) {
+          const int64_t row = (int64_t)pass * G * R + t * R + kk * 4 + e;
+          a[e] = row < nA ? (int)__ldg(p.res + oA + row) : -1;
+          b[e] = row < nB ? (int)__ldg(p.res + oB + row) : -1;
         }
-        ca = na;
-      }
-      S = haddmax(S, kneg_prev, H[0]);
+        for (int c = 0; c < kNL; ++c) {
+          uint32_t w[4];
 #pragma unroll
-      for (int r = 1; r + 1 < R; r += 2) S = hmax3(S, H[r], H[r + 1]);
-      if ((R & 1) == 0) S = hmax(S, H[R - 1]);
-      const uint32_t so = hmax(sc_in, S);
+          for (int e = 0; e < 4; ++e) {
+            const int lo = a[e] >= 0 ? sM[c * kNL + a[e]] : kDummy16;
+            const int hi = b[e] >= 0 ? sM[c * kNL + b[e]] : kDummy16;
+            w[e] = (uint32_t)(hi * 65536 + lo);
+          }
+          st_shared_v4(s_qp + c * kRowsLS + kk * G * 16, w[0], w[1], w[2], w[3]);
+        }
+      }
+      __syncwarp();
+      // inputs: pass 0 none; warp w > 0 from ring[w-1]; warp 0 from the wrap buffer
+      const bool has_in = pass > 0;
+      const bool in_ring = has_in && warp > 0;
+      const int in_base = in_ring ? (pass / NW) * ncq : (pass / NW - 1) * ncq;   // producer's running column
+      // outputs: the last pass none; warp w < 7 into ring[w]; warp 7 into the wrap buffer
+      const bool has_out = pass + 1 < npass;
+      const bool out_ring = has_out && warp < NW - 1;
+      const int out_base = (pass / NW) * ncq;
+      uint4 *const rin = ring + (warp > 0 ? warp - 1 : 0) * RS;
+      uint4 *const rout = ring + (warp < NW - 1 ? warp : 0) * RS;
+
+      uint32_t H[R], E[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) { H[r] = kB2; E[r] = kB2; }
+      uint32_t S = 0u, hprev = kB2, kneg = 0u, final_sc = 0u;
+      uint32_t w0 = nul.w0, ngoe = nul.ngoe, nge = nul.nge, knext = nul.kneg;
+      uint32_t hout = kB2, fout = kB2, sc = 0u;
+      // lane 31's prefetch ring: slot j holds column s + 1 (+ j rotation); D columns ahead
+      int rl[D];
+      uint4 rv[D];
+      auto fetch = [&](int col, int &l, uint4 &v) {
+        l = kNul;
+        v = make_uint4(kB2, kB2, 0u, 0u);
+        if (col < ncq) {
+          l = col < m ? (int)__ldg(p.query + col) : (col == m ? kEnd : kNul);
+          if (has_in) {
+            const int tix = in_base + col;
+            volatile int *pc = in_ring ? prod + (warp - 1) : prod + (NW - 1);
+            while (*pc < tix + 1) __nanosleep(20);
+            __threadfence_block();
+            v = in_ring ? rin[tix & (RS - 1)] : wrap[col];
+            if (in_ring && ((tix + 1) & 7) == 0) {   // free 8 slots (the loads complete first)
+              __threadfence_block();
+              cons[warp - 1] = tix + 1;
+            }
+          }
+        }
+      };
       if (last) {
-        const int col = s - (G - 1);
-        if (col >= 0 && col < ncq) {
-          st_global_u32(scc + col, so);
-          if (bnd_out) st_global_v2(bnd_out + col, H[R - 1], F);
-          if (col == m) final_sc = so;
-          // a release store waits for the earlier stores: publish every kRowsPublish columns
-          if (((col + 1) & (kRowsPublish - 1)) == 0 || col + 1 == ncq) st_release(p.progress + u, col + 1);
-        }
-        const DescWords d = load_desc(sbase + cnext * 16);
+#pragma unroll
+        for (int j = 0; j < D; ++j) fetch(j + 1, rl[j], rv[j]);
+        int l0;
+        uint4 v0;
+        fetch(0, l0, v0);
+        const DescWords d = load_desc(sbase + l0 * 16);
         w0 = d.w0; ngoe = d.ngoe; nge = d.nge; knext = d.kneg;
+        hout = v0.x;
+        fout = v0.y;
+        sc = v0.z;
       }
-      hout = imad(H[R - 1], nlast, bnext.x);
-      fout = imad(F, nlast, bnext.y);
-      sc = imad(so, nlast, scnext);
+      const int nsteps = ncq + G - 1;
+      for (int s0 = 0; s0 < nsteps; s0 += D) {
+#pragma unroll
+        for (int v = 0; v < D; ++v) {
+          const int s = s0 + v;
+          w0 = __shfl_sync(0xffffffffu, w0, src);
+          ngoe = __shfl_sync(0xffffffffu, ngoe, src);
+          nge = __shfl_sync(0xffffffffu, nge, src);
+          knext = __shfl_sync(0xffffffffu, knext, src);
+          const uint32_t hu = __shfl_sync(0xffffffffu, hout, src);
+          uint32_t F = __shfl_sync(0xffffffffu, fout, src);
+          const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
+          const uint32_t kneg_prev = kneg;
+          kneg = knext;
+          uint2 bnext = make_uint2(bdef, bdef);
+          uint32_t scnext = 0u;
+          int cnext = kNul;
+          if (last) {   // slot v holds column s + 1; refill it with column s + 1 + D
+            cnext = rl[v];
+            bnext = make_uint2(rv[v].x, rv[v].y);
+            scnext = rv[v].z;
+            fetch(s + 1 + D, rl[v], rv[v]);
+          }
+          uint32_t hd = hprev;
+          hprev = hu;
+          const uint32_t aA = imad(w0, 16u, s_qp);
+          uint4 ca = lds128(aA);
+          uint32_t tcur = imad(hd, one, ca.x);
+#pragma unroll
+          for (int kk = 0; kk < KC; ++kk) {
+            uint4 na = make_uint4(0u, 0u, 0u, 0u);
+            if (kk + 1 < KC) na = lds128(aA + (kk + 1) * G * 16);
+            const uint32_t av[8] = {ca.x, ca.y, ca.z, ca.w, na.x, na.y, na.z, na.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int r = kk * 4 + j;
+              uint32_t tnext = 0u;
+              if (r + 1 < R) tnext = imad(H[r], one, av[j + 1]);
+              const uint32_t h = hmax3(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
+              H[r] = h;
+              const uint32_t hg = haddmax(h, ngoe, kB2);  // max(H-Goe, 0)
+              E[r] = haddmax(E[r], nge, hg);              // Eq. 2 (along the query)
+              F = haddmax(F, nge, hg);                    // Eq. 3 (along the database sequence)
+              tcur = tnext;
+            }
+            ca = na;
+          }
+          S = haddmax(S, kneg_prev, H[0]);
+#pragma unroll
+          for (int r = 1; r + 1 < R; r += 2) S = hmax3(S, H[r], H[r + 1]);
+          if ((R & 1) == 0) S = hmax(S, H[R - 1]);
+          const uint32_t so = hmax(sc_in, S);
+          if (last) {
+            const int col = s - (G - 1);
+            if (col >= 0 && col < ncq) {
+              if (col == m) final_sc = so;
+              if (has_out) {
+                const int tix = out_base + col;
+                const uint4 o = make_uint4(H[R - 1], F, so, 0u);
+                if (out_ring) {
+                  while (tix - cons[warp] >= RS) __nanosleep(20);   // ring full: wait for warp w+1
+                  rout[tix & (RS - 1)] = o;
+                } else {
+                  wrap[col] = o;
+                }
+                if (((col + 1) & (kRowsPublish - 1)) == 0 || col + 1 == ncq) {
+                  __threadfence_block();
+                  prod[warp] = tix + 1;
+                }
+              }
+            }
+            const DescWords d = load_desc(sbase + cnext * 16);
+            w0 = d.w0; ngoe = d.ngoe; nge = d.nge; knext = d.kneg;
+          }
+          hout = imad(H[R - 1], nlast, bnext.x);
+          fout = imad(F, nlast, bnext.y);
+          sc = imad(so, nlast, scnext);
+        }
+      }
+      // the pair's scores (chain at the END column after the last pass) into
+      // the END columns of its sequences in the stream image
+      if (last && pass + 1 == npass) {
+        st_global_u32(p.sc_out + (p.endcol[sA] >> 1), final_sc);
+        if (sB >= 0) st_global_u32(p.sc_out + (p.endcol[sB] >> 1), final_sc);
+      }
     }
-    }
-    // the pair's scores (chain at the END column after the last pass) into the
-    // END columns of its sequences in the stream image
-    if (last && pass + 1 == npass) {
-      st_global_u32(p.sc_out + (p.endcol[sA] >> 1), final_sc);
-      if (sB >= 0) st_global_u32(p.sc_out + (p.endcol[sB] >> 1), final_sc);
-    }
-#if SW_ROWS_TRACE
-    if (last && p.trace) { p.trace[4 * u + 2] = globaltimer(); p.trace[4 * u + 3] = (blockIdx.x << 8) | warp; }
-#endif
-    __syncwarp();
   }
 }
 
@@ -1760,7 +1759,10 @@ cudaError_t launch_scatter_scores(const int32_t *src, const int64_t *index, int6
   return cudaGetLastError();
 }
 
-size_t rows_smem_bytes() { return (size_t)kRowsHeadBytes + (size_t)kRowsWarps * kNL * kRowsLS; }
+size_t rows_smem_bytes() {
+  return (size_t)kRowsHeadBytes + (size_t)kRowsWarps * kNL * kRowsLS + (size_t)(kRowsWarps - 1) * kRowsRing * 16 +
+         (2 * kRowsWarps + 4) * sizeof(int);
+}
 
 cudaError_t launch_sw16_rows(int grid, const RowsParams &p, cudaStream_t st) {
   static bool attr = false;

@@ -97,8 +97,9 @@ struct SW16Params {
 
 // Rows mode (long database sequences along the rows, kernels.cu).
 constexpr int kRowsR = 8;                           // rows per lane (one 32-lane group per warp)
-constexpr int kRowsWarps = 8;                       // warps per CTA (one CTA per SM)
-constexpr int kRowsPublish = 16;                    // columns between progress publications
+constexpr int kRowsWarps = 8;                       // warps per CTA = passes in flight per item
+constexpr int kRowsRing = 128;                      // shared-memory ring between consecutive warps (columns)
+constexpr int kRowsPublish = 4;                     // columns between producer-count updates
 constexpr int kRowsAhead = 8;                       // lane 31's prefetch distance (columns)
 constexpr int kRowsLS = (kRowsR / 4) * 32 * 16;     // profile bytes per query letter of a warp
 constexpr int kRowsHeadBytes = 26 * 16 + 26 * 26 * 4 + 16;   // descriptors + matrix (+ pad to 16 B)
@@ -110,19 +111,15 @@ struct RowsParams {
   const int8_t *matrix;     // device [24][24], matrix[q*24 + d]
   const uint8_t *res;       // plain database, original order
   const int64_t *offs;
-  const Item *items;        // the image's items; the long pairs are items 0 .. n_pairs-1
+  const Item *items;        // the image's items; the long pairs are items 0 .. n_items-1
   const int32_t *slots;
-  const int2 *units;        // (item, pass), item-major, passes consecutive
-  int n_units;
-  int *counter;             // zeroed
-  int *progress;            // per unit: columns written (zeroed)
-  uint2 *bnd;               // per item: 2 x ncq boundary (H, F), double-buffered by pass parity
-  uint32_t *sc;             // per item: ncq score-chain values, carried through the passes
+  int n_items;
+  int *counter;             // zeroed: next item
+  uint4 *wrap;              // per CTA: ncq entries (warp 7 -> warp 0 hand-over)
   const int64_t *endcol;    // the image's END columns (2 * column + half)
   uint32_t *sc_out;         // the image's per-column chain buffer (the gather reads the END columns)
   int goe, ge;
   uint32_t one;
-  unsigned long long *trace;   // SW_ROWS_TRACE builds: per unit (claim, loop start, end ns, block<<8|warp)
 };
 
 struct SW32Params {
@@ -219,7 +216,7 @@ cudaError_t launch_block_topk(const int32_t *scores, const int64_t *index, const
                               int k, uint64_t *out, int blocks, cudaStream_t st);
 cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score,
                                cudaStream_t st);
-size_t rows_smem_bytes();
+size_t rows_smem_bytes();   // head + 8 profiles + 7 rings + counters
 cudaError_t launch_sw16_rows(int grid, const RowsParams &p, cudaStream_t st);
 // Streamed database: out[i] = in[i] * kDescBytes (compact letter-pair index ->
 // column word) for i < n.

@@ -21,7 +21,7 @@ _NAMES = {SW_EINVAL: "SW_EINVAL", SW_ENOMEM: "SW_ENOMEM", SW_ECUDA: "SW_ECUDA",
 
 EXPORTS = ["sw_db_load", "sw_db_load_streamed", "sw_db_chunks", "sw_db_free", "sw_db_count", "sw_db_residues", "sw_search",
            "sw_search_dev", "sw_search_batch", "sw_search_batch_dev", "sw_topk", "sw_topk_dev", "sw_scatter_dev", "sw_last_stats", "sw_last_timing", "sw_set_tile",
-           "sw_tile_supported", "sw_set_wave", "sw_set_latency_mode", "sw_set_profile", "sw_set_rows_mode", "sw_rows_trace", "sw_last_error", "sw_version", "sw_launch_count"]
+           "sw_tile_supported", "sw_set_wave", "sw_set_latency_mode", "sw_set_profile", "sw_set_rows_mode", "sw_last_error", "sw_version", "sw_launch_count"]
 
 
 class SWError(RuntimeError):
@@ -69,7 +69,6 @@ def load_library():
         "sw_set_latency_mode": (ctypes.c_int, [i32]),
         "sw_set_profile": (ctypes.c_int, [i32]),
         "sw_set_rows_mode": (ctypes.c_int, [i32]),
-        "sw_rows_trace": (i64, [p, i64]),
         "sw_last_error": (ctypes.c_char_p, []),
         "sw_version": (ctypes.c_char_p, []),
         "sw_launch_count": (i64, []),
@@ -254,13 +253,6 @@ def sw_set_wave(mode: int) -> None:
 def sw_set_latency_mode(mode: int) -> None:
     """Low-latency (LAT) tiles: 0 auto (default), 1 always, -1 never (swdb.h)."""
     _check(load_library().sw_set_latency_mode(int(mode)))
-
-
-def sw_rows_trace(n: int) -> np.ndarray:
-    """Per-unit timestamps of the last rows-mode launch (experiment builds)."""
-    out = np.zeros(max(int(n), 1), dtype=np.uint64)
-    r = _check(load_library().sw_rows_trace(_ptr(out), int(n)))
-    return out[:r]
 
 
 def sw_set_rows_mode(mode: int) -> None:
