@@ -355,7 +355,8 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // (profiles/r02_rows_mode.jsonl) -- the cross-SM progress hand-over between
   // consecutive passes costs more than the shorter chain saves.  Single-pass
   // resident single-query searches without the wavefront.
-  const bool rows_cand = !pair && !g.streamed && I0.n_long > 0 && I0.n_units > 0 && g.rows_mode == 1;
+  const bool rows_cand = !pair && !g.streamed && I0.n_long > 0 && I0.n_units > 0 && g.rows_mode == 1 &&
+                         ((m + 2 + 3) & ~3) <= kRowsMaxNcq;
   const Image &I = I0;
   // the tile model's view of the items the pass kernel runs (rows mode: all
   // but the long pairs); device buffers are shared, only these sizes differ

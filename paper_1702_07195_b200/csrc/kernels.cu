@@ -675,6 +675,7 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
   volatile int *prod = reinterpret_cast<volatile int *>(ring + (NW - 1) * RS);          // [NW] columns produced
   volatile int *cons = prod + NW;                                                       // [NW] columns consumed
   volatile int *s_item = cons + NW;
+  uint8_t *sq = reinterpret_cast<uint8_t *>(const_cast<int *>(s_item + 4));   // [ncq] query stream letters
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(rsm);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane;
@@ -698,6 +699,8 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
     sM[i] = (c < kAlpha && d < kAlpha) ? (int32_t)p.matrix[c * kAlpha + d] : kDummy16;
   }
   const int ncq = p.ncq, m = p.m;
+  for (int i = threadIdx.x; i < ncq; i += blockDim.x)
+    sq[i] = (uint8_t)(i < m ? p.query[i] : (i == m ? kEnd : kNul));
 
   for (;;) {
     __syncthreads();   // every warp has left the previous item
@@ -757,21 +760,28 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
       uint32_t S = 0u, hprev = kB2, kneg = 0u, final_sc = 0u;
       uint32_t w0 = nul.w0, ngoe = nul.ngoe, nge = nul.nge, knext = nul.kneg;
       uint32_t hout = kB2, fout = kB2, sc = 0u;
-      // lane 31's prefetch ring: slot j holds column s + 1 (+ j rotation); D columns ahead
+      // lane 31's prefetch ring: slot j holds column s + 1 (+ j rotation); D
+      // columns ahead.  The producer's count is re-read (and fenced) only when
+      // the cached value does not cover the column; consumed slots are freed
+      // every 16 columns.
       int rl[D];
       uint4 rv[D];
+      int avail = 0, room = 0;
       auto fetch = [&](int col, int &l, uint4 &v) {
         l = kNul;
         v = make_uint4(kB2, kB2, 0u, 0u);
         if (col < ncq) {
-          l = col < m ? (int)__ldg(p.query + col) : (col == m ? kEnd : kNul);
+          l = (int)sq[col];
           if (has_in) {
             const int tix = in_base + col;
-            volatile int *pc = in_ring ? prod + (warp - 1) : prod + (NW - 1);
-            while (*pc < tix + 1) __nanosleep(20);
-            __threadfence_block();
+            if (avail < tix + 1) {
+              volatile int *pc = in_ring ? prod + (warp - 1) : prod + (NW - 1);
+              while ((avail = *pc) < tix + 1) {
+              }
+              __threadfence_block();
+            }
             v = in_ring ? rin[tix & (RS - 1)] : wrap[col];
-            if (in_ring && ((tix + 1) & 7) == 0) {   // free 8 slots (the loads complete first)
+            if (in_ring && ((tix + 1) & 15) == 0) {   // free 16 slots (the loads complete first)
               __threadfence_block();
               cons[warp - 1] = tix + 1;
             }
@@ -850,7 +860,10 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
                 const int tix = out_base + col;
                 const uint4 o = make_uint4(H[R - 1], F, so, 0u);
                 if (out_ring) {
-                  while (tix - cons[warp] >= RS) __nanosleep(20);   // ring full: wait for warp w+1
+                  if (tix - room >= RS) {   // ring full as far as known: re-read the consumer's count
+                    while (tix - (room = cons[warp]) >= RS) {
+                    }
+                  }
                   rout[tix & (RS - 1)] = o;
                 } else {
                   wrap[col] = o;
@@ -1759,21 +1772,17 @@ cudaError_t launch_scatter_scores(const int32_t *src, const int64_t *index, int6
   return cudaGetLastError();
 }
 
-size_t rows_smem_bytes() {
+size_t rows_smem_bytes(int ncq) {
   return (size_t)kRowsHeadBytes + (size_t)kRowsWarps * kNL * kRowsLS + (size_t)(kRowsWarps - 1) * kRowsRing * 16 +
-         (2 * kRowsWarps + 4) * sizeof(int);
+         (2 * kRowsWarps + 4) * sizeof(int) + (size_t)((ncq + 15) & ~15);
 }
 
 cudaError_t launch_sw16_rows(int grid, const RowsParams &p, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(sw16_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)rows_smem_bytes());
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const size_t smem = rows_smem_bytes(p.ncq);
+  cudaError_t e = cudaFuncSetAttribute(sw16_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   ++g_launches;
-  sw16_rows_kernel<<<grid, kRowsWarps * 32, rows_smem_bytes(), st>>>(p);
+  sw16_rows_kernel<<<grid, kRowsWarps * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
 

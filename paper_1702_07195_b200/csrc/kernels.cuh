@@ -216,7 +216,8 @@ cudaError_t launch_block_topk(const int32_t *scores, const int64_t *index, const
                               int k, uint64_t *out, int blocks, cudaStream_t st);
 cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score,
                                cudaStream_t st);
-size_t rows_smem_bytes();   // head + 8 profiles + 7 rings + counters
+size_t rows_smem_bytes(int ncq);   // head + 8 profiles + 7 rings + counters + the query stream
+constexpr int kRowsMaxNcq = 1792;  // rows mode needs the query stream in shared memory
 cudaError_t launch_sw16_rows(int grid, const RowsParams &p, cudaStream_t st);
 // Streamed database: out[i] = in[i] * kDescBytes (compact letter-pair index ->
 // column word) for i < n.
