@@ -272,13 +272,15 @@ int sw_set_profile(int32_t mode);
  * lane group (at least 512 residues) a work item of its own, paired with the
  * next long one.  In rows mode those pairs are scored with the database
  * sequence along the rows and the query as the column stream (the same
- * recurrence on the transposed matrix; scores are identical): the passes over
- * the sequence run as a wavefront on many lane groups at once, so the
- * critical path is about m + (n / 256) x 55 steps instead of n.  mode 1: use
- * it whenever possible; 0 (default) and -1: do not.  (Measured slower than the
- * ordinary path on every database tried, so the default never
- * uses it.)  Resident single-query searches whose pass kernel makes one pass,
- * without the cross-pass wavefront.
+ * recurrence on the transposed matrix; scores are identical), one CTA per
+ * pair with its 8 warps on consecutive passes over the sequence (hand-over
+ * through shared memory), so the pair's critical path is about
+ * ceil(n / 2048) x (m + 31) + 7 x 44 column steps instead of n.  mode 0
+ * (default): used when the pass time model says the search is bound by the
+ * longest sequence's chain and rows mode is >= 20% faster (one long sequence,
+ * short queries); 1: whenever possible; -1: never.  Resident single-query
+ * searches whose pass kernel makes one pass, without the cross-pass
+ * wavefront, queries of at most 8,188 residues.
  * Returns SW_OK or SW_EINVAL.
  */
 int sw_set_rows_mode(int32_t mode);

@@ -38,7 +38,7 @@ if os.environ.get("SW_BRING"):    # boundary prefetch ring in every boundary-rea
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_BRING=" + os.environ["SW_BRING"]]
 if os.environ.get("SW_S32ROWS"):  # rows per lane of the 32-bit kernel (experiment)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_S32ROWS=" + os.environ["SW_S32ROWS"]]
-for _k in ("SW_QPTAIL", "SW_TAILADDR"):   # profile tail layout experiments (kernels.cuh)
+for _k in ("SW_QPTAIL", "SW_TAILADDR", "SW_ROWS_TRACE"):   # profile tail layout experiments (kernels.cuh)
     if os.environ.get(_k):
         NVCC_FLAGS = NVCC_FLAGS + [f"-D{_k}=" + os.environ[_k]]
 if os.environ.get("SW_DEBUG"):    # device-side bounds checks (slow; debug builds)

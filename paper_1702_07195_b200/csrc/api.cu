@@ -80,6 +80,7 @@ struct Image {
   // sequence per half; units (item, pass) of the rows kernel
   int n_long = 0;
   int64_t long_min_len = 0;       // shortest long sequence
+  int64_t long_max_len = 0;       // longest long sequence
   int64_t long_cols = 0;          // pair-columns of the long items
   int64_t max_item_cols_rest = 0; // longest item after them
   DevBuf<int2> units;
@@ -91,7 +92,7 @@ struct Image {
     num_items = 0;
     n_long = 0;
     n_units = 0;
-    long_min_len = long_cols = max_item_cols_rest = 0;
+    long_min_len = long_max_len = long_cols = max_item_cols_rest = 0;
   }
 };
 
@@ -272,6 +273,9 @@ int choose_tile(int m, int qpm, const Image &I, bool wave_only = false) {
 // a pass lasts about max(bulk, chain).  Latency tiles (small R, one
 // 256-thread CTA per SM) shorten the chain at lower throughput.
 constexpr double kStepC0 = 145.0, kStepC1 = 14.0;
+// rows kernel (profiles/r02_rows_mode.jsonl, traces): ~850 cycles per column
+// step with 8 warps per SM, ~44 steps between consecutive passes
+constexpr double kRowsStep = 850.0, kRowsLag = 44.0;
 constexpr double kLatThroughput = 0.6;   // latency-tile throughput relative to a 512-thread tile's eff0
 
 double pass_time_model(const TileInfo &T, int m, const Image &I, bool lat) {
@@ -355,8 +359,30 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // (profiles/r02_rows_mode.jsonl) -- the cross-SM progress hand-over between
   // consecutive passes costs more than the shorter chain saves.  Single-pass
   // resident single-query searches without the wavefront.
-  const bool rows_cand = !pair && !g.streamed && I0.n_long > 0 && I0.n_units > 0 && g.rows_mode == 1 &&
-                         ((m + 2 + 3) & ~3) <= kRowsMaxNcq;
+  const bool rows_possible = !pair && !g.streamed && I0.n_long > 0 && I0.n_units > 0 && g.rows_mode >= 0 &&
+                             ((m + 2 + 3) & ~3) <= kRowsMaxNcq;
+  bool rows_cand = rows_possible && g.rows_mode == 1;
+  if (rows_possible && g.rows_mode == 0 && I0.n_long <= g.num_sms) {
+    // auto: the longest sequence's chain in the rows kernel (one CTA per item,
+    // warps on consecutive passes) against its chain in the pass kernel, when
+    // that chain bounds the search (profiles/r02_rows_mode.jsonl)
+    const int tn = choose_tile(mm, 0, I0);
+    if (tn >= 0) {
+      const TileInfo tt = tile(tn);
+      const double f = 1.9e9;
+      const double chain_normal = ((double)I0.long_max_len + tt.G) * (kStepC0 + kStepC1 * tt.R) / f;
+      const double P = std::ceil((double)I0.long_max_len / kRowsRows);
+      const double ncq = (double)((m + 2 + 3) & ~3);
+      const double rows_t = kRowsStep * (std::ceil(P / kRowsWarps) * (ncq + 31.0) +
+                                         (std::min(P, (double)kRowsWarps) - 1.0) * kRowsLag) / f;
+      Image Iv2 = I0;
+      Iv2.max_item_cols = I0.max_item_cols_rest;
+      Iv2.total_cols = std::max<int64_t>(1, I0.total_cols - I0.long_cols);
+      const double t_rest = pass_time_model(tt, mm, Iv2, false);
+      const double t_all = pass_time_model(tt, mm, I0, false);
+      rows_cand = chain_normal >= t_all * 0.99 && t_rest + rows_t < 0.8 * t_all;
+    }
+  }
   const Image &I = I0;
   // the tile model's view of the items the pass kernel runs (rows mode: all
   // but the long pairs); device buffers are shared, only these sizes differ
@@ -849,6 +875,7 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
         const int32_t sq = H.slots[it.seqA + h];
         const int64_t n = offsets[sq + 1] - offsets[sq];
         I.long_min_len = std::min(I.long_min_len, n);
+        I.long_max_len = std::max(I.long_max_len, n);
         nmax = std::max(nmax, n);
       }
       for (int64_t ps = 0; ps < (nmax + kRowsRows - 1) / kRowsRows; ++ps) units.push_back(make_int2((int)i, (int)ps));

@@ -44,6 +44,9 @@
 #ifndef SW_ROWAHEAD
 #define SW_ROWAHEAD 1
 #endif
+#ifndef SW_ROWS_TRACE
+#define SW_ROWS_TRACE 0   // 1: the rows kernel prints per-pass cycle counts of item 0 (experiments)
+#endif
 #ifndef SW_TAILADDR
 #define SW_TAILADDR 0   // narrow-tail address: 0 = IMAD from the profile offset, 1 = from the chunk address
 #endif
@@ -138,6 +141,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
   asm volatile("{\n\t.reg .pred P;\n"
                "WAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
                "\t@!P bra WAIT_%=;\n}" :: "r"(mbar), "r"(phase) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {   // release.cta: prior writes are visible to waiters
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(mbar) : "memory");
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -672,7 +679,13 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
   int32_t *sM = reinterpret_cast<int32_t *>(rsm + kNL);        // [kNL][kNL]: SM(query letter, db letter)
   char *const sraw = reinterpret_cast<char *>(rsm);
   uint4 *ring = reinterpret_cast<uint4 *>(sraw + kRowsHeadBytes + NW * kNL * kRowsLS);   // [NW-1][RS]
-  volatile int *prod = reinterpret_cast<volatile int *>(ring + (NW - 1) * RS);          // [NW] columns produced
+  // ring w: NB batch slots of kRowsBatch columns, each with a "full" and an "empty" mbarrier
+  constexpr int B = kRowsBatch, NB = RS / B;
+  uint64_t *mb = reinterpret_cast<uint64_t *>(ring + (NW - 1) * RS);                    // [NW-1][2][NB]
+  const uint32_t s_mb = (uint32_t)__cvta_generic_to_shared(mb);
+  auto mb_full = [&](int w, int j) { return s_mb + (uint32_t)(((w * 2 + 0) * NB + j) * 8); };
+  auto mb_empty = [&](int w, int j) { return s_mb + (uint32_t)(((w * 2 + 1) * NB + j) * 8); };
+  volatile int *prod = reinterpret_cast<volatile int *>(mb + (NW - 1) * 2 * NB);        // [NW] (prod[7]: the wrap)
   volatile int *cons = prod + NW;                                                       // [NW] columns consumed
   volatile int *s_item = cons + NW;
   uint8_t *sq = reinterpret_cast<uint8_t *>(const_cast<int *>(s_item + 4));   // [ncq] query stream letters
@@ -707,6 +720,11 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
     if (threadIdx.x == 0) {
       *s_item = atomicAdd(p.counter, 1);
       for (int w = 0; w < NW; ++w) { prod[w] = 0; cons[w] = 0; }
+      for (int w = 0; w + 1 < NW; ++w)
+        for (int j = 0; j < NB; ++j) {
+          mbar_init(mb_full(w, j), 1);
+          mbar_init(mb_empty(w, j), 1);
+        }
     }
     __syncthreads();
     const int k = *s_item;
@@ -746,11 +764,12 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
       // inputs: pass 0 none; warp w > 0 from ring[w-1]; warp 0 from the wrap buffer
       const bool has_in = pass > 0;
       const bool in_ring = has_in && warp > 0;
-      const int in_base = in_ring ? (pass / NW) * ncq : (pass / NW - 1) * ncq;   // producer's running column
+      const int nbp = (ncq + B - 1) / B;   // ring batches per pass (a pass starts a batch)
+      const int in_base = in_ring ? (pass / NW) * nbp * B : (pass / NW - 1) * ncq;   // producer's running column
       // outputs: the last pass none; warp w < 7 into ring[w]; warp 7 into the wrap buffer
       const bool has_out = pass + 1 < npass;
       const bool out_ring = has_out && warp < NW - 1;
-      const int out_base = (pass / NW) * ncq;
+      const int out_base = out_ring ? (pass / NW) * nbp * B : (pass / NW) * ncq;
       uint4 *const rin = ring + (warp > 0 ? warp - 1 : 0) * RS;
       uint4 *const rout = ring + (warp < NW - 1 ? warp : 0) * RS;
 
@@ -766,7 +785,7 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
       // every 16 columns.
       int rl[D];
       uint4 rv[D];
-      int avail = 0, room = 0;
+      int avail = 0;
       auto fetch = [&](int col, int &l, uint4 &v) {
         l = kNul;
         v = make_uint4(kB2, kB2, 0u, 0u);
@@ -774,16 +793,21 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
           l = (int)sq[col];
           if (has_in) {
             const int tix = in_base + col;
-            if (avail < tix + 1) {
-              volatile int *pc = in_ring ? prod + (warp - 1) : prod + (NW - 1);
-              while ((avail = *pc) < tix + 1) {
+            if (in_ring) {
+              // the first column of a batch: wait (suspended, no spinning) for the producer's arrival
+              const int bt = tix / B;
+              if ((tix & (B - 1)) == 0) mbar_wait(mb_full(warp - 1, bt & (NB - 1)), (uint32_t)((bt / NB) & 1));
+              v = rin[tix & (RS - 1)];
+              if ((tix & (B - 1)) == B - 1 || col + 1 == ncq) {   // the batch is read: free its slot
+                __threadfence_block();
+                mbar_arrive(mb_empty(warp - 1, bt & (NB - 1)));
               }
-              __threadfence_block();
-            }
-            v = in_ring ? rin[tix & (RS - 1)] : wrap[col];
-            if (in_ring && ((tix + 1) & 15) == 0) {   // free 16 slots (the loads complete first)
-              __threadfence_block();
-              cons[warp - 1] = tix + 1;
+            } else {   // the wrap from warp 7: a count, polled with a sleep (one waiter per CTA)
+              if (avail < tix + 1) {
+                while ((avail = prod[NW - 1]) < tix + 1) __nanosleep(64);
+                __threadfence_block();
+              }
+              v = wrap[col];
             }
           }
         }
@@ -801,6 +825,9 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
         sc = v0.z;
       }
       const int nsteps = ncq + G - 1;
+#if SW_ROWS_TRACE
+      const long long tr0 = clock64();
+#endif
       for (int s0 = 0; s0 < nsteps; s0 += D) {
 #pragma unroll
         for (int v = 0; v < D; ++v) {
@@ -860,17 +887,18 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
                 const int tix = out_base + col;
                 const uint4 o = make_uint4(H[R - 1], F, so, 0u);
                 if (out_ring) {
-                  if (tix - room >= RS) {   // ring full as far as known: re-read the consumer's count
-                    while (tix - (room = cons[warp]) >= RS) {
-                    }
-                  }
+                  const int bt = tix / B;
+                  // a new batch slot: wait until warp w+1 has read it in the previous round
+                  if ((tix & (B - 1)) == 0 && bt >= NB)
+                    mbar_wait(mb_empty(warp, bt & (NB - 1)), (uint32_t)((bt / NB - 1) & 1));
                   rout[tix & (RS - 1)] = o;
+                  if ((tix & (B - 1)) == B - 1 || col + 1 == ncq) mbar_arrive(mb_full(warp, bt & (NB - 1)));
                 } else {
                   wrap[col] = o;
-                }
-                if (((col + 1) & (kRowsPublish - 1)) == 0 || col + 1 == ncq) {
-                  __threadfence_block();
-                  prod[warp] = tix + 1;
+                  if (((col + 1) & (kRowsPublish - 1)) == 0 || col + 1 == ncq) {
+                    __threadfence_block();
+                    prod[warp] = tix + 1;
+                  }
                 }
               }
             }
@@ -882,6 +910,11 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
           sc = imad(so, nlast, scnext);
         }
       }
+#if SW_ROWS_TRACE
+      if (last && k == 0 && pass < 64)
+        printf("trace item 0 pass %d warp %d block %d: %lld cycles for %d steps (%lld per step), start %lld\n", pass,
+               warp, blockIdx.x, clock64() - tr0, nsteps, (clock64() - tr0) / nsteps, tr0);
+#endif
       // the pair's scores (chain at the END column after the last pass) into
       // the END columns of its sequences in the stream image
       if (last && pass + 1 == npass) {
@@ -1774,7 +1807,8 @@ cudaError_t launch_scatter_scores(const int32_t *src, const int64_t *index, int6
 
 size_t rows_smem_bytes(int ncq) {
   return (size_t)kRowsHeadBytes + (size_t)kRowsWarps * kNL * kRowsLS + (size_t)(kRowsWarps - 1) * kRowsRing * 16 +
-         (2 * kRowsWarps + 4) * sizeof(int) + (size_t)((ncq + 15) & ~15);
+         (size_t)(kRowsWarps - 1) * 2 * (kRowsRing / kRowsBatch) * 8 + (2 * kRowsWarps + 4) * sizeof(int) +
+         (size_t)((ncq + 15) & ~15);
 }
 
 cudaError_t launch_sw16_rows(int grid, const RowsParams &p, cudaStream_t st) {

@@ -98,9 +98,10 @@ struct SW16Params {
 // Rows mode (long database sequences along the rows, kernels.cu).
 constexpr int kRowsR = 8;                           // rows per lane (one 32-lane group per warp)
 constexpr int kRowsWarps = 8;                       // warps per CTA = passes in flight per item
-constexpr int kRowsRing = 128;                      // shared-memory ring between consecutive warps (columns)
+constexpr int kRowsRing = 64;                       // shared-memory ring between consecutive warps (columns)
+constexpr int kRowsBatch = 8;                       // columns per ring slot (one full / empty mbarrier each)
 constexpr int kRowsPublish = 4;                     // columns between producer-count updates
-constexpr int kRowsAhead = 8;                       // lane 31's prefetch distance (columns)
+constexpr int kRowsAhead = 4;                       // lane 31's prefetch distance (columns)
 constexpr int kRowsLS = (kRowsR / 4) * 32 * 16;     // profile bytes per query letter of a warp
 constexpr int kRowsHeadBytes = 26 * 16 + 26 * 26 * 4 + 16;   // descriptors + matrix (+ pad to 16 B)
 constexpr int kRowsRows = 32 * kRowsR;              // database rows per pass
@@ -217,7 +218,7 @@ cudaError_t launch_block_topk(const int32_t *scores, const int64_t *index, const
 cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, int32_t *score,
                                cudaStream_t st);
 size_t rows_smem_bytes(int ncq);   // head + 8 profiles + 7 rings + counters + the query stream
-constexpr int kRowsMaxNcq = 1792;  // rows mode needs the query stream in shared memory
+constexpr int kRowsMaxNcq = 8192;  // rows mode needs the query stream in shared memory
 cudaError_t launch_sw16_rows(int grid, const RowsParams &p, cudaStream_t st);
 // Streamed database: out[i] = in[i] * kDescBytes (compact letter-pair index ->
 // column word) for i < n.

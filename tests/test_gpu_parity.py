@@ -608,8 +608,8 @@ def test_rows_mode_matches_oracle():
     as the column stream, passes as a wavefront.  Random
     and asymmetric matrices, zero gap-open, sequences of odd count (an empty
     half), saturating sequences (flag, carry propagation, 32-bit re-scoring),
-    query lengths around the stream's 4-column rounding.  (Rows mode is used
-    on request only: sw_set_rows_mode(1).)"""
+    query lengths around the stream's 4-column rounding; the automatic choice
+    for a chain-bound database."""
     rng = np.random.default_rng(2048)
     longs = [si.rr_residues(rng, int(L)) for L in rng.integers(600, 9000, 11)]
     longs += [encode("W" * 3100), encode("W" * 2990 + "A" * 20)]
@@ -643,8 +643,17 @@ def test_rows_mode_matches_oracle():
         got = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
         assert sw.sw_last_stats()["rows_pairs"] > 0
         assert (got == oracle.batch(w.queries[0], w.db.residues, w.db.offsets, BLOSUM62, 10, 2)).all()
-        sw.sw_set_rows_mode(0)
+        sw.sw_set_rows_mode(-1)
         got2 = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
         assert sw.sw_last_stats()["rows_pairs"] == 0 and (got2 == got).all()
+        # automatic choice: one long sequence and a short query is bound by its
+        # chain, which the rows kernel shortens
+        sw.sw_set_rows_mode(0)
+        db1 = _db([si.rr_residues(rng, 12000), si.rr_residues(rng, 300)])
+        sw.sw_db_load(db1.residues, db1.offsets)
+        q = si.rr_residues(rng, 100)
+        got = sw.sw_search(q, BLOSUM62, 10, 2)
+        assert sw.sw_last_stats()["rows_pairs"] > 0
+        assert (got == oracle.batch(q, db1.residues, db1.offsets, BLOSUM62, 10, 2)).all()
     finally:
         sw.sw_set_rows_mode(0)
