@@ -813,11 +813,11 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
         }
       };
       if (last) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) fetch(j + 1, rl[j], rv[j]);
         int l0;
         uint4 v0;
-        fetch(0, l0, v0);
+        fetch(0, l0, v0);   // columns in order: a batch's first column waits for the batch
+#pragma unroll
+        for (int j = 0; j < D; ++j) fetch(j + 1, rl[j], rv[j]);
         const DescWords d = load_desc(sbase + l0 * 16);
         w0 = d.w0; ngoe = d.ngoe; nge = d.nge; knext = d.kneg;
         hout = v0.x;
