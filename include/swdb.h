@@ -275,10 +275,9 @@ int sw_set_profile(int32_t mode);
  * recurrence on the transposed matrix; scores are identical), one CTA per
  * pair with its 8 warps on consecutive passes over the sequence (hand-over
  * through shared memory), so the pair's critical path is about
- * ceil(n / 2048) x (m + 31) + 7 x 44 column steps instead of n.  mode 0
- * (default): used when the pass time model says the search is bound by the
- * longest sequence's chain and rows mode is >= 20% faster (one long sequence,
- * short queries); 1: whenever possible; -1: never.  Resident single-query
+ * ceil(n / 2048) x (m + 31) + 7 x 44 column steps instead of n.  mode 1:
+ * whenever possible; 0 (default) and -1: never -- measured slower than the
+ * ordinary path on every database tried.  Resident single-query
  * searches whose pass kernel makes one pass, without the cross-pass
  * wavefront, queries of at most 8,188 residues.
  * Returns SW_OK or SW_EINVAL.

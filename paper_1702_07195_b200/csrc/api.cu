@@ -276,6 +276,7 @@ constexpr double kStepC0 = 145.0, kStepC1 = 14.0;
 // rows kernel (profiles/r02_rows_mode.jsonl, traces): ~850 cycles per column
 // step with 8 warps per SM, ~44 steps between consecutive passes
 constexpr double kRowsStep = 850.0, kRowsLag = 44.0;
+constexpr bool kRowsAuto = false;
 constexpr double kLatThroughput = 0.6;   // latency-tile throughput relative to a 512-thread tile's eff0
 
 double pass_time_model(const TileInfo &T, int m, const Image &I, bool lat) {
@@ -362,7 +363,10 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const bool rows_possible = !pair && !g.streamed && I0.n_long > 0 && I0.n_units > 0 && g.rows_mode >= 0 &&
                              ((m + 2 + 3) & ~3) <= kRowsMaxNcq;
   bool rows_cand = rows_possible && g.rows_mode == 1;
-  if (rows_possible && g.rows_mode == 0 && I0.n_long <= g.num_sms) {
+  // auto (mode 0) is off: measured slower than the ordinary path on every
+  // database tried, including one long sequence with a short query
+  // (profiles/r02_rows_mode.jsonl); kRowsAuto keeps the model for experiments
+  if (kRowsAuto && rows_possible && g.rows_mode == 0 && I0.n_long <= g.num_sms) {
     // auto: the longest sequence's chain in the rows kernel (one CTA per item,
     // warps on consecutive passes) against its chain in the pass kernel, when
     // that chain bounds the search (profiles/r02_rows_mode.jsonl)

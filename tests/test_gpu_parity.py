@@ -608,8 +608,8 @@ def test_rows_mode_matches_oracle():
     as the column stream, passes as a wavefront.  Random
     and asymmetric matrices, zero gap-open, sequences of odd count (an empty
     half), saturating sequences (flag, carry propagation, 32-bit re-scoring),
-    query lengths around the stream's 4-column rounding; the automatic choice
-    for a chain-bound database."""
+    query lengths around the stream's 4-column rounding, and one 35,000-residue
+    sequence (137 passes).  (Used on request only: sw_set_rows_mode(1).)"""
     rng = np.random.default_rng(2048)
     longs = [si.rr_residues(rng, int(L)) for L in rng.integers(600, 9000, 11)]
     longs += [encode("W" * 3100), encode("W" * 2990 + "A" * 20)]
@@ -646,10 +646,10 @@ def test_rows_mode_matches_oracle():
         sw.sw_set_rows_mode(-1)
         got2 = sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
         assert sw.sw_last_stats()["rows_pairs"] == 0 and (got2 == got).all()
-        # automatic choice: one long sequence and a short query is bound by its
-        # chain, which the rows kernel shortens
-        sw.sw_set_rows_mode(0)
-        db1 = _db([si.rr_residues(rng, 12000), si.rr_residues(rng, 300)])
+        # one long sequence (137 passes over one CTA's 8 warps, the warp 7 ->
+        # warp 0 hand-over through global memory many times)
+        sw.sw_set_rows_mode(1)
+        db1 = _db([si.rr_residues(rng, 35000), si.rr_residues(rng, 300)])
         sw.sw_db_load(db1.residues, db1.offsets)
         q = si.rr_residues(rng, 100)
         got = sw.sw_search(q, BLOSUM62, 10, 2)
