@@ -237,6 +237,19 @@ int sw_last_stats(int64_t *stats, int n);
 int sw_last_timing(float *ms, int n);
 
 /*
+ * sw_timing_history -- the s16x2 pass-kernel device time (ms, sum of its
+ * pass-kernel launches, from the same CUDA events as sw_last_timing) of each
+ * of the last n searches, a batch counting as one search, oldest first, so
+ * that a caller can time a run of back-to-back searches without a
+ * synchronisation per search.  At most the last 64 searches are kept (their
+ * events are reused after that).  Synchronises with the last search.
+ *   ms : host, float[n], written.
+ * Returns the number of entries written (min(n, searches kept)) or a
+ * negative status (SW_EINVAL: NULL or n < 0; SW_ESTATE: no search yet).
+ */
+int sw_timing_history(float *ms, int n);
+
+/*
  * sw_set_tile -- override the (G, R) tile choice for subsequent searches
  * (tests of tile invariance).  G in {8,16,32}; R must be
  * one of the compiled row counts (sw_tile_supported).  G = 0 restores the

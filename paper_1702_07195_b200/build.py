@@ -41,6 +41,8 @@ if os.environ.get("SW_S32ROWS"):  # rows per lane of the 32-bit kernel (experime
 for _k in ("SW_QPTAIL", "SW_TAILADDR", "SW_ROWS_TRACE"):   # profile tail layout experiments (kernels.cuh)
     if os.environ.get(_k):
         NVCC_FLAGS = NVCC_FLAGS + [f"-D{_k}=" + os.environ[_k]]
+if os.environ.get("SW_DEFS"):     # experiment macros: SW_DEFS="SW_X=1 SW_Y=0"
+    NVCC_FLAGS = NVCC_FLAGS + ["-D" + d for d in os.environ["SW_DEFS"].split()]
 if os.environ.get("SW_DEBUG"):    # device-side bounds checks (slow; debug builds)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_DEBUG=1"]
 

@@ -68,7 +68,7 @@ struct DevBuf {
 
 // A device-resident stream image.
 struct Image {
-  DevBuf<uint32_t> stream;  // column words
+  DevBuf<uint16_t> stream;  // column words (16-bit descriptor offsets, 1 B per residue)
   DevBuf<Item> items;
   DevBuf<int64_t> endcol;   // per sequence: 2 * END column + half
   DevBuf<int32_t> slots;    // slot -> original sequence (items' sequences in column order)
@@ -118,8 +118,10 @@ struct State {
   DevBuf<int> pcounters;    // per (chunk, pass) item cursors
   const uint8_t *res_dev = nullptr;  // residues for s32 re-scoring (device or mapped host)
   DevBuf<int64_t> cells32;
-  DevBuf<uint8_t> query, query2;
-  DevBuf<int8_t> matrix;
+  // per-search inputs in one device buffer: matrix (576 B), query, query 2
+  DevBuf<uint8_t> qin;
+  const uint8_t *q_d = nullptr, *q2_d = nullptr;
+  const int8_t *mat_d = nullptr;
   DevBuf<uint8_t> qp;
   DevBuf<uint4> desc;
   DevBuf<int32_t> qp32, qp32b;
@@ -127,7 +129,7 @@ struct State {
   DevBuf<int32_t> skip;     // per item: dead leading columns for the next pass
   DevBuf<uint8_t> item_hot; // per item: a low-half sequence flagged (carry propagation, R7)
   DevBuf<uint2> dummy;      // scratch for idle-lane stores (16-B slot per thread)
-  DevBuf<uint32_t> nulcols; // 16 NUL column words
+  DevBuf<uint16_t> nulcols; // 16 NUL column words
   DevBuf<uint2> zerocols;   // 16 zero boundary columns
   DevBuf<uint2> scratch32;
   DevBuf<uint64_t> keys;
@@ -157,7 +159,14 @@ struct State {
   DevBuf<int> progress;     // wavefront: finished columns per (pass, item)
   // timing events of the last search
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  std::vector<cudaEvent_t> pev;   // (start, end) of every pass-kernel launch of the last search
+  // (start, end) of every pass-kernel launch of the last kHist searches (a
+  // batch is one), a ring: slot hslot is the last search's (sw_timing_history)
+  static constexpr int kHist = 64;
+  std::vector<cudaEvent_t> hpev[kHist];
+  int hnpev[kHist] = {};
+  int hslot = 0;
+  int64_t nsearch = 0;
+  std::vector<cudaEvent_t> *pevp = &hpev[0];
   int npev = 0;                   // pairs recorded by the last search (or batch)
   bool batch_cont = false;        // search_core continues a batch: keep ev[0] and the pass events
   // ---- streamed (out-of-core) database, SURVEY 8(f) NEXT-3
@@ -169,9 +178,8 @@ struct State {
   bool streamed = false;
   std::vector<Chunk> chunks;
   int64_t chunk_span = 0;       // max columns of a chunk
-  uint16_t *h_stream = nullptr; // pinned host image, compact: letter-pair index per column (2 B)
+  uint16_t *h_stream = nullptr; // pinned host image: 16-bit column words (1 B per residue)
   uint8_t *h_res = nullptr;     // pinned, mapped host copy of the residues (s32 re-scoring)
-  DevBuf<uint32_t> cbuf[2];     // device chunk buffers (double-buffered), column words
   DevBuf<uint16_t> cbuf16[2];   // their compact copies as they arrive over the host link
   DevBuf<int32_t> cseq_idx;     // sequences grouped by chunk
   DevBuf<int64_t> cseq_endcol;  // their END columns (global image columns)
@@ -183,7 +191,7 @@ struct State {
     if (h_res) cudaFreeHost(h_res);
     h_stream = nullptr;
     h_res = nullptr;
-    cbuf[0].release(); cbuf[1].release(); cbuf16[0].release(); cbuf16[1].release();
+    cbuf16[0].release(); cbuf16[1].release();
     cseq_idx.release(); cseq_endcol.release();
     for (int k = 0; k < 2; ++k) {
       if (ev_copied[k]) cudaEventDestroy(ev_copied[k]);
@@ -202,7 +210,7 @@ struct State {
     sc_out.release(); res.release(); offs.release();
     scores.release(); bscores.release(); flagged.release(); flagged2.release(); flag_list.release();
     flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release(); progress.release();
-    query.release(); query2.release(); matrix.release(); qp.release(); desc.release(); qp32.release();
+    qin.release(); qp.release(); desc.release(); qp32.release();
     qp32b.release(); bnd.release(); skip.release(); item_hot.release();
     rows_wrap.release(); rows_prog.release();
     scratch32.release(); dummy.release(); nulcols.release(); zerocols.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
@@ -214,6 +222,21 @@ struct State {
 
 State g;
 constexpr int kMaxPass = 4096;
+
+// The per-search inputs (matrix, query, query 2) cross the host link in ONE
+// copy from a pinned staging slot: a copy from pageable memory may wait for
+// the stream (the host could not enqueue a search before the previous one
+// ends, and every launch latency would be exposed).  Slots are reused round
+// robin, each guarded by the event recorded after its copy.  Independent of
+// the loaded database (kept across sw_db_load / sw_db_free).
+struct Staging {
+  static constexpr int kSlots = 4;
+  uint8_t *h[kSlots] = {};
+  size_t cap[kSlots] = {};
+  cudaEvent_t ev[kSlots] = {};
+  int next = 0;
+};
+Staging g_stage;
 bool g_kernels_ready = false;
 
 int ensure_device_ready() {
@@ -464,9 +487,26 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   g.last_thresh = thresh - kBias16;  // in score units
   const int goe = gap_open + gap_extend, ge = gap_extend;
 
-  CUDA_TRY(g.query.ensure((size_t)m));
-  if (pair) CUDA_TRY(g.query2.ensure((size_t)m2));
-  CUDA_TRY(g.matrix.ensure(kAlpha * kAlpha));
+  const size_t in_bytes = (size_t)kAlpha * kAlpha + (size_t)m + (pair ? (size_t)m2 : 0);
+  CUDA_TRY(g.qin.ensure(in_bytes));
+  const int slot = g_stage.next;
+  g_stage.next = (slot + 1) % Staging::kSlots;
+  if (g_stage.ev[slot]) CUDA_TRY(cudaEventSynchronize(g_stage.ev[slot]));   // its previous copy is done
+  else CUDA_TRY(cudaEventCreateWithFlags(&g_stage.ev[slot], cudaEventDisableTiming));
+  if (g_stage.cap[slot] < in_bytes) {
+    if (g_stage.h[slot]) cudaFreeHost(g_stage.h[slot]);
+    g_stage.h[slot] = nullptr;
+    g_stage.cap[slot] = 0;
+    const size_t cap = std::max<size_t>(in_bytes, 64 * 1024);
+    CUDA_TRY(cudaHostAlloc(&g_stage.h[slot], cap, cudaHostAllocDefault));
+    g_stage.cap[slot] = cap;
+  }
+  std::memcpy(g_stage.h[slot], matrix, (size_t)kAlpha * kAlpha);
+  std::memcpy(g_stage.h[slot] + kAlpha * kAlpha, q, (size_t)m);
+  if (pair) std::memcpy(g_stage.h[slot] + kAlpha * kAlpha + m, q2, (size_t)m2);
+  g.mat_d = reinterpret_cast<const int8_t *>(g.qin.p);
+  g.q_d = g.qin.p + kAlpha * kAlpha;
+  g.q2_d = pair ? g.q_d + m : nullptr;
   CUDA_TRY(g.qp.ensure(qp_bytes(T.G, T.R, P, T.qpm)));
   CUDA_TRY(g.desc.ensure((size_t)kNL * kNL));
   CUDA_TRY(g.qp32.ensure((size_t)kNL * mm));
@@ -476,39 +516,39 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // is shared by every search: order this search's device work after the
   // previous one's, whatever stream that ran on (ev[3] marks its end).
   if (g.has_search && g.ev[3]) CUDA_TRY(cudaStreamWaitEvent(st, g.ev[3], 0));
-  CUDA_TRY(cudaMemcpyAsync(g.query.p, q, (size_t)m, cudaMemcpyHostToDevice, st));
-  if (pair) CUDA_TRY(cudaMemcpyAsync(g.query2.p, q2, (size_t)m2, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(g.matrix.p, matrix, kAlpha * kAlpha, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(g.qin.p, g_stage.h[slot], in_bytes, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaEventRecord(g_stage.ev[slot], st));
   // 32-bit re-scoring counters: (count, cursor) per (pass, query of the pair),
-  // plus one set for the end-of-search launch
+  // plus one set for the end-of-search launch; flags; carry marks
   CUDA_TRY(g.fcounters.ensure((size_t)4 * (P + 1)));
-  CUDA_TRY(cudaMemsetAsync(g.fcounters.p, 0, sizeof(int) * 4 * (P + 1), st));
-  CUDA_TRY(cudaMemsetAsync(g.flagged.p, 0, (size_t)g.count, st));
-  if (pair) CUDA_TRY(cudaMemsetAsync(g.flagged2.p, 0, (size_t)g.count, st));
-  CUDA_TRY(cudaMemsetAsync(g.cells32.p, 0, sizeof(int64_t), st));
   const int32_t *item_of = pair ? nullptr : g.img[0].item_of.p;
-  if (!pair) {
-    CUDA_TRY(g.item_hot.ensure((size_t)std::max(1, g.img[0].num_items)));
-    CUDA_TRY(cudaMemsetAsync(g.item_hot.p, 0, (size_t)std::max(1, g.img[0].num_items), st));
-  }
+  if (!pair) CUDA_TRY(g.item_hot.ensure((size_t)std::max(1, g.img[0].num_items)));
+  CUDA_TRY(launch_search_init(g.fcounters.p, 4 * (P + 1), g.flagged.p, pair ? g.flagged2.p : nullptr, g.count,
+                              g.cells32.p, pair ? nullptr : g.item_hot.p, pair ? 0 : std::max(1, g.img[0].num_items),
+                              st));
   if (!g.ev[0])
     for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g.ev[i]));
   // a batch's timing spans all of its searches (sw_last_timing)
   if (!g.batch_cont) {
     CUDA_TRY(cudaEventRecord(g.ev[0], st));
+    g.hslot = (g.hslot + 1) % State::kHist;
+    g.pevp = &g.hpev[g.hslot];
+    g.hnpev[g.hslot] = 0;
+    ++g.nsearch;
     g.npev = 0;
   }
+  std::vector<cudaEvent_t> &pev = *g.pevp;
   auto pass_event = [&](int idx) -> cudaError_t {   // event slot idx of this search's launches
-    while (g.pev.size() < (size_t)idx + 1) {
+    while (pev.size() < (size_t)idx + 1) {
       cudaEvent_t e;
       cudaError_t er = cudaEventCreate(&e);
       if (er != cudaSuccess) return er;
-      g.pev.push_back(e);
+      pev.push_back(e);
     }
     return cudaSuccess;
   };
   const int pev0 = 2 * g.npev;
-  CUDA_TRY(launch_qp_build(g.query.p, m, pair ? g.query2.p : nullptr, m2, g.matrix.p, T.G, T.R, P, g.qp.p,
+  CUDA_TRY(launch_qp_build(g.q_d, m, pair ? g.q2_d : nullptr, m2, g.mat_d, T.G, T.R, P, g.qp.p,
                            g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr,
                            goe, ge, st, use_sp ? 1 : 0));
 
@@ -521,15 +561,17 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // the end, from row 0.
   // The flag byte is min(pass + 1, 255): passes >= 254 share the value 255 and
   // are re-scored at the end, from row 0.
-  auto rescore = [&](int k, int pass, const uint2 *bnd16) -> cudaError_t {
+  // compacted: the flag list of (pass, k) was already written by the update launch
+  auto rescore = [&](int k, int pass, const uint2 *bnd16, bool compacted = false) -> cudaError_t {
     const bool early = pass >= 0 && pass + 1 < 255;
     const int slot = early ? pass : P;
     int *cnt = g.fcounters.p + 4 * slot + 2 * k;
     const int row0 = early ? pass * rows : 0;
     const int want = pass < 0 ? 0 : (early ? pass + 1 : 255);
     const int len = k ? m2 : m;
-    cudaError_t e = launch_flag_compact(k ? g.flagged2.p : g.flagged.p, g.count, k ? g.flag_list2.p : g.flag_list.p,
-                                        cnt, want, st);
+    cudaError_t e = compacted ? cudaSuccess
+                              : launch_flag_compact(k ? g.flagged2.p : g.flagged.p, g.count,
+                                                    k ? g.flag_list2.p : g.flag_list.p, cnt, want, st);
     if (e != cudaSuccess || row0 >= len) return e;
     SW32Params q{};
     q.flag_list = k ? g.flag_list2.p : g.flag_list.p;
@@ -601,17 +643,18 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     p.bndbuf[0] = g.bnd.p;
     p.bndbuf[1] = g.bnd.p + span;
     CUDA_TRY(pass_event(pev0 + 1));
-    CUDA_TRY(cudaEventRecord(g.pev[pev0], st));
+    CUDA_TRY(cudaEventRecord(pev[pev0], st));
     // every CTA must be resident: a wavefront CTA may wait on another's progress
     CUDA_TRY(launch_sw16_pass(ti, g.num_sms * tile_wave_ctas_per_sm(ti), p, st));
-    CUDA_TRY(cudaEventRecord(g.pev[pev0 + 1], st));
+    CUDA_TRY(cudaEventRecord(pev[pev0 + 1], st));
     g.npev = pev0 / 2 + 1;
+    g.hnpev[g.hslot] = g.npev;
     // the score chain was carried through the passes: one gather of the maxima
     CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p, nullptr, nullptr, 0,
                                 thresh, st, nullptr, item_of, g.item_hot.p));
   }
   for (int k = 0; k < (wave ? 0 : nch); ++k) {
-    const uint32_t *stream_base = I.stream.p;
+    const uint16_t *stream_base = I.stream.p;
     const Item *items = I.items.p;
     int nitems = I.num_items;
     int64_t base = 0;
@@ -620,15 +663,14 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       const State::Chunk &c = g.chunks[k];
       // the buffer is free once the passes of the chunk that used it last are done
       CUDA_TRY(cudaStreamWaitEvent(g.copy_st, g.ev_free[b], 0));
-      // the compact image crosses the host link (2 B per column, 1 B per
-      // residue) and is expanded to column words on the device
+      // the image crosses the host link as it is (2 B per column, 1 B per
+      // residue) and the passes read it in the device buffer
       CUDA_TRY(cudaMemcpyAsync(g.cbuf16[b].p, g.h_stream + c.col_begin, (size_t)(c.col_end - c.col_begin) * 2,
                                cudaMemcpyHostToDevice, g.copy_st));
       CUDA_TRY(cudaEventRecord(g.ev_copied[b], g.copy_st));
       CUDA_TRY(cudaStreamWaitEvent(st, g.ev_copied[b], 0));
-      CUDA_TRY(launch_expand_columns(g.cbuf16[b].p, c.col_end - c.col_begin, g.cbuf[b].p, st));
       base = c.col_begin;
-      stream_base = g.cbuf[b].p - base;     // so that item.col_begin indexes the buffer
+      stream_base = g.cbuf16[b].p - base;     // so that item.col_begin indexes the buffer
       items = I.items.p + c.item_begin;
       nitems = c.item_end - c.item_begin;
     }
@@ -656,18 +698,18 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       // its leading run of flagged sequences (item_skip_kernel below)
       const bool skipping = !strm && !pair && P > 1;
       p.skip = (skipping && pass > 0) ? g.skip.p : nullptr;
-      p.query = g.query.p;
+      p.query = g.q_d;
       p.m = m;
       const int pe = pev0 + 2 * (k * P + pass);
       CUDA_TRY(pass_event(pe + 1));
-      CUDA_TRY(cudaEventRecord(g.pev[pe], st));
+      CUDA_TRY(cudaEventRecord(pev[pe], st));
       CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
       if (rowsm) {   // the long pairs, rows along the database sequence (before the gather reads sc_out)
         RowsParams r{};
-        r.query = g.query.p;
+        r.query = g.q_d;
         r.m = m;
         r.ncq = ncq;
-        r.matrix = g.matrix.p;
+        r.matrix = g.mat_d;
         r.res = g.res.p;
         r.offs = g.offs.p;
         r.items = I0.items.p;
@@ -682,19 +724,25 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
         r.one = 1u;
         CUDA_TRY(launch_sw16_rows(g.num_sms, r, st));
       }
-      CUDA_TRY(cudaEventRecord(g.pev[pe + 1], st));
+      CUDA_TRY(cudaEventRecord(pev[pe + 1], st));
       g.npev = pe / 2 + 1;
+      g.hnpev[g.hslot] = g.npev;
       if (strm) {
         const State::Chunk &c = g.chunks[k];
         CUDA_TRY(launch_sw16_gather(g.cseq_endcol.p + c.seq_begin, c.seq_end - c.seq_begin, g.sc_out.p - base,
                                     d_scores, g.flagged.p, nullptr, nullptr, pass, thresh, st,
                                     g.cseq_idx.p + c.seq_begin, item_of, g.item_hot.p));
       } else {
+        // the update launch also compacts the sequences first flagged in this
+        // pass for the 32-bit kernel (passes < 254; flag byte pass + 1)
+        const bool fuse = pass + 1 < 255;
         CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p,
                                     pair ? d_scores2 : nullptr, pair ? g.flagged2.p : nullptr, pass, thresh, st,
-                                    nullptr, item_of, pair ? nullptr : g.item_hot.p));
-        if (pass + 1 < 255)
-          for (int k = 0; k < (pair ? 2 : 1); ++k) CUDA_TRY(rescore(k, pass, p.bnd_in));
+                                    nullptr, item_of, pair ? nullptr : g.item_hot.p, g.flag_list.p,
+                                    g.fcounters.p + 4 * pass, pair ? g.flag_list2.p : nullptr,
+                                    g.fcounters.p + 4 * pass + 2, fuse ? pass + 1 : 0));
+        if (fuse)
+          for (int k = 0; k < (pair ? 2 : 1); ++k) CUDA_TRY(rescore(k, pass, p.bnd_in, true));
         if (skipping && pass + 1 < P)
           CUDA_TRY(launch_item_skip(I.items.p, I.num_items, I.slots.p, g.offs.p, g.flagged.p, g.skip.p, st));
       }
@@ -900,14 +948,14 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
     if (strm) continue;
     CUDA_TRY(I.stream.ensure(H.stream.size()));
     CUDA_TRY(I.endcol.ensure(H.endcol.size()));
-    CUDA_TRY(cudaMemcpy(I.stream.p, H.stream.data(), H.stream.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(I.stream.p, H.stream.data(), H.stream.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(I.endcol.p, H.endcol.data(), H.endcol.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     CUDA_TRY(I.slots.ensure(H.slots.size()));
     CUDA_TRY(cudaMemcpy(I.slots.p, H.slots.data(), H.slots.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
   if (strm) {
     const HostImage &H = himg[0];
-    const int64_t chunk_cols = std::max<int64_t>(chunk_bytes / 4, 1);
+    const int64_t chunk_cols = std::max<int64_t>(chunk_bytes / 2, 1);
     // chunks: maximal runs of consecutive items whose columns (with the NUL
     // padding on both sides) fit chunk_cols; an item longer than that is a
     // chunk of its own
@@ -954,9 +1002,8 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
     CUDA_TRY(cudaMemcpy(g.cseq_idx.p, idx.data(), idx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(g.cseq_endcol.p, ecol.data(), ecol.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaHostAlloc(&g.h_stream, H.stream.size() * sizeof(uint16_t), cudaHostAllocDefault));
-    for (size_t i = 0; i < H.stream.size(); ++i) g.h_stream[i] = (uint16_t)(H.stream[i] / kDescBytes);
+    std::memcpy(g.h_stream, H.stream.data(), H.stream.size() * sizeof(uint16_t));
     for (int k = 0; k < 2; ++k) {
-      CUDA_TRY(g.cbuf[k].ensure((size_t)span));
       CUDA_TRY(g.cbuf16[k].ensure((size_t)span + 8));
       CUDA_TRY(cudaEventCreateWithFlags(&g.ev_copied[k], cudaEventDisableTiming));
       CUDA_TRY(cudaEventCreateWithFlags(&g.ev_free[k], cudaEventDisableTiming));
@@ -988,8 +1035,8 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
   {
     CUDA_TRY(g.nulcols.ensure(16));
     CUDA_TRY(g.zerocols.ensure(16));
-    std::vector<uint32_t> nw(16, column_word(kNul, kNul));
-    CUDA_TRY(cudaMemcpy(g.nulcols.p, nw.data(), 16 * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    std::vector<uint16_t> nw(16, column_word(kNul, kNul));
+    CUDA_TRY(cudaMemcpy(g.nulcols.p, nw.data(), 16 * sizeof(uint16_t), cudaMemcpyHostToDevice));
     {
       std::vector<uint2> zc(16, make_uint2((uint32_t)kBias16 * 0x10001u, (uint32_t)kBias16 * 0x10001u));
       CUDA_TRY(cudaMemcpy(g.zerocols.p, zc.data(), 16 * sizeof(uint2), cudaMemcpyHostToDevice));
@@ -1173,13 +1220,35 @@ int sw_last_timing(float *ms, int n) {
   float a = 0.f, b = 0.f;
   for (int i = 0; i < g.npev; ++i) {   // sum of the pass-kernel launches only
     float x = 0.f;
-    CUDA_TRY(cudaEventElapsedTime(&x, g.pev[2 * i], g.pev[2 * i + 1]));
+    CUDA_TRY(cudaEventElapsedTime(&x, (*g.pevp)[2 * i], (*g.pevp)[2 * i + 1]));
     a += x;
   }
   CUDA_TRY(cudaEventElapsedTime(&b, g.ev[0], g.ev[3]));
   const float v[2] = {a, b};
   const int m = std::min(n, 2);
   for (int i = 0; i < m; ++i) ms[i] = v[i];
+  return m;
+}
+
+int sw_timing_history(float *ms, int n) {
+  t_err.clear();
+  if (!ms || n < 0) return fail(SW_EINVAL, "bad arguments");
+  if (!g.has_search || !g.ev[0]) return fail(SW_ESTATE, "no completed search");
+  // every search waits for the previous one's end (ev[3]): the last search's
+  // end orders all of them
+  CUDA_TRY(cudaEventSynchronize(g.ev[3]));
+  const int avail = (int)std::min<int64_t>(g.nsearch, State::kHist);
+  const int m = std::min(n, avail);
+  for (int i = 0; i < m; ++i) {   // oldest first
+    const int slot = ((g.hslot - (m - 1 - i)) % State::kHist + State::kHist) % State::kHist;
+    float a = 0.f;
+    for (int j = 0; j < g.hnpev[slot]; ++j) {
+      float x = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&x, g.hpev[slot][2 * j], g.hpev[slot][2 * j + 1]));
+      a += x;
+    }
+    ms[i] = a;
+  }
   return m;
 }
 

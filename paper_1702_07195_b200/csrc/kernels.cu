@@ -47,6 +47,18 @@
 #ifndef SW_ROWS_TRACE
 #define SW_ROWS_TRACE 0   // 1: the rows kernel prints per-pass cycle counts of item 0 (experiments)
 #endif
+#ifndef SW_EARLY
+#define SW_EARLY 1   // latency tiles load each column's descriptor and profile one step ahead
+#endif
+#ifndef SW_LATROWS
+#define SW_LATROWS 1   // EARLY tiles: Eq. 3 with a one-instruction vertical chain (Goe >= Ge)
+#endif
+#ifndef SW_SCEND
+#define SW_SCEND 0   // 1: lane G-1 stores the score chain at separator columns only (experiment)
+#endif
+#ifndef SW_DESCADDR
+#define SW_DESCADDR 0   // 1: lane G-1's descriptor address from s_qp instead of s_desc (experiment)
+#endif
 #ifndef SW_TAILADDR
 #define SW_TAILADDR 0   // narrow-tail address: 0 = IMAD from the profile offset, 1 = from the chunk address
 #endif
@@ -235,6 +247,7 @@ template <int R, int G, bool BIN, int QPM, int NT, int U, bool WAVE = false>
 __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   static_assert(!WAVE || BIN, "the wavefront kernel reads boundaries (from pass 1 on)");
   static_assert(U == 1 || U == 2 || U == 4, "U: columns per unrolled block / prefetch distance");
+  static_assert(!(SW_EARLY && NT == 256) || U % 2 == 0, "EARLY alternates two profile sets per column");
   static_assert(QPM == 0 || QPM == 1 || QPM == 3, "profile mode");
   static_assert(QPM != 1 || kBiased, "the score profile is built for the biased arithmetic");
   constexpr int RPC = 4;                    // rows per 16-B profile chunk
@@ -312,9 +325,13 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   // boundary for the next pass.  A group without items keeps feeding NUL
   // columns; its pointers stop (increment 0) on the NUL padding / own slot.
   uint2 *const dummy = p.dummy + (blockIdx.x * blockDim.x + threadIdx.x);
-  const uint32_t *sptr = p.nul_stream;
+  const uint16_t *sptr = p.nul_stream;
   const uint2 *bptr = p.zero_bnd;
+  // SW_SCEND (not in the wavefront): every lane stores the chain at separator
+  // columns, lanes t < G-1 into their own dummy slot (no lane predicate)
+  constexpr bool SCEND = SW_SCEND && !WAVE;
   uint32_t *scp = reinterpret_cast<uint32_t *>(dummy);
+  uint32_t scinc = 0u;
   uint2 *bop = dummy;
   uint32_t inc = 0u;
   int rem = 0;                                   // steps left in the current item
@@ -330,6 +347,52 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   for (int u = 0; u < (WAVE ? U : 1); ++u) scring[u] = 0u;
   const uint32_t *scin = nullptr;  // WAVE: sc_out of the item's columns (previous pass)
   int cur_it = 0, cur_ncols = 0, sdone = 0, avail = 0;   // WAVE progress bookkeeping
+  // EARLY (latency tiles): a group's step is a latency chain
+  // when one long item bounds the pass.  Each lane receives its NEXT column's
+  // profile offsets one step early and loads that column's profile chunks
+  // during the current column's rows; lane G-1 loads lane 0's descriptors one
+  // column ahead.  The per-step chain is then shuffle -> rows -> shuffle,
+  // without the descriptor load, the second shuffle and the profile load.
+  constexpr bool EARLY = SW_EARLY && NT == 256 && QPM == 0 && !WAVE;
+  // LROWS (EARLY tiles): with the loads off the step's chain, the chain is the
+  // vertical F recurrence through the lane's R rows (3 dependent DPX per row).
+  // Eq. 3 as F' = max(F - Ge, max(max(t, E) - Goe, 0)) -- equal to
+  // max(F - Ge, max(H - Goe, 0)) since Goe >= Ge (H - Goe's F term is below
+  // F - Ge) -- is one VIADDMNMX per row on the chain, for 1.5 more ALU
+  // instructions per pair of cells off it.
+  constexpr bool LROWS = EARLY && SW_LATROWS;
+  constexpr int KCE = EARLY ? KC : 1;
+  // EARLY: profile chunks and offsets (descriptor word 0) of the lane's
+  // current column ([u & 1]) and next column ([(u + 1) & 1]): U is even, so
+  // the two sets alternate through the unrolled block without copies
+  uint4 pa[2][KCE], pb[2][KCE];
+  uint32_t w0b[2] = {nul.w0, nul.w0};
+  // EARLY, lane G-1: descriptors of lane 0's next column ([u & 1]) and the one
+  // after ([(u + 1) & 1]); other lanes keep zeros (word 0 enters an IMAD)
+  DescWords dq[2] = {{0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}};
+  // EARLY: all KC profile chunks (4 rows each; the narrow tail) of the column whose
+  // descriptor word 0 is w
+  auto load_prof = [&](uint32_t w, uint4 *xa, uint4 *xb) {
+    const uint32_t oB = umulhi(w, 65536u);
+    const uint32_t oA = imad(oB, 0xffff0000u, w);
+    const uint32_t a = imad(oA, 16u, s_qp), b = imad(oB, 16u, s_qp);
+    const uint32_t at = TW ? imad(oA, 16u, s_qpt) : 0u, bt = TW ? imad(oB, 16u, s_qpt) : 0u;
+#pragma unroll
+    for (int kk = 0; kk < KCE; ++kk) {
+      if (kk < KCF) {
+        xa[kk] = lds128(a + kk * G * 16);
+        xb[kk] = lds128(b + kk * G * 16);
+      } else if (TW == 4) {
+        xa[kk] = make_uint4(lds32(at), 0u, 0u, 0u);
+        xb[kk] = make_uint4(lds32(bt), 0u, 0u, 0u);
+      } else {
+        const uint2 va = lds64(at), vb = lds64(bt);
+        xa[kk] = make_uint4(va.x, va.y, 0u, 0u);
+        xb[kk] = make_uint4(vb.x, vb.y, 0u, 0u);
+      }
+    }
+  };
+  if (EARLY) load_prof(nul.w0, pa[0], pb[0]);
 
   // Passes: one per launch (p.pass), or all of them in a cross-pass wavefront
   // (WAVE): the CTA runs pass p's items (profile slice p in shared memory)
@@ -363,7 +426,8 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         sptr = p.stream + c0;
         if (BIN) bptr = bnd_in ? bnd_in + c0 : p.zero_bnd;
         bcols = (BIN && bnd_in) ? ncols : 0;   // no input boundary: every column reads as zero
-        scp = p.sc_out + (c0 - (G - 1));
+        scp = (SCEND && !last) ? reinterpret_cast<uint32_t *>(dummy) : p.sc_out + (c0 - (G - 1));
+        scinc = (SCEND && !last) ? 0u : (uint32_t)U;
         if (bnd_out) bop = bnd_out + (c0 - (G - 1));
         if (WAVE) {
           scin = p.sc_out + c0;
@@ -377,10 +441,11 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           }
         }
         if (last) {
-          // ring slot x % U holds column x; columns 1..U are prefetched here
+          // ring slot x % U holds column x; columns 1..U (EARLY: 2..U+1) are prefetched here
+          if (EARLY) dq[0] = load_desc(s_desc + __ldg(sptr + 1));   // lane 0's second column (u = 0 next)
 #pragma unroll
           for (int u = 1; u <= U; ++u) {
-            sring[u % U] = __ldg(sptr + u);
+            sring[(u + EARLY) % U] = __ldg(sptr + u + EARLY);
             if (BIN && BRING)
               bring[u % U] = u < bcols ? (WAVE ? ld_cg_v2(bptr + u) : __ldg(bptr + u)) : make_uint2(kB2, kB2);
             if (WAVE) scring[u % U] = u < bcols ? ld_cg(scin + u) : 0u;
@@ -403,6 +468,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         sptr = p.nul_stream;               // NUL columns
         if (BIN) bptr = p.zero_bnd;        // zero boundary
         scp = reinterpret_cast<uint32_t *>(dummy);
+        scinc = 0u;
         bop = dummy;
         if (WAVE) {
           scin = nullptr;
@@ -417,9 +483,17 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           ngoe = nul.ngoe;
           nge = nul.nge;
           knext = nul.kneg;
+          if (EARLY) dq[0] = nul;
           hout = kB2;
           fout = kB2;
           sc = 0u;
+        }
+      }
+      if (EARLY) {   // lane 0 starts a new stream: its current column's profile (others keep theirs)
+        const uint32_t w00 = __shfl_sync(gmask, w0, gbase + G - 1);
+        if (t == 0) {   // the block starts at u = 0
+          w0b[0] = w00;
+          load_prof(w00, pa[0], pb[0]);
         }
       }
     }
@@ -437,13 +511,19 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       // ---- this column's inputs from lane t-1 (lane 0: from lane G-1)
-      w0 = __shfl_sync(0xffffffffu, w0, src);
+      if (!EARLY) w0 = __shfl_sync(0xffffffffu, w0, src);
       ngoe = __shfl_sync(0xffffffffu, ngoe, src);
       nge = __shfl_sync(0xffffffffu, nge, src);
       knext = __shfl_sync(0xffffffffu, knext, src);
       const uint32_t hu = __shfl_sync(0xffffffffu, hout, src);
       uint32_t F = __shfl_sync(0xffffffffu, fout, src);
       const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
+      // EARLY: the next column's profile offsets (lane G-1 sends lane 0's next
+      // column's) and its profile chunks, loaded during this column's rows
+      if (EARLY) {
+        w0b[(u + 1) & 1] = __shfl_sync(0xffffffffu, imad(w0b[u & 1], nlast, dq[u & 1].w0), src);
+        load_prof(w0b[(u + 1) & 1], pa[(u + 1) & 1], pb[(u + 1) & 1]);
+      }
       // ---- profile addresses (FMA pipe)
       const uint32_t offB = umulhi(w0, 65536u);           // profile offsets / 16
       const uint32_t offA = imad(offB, 0xffff0000u, w0);
@@ -474,10 +554,16 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       // still needs its own column's penalty words)
       const uint32_t dnext = sring[(u + 1) % U];
       if (last) {
-        SW_CHECK(sptr == p.nul_stream ? (u + 1 + U < 16)
-                                      : (sptr + u + 1 + U - p.stream >= p.col_lo &&
-                                         sptr + u + 1 + U - p.stream < p.col_hi));
-        sring[(u + 1) % U] = __ldg(sptr + u + 1 + U);
+        SW_CHECK(sptr == p.nul_stream ? (u + 1 + EARLY + U < 16)
+                                      : (sptr + u + 1 + EARLY + U - p.stream >= p.col_lo &&
+                                         sptr + u + 1 + EARLY + U - p.stream < p.col_hi));
+        if (EARLY) {   // lane 0's column after next
+          // (s_desc + word, from lane G-1's s_qp: s_desc is otherwise rematerialised per column)
+          dq[(u + 1) & 1] = load_desc(s_qp + sring[(u + 2) % U] - (uint32_t)(DESC_U4 * 16 + (G - 1) * 16));
+          sring[(u + 2) % U] = __ldg(sptr + u + 2 + U);
+        } else {
+          sring[(u + 1) % U] = __ldg(sptr + u + 1 + U);
+        }
         if (BIN && BRING) {
           bnext = bring[(u + 1) % U];
           SW_CHECK(u + 1 + U >= bcols || (bptr + u + 1 + U - bnd_in >= p.col_lo &&
@@ -520,7 +606,8 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         // register (no per-column rotation of the H registers, which otherwise
         // costs a register permutation at every loop back-edge).
         // P(r) = SM(q_r, dB) * 65536 + SM(q_r, dA) (QPM 0) or the profile word (QPM 3).
-        uint4 ca = ldq(aA, aAt, 0), cb = QPM == 0 ? ldq(aB, aBt, 0) : make_uint4(0u, 0u, 0u, 0u);
+        uint4 ca = EARLY ? pa[u & 1][0] : ldq(aA, aAt, 0);
+        uint4 cb = EARLY ? pb[u & 1][0] : (QPM == 0 ? ldq(aB, aBt, 0) : make_uint4(0u, 0u, 0u, 0u));
         uint32_t tcur = imad(hd, one, QPM == 0 ? imad(cb.x, 65536u, ca.x) : ca.x);
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk) {
@@ -530,8 +617,8 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
                                 aBt + TW <= s_desc + (DESC_U4 + QP_U4) * 16));
           uint4 na = make_uint4(0u, 0u, 0u, 0u), nb = make_uint4(0u, 0u, 0u, 0u);
           if (kk + 1 < KC) {
-            na = ldq(aA, aAt, kk + 1);
-            if (QPM == 0) nb = ldq(aB, aBt, kk + 1);
+            na = EARLY ? pa[u & 1][EARLY ? kk + 1 : 0] : ldq(aA, aAt, kk + 1);
+            if (QPM == 0) nb = EARLY ? pb[u & 1][EARLY ? kk + 1 : 0] : ldq(aB, aBt, kk + 1);
           }
           const uint32_t av[8] = {ca.x, ca.y, ca.z, ca.w, na.x, na.y, na.z, na.w};
           const uint32_t bv[8] = {cb.x, cb.y, cb.z, cb.w, nb.x, nb.y, nb.z, nb.w};
@@ -542,11 +629,21 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
               uint32_t tnext = 0u;
               if (r + 1 < R)
                 tnext = imad(H[r], one, QPM == 0 ? imad(bv[j + 1], 65536u, av[j + 1]) : av[j + 1]);
-              const uint32_t h = hmax3(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
-              H[r] = h;
-              const uint32_t hg = haddmax(h, ngoe, kB2);  // max(H-Goe, 0)
-              E[r] = haddmax(E[r], nge, hg);              // Eq. 2 (next column)
-              F = haddmax(F, nge, hg);                    // Eq. 3 (next row)
+              if (LROWS) {
+                const uint32_t a = hmax(tcur, E[r]);
+                const uint32_t uu = haddmax(a, ngoe, kB2);  // max(max(t, E) - Goe, 0): off the F chain
+                const uint32_t h = hmax(a, F);              // Eq. 1
+                H[r] = h;
+                const uint32_t hg = haddmax(h, ngoe, kB2);  // max(H-Goe, 0)
+                E[r] = haddmax(E[r], nge, hg);              // Eq. 2 (next column)
+                F = haddmax(F, nge, uu);                    // Eq. 3 (next row), Goe >= Ge
+              } else {
+                const uint32_t h = hmax3(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
+                H[r] = h;
+                const uint32_t hg = haddmax(h, ngoe, kB2);  // max(H-Goe, 0)
+                E[r] = haddmax(E[r], nge, hg);              // Eq. 2 (next column)
+                F = haddmax(F, nge, hg);                    // Eq. 3 (next row)
+              }
               tcur = tnext;
             }
           }
@@ -610,13 +707,22 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
                (scp + u - p.sc_out >= p.col_lo && scp + u - p.sc_out < p.col_hi));
       SW_CHECK(!bout || bop == dummy || (bop + u - bnd_out >= p.col_lo && bop + u - bnd_out < p.col_hi));
       if (last) {
-        const DescWords d = load_desc(s_desc + dnext);
-        w0 = d.w0;
+        // s_desc + dnext, written from lane G-1's own s_qp (t = G-1): a register
+        // the loop keeps anyway (s_desc itself is rematerialised per column
+        // from SR_CgaCtaId under the register cap: 4 instructions)
+#if SW_DESCADDR
+        const DescWords d = EARLY ? dq[u & 1] : load_desc(s_qp + dnext - (uint32_t)(DESC_U4 * 16 + (G - 1) * 16));
+#else
+        const DescWords d = EARLY ? dq[u & 1] : load_desc(s_desc + dnext);
+#endif
+        if (!EARLY) w0 = d.w0;   // (EARLY: word 0 went to lane 0 one step ago)
         ngoe = d.ngoe;
         nge = d.nge;
         knext = d.kneg;
       }
-      if (last) st_global_u32(scp + u, so);
+      // the score chain is read at END columns only (and, in the wavefront,
+      // at every column by the next pass): SW_SCEND stores separator columns only
+      if (SCEND ? kneg != 0u : last) st_global_u32(scp + u, so);
       if (bout) st_global_v2(bop + u, H[R - 1], F);
       // outgoing registers; lane G-1 hands over lane 0's next-column inputs
       hout = imad(H[R - 1], nlast, bnext.x);
@@ -627,7 +733,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
     if (BIN) bcols -= U;
     sptr = ptr_add(sptr, inc);
     if (BIN) bptr = ptr_add(bptr, inc);
-    scp = ptr_add(scp, inc);
+    scp = ptr_add(scp, SCEND ? scinc : inc);
     bop = ptr_add(bop, inc);
     if (WAVE) {
       if (scin) scin += U;
@@ -971,23 +1077,49 @@ __global__ void sw16_update_kernel(const int64_t *__restrict__ endcol, int64_t c
                                    const uint32_t *__restrict__ sc_out, int32_t *scores, uint8_t *flagged,
                                    int32_t *scores2, const uint8_t *__restrict__ flagged2, int pass,
                                    const int32_t *__restrict__ seq_idx, const int32_t *__restrict__ item_of,
-                                   const uint8_t *__restrict__ item_hot) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = seq_idx ? (int64_t)seq_idx[i] : i;
-    const int64_t e = endcol[i];
-    const uint32_t w = sc_out[e >> 1];
-    // once flagged, the 32-bit kernel owns the score (started from the last
-    // exact pass boundary, or from row 0)
-    if (flagged[o] == 0) {
-      if (kArith == 2 && !scores2 && (e & 1) && item_of && item_hot[item_of[o]]) {
-        flagged[o] = (uint8_t)min(pass + 1, 255);
-      } else {
-        const int v = (int)((!scores2 && (e & 1)) ? (w >> 16) : (w & 0xffffu));
-        scores[o] = max(pass == 0 ? 0 : scores[o], v - kBias16);
+                                   const uint8_t *__restrict__ item_hot, int32_t *list, int *nlist,
+                                   int32_t *list2, int *nlist2, int want) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < count; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool f1 = false, f2 = false;
+    int64_t o = 0;
+    if (i < count) {
+      o = seq_idx ? (int64_t)seq_idx[i] : i;
+      const int64_t e = endcol[i];
+      const uint32_t w = sc_out[e >> 1];
+      // once flagged, the 32-bit kernel owns the score (started from the last
+      // exact pass boundary, or from row 0)
+      int fl = flagged[o];
+      if (fl == 0) {
+        if (kArith == 2 && !scores2 && (e & 1) && item_of && item_hot[item_of[o]]) {
+          fl = min(pass + 1, 255);
+          flagged[o] = (uint8_t)fl;
+        } else {
+          const int v = (int)((!scores2 && (e & 1)) ? (w >> 16) : (w & 0xffffu));
+          scores[o] = max(pass == 0 ? 0 : scores[o], v - kBias16);
+        }
       }
+      if (scores2 && flagged2[o] == 0) scores2[o] = max(pass == 0 ? 0 : scores2[o], (int)(w >> 16) - kBias16);
+      // the sequences first flagged in this pass, compacted for the 32-bit
+      // kernel (flag_compact_kernel's job, fused: one launch fewer per pass)
+      f1 = want && fl == want;
+      f2 = want && list2 && flagged2[o] == want;
     }
-    if (scores2 && flagged2[o] == 0) scores2[o] = max(pass == 0 ? 0 : scores2[o], (int)(w >> 16) - kBias16);
+    if (!want) continue;   // uniform
+    const unsigned b1 = __ballot_sync(0xffffffffu, f1), b2 = __ballot_sync(0xffffffffu, f2);
+    if (b1) {
+      int pos = 0;
+      if (lane == 0) pos = atomicAdd(nlist, __popc(b1));
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      if (f1) list[pos + __popc(b1 & ((1u << lane) - 1u))] = (int32_t)o;
+    }
+    if (b2) {
+      int pos = 0;
+      if (lane == 0) pos = atomicAdd(nlist2, __popc(b2));
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      if (f2) list2[pos + __popc(b2 & ((1u << lane) - 1u))] = (int32_t)o;
+    }
   }
 }
 
@@ -1258,6 +1390,28 @@ __global__ void item_skip_kernel(const Item *__restrict__ items, int nitems, con
   }
 }
 
+// Per-search zeroing (replaces four memsets: one launch).  16-B stores for
+// the byte arrays' aligned bulk.
+__device__ __forceinline__ void zero_bytes(uint8_t *p, int64_t n, int64_t tid, int64_t nth) {
+  if (!p || n <= 0) return;
+  const int64_t mis = (16 - (int64_t)(reinterpret_cast<uintptr_t>(p) & 15)) & 15;
+  const int64_t head = n < mis ? n : mis;
+  const int64_t n16 = (n - head) >> 4;
+  uint4 *q = reinterpret_cast<uint4 *>(p + head);
+  for (int64_t i = tid; i < n16; i += nth) q[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int64_t i = tid; i < head; i += nth) p[i] = 0;
+  for (int64_t i = head + 16 * n16 + tid; i < n; i += nth) p[i] = 0;
+}
+__global__ void search_init_kernel(int *fcounters, int nfc, uint8_t *flagged, uint8_t *flagged2, int64_t count,
+                                   int64_t *cells32, uint8_t *item_hot, int64_t nitems) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < nfc; i += nth) fcounters[i] = 0;
+  if (tid == 0 && cells32) *cells32 = 0;
+  zero_bytes(flagged, count, tid, nth);
+  zero_bytes(flagged2, count, tid, nth);
+  zero_bytes(item_hot, nitems, tid, nth);
+}
+
 __global__ void flag_compact_kernel(const uint8_t *__restrict__ flagged, int64_t count, int32_t *list,
                                     int *n, int want) {
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < count;
@@ -1371,23 +1525,6 @@ __global__ void __launch_bounds__(1024) block_topk_kernel(const int32_t *scores,
     for (int w = 0; w < nwarps; ++w) warp_topk_insert(s_lists[w * 32 + lane], L, thr, k, lane);
     if (lane < k) out[(int64_t)blockIdx.x * k + lane] = L;
   }
-}
-
-// Out-of-core database: a chunk arrives over the host
-// link as one 16-bit letter-pair index per column (1 B per residue) and is
-// expanded here to the pass kernel's column words (descriptor byte offsets).
-__global__ void expand_columns_kernel(const uint16_t *__restrict__ in, int64_t n, uint32_t *__restrict__ out) {
-  const int64_t n4 = n >> 2;
-  const bool vec = ((reinterpret_cast<uintptr_t>(in) & 7) | (reinterpret_cast<uintptr_t>(out) & 15)) == 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (vec ? n4 : 0);
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(in) + i);
-    reinterpret_cast<uint4 *>(out)[i] = make_uint4((v.x & 0xffffu) * kDescBytes, (v.x >> 16) * kDescBytes,
-                                                   (v.y & 0xffffu) * kDescBytes, (v.y >> 16) * kDescBytes);
-  }
-  for (int64_t i = (vec ? 4 * n4 : 0) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = (uint32_t)in[i] * kDescBytes;
 }
 
 // Sorting stage for k > 32: radix select of the k-th largest
@@ -1721,7 +1858,8 @@ cudaError_t launch_sw16_pass(int ti, int grid, const SW16Params &p, cudaStream_t
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
                                cudaStream_t st, const int32_t *seq_idx, const int32_t *item_of,
-                               uint8_t *item_hot) {
+                               uint8_t *item_hot, int32_t *list, int *nlist, int32_t *list2, int *nlist2,
+                               int want) {
   if (count <= 0) return cudaSuccess;
   ++g_launches;
   sw16_detect_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, flagged, flagged2,
@@ -1729,7 +1867,8 @@ cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint3
                                                             item_hot);
   ++g_launches;
   sw16_update_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, scores, flagged, scores2,
-                                                            flagged2, pass, seq_idx, item_of, item_hot);
+                                                            flagged2, pass, seq_idx, item_of, item_hot, list,
+                                                            nlist, list2, nlist2, want);
   return cudaGetLastError();
 }
 
@@ -1820,10 +1959,12 @@ cudaError_t launch_sw16_rows(int grid, const RowsParams &p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_expand_columns(const uint16_t *in, int64_t n, uint32_t *out, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
+cudaError_t launch_search_init(int *fcounters, int nfc, uint8_t *flagged, uint8_t *flagged2, int64_t count,
+                               int64_t *cells32, uint8_t *item_hot, int64_t nitems, cudaStream_t st) {
   ++g_launches;
-  expand_columns_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, st>>>(in, n, out);
+  const int64_t work = std::max<int64_t>(std::max<int64_t>(count, nitems) / 16, (int64_t)nfc) + 1;
+  search_init_kernel<<<grid_for(work, 256), 256, 0, st>>>(fcounters, nfc, flagged, flagged2, count, cells32,
+                                                             item_hot, nitems);
   return cudaGetLastError();
 }
 

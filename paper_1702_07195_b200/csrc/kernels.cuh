@@ -60,7 +60,7 @@ constexpr int kSPBytes = 26 * 26 * kSPL * 4;
 static_assert(kSPBytes % 16 == 0, "bulk copy size");
 
 struct SW16Params {
-  const uint32_t *stream;   // column words (descriptor byte offsets)
+  const uint16_t *stream;   // column words (descriptor byte offsets, 16-bit)
   const Item *items;
   int num_items;
   int *counter;             // atomic item cursor for this pass (zeroed)
@@ -69,7 +69,7 @@ struct SW16Params {
   const uint2 *bnd_in;      // boundary (H,F) per column from the previous pass, or null
   uint2 *bnd_out;           // boundary for the next pass, or null
   uint2 *dummy;             // one 16-B scratch slot per launched thread (idle-lane stores)
-  const uint32_t *nul_stream;  // >= 16 NUL column words (groups without items)
+  const uint16_t *nul_stream;  // >= 16 NUL column words (groups without items)
   const uint2 *zero_bnd;       // >= 16 zero boundary columns
   int64_t col_lo, col_hi;      // valid column range of stream / bnd / sc_out (SW_DEBUG checks)
   uint32_t *sc_out;         // per column: score chain value at the last lane
@@ -188,7 +188,11 @@ int tile_wave_ctas_per_sm(int i);
 cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint32_t *sc_out, int32_t *scores,
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
                                cudaStream_t st, const int32_t *seq_idx, const int32_t *item_of,
-                               uint8_t *item_hot);
+                               uint8_t *item_hot, int32_t *list = nullptr, int *nlist = nullptr,
+                               int32_t *list2 = nullptr, int *nlist2 = nullptr, int want = 0);
+// want > 0: the update launch also compacts the sequences with flag byte ==
+// want (those first flagged in this pass) into list / list2 (counts nlist /
+// nlist2, zeroed by the caller), as launch_flag_compact would.
 // thresh: in stored 16-bit units (32768 - smax); scores are stored - kBias16.
 // A sequence already flagged is skipped; one flagged in this pass gets
 // flagged = pass + 1 and keeps in scores the exact maximum of the earlier passes
@@ -207,6 +211,11 @@ constexpr int kSW32Rows = SW_S32ROWS;  // rows per lane of the 32-bit kernel
 constexpr int kSW32Threads = 256;
 cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st);
 
+// Per-search zeroing of the flag bytes, the re-scoring counters, the 32-bit
+// cell counter and the per-item carry marks in one launch (null / 0 = skip).
+cudaError_t launch_search_init(int *fcounters, int nfc, uint8_t *flagged, uint8_t *flagged2, int64_t count,
+                               int64_t *cells32, uint8_t *item_hot, int64_t nitems, cudaStream_t st);
+
 // Sorting stage.
 cudaError_t launch_make_keys(const int32_t *scores, const int64_t *index, int64_t n,
                              uint64_t *keys, int64_t npad, cudaStream_t st);
@@ -220,9 +229,6 @@ cudaError_t launch_decode_keys(const uint64_t *keys, int64_t k, int64_t *idx, in
 size_t rows_smem_bytes(int ncq);   // head + 8 profiles + 7 rings + counters + the query stream
 constexpr int kRowsMaxNcq = 8192;  // rows mode needs the query stream in shared memory
 cudaError_t launch_sw16_rows(int grid, const RowsParams &p, cudaStream_t st);
-// Streamed database: out[i] = in[i] * kDescBytes (compact letter-pair index ->
-// column word) for i < n.
-cudaError_t launch_expand_columns(const uint16_t *in, int64_t n, uint32_t *out, cudaStream_t st);
 // k > 32: radix select (8 digit passes of the 64-bit key) + compaction of the
 // k largest keys into out[0, k); sorted descending when k <= 4096 (otherwise
 // unsorted: the caller sorts them).  scratch: radix_topk_scratch_bytes().

@@ -30,8 +30,10 @@ constexpr int kItemPad = 40;
 
 // Column word of the s16x2 stream: byte offset of the descriptor of the
 // letter pair (cA, cB) = (cA * kNL + cB) * kDescBytes.  cA is the low 16-bit
-// lane ("half A"), cB the high lane ("half B").
-inline uint32_t column_word(int cA, int cB) { return (uint32_t)((cA * kNL + cB) * kDescBytes); }
+// lane ("half A"), cB the high lane ("half B").  16 bits per column, i.e.
+// 1 B per residue of the pair image (a pair column holds two residues).
+static_assert(kNL * kNL * kDescBytes <= 65536, "column words are 16-bit");
+inline uint16_t column_word(int cA, int cB) { return (uint16_t)((cA * kNL + cB) * kDescBytes); }
 
 // A work item: two lane streams ("halves") of equal column count, each the
 // concatenation [seq, END, NUL, seq, END, NUL, ...] padded with NUL.
@@ -47,7 +49,7 @@ struct Item {
 static_assert(sizeof(Item) == 32, "Item layout");
 
 struct HostImage {
-  std::vector<uint32_t> stream;   // column words, total_cols
+  std::vector<uint16_t> stream;   // column words, total_cols
   std::vector<Item> items;        // sorted by ncols descending (claim order)
   std::vector<int32_t> slots;     // slot -> original sequence index
   std::vector<int64_t> endcol;    // per original sequence: 2 * (END column) + half (0 = A, 1 = B)

@@ -20,7 +20,7 @@ _NAMES = {SW_EINVAL: "SW_EINVAL", SW_ENOMEM: "SW_ENOMEM", SW_ECUDA: "SW_ECUDA",
           SW_ENODB: "SW_ENODB", SW_ESTATE: "SW_ESTATE"}
 
 EXPORTS = ["sw_db_load", "sw_db_load_streamed", "sw_db_chunks", "sw_db_free", "sw_db_count", "sw_db_residues", "sw_search",
-           "sw_search_dev", "sw_search_batch", "sw_search_batch_dev", "sw_topk", "sw_topk_dev", "sw_scatter_dev", "sw_last_stats", "sw_last_timing", "sw_set_tile",
+           "sw_search_dev", "sw_search_batch", "sw_search_batch_dev", "sw_topk", "sw_topk_dev", "sw_scatter_dev", "sw_last_stats", "sw_last_timing", "sw_timing_history", "sw_set_tile",
            "sw_tile_supported", "sw_set_wave", "sw_set_latency_mode", "sw_set_profile", "sw_set_rows_mode", "sw_last_error", "sw_version", "sw_launch_count"]
 
 
@@ -63,6 +63,7 @@ def load_library():
         "sw_scatter_dev": (ctypes.c_int, [p, p, i64, p, i64, p]),
         "sw_last_stats": (ctypes.c_int, [p, ctypes.c_int]),
         "sw_last_timing": (ctypes.c_int, [p, ctypes.c_int]),
+        "sw_timing_history": (ctypes.c_int, [p, ctypes.c_int]),
         "sw_set_tile": (ctypes.c_int, [i32, i32]),
         "sw_tile_supported": (ctypes.c_int, [i32, i32]),
         "sw_set_wave": (ctypes.c_int, [i32]),
@@ -239,6 +240,13 @@ def sw_last_timing() -> dict:
     a = np.zeros(2, dtype=np.float32)
     _check(load_library().sw_last_timing(_ptr(a), 2))
     return {"pass_kernels_ms": float(a[0]), "search_ms": float(a[1])}
+
+
+def sw_timing_history(n: int) -> list:
+    """Pass-kernel ms of each of the last n searches, oldest first (swdb.h)."""
+    a = np.zeros(max(int(n), 1), dtype=np.float32)
+    k = _check(load_library().sw_timing_history(_ptr(a), int(n)))
+    return [float(x) for x in a[:k]]
 
 
 def sw_set_tile(G: int, R: int = 0) -> None:
