@@ -85,8 +85,10 @@ struct Image {
   int64_t max_item_cols_rest = 0; // longest item after them
   DevBuf<int2> units;
   int n_units = 0;
+  std::vector<int32_t> item_ncols;  // host: columns of each item (claim order, descending)
   void release() {
     stream.release(); items.release(); endcol.release(); slots.release(); item_of.release(); units.release();
+    item_ncols.clear();
     total_cols = 0;
     max_item_cols = 0;
     num_items = 0;
@@ -124,6 +126,8 @@ struct State {
   const int8_t *mat_d = nullptr;
   DevBuf<uint8_t> qp;
   DevBuf<uint4> desc;
+  DevBuf<uint8_t> qp2;      // streamed: profile / descriptors of the latency tile of chain-bound chunks
+  DevBuf<uint4> desc2;
   DevBuf<int32_t> qp32, qp32b;
   DevBuf<uint2> bnd;        // 2 * max_cols
   DevBuf<int32_t> skip;     // per item: dead leading columns for the next pass
@@ -210,7 +214,7 @@ struct State {
     sc_out.release(); res.release(); offs.release();
     scores.release(); bscores.release(); flagged.release(); flagged2.release(); flag_list.release();
     flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release(); progress.release();
-    qin.release(); qp.release(); desc.release(); qp32.release();
+    qin.release(); qp.release(); qp2.release(); desc2.release(); desc.release(); qp32.release();
     qp32b.release(); bnd.release(); skip.release(); item_hot.release();
     rows_wrap.release(); rows_prog.release();
     scratch32.release(); dummy.release(); nulcols.release(); zerocols.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
@@ -222,6 +226,14 @@ struct State {
 
 State g;
 constexpr int kMaxPass = 4096;
+
+bool solo_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("SWDB_SOLO");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // The per-search inputs (matrix, query, query 2) cross the host link in ONE
 // copy from a pinned staging slot: a copy from pageable memory may wait for
@@ -300,27 +312,38 @@ constexpr double kStepC0 = 145.0, kStepC1 = 14.0;
 // step with 8 warps per SM, ~44 steps between consecutive passes
 constexpr double kRowsStep = 850.0, kRowsLag = 44.0;
 constexpr bool kRowsAuto = false;
-constexpr double kLatThroughput = 0.6;   // latency-tile throughput relative to a 512-thread tile's eff0
 
-double pass_time_model(const TileInfo &T, int m, const Image &I, bool lat) {
+// What the pass time model sees of a database (or of one streamed chunk).
+struct Shape {
+  int64_t total_cols, max_item_cols;
+};
+Shape shape_of(const Image &I) { return Shape{I.total_cols, I.max_item_cols}; }
+
+double pass_time_model(const TileInfo &T, int m, Shape I, bool lat) {
   const int rows = T.G * T.R;
   const int P = (m + rows - 1) / rows;
   const double f = 1.9e9;   // SM cycles per second
   const double cells = (double)rows * P * 2.0 * (double)I.total_cols;
-  const double bulk = cells / ((lat ? kLatThroughput : 1.0) * T.eff0 * 1e9);
-  const double chain = (double)P * ((double)I.max_item_cols + T.G) * (kStepC0 + kStepC1 * T.R) / f;
+  // latency tiles: their own measured bulk rate (eff0) and step (kernels.cu kLatEff)
+  (void)lat;
+  const double bulk = cells / (T.eff0 * 1e9);
+  const double step = T.step > 0.f ? (double)T.step : kStepC0 + kStepC1 * T.R;
+  const double chain = (double)P * ((double)I.max_item_cols + T.G) * step / f;
   return std::max(bulk, chain);
 }
 
 // The latency tile with the smallest modelled time, if it beats the throughput
 // tile `ti` by 10% (or the best latency tile when forced); -1 if none.
-int choose_lat_tile(int m, const Image &I, int ti, bool forced) {
+// single_pass: only latency tiles that hold the query in one pass (rows mode
+// runs beside a single pass of the pass kernel)
+int choose_lat_tile(int m, Shape I, int ti, bool forced, bool single_pass = false) {
   const double base = pass_time_model(tile(ti), m, I, false);
   double best = forced ? 1e300 : 0.9 * base;
   int bi = -1;
   for (int i = 0; i < num_tiles(); ++i) {
     const TileInfo t = tile(i);
     if (!t.lat || t.qpm != 0 || tile_ctas_per_sm(i) < 1) continue;
+    if (single_pass && t.G * t.R < m) continue;
     const double c = pass_time_model(t, m, I, true);
     if (c < best) {
       best = c;
@@ -405,8 +428,8 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       Image Iv2 = I0;
       Iv2.max_item_cols = I0.max_item_cols_rest;
       Iv2.total_cols = std::max<int64_t>(1, I0.total_cols - I0.long_cols);
-      const double t_rest = pass_time_model(tt, mm, Iv2, false);
-      const double t_all = pass_time_model(tt, mm, I0, false);
+      const double t_rest = pass_time_model(tt, mm, shape_of(Iv2), false);
+      const double t_all = pass_time_model(tt, mm, shape_of(I0), false);
       rows_cand = chain_normal >= t_all * 0.99 && t_rest + rows_t < 0.8 * t_all;
     }
   }
@@ -467,9 +490,9 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     if (g.force_G) {   // a forced latency tile: used when forced or when it is latency-only
       const int tf = find_tile_mode(g.force_G, g.force_R, 0, 1);
       if (tf >= 0 && (g.lat_mode == 1 || find_tile_mode(g.force_G, g.force_R, 0, 0) < 0)) tl = tf;
-      else if (g.lat_mode == 1) tl = choose_lat_tile(mm, Im, ti, true);
+      else if (g.lat_mode == 1) tl = choose_lat_tile(mm, shape_of(Im), ti, true, rows_ok);
     } else {
-      tl = choose_lat_tile(mm, Im, ti, g.lat_mode == 1);
+      tl = choose_lat_tile(mm, shape_of(Im), ti, g.lat_mode == 1, rows_ok);
     }
     if (tl >= 0) {
       ti = tl;
@@ -481,6 +504,30 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int P = (mm + rows - 1) / rows;
   if (P > kMaxPass) return fail(SW_EINVAL, "query too long");
   const bool rowsm = rows_ok && !wave && P == 1;   // (a forced multi-pass latency tile turns it off)
+  // Streamed database: a chunk whose pass is bound by one long item's chain
+  // (the chunk holding a very long sequence) runs a latency tile of its own
+  // (DESIGN.md 4.7); its profile and descriptors are built beside the main ones.
+  std::vector<char> chunk_lat;
+  int ti2 = -1, P2 = 0;
+  if (g.streamed && !lat && !pair && !use_sp && !wave && g.lat_mode >= 0 && !g.force_G) {
+    chunk_lat.assign(g.chunks.size(), 0);
+    for (size_t k = 0; k < g.chunks.size(); ++k) {
+      const State::Chunk &c = g.chunks[k];
+      if (c.item_end <= c.item_begin) continue;
+      const Shape sh{c.col_end - c.col_begin, (int64_t)I0.item_ncols[c.item_begin]};
+      const int tl = choose_lat_tile(mm, sh, ti, false);
+      if (tl >= 0 && (ti2 < 0 || tl == ti2)) {
+        ti2 = tl;
+        chunk_lat[k] = 1;
+      }
+    }
+    if (ti2 >= 0) P2 = (mm + tile(ti2).G * tile(ti2).R - 1) / (tile(ti2).G * tile(ti2).R);
+    if (P2 > kMaxPass) {
+      ti2 = -1;
+      chunk_lat.clear();
+    }
+  }
+  const int PP = std::max(P, P2);   // cursor / event slots per chunk
   int smax = 1;
   for (int i = 0; i < kAlpha * kAlpha; ++i) smax = std::max(smax, (int)matrix[i]);
   const int thresh = kHalfTop - smax;   // stored 16-bit units (R7)
@@ -523,9 +570,24 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(g.fcounters.ensure((size_t)4 * (P + 1)));
   const int32_t *item_of = pair ? nullptr : g.img[0].item_of.p;
   if (!pair) CUDA_TRY(g.item_hot.ensure((size_t)std::max(1, g.img[0].num_items)));
+  // Item cursors per (chunk, pass), then per pass the solo cursors (latency
+  // tiles, resident: the leading items of at least solo_cols columns are
+  // claimed only by warps 0-3 of a CTA, one per SM sub-partition, whose
+  // partner warp then claims nothing: the chain-bound item streams alone).
+  // Rows mode: the pass kernel starts claiming after the long items.
+  const int nchk = g.streamed ? (int)g.chunks.size() : 1;
+  const int first = rowsm ? I0.n_long : 0;
+  int solo_cols = 0, n_solo = 0;
+  if (lat && !g.streamed && T.G == 32 && solo_enabled()) {
+    solo_cols = (int)std::max<int64_t>(512, Im.max_item_cols / 2);
+    while (first + n_solo < I0.num_items && n_solo < 4 * g.num_sms && I0.item_ncols[first + n_solo] >= solo_cols)
+      ++n_solo;   // at most one per SM sub-partition
+    if (n_solo == 0) solo_cols = 0;
+  }
+  CUDA_TRY(g.pcounters.ensure((size_t)nchk * PP + P));
   CUDA_TRY(launch_search_init(g.fcounters.p, 4 * (P + 1), g.flagged.p, pair ? g.flagged2.p : nullptr, g.count,
                               g.cells32.p, pair ? nullptr : g.item_hot.p, pair ? 0 : std::max(1, g.img[0].num_items),
-                              st));
+                              g.pcounters.p, nchk * PP + P, P, first + n_solo, nchk * PP, first, st));
   if (!g.ev[0])
     for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g.ev[i]));
   // a batch's timing spans all of its searches (sw_last_timing)
@@ -551,6 +613,12 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(launch_qp_build(g.q_d, m, pair ? g.q2_d : nullptr, m2, g.mat_d, T.G, T.R, P, g.qp.p,
                            g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr,
                            goe, ge, st, use_sp ? 1 : 0));
+  if (ti2 >= 0) {
+    CUDA_TRY(g.qp2.ensure(qp_bytes(tile(ti2).G, tile(ti2).R, P2, 0)));
+    CUDA_TRY(g.desc2.ensure((size_t)kNL * kNL));
+    CUDA_TRY(launch_qp_build(g.q_d, m, nullptr, 0, g.mat_d, tile(ti2).G, tile(ti2).R, P2, g.qp2.p, g.desc2.p,
+                             g.qp32.p, nullptr, goe, ge, st, 0));
+  }
 
   const int grid = g.num_sms * (lat ? 1 : std::max(1, tile_ctas_per_sm(ti)));
   // Exact s32 re-scoring ("recalculated using the next wider
@@ -601,18 +669,13 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const bool strm = g.streamed;
   const int nch = strm ? (int)g.chunks.size() : 1;
   const int64_t span = strm ? g.chunk_span : I.total_cols;
-  CUDA_TRY(g.pcounters.ensure((size_t)nch * P));
-  CUDA_TRY(cudaMemsetAsync(g.pcounters.p, 0, sizeof(int) * (size_t)nch * P, st));
   const int ncq = (m + 2 + 3) & ~3;   // rows mode: the query stream (m letters, END, NUL, padding)
   if (rowsm) {
-    // the pass kernel starts claiming after the long items
-    const int first = I0.n_long;
-    CUDA_TRY(cudaMemcpyAsync(g.pcounters.p, &first, sizeof(int), cudaMemcpyHostToDevice, st));
     CUDA_TRY(g.rows_wrap.ensure((size_t)g.num_sms * ncq));
     CUDA_TRY(g.rows_prog.ensure(1));
     CUDA_TRY(cudaMemsetAsync(g.rows_prog.p, 0, sizeof(int), st));
   }
-  if (P > 1 && g.bnd.n < (size_t)span * 2) CUDA_TRY(g.bnd.ensure((size_t)span * 2));
+  if (PP > 1 && g.bnd.n < (size_t)span * 2) CUDA_TRY(g.bnd.ensure((size_t)span * 2));
   if (!strm && !pair && P > 1) CUDA_TRY(g.skip.ensure((size_t)std::max(1, I.num_items)));
   CUDA_TRY(cudaEventRecord(g.ev[1], st));
   if (wave) {
@@ -653,6 +716,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p, nullptr, nullptr, 0,
                                 thresh, st, nullptr, item_of, g.item_hot.p));
   }
+  int npl = 0;   // pass launches so far (per-pass path)
   for (int k = 0; k < (wave ? 0 : nch); ++k) {
     const uint16_t *stream_base = I.stream.p;
     const Item *items = I.items.p;
@@ -674,16 +738,20 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       items = I.items.p + c.item_begin;
       nitems = c.item_end - c.item_begin;
     }
-    for (int pass = 0; pass < P; ++pass) {
+    // this chunk's tile: the search's, or the latency tile of a chain-bound chunk
+    const bool cl = !chunk_lat.empty() && chunk_lat[k];
+    const int tik = cl ? ti2 : ti, Pk = cl ? P2 : P;
+    const int gridk = cl ? g.num_sms : grid;
+    for (int pass = 0; pass < Pk; ++pass) {
       SW16Params p{};   // npass = 0: one pass per launch
       p.stream = stream_base;
       p.items = items;
       p.num_items = nitems;
-      p.counter = g.pcounters.p + (size_t)k * P + pass;
-      p.qp = reinterpret_cast<const uint4 *>(g.qp.p);
-      p.desc = g.desc.p;
+      p.counter = g.pcounters.p + (size_t)k * PP + pass;
+      p.qp = reinterpret_cast<const uint4 *>(cl ? g.qp2.p : g.qp.p);
+      p.desc = cl ? g.desc2.p : g.desc.p;
       p.bnd_in = pass == 0 ? nullptr : g.bnd.p + (size_t)((pass - 1) & 1) * span - base;
-      p.bnd_out = pass == P - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * span - base;
+      p.bnd_out = pass == Pk - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * span - base;
       p.dummy = g.dummy.p;
       p.nul_stream = g.nulcols.p;
       p.col_lo = base;
@@ -700,10 +768,14 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       p.skip = (skipping && pass > 0) ? g.skip.p : nullptr;
       p.query = g.q_d;
       p.m = m;
-      const int pe = pev0 + 2 * (k * P + pass);
+      // latency tiles: the solo items [first, first + n_solo) (
+      // SWDB_SOLO=0 turns it off for experiments)
+      p.solo_counter = (solo_cols && k == 0) ? g.pcounters.p + (size_t)nchk * PP + pass : nullptr;
+      p.solo_end = first + n_solo;
+      const int pe = pev0 + 2 * npl++;   // event slots: this search's pass launches in order
       CUDA_TRY(pass_event(pe + 1));
       CUDA_TRY(cudaEventRecord(pev[pe], st));
-      CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
+      CUDA_TRY(launch_sw16_pass(tik, gridk, p, st));
       if (rowsm) {   // the long pairs, rows along the database sequence (before the gather reads sc_out)
         RowsParams r{};
         r.query = g.q_d;
@@ -908,6 +980,8 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
     const HostImage &H = himg[k];
     I.total_cols = H.total_cols;
     I.num_items = (int)H.items.size();
+    I.item_ncols.resize(H.items.size());
+    for (size_t i = 0; i < H.items.size(); ++i) I.item_ncols[i] = H.items[i].ncols;
     I.max_item_cols = 0;
     for (const Item &it : H.items) I.max_item_cols = std::max<int64_t>(I.max_item_cols, it.ncols);
     I.n_long = H.n_long_items;

@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   constexpr bool BRING = WAVE || SW_BRING;
   extern __shared__ uint4 smem[];
   __shared__ uint64_t s_mbar;
+  __shared__ int s_solo[4];   // EARLY solo items: per SM sub-partition, warp q's first claim (-1: not yet, 1: solo)
   {
     // the descriptor table and this pass's profile slice arrive by two 1-D
     // bulk copies (TMA) on one mbarrier
@@ -278,6 +279,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       // QPM 1: the score profile does not depend on the pass
       bulk_g2s(sbase + DESC_U4 * 16, p.qp + (QPM == 1 ? (size_t)0 : (size_t)p.pass * QP_U4), QP_U4 * 16, mbar);
     }
+    if (threadIdx.x < 4) s_solo[threadIdx.x] = -1;
     __syncthreads();   // the barrier is initialised before anyone waits on it
     mbar_wait(mbar, 0);
   }
@@ -359,14 +361,15 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   // Eq. 3 as F' = max(F - Ge, max(max(t, E) - Goe, 0)) -- equal to
   // max(F - Ge, max(H - Goe, 0)) since Goe >= Ge (H - Goe's F term is below
   // F - Ge) -- is one VIADDMNMX per row on the chain, for 1.5 more ALU
-  // instructions per pair of cells off it.
-  constexpr bool LROWS = EARLY && SW_LATROWS;
+  // instructions per pair of cells off it (profiles/r02_lat_calibration_early.jsonl).
+  constexpr bool LROWS = EARLY && SW_LATROWS && R >= 5;   // measured slower at R = 3, 4
   constexpr int KCE = EARLY ? KC : 1;
   // EARLY: profile chunks and offsets (descriptor word 0) of the lane's
   // current column ([u & 1]) and next column ([(u + 1) & 1]): U is even, so
   // the two sets alternate through the unrolled block without copies
   uint4 pa[2][KCE], pb[2][KCE];
   uint32_t w0b[2] = {nul.w0, nul.w0};
+  bool solo_left = true, solo_checked = false, solo_idle = false;   // EARLY solo claims (lane G-1)
   // EARLY, lane G-1: descriptors of lane 0's next column ([u & 1]) and the one
   // after ([(u + 1) & 1]); other lanes keep zeros (word 0 enters an IMAD)
   DescWords dq[2] = {{0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}};
@@ -415,7 +418,33 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   for (;;) {
     if (rem <= 0) {  // group-uniform: claim the next work item
       int it = 0;
-      if (last) it = atomicAdd(counter, 1);
+      if (last) {
+        if (EARLY && G == 32 && p.solo_counter) {
+          // solo items (chain-bound, the longest): claimed by warps 0-3 only;
+          // warp q + 4 shares warp q's SM sub-partition and stays idle when
+          // q's first item is one (the chain keeps the issue slots)
+          const int w = (int)(threadIdx.x >> 5);
+          volatile int *sl = &s_solo[w & 3];
+          if (w < 4) {
+            it = solo_left ? atomicAdd(p.solo_counter, 1) : p.solo_end;
+            if (it >= p.solo_end) {
+              solo_left = false;
+              it = atomicAdd(counter, 1);
+            }
+            if (*sl < 0) *sl = it < p.solo_end ? 1 : 0;
+          } else if (!solo_checked) {
+            int v;
+            while ((v = *sl) < 0) __nanosleep(100);   // warp q claims at once: no dependency
+            solo_checked = true;
+            solo_idle = v == 1;
+            it = solo_idle ? INT_MAX : atomicAdd(counter, 1);
+          } else {
+            it = solo_idle ? INT_MAX : atomicAdd(counter, 1);
+          }
+        } else {
+          it = atomicAdd(counter, 1);
+        }
+      }
       it = __shfl_sync(gmask, it, gbase + G - 1);
       if (it < p.num_items) {
         const int sk = (!WAVE && p.skip) ? p.skip[it] : 0;   // dead leading columns (flagged)
@@ -1403,9 +1432,12 @@ __device__ __forceinline__ void zero_bytes(uint8_t *p, int64_t n, int64_t tid, i
   for (int64_t i = head + 16 * n16 + tid; i < n; i += nth) p[i] = 0;
 }
 __global__ void search_init_kernel(int *fcounters, int nfc, uint8_t *flagged, uint8_t *flagged2, int64_t count,
-                                   int64_t *cells32, uint8_t *item_hot, int64_t nitems) {
+                                   int64_t *cells32, uint8_t *item_hot, int64_t nitems, int *pc, int npc, int nset,
+                                   int v0, int off, int v1) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = tid; i < nfc; i += nth) fcounters[i] = 0;
+  for (int64_t i = tid; i < npc; i += nth)
+    pc[i] = i < nset ? v0 : (i >= off && i < off + nset ? v1 : 0);
   if (tid == 0 && cells32) *cells32 = 0;
   zero_bytes(flagged, count, tid, nth);
   zero_bytes(flagged2, count, tid, nth);
@@ -1773,6 +1805,16 @@ const TileEff kTileEff[] = {
     {32, 30, 5568.9f, 5423.8f},
     {32, 32, 5717.9f, 5473.8f}};
 
+// Latency tiles (EARLY + LROWS, 256 threads, one CTA per SM;
+// tools/lat_calibrate.py, profiles/r02_lat_calibration_early.jsonl): SM cycles
+// per column step of a group running alone (one 12,000-residue sequence) and
+// bulk GCUPS (configs[1] at 0.2 scale, one pass).
+struct LatEff { int G, R; float step, bulk; };
+const LatEff kLatEff[] = {
+    {32, 3, 104.8f, 2476.9f}, {32, 4, 130.2f, 2899.2f}, {32, 5, 129.2f, 3073.5f},
+    {32, 6, 164.7f, 3277.4f}, {32, 8, 188.5f, 3597.0f}, {16, 9, 202.4f, 3773.3f},
+};
+
 TileEff tile_eff(int G, int R) {
   for (const TileEff &e : kTileEff)
     if (e.G == G && e.R == R) return e;
@@ -1794,7 +1836,14 @@ int64_t launch_count() { return g_launches; }
 int num_tiles() { return kNumTiles; }
 TileInfo tile(int i) {
   const TileEff e = tile_eff(g_tiles[i].G, g_tiles[i].R);
-  return TileInfo{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem, g_tiles[i].qpm, e.eff0, e.eff1, g_tiles[i].lat};
+  TileInfo t{g_tiles[i].G, g_tiles[i].R, g_tiles[i].smem, g_tiles[i].qpm, e.eff0, e.eff1, g_tiles[i].lat, 0.f};
+  if (t.lat)
+    for (const LatEff &l : kLatEff)
+      if (l.G == t.G && l.R == t.R) {
+        t.eff0 = t.eff1 = l.bulk;
+        t.step = l.step;
+      }
+  return t;
 }
 int find_tile_mode(int G, int R, int qpm, int lat) {
   for (int i = 0; i < kNumTiles; ++i)
@@ -1960,11 +2009,12 @@ cudaError_t launch_sw16_rows(int grid, const RowsParams &p, cudaStream_t st) {
 }
 
 cudaError_t launch_search_init(int *fcounters, int nfc, uint8_t *flagged, uint8_t *flagged2, int64_t count,
-                               int64_t *cells32, uint8_t *item_hot, int64_t nitems, cudaStream_t st) {
+                               int64_t *cells32, uint8_t *item_hot, int64_t nitems, int *pc, int npc, int nset,
+                               int v0, int off, int v1, cudaStream_t st) {
   ++g_launches;
-  const int64_t work = std::max<int64_t>(std::max<int64_t>(count, nitems) / 16, (int64_t)nfc) + 1;
+  const int64_t work = std::max<int64_t>(std::max<int64_t>(count, nitems) / 16, (int64_t)std::max(nfc, npc)) + 1;
   search_init_kernel<<<grid_for(work, 256), 256, 0, st>>>(fcounters, nfc, flagged, flagged2, count, cells32,
-                                                             item_hot, nitems);
+                                                             item_hot, nitems, pc, npc, nset, v0, off, v1);
   return cudaGetLastError();
 }
 

@@ -93,6 +93,11 @@ struct SW16Params {
   // QPM 1 (score profile): the query and its length (each lane's row letters)
   const uint8_t *query;
   int m;
+  // Latency tiles (EARLY, G = 32): items [*solo_counter, solo_end) are claimed
+  // only by warps 0-3 of a CTA (one per SM sub-partition); a warp 4-7 whose
+  // partner's first item is one of them claims nothing (null: off).
+  int *solo_counter;
+  int solo_end;
 };
 
 // Rows mode (long database sequences along the rows, kernels.cu).
@@ -153,6 +158,7 @@ struct TileInfo {
   int qpm;                  // profile mode (see kernels.cu)
   float eff0, eff1;         // measured full-row GCUPS: first pass / boundary-reading pass
   int lat;                  // latency tile (critical-path-bound launches)
+  float step;               // latency tile: measured SM cycles per column step of a lone group (0: model)
 };
 
 // Number of kernel launches issued by the library since it was loaded.
@@ -213,8 +219,11 @@ cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st);
 
 // Per-search zeroing of the flag bytes, the re-scoring counters, the 32-bit
 // cell counter and the per-item carry marks in one launch (null / 0 = skip).
+// Item cursors: pc[i] = v0 for i < nset, pc[off + i] = v1 for i < nset, other
+// entries < npc zero.
 cudaError_t launch_search_init(int *fcounters, int nfc, uint8_t *flagged, uint8_t *flagged2, int64_t count,
-                               int64_t *cells32, uint8_t *item_hot, int64_t nitems, cudaStream_t st);
+                               int64_t *cells32, uint8_t *item_hot, int64_t nitems, int *pc, int npc, int nset,
+                               int v0, int off, int v1, cudaStream_t st);
 
 // Sorting stage.
 cudaError_t launch_make_keys(const int32_t *scores, const int64_t *index, int64_t n,
