@@ -178,8 +178,10 @@ int64_t sw_topk(int64_t k, int64_t *idx_out, int32_t *score_out);
  *              0 <= index < 2^32), or NULL meaning index = position.
  *   k        : results wanted; d_idx_out int64[min(k,n)], d_score_out
  *              int32[min(k,n)] are DEVICE pointers.
- *   cuda_stream : stream to enqueue on (NULL = legacy default); synchronous
- *              with respect to that stream on return.
+ *   cuda_stream : stream to enqueue on (NULL = legacy default).  Stream-
+ *              ordered: returns once the work is enqueued; the outputs are
+ *              ready when the stream reaches this point.  Calls are ordered
+ *              among themselves whatever their streams (shared scratch).
  * Returns min(k, n) or a negative status.
  */
 int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, int64_t k,

@@ -126,8 +126,6 @@ struct State {
   const int8_t *mat_d = nullptr;
   DevBuf<uint8_t> qp;
   DevBuf<uint4> desc;
-  DevBuf<uint8_t> qp2;      // streamed: profile / descriptors of the latency tile of chain-bound chunks
-  DevBuf<uint4> desc2;
   DevBuf<int32_t> qp32, qp32b;
   DevBuf<uint2> bnd;        // 2 * max_cols
   DevBuf<int32_t> skip;     // per item: dead leading columns for the next pass
@@ -163,6 +161,7 @@ struct State {
   DevBuf<int> progress;     // wavefront: finished columns per (pass, item)
   // timing events of the last search
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t tk_ev = nullptr;    // end of the last sw_topk_dev (its key scratch is shared)
   // (start, end) of every pass-kernel launch of the last kHist searches (a
   // batch is one), a ring: slot hslot is the last search's (sw_timing_history)
   static constexpr int kHist = 64;
@@ -214,7 +213,7 @@ struct State {
     sc_out.release(); res.release(); offs.release();
     scores.release(); bscores.release(); flagged.release(); flagged2.release(); flag_list.release();
     flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release(); progress.release();
-    qin.release(); qp.release(); qp2.release(); desc2.release(); desc.release(); qp32.release();
+    qin.release(); qp.release(); desc.release(); qp32.release();
     qp32b.release(); bnd.release(); skip.release(); item_hot.release();
     rows_wrap.release(); rows_prog.release();
     scratch32.release(); dummy.release(); nulcols.release(); zerocols.release(); keys.release(); keys2.release(); tk_idx.release(); tk_score.release();
@@ -504,30 +503,6 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int P = (mm + rows - 1) / rows;
   if (P > kMaxPass) return fail(SW_EINVAL, "query too long");
   const bool rowsm = rows_ok && !wave && P == 1;   // (a forced multi-pass latency tile turns it off)
-  // Streamed database: a chunk whose pass is bound by one long item's chain
-  // (the chunk holding a very long sequence) runs a latency tile of its own
-  // (DESIGN.md 4.7); its profile and descriptors are built beside the main ones.
-  std::vector<char> chunk_lat;
-  int ti2 = -1, P2 = 0;
-  if (g.streamed && !lat && !pair && !use_sp && !wave && g.lat_mode >= 0 && !g.force_G) {
-    chunk_lat.assign(g.chunks.size(), 0);
-    for (size_t k = 0; k < g.chunks.size(); ++k) {
-      const State::Chunk &c = g.chunks[k];
-      if (c.item_end <= c.item_begin) continue;
-      const Shape sh{c.col_end - c.col_begin, (int64_t)I0.item_ncols[c.item_begin]};
-      const int tl = choose_lat_tile(mm, sh, ti, false);
-      if (tl >= 0 && (ti2 < 0 || tl == ti2)) {
-        ti2 = tl;
-        chunk_lat[k] = 1;
-      }
-    }
-    if (ti2 >= 0) P2 = (mm + tile(ti2).G * tile(ti2).R - 1) / (tile(ti2).G * tile(ti2).R);
-    if (P2 > kMaxPass) {
-      ti2 = -1;
-      chunk_lat.clear();
-    }
-  }
-  const int PP = std::max(P, P2);   // cursor / event slots per chunk
   int smax = 1;
   for (int i = 0; i < kAlpha * kAlpha; ++i) smax = std::max(smax, (int)matrix[i]);
   const int thresh = kHalfTop - smax;   // stored 16-bit units (R7)
@@ -584,10 +559,10 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       ++n_solo;   // at most one per SM sub-partition
     if (n_solo == 0) solo_cols = 0;
   }
-  CUDA_TRY(g.pcounters.ensure((size_t)nchk * PP + P));
+  CUDA_TRY(g.pcounters.ensure((size_t)nchk * P + P));
   CUDA_TRY(launch_search_init(g.fcounters.p, 4 * (P + 1), g.flagged.p, pair ? g.flagged2.p : nullptr, g.count,
                               g.cells32.p, pair ? nullptr : g.item_hot.p, pair ? 0 : std::max(1, g.img[0].num_items),
-                              g.pcounters.p, nchk * PP + P, P, first + n_solo, nchk * PP, first, st));
+                              g.pcounters.p, nchk * P + P, P, first + n_solo, nchk * P, first, st));
   if (!g.ev[0])
     for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g.ev[i]));
   // a batch's timing spans all of its searches (sw_last_timing)
@@ -613,12 +588,6 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(launch_qp_build(g.q_d, m, pair ? g.q2_d : nullptr, m2, g.mat_d, T.G, T.R, P, g.qp.p,
                            g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr,
                            goe, ge, st, use_sp ? 1 : 0));
-  if (ti2 >= 0) {
-    CUDA_TRY(g.qp2.ensure(qp_bytes(tile(ti2).G, tile(ti2).R, P2, 0)));
-    CUDA_TRY(g.desc2.ensure((size_t)kNL * kNL));
-    CUDA_TRY(launch_qp_build(g.q_d, m, nullptr, 0, g.mat_d, tile(ti2).G, tile(ti2).R, P2, g.qp2.p, g.desc2.p,
-                             g.qp32.p, nullptr, goe, ge, st, 0));
-  }
 
   const int grid = g.num_sms * (lat ? 1 : std::max(1, tile_ctas_per_sm(ti)));
   // Exact s32 re-scoring ("recalculated using the next wider
@@ -675,7 +644,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     CUDA_TRY(g.rows_prog.ensure(1));
     CUDA_TRY(cudaMemsetAsync(g.rows_prog.p, 0, sizeof(int), st));
   }
-  if (PP > 1 && g.bnd.n < (size_t)span * 2) CUDA_TRY(g.bnd.ensure((size_t)span * 2));
+  if (P > 1 && g.bnd.n < (size_t)span * 2) CUDA_TRY(g.bnd.ensure((size_t)span * 2));
   if (!strm && !pair && P > 1) CUDA_TRY(g.skip.ensure((size_t)std::max(1, I.num_items)));
   CUDA_TRY(cudaEventRecord(g.ev[1], st));
   if (wave) {
@@ -738,20 +707,16 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       items = I.items.p + c.item_begin;
       nitems = c.item_end - c.item_begin;
     }
-    // this chunk's tile: the search's, or the latency tile of a chain-bound chunk
-    const bool cl = !chunk_lat.empty() && chunk_lat[k];
-    const int tik = cl ? ti2 : ti, Pk = cl ? P2 : P;
-    const int gridk = cl ? g.num_sms : grid;
-    for (int pass = 0; pass < Pk; ++pass) {
+    for (int pass = 0; pass < P; ++pass) {
       SW16Params p{};   // npass = 0: one pass per launch
       p.stream = stream_base;
       p.items = items;
       p.num_items = nitems;
-      p.counter = g.pcounters.p + (size_t)k * PP + pass;
-      p.qp = reinterpret_cast<const uint4 *>(cl ? g.qp2.p : g.qp.p);
-      p.desc = cl ? g.desc2.p : g.desc.p;
+      p.counter = g.pcounters.p + (size_t)k * P + pass;
+      p.qp = reinterpret_cast<const uint4 *>(g.qp.p);
+      p.desc = g.desc.p;
       p.bnd_in = pass == 0 ? nullptr : g.bnd.p + (size_t)((pass - 1) & 1) * span - base;
-      p.bnd_out = pass == Pk - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * span - base;
+      p.bnd_out = pass == P - 1 ? nullptr : g.bnd.p + (size_t)(pass & 1) * span - base;
       p.dummy = g.dummy.p;
       p.nul_stream = g.nulcols.p;
       p.col_lo = base;
@@ -770,12 +735,12 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       p.m = m;
       // latency tiles: the solo items [first, first + n_solo) (
       // SWDB_SOLO=0 turns it off for experiments)
-      p.solo_counter = (solo_cols && k == 0) ? g.pcounters.p + (size_t)nchk * PP + pass : nullptr;
+      p.solo_counter = (solo_cols && k == 0) ? g.pcounters.p + (size_t)nchk * P + pass : nullptr;
       p.solo_end = first + n_solo;
       const int pe = pev0 + 2 * npl++;   // event slots: this search's pass launches in order
       CUDA_TRY(pass_event(pe + 1));
       CUDA_TRY(cudaEventRecord(pev[pe], st));
-      CUDA_TRY(launch_sw16_pass(tik, gridk, p, st));
+      CUDA_TRY(launch_sw16_pass(ti, grid, p, st));
       if (rowsm) {   // the long pairs, rows along the database sequence (before the gather reads sc_out)
         RowsParams r{};
         r.query = g.q_d;
@@ -1200,6 +1165,10 @@ int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, 
   int rc = ensure_device_ready();
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)cuda_stream;
+  // stream-ordered: the key scratch is shared by every call, so this call's
+  // work waits for the previous call's (whatever stream that ran on)
+  if (!g.tk_ev) CUDA_TRY(cudaEventCreateWithFlags(&g.tk_ev, cudaEventDisableTiming));
+  else CUDA_TRY(cudaStreamWaitEvent(st, g.tk_ev, 0));
   if (kk <= 32) {
     // one block per SM (at most), each warp >= 4 batches of 32 scores
     const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, g.num_sms > 0 ? g.num_sms : 148));
@@ -1231,7 +1200,7 @@ int64_t sw_topk_dev(const int32_t *d_scores, const int64_t *d_index, int64_t n, 
     CUDA_TRY(launch_bitonic_sort_desc(g.keys.p, np2, st));
     CUDA_TRY(launch_decode_keys(g.keys.p, kk, d_idx_out, d_score_out, st));
   }
-  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaEventRecord(g.tk_ev, st));
   return kk;
 }
 
@@ -1258,8 +1227,11 @@ int64_t sw_topk(int64_t k, int64_t *idx_out, int32_t *score_out) {
   CUDA_TRY(g.tk_score.ensure((size_t)kk));
   int64_t r = sw_topk_dev(g.last_scores, nullptr, g.count, kk, g.tk_idx.p, g.tk_score.p, g.last_stream);
   if (r < 0) return r;
-  CUDA_TRY(cudaMemcpy(idx_out, g.tk_idx.p, (size_t)kk * sizeof(int64_t), cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(score_out, g.tk_score.p, (size_t)kk * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpyAsync(idx_out, g.tk_idx.p, (size_t)kk * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                           g.last_stream));
+  CUDA_TRY(cudaMemcpyAsync(score_out, g.tk_score.p, (size_t)kk * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                           g.last_stream));
+  CUDA_TRY(cudaStreamSynchronize(g.last_stream));
   return kk;
 }
 
