@@ -68,7 +68,7 @@ struct DevBuf {
 
 // A device-resident stream image.
 struct Image {
-  DevBuf<uint16_t> stream;  // column words (16-bit descriptor offsets, 1 B per residue)
+  DevBuf<uint32_t> stream;  // column words (descriptor byte offsets; host image: 16-bit)
   DevBuf<Item> items;
   DevBuf<int64_t> endcol;   // per sequence: 2 * END column + half
   DevBuf<int32_t> slots;    // slot -> original sequence (items' sequences in column order)
@@ -131,7 +131,7 @@ struct State {
   DevBuf<int32_t> skip;     // per item: dead leading columns for the next pass
   DevBuf<uint8_t> item_hot; // per item: a low-half sequence flagged (carry propagation, R7)
   DevBuf<uint2> dummy;      // scratch for idle-lane stores (16-B slot per thread)
-  DevBuf<uint16_t> nulcols; // 16 NUL column words
+  DevBuf<uint32_t> nulcols; // 16 NUL column words
   DevBuf<uint2> zerocols;   // 16 zero boundary columns
   DevBuf<uint2> scratch32;
   DevBuf<uint64_t> keys;
@@ -183,6 +183,7 @@ struct State {
   int64_t chunk_span = 0;       // max columns of a chunk
   uint16_t *h_stream = nullptr; // pinned host image: 16-bit column words (1 B per residue)
   uint8_t *h_res = nullptr;     // pinned, mapped host copy of the residues (s32 re-scoring)
+  DevBuf<uint32_t> cbuf[2];     // device chunk buffers (double-buffered), 32-bit column words
   DevBuf<uint16_t> cbuf16[2];   // their compact copies as they arrive over the host link
   DevBuf<int32_t> cseq_idx;     // sequences grouped by chunk
   DevBuf<int64_t> cseq_endcol;  // their END columns (global image columns)
@@ -194,7 +195,7 @@ struct State {
     if (h_res) cudaFreeHost(h_res);
     h_stream = nullptr;
     h_res = nullptr;
-    cbuf16[0].release(); cbuf16[1].release();
+    cbuf[0].release(); cbuf[1].release(); cbuf16[0].release(); cbuf16[1].release();
     cseq_idx.release(); cseq_endcol.release();
     for (int k = 0; k < 2; ++k) {
       if (ev_copied[k]) cudaEventDestroy(ev_copied[k]);
@@ -687,7 +688,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   }
   int npl = 0;   // pass launches so far (per-pass path)
   for (int k = 0; k < (wave ? 0 : nch); ++k) {
-    const uint16_t *stream_base = I.stream.p;
+    const uint32_t *stream_base = I.stream.p;
     const Item *items = I.items.p;
     int nitems = I.num_items;
     int64_t base = 0;
@@ -696,14 +697,15 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       const State::Chunk &c = g.chunks[k];
       // the buffer is free once the passes of the chunk that used it last are done
       CUDA_TRY(cudaStreamWaitEvent(g.copy_st, g.ev_free[b], 0));
-      // the image crosses the host link as it is (2 B per column, 1 B per
-      // residue) and the passes read it in the device buffer
+      // the 16-bit image crosses the host link (2 B per column, 1 B per
+      // residue) and is expanded to 32-bit column words on the device
       CUDA_TRY(cudaMemcpyAsync(g.cbuf16[b].p, g.h_stream + c.col_begin, (size_t)(c.col_end - c.col_begin) * 2,
                                cudaMemcpyHostToDevice, g.copy_st));
       CUDA_TRY(cudaEventRecord(g.ev_copied[b], g.copy_st));
       CUDA_TRY(cudaStreamWaitEvent(st, g.ev_copied[b], 0));
+      CUDA_TRY(launch_expand_columns(g.cbuf16[b].p, c.col_end - c.col_begin, g.cbuf[b].p, st));
       base = c.col_begin;
-      stream_base = g.cbuf16[b].p - base;     // so that item.col_begin indexes the buffer
+      stream_base = g.cbuf[b].p - base;     // so that item.col_begin indexes the buffer
       items = I.items.p + c.item_begin;
       nitems = c.item_end - c.item_begin;
     }
@@ -987,14 +989,23 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
     if (strm) continue;
     CUDA_TRY(I.stream.ensure(H.stream.size()));
     CUDA_TRY(I.endcol.ensure(H.endcol.size()));
-    CUDA_TRY(cudaMemcpy(I.stream.p, H.stream.data(), H.stream.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    {   // the 16-bit host image crosses the link, expanded to 32-bit words on the device
+      DevBuf<uint16_t> tmp;
+      cudaError_t e = tmp.ensure(H.stream.size() + 8);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(tmp.p, H.stream.data(), H.stream.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) e = launch_expand_columns(tmp.p, (int64_t)H.stream.size(), I.stream.p, nullptr);
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      tmp.release();
+      CUDA_TRY(e);
+    }
     CUDA_TRY(cudaMemcpy(I.endcol.p, H.endcol.data(), H.endcol.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     CUDA_TRY(I.slots.ensure(H.slots.size()));
     CUDA_TRY(cudaMemcpy(I.slots.p, H.slots.data(), H.slots.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
   if (strm) {
     const HostImage &H = himg[0];
-    const int64_t chunk_cols = std::max<int64_t>(chunk_bytes / 2, 1);
+    const int64_t chunk_cols = std::max<int64_t>(chunk_bytes / 4, 1);   // device buffer of 32-bit words
     // chunks: maximal runs of consecutive items whose columns (with the NUL
     // padding on both sides) fit chunk_cols; an item longer than that is a
     // chunk of its own
@@ -1043,6 +1054,7 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
     CUDA_TRY(cudaHostAlloc(&g.h_stream, H.stream.size() * sizeof(uint16_t), cudaHostAllocDefault));
     std::memcpy(g.h_stream, H.stream.data(), H.stream.size() * sizeof(uint16_t));
     for (int k = 0; k < 2; ++k) {
+      CUDA_TRY(g.cbuf[k].ensure((size_t)span));
       CUDA_TRY(g.cbuf16[k].ensure((size_t)span + 8));
       CUDA_TRY(cudaEventCreateWithFlags(&g.ev_copied[k], cudaEventDisableTiming));
       CUDA_TRY(cudaEventCreateWithFlags(&g.ev_free[k], cudaEventDisableTiming));
@@ -1074,8 +1086,8 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
   {
     CUDA_TRY(g.nulcols.ensure(16));
     CUDA_TRY(g.zerocols.ensure(16));
-    std::vector<uint16_t> nw(16, column_word(kNul, kNul));
-    CUDA_TRY(cudaMemcpy(g.nulcols.p, nw.data(), 16 * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    std::vector<uint32_t> nw(16, column_word(kNul, kNul));
+    CUDA_TRY(cudaMemcpy(g.nulcols.p, nw.data(), 16 * sizeof(uint32_t), cudaMemcpyHostToDevice));
     {
       std::vector<uint2> zc(16, make_uint2((uint32_t)kBias16 * 0x10001u, (uint32_t)kBias16 * 0x10001u));
       CUDA_TRY(cudaMemcpy(g.zerocols.p, zc.data(), 16 * sizeof(uint2), cudaMemcpyHostToDevice));

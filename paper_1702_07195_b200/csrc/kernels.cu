@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   // boundary for the next pass.  A group without items keeps feeding NUL
   // columns; its pointers stop (increment 0) on the NUL padding / own slot.
   uint2 *const dummy = p.dummy + (blockIdx.x * blockDim.x + threadIdx.x);
-  const uint16_t *sptr = p.nul_stream;
+  const uint32_t *sptr = p.nul_stream;
   const uint2 *bptr = p.zero_bnd;
   // SW_SCEND (not in the wavefront): every lane stores the chain at separator
   // columns, lanes t < G-1 into their own dummy slot (no lane predicate)
@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const RowsParams p) {
   constexpr int R = kRowsR, G = 32, KC = R / 4, NW = kRowsWarps, RS = kRowsRing, D = kRowsAhead;
   static_assert(R % 4 == 0, "rows-mode profile chunks");
-  static_assert((RS & (RS - 1)) == 0 && (D & (D - 1)) == 0, "ring sizes");
+  static_assert((RS & (RS - 1)) == 0 && (D & (D - 1)) == 0 && D >= 2, "ring sizes (D even: two column register sets)");
   extern __shared__ uint4 rsm[];
   uint4 *sdesc = rsm;                                          // [kNL] column descriptors
   int32_t *sM = reinterpret_cast<int32_t *>(rsm + kNL);        // [kNL][kNL]: SM(query letter, db letter)
@@ -864,7 +864,6 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
     __syncthreads();
     const int k = *s_item;
     if (k >= p.n_items) break;
-    const DescWords nul = load_desc(sbase + kNul * 16);
     const Item it = p.items[k];
     const int32_t sA = p.slots[it.seqA];
     const int32_t sB = it.nB ? p.slots[it.seqB] : -1;
@@ -911,50 +910,56 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
       uint32_t H[R], E[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) { H[r] = kB2; E[r] = kB2; }
-      uint32_t S = 0u, hprev = kB2, kneg = 0u, final_sc = 0u;
-      uint32_t w0 = nul.w0, ngoe = nul.ngoe, nge = nul.nge, knext = nul.kneg;
+      uint32_t S = 0u, hprev = kB2, kneg_prev = 0u, final_sc = 0u;
       uint32_t hout = kB2, fout = kB2, sc = 0u;
-      // lane 31's prefetch ring: slot j holds column s + 1 (+ j rotation); D
+      // Every lane knows its own column (lane t: s - t at step s): the query
+      // is the column stream.  Its letter, descriptor and profile chunks are
+      // loaded one step ahead, into two register sets that alternate with the
+      // unrolled step index (the pass kernel's EARLY scheme, without the
+      // descriptor shuffles): the step's chain is shuffle -> rows -> shuffle.
+      DescWords dc[2];
+      uint4 pc[2][KC];
+      auto load_col = [&](int x, DescWords &d, uint4 *pk) {
+        const int l = (x >= 0 && x < ncq) ? (int)sq[x] : kNul;
+        d = load_desc(sbase + (uint32_t)l * 16u);
+        const uint32_t a = imad(d.w0, 16u, s_qp);
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) pk[kk] = lds128(a + kk * G * 16);
+      };
+      load_col(-t, dc[0], pc[0]);
+      // lane 31's prefetch ring of the previous pass's boundary (H, F, chain)
+      // for lane 0's columns: slot j holds column s + 1 (+ j rotation), D
       // columns ahead.  The producer's count is re-read (and fenced) only when
-      // the cached value does not cover the column; consumed slots are freed
-      // every 16 columns.
-      int rl[D];
+      // the cached value does not cover the column.
       uint4 rv[D];
       int avail = 0;
-      auto fetch = [&](int col, int &l, uint4 &v) {
-        l = kNul;
+      auto fetch = [&](int col, uint4 &v) {
         v = make_uint4(kB2, kB2, 0u, 0u);
-        if (col < ncq) {
-          l = (int)sq[col];
-          if (has_in) {
-            const int tix = in_base + col;
-            if (in_ring) {
-              // the first column of a batch: wait (suspended, no spinning) for the producer's arrival
-              const int bt = tix / B;
-              if ((tix & (B - 1)) == 0) mbar_wait(mb_full(warp - 1, bt & (NB - 1)), (uint32_t)((bt / NB) & 1));
-              v = rin[tix & (RS - 1)];
-              if ((tix & (B - 1)) == B - 1 || col + 1 == ncq) {   // the batch is read: free its slot
-                __threadfence_block();
-                mbar_arrive(mb_empty(warp - 1, bt & (NB - 1)));
-              }
-            } else {   // the wrap from warp 7: a count, polled with a sleep (one waiter per CTA)
-              if (avail < tix + 1) {
-                while ((avail = prod[NW - 1]) < tix + 1) __nanosleep(64);
-                __threadfence_block();
-              }
-              v = wrap[col];
+        if (col < ncq && has_in) {
+          const int tix = in_base + col;
+          if (in_ring) {
+            // the first column of a batch: wait (suspended, no spinning) for the producer's arrival
+            const int bt = tix / B;
+            if ((tix & (B - 1)) == 0) mbar_wait(mb_full(warp - 1, bt & (NB - 1)), (uint32_t)((bt / NB) & 1));
+            v = rin[tix & (RS - 1)];
+            if ((tix & (B - 1)) == B - 1 || col + 1 == ncq) {   // the batch is read: free its slot
+              __threadfence_block();
+              mbar_arrive(mb_empty(warp - 1, bt & (NB - 1)));
             }
+          } else {   // the wrap from warp 7: a count, polled with a sleep (one waiter per CTA)
+            if (avail < tix + 1) {
+              while ((avail = prod[NW - 1]) < tix + 1) __nanosleep(64);
+              __threadfence_block();
+            }
+            v = wrap[col];
           }
         }
       };
       if (last) {
-        int l0;
         uint4 v0;
-        fetch(0, l0, v0);   // columns in order: a batch's first column waits for the batch
+        fetch(0, v0);   // columns in order: a batch's first column waits for the batch
 #pragma unroll
-        for (int j = 0; j < D; ++j) fetch(j + 1, rl[j], rv[j]);
-        const DescWords d = load_desc(sbase + l0 * 16);
-        w0 = d.w0; ngoe = d.ngoe; nge = d.nge; knext = d.kneg;
+        for (int j = 0; j < D; ++j) fetch(j + 1, rv[j]);
         hout = v0.x;
         fout = v0.y;
         sc = v0.z;
@@ -967,52 +972,47 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
 #pragma unroll
         for (int v = 0; v < D; ++v) {
           const int s = s0 + v;
-          w0 = __shfl_sync(0xffffffffu, w0, src);
-          ngoe = __shfl_sync(0xffffffffu, ngoe, src);
-          nge = __shfl_sync(0xffffffffu, nge, src);
-          knext = __shfl_sync(0xffffffffu, knext, src);
           const uint32_t hu = __shfl_sync(0xffffffffu, hout, src);
           uint32_t F = __shfl_sync(0xffffffffu, fout, src);
           const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
-          const uint32_t kneg_prev = kneg;
-          kneg = knext;
+          load_col(s + 1 - t, dc[(v + 1) & 1], pc[(v + 1) & 1]);   // the next column, during these rows
+          const uint32_t ngoe = dc[v & 1].ngoe, nge = dc[v & 1].nge;
           uint2 bnext = make_uint2(bdef, bdef);
           uint32_t scnext = 0u;
-          int cnext = kNul;
           if (last) {   // slot v holds column s + 1; refill it with column s + 1 + D
-            cnext = rl[v];
             bnext = make_uint2(rv[v].x, rv[v].y);
             scnext = rv[v].z;
-            fetch(s + 1 + D, rl[v], rv[v]);
+            fetch(s + 1 + D, rv[v]);
           }
           uint32_t hd = hprev;
           hprev = hu;
-          const uint32_t aA = imad(w0, 16u, s_qp);
-          uint4 ca = lds128(aA);
-          uint32_t tcur = imad(hd, one, ca.x);
+          uint32_t tcur = imad(hd, one, pc[v & 1][0].x);
 #pragma unroll
           for (int kk = 0; kk < KC; ++kk) {
-            uint4 na = make_uint4(0u, 0u, 0u, 0u);
-            if (kk + 1 < KC) na = lds128(aA + (kk + 1) * G * 16);
+            const uint4 ca = pc[v & 1][kk];
+            const uint4 na = kk + 1 < KC ? pc[v & 1][kk + 1 < KC ? kk + 1 : 0] : make_uint4(0u, 0u, 0u, 0u);
             const uint32_t av[8] = {ca.x, ca.y, ca.z, ca.w, na.x, na.y, na.z, na.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const int r = kk * 4 + j;
               uint32_t tnext = 0u;
               if (r + 1 < R) tnext = imad(H[r], one, av[j + 1]);
-              const uint32_t h = hmax3(tcur, E[r], F);     // Eq. 1 (0 implicit: E >= kB2)
+              // Eq. 3 with a one-instruction chain (LROWS, the pass kernel): Goe >= Ge
+              const uint32_t a = hmax(tcur, E[r]);
+              const uint32_t uu = haddmax(a, ngoe, kB2);  // max(max(t, E) - Goe, 0)
+              const uint32_t h = hmax(a, F);              // Eq. 1
               H[r] = h;
               const uint32_t hg = haddmax(h, ngoe, kB2);  // max(H-Goe, 0)
               E[r] = haddmax(E[r], nge, hg);              // Eq. 2 (along the query)
-              F = haddmax(F, nge, hg);                    // Eq. 3 (along the database sequence)
+              F = haddmax(F, nge, uu);                    // Eq. 3 (along the database sequence)
               tcur = tnext;
             }
-            ca = na;
           }
           S = haddmax(S, kneg_prev, H[0]);
 #pragma unroll
           for (int r = 1; r + 1 < R; r += 2) S = hmax3(S, H[r], H[r + 1]);
           if ((R & 1) == 0) S = hmax(S, H[R - 1]);
+          kneg_prev = dc[v & 1].kneg;
           const uint32_t so = hmax(sc_in, S);
           if (last) {
             const int col = s - (G - 1);
@@ -1037,8 +1037,6 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) sw16_rows_kernel(const Row
                 }
               }
             }
-            const DescWords d = load_desc(sbase + cnext * 16);
-            w0 = d.w0; ngoe = d.ngoe; nge = d.nge; knext = d.kneg;
           }
           hout = imad(H[R - 1], nlast, bnext.x);
           fout = imad(F, nlast, bnext.y);
@@ -1442,6 +1440,21 @@ __global__ void search_init_kernel(int *fcounters, int nfc, uint8_t *flagged, ui
   zero_bytes(flagged, count, tid, nth);
   zero_bytes(flagged2, count, tid, nth);
   zero_bytes(item_hot, nitems, tid, nth);
+}
+
+// 16-bit column words -> 32-bit words (device image upload, out-of-core
+// chunks as they arrive over the host link).
+__global__ void expand_columns_kernel(const uint16_t *__restrict__ in, int64_t n, uint32_t *__restrict__ out) {
+  const int64_t n4 = n >> 2;
+  const bool vec = ((reinterpret_cast<uintptr_t>(in) & 7) | (reinterpret_cast<uintptr_t>(out) & 15)) == 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (vec ? n4 : 0);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(in) + i);
+    reinterpret_cast<uint4 *>(out)[i] = make_uint4(v.x & 0xffffu, v.x >> 16, v.y & 0xffffu, v.y >> 16);
+  }
+  for (int64_t i = (vec ? 4 * n4 : 0) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
 }
 
 __global__ void flag_compact_kernel(const uint8_t *__restrict__ flagged, int64_t count, int32_t *list,
@@ -2015,6 +2028,13 @@ cudaError_t launch_search_init(int *fcounters, int nfc, uint8_t *flagged, uint8_
   const int64_t work = std::max<int64_t>(std::max<int64_t>(count, nitems) / 16, (int64_t)std::max(nfc, npc)) + 1;
   search_init_kernel<<<grid_for(work, 256), 256, 0, st>>>(fcounters, nfc, flagged, flagged2, count, cells32,
                                                              item_hot, nitems, pc, npc, nset, v0, off, v1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand_columns(const uint16_t *in, int64_t n, uint32_t *out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  expand_columns_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, st>>>(in, n, out);
   return cudaGetLastError();
 }
 

@@ -60,7 +60,7 @@ constexpr int kSPBytes = 26 * 26 * kSPL * 4;
 static_assert(kSPBytes % 16 == 0, "bulk copy size");
 
 struct SW16Params {
-  const uint16_t *stream;   // column words (descriptor byte offsets, 16-bit)
+  const uint32_t *stream;   // column words (descriptor byte offsets)
   const Item *items;
   int num_items;
   int *counter;             // atomic item cursor for this pass (zeroed)
@@ -69,7 +69,7 @@ struct SW16Params {
   const uint2 *bnd_in;      // boundary (H,F) per column from the previous pass, or null
   uint2 *bnd_out;           // boundary for the next pass, or null
   uint2 *dummy;             // one 16-B scratch slot per launched thread (idle-lane stores)
-  const uint16_t *nul_stream;  // >= 16 NUL column words (groups without items)
+  const uint32_t *nul_stream;  // >= 16 NUL column words (groups without items)
   const uint2 *zero_bnd;       // >= 16 zero boundary columns
   int64_t col_lo, col_hi;      // valid column range of stream / bnd / sc_out (SW_DEBUG checks)
   uint32_t *sc_out;         // per column: score chain value at the last lane
@@ -217,6 +217,9 @@ constexpr int kSW32Rows = SW_S32ROWS;  // rows per lane of the 32-bit kernel
 constexpr int kSW32Threads = 256;
 cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st);
 
+// 16-bit column words (host image, streamed chunks) -> the pass kernel's
+// 32-bit words: out[i] = in[i] for i < n.
+cudaError_t launch_expand_columns(const uint16_t *in, int64_t n, uint32_t *out, cudaStream_t st);
 // Per-search zeroing of the flag bytes, the re-scoring counters, the 32-bit
 // cell counter and the per-item carry marks in one launch (null / 0 = skip).
 // Item cursors: pc[i] = v0 for i < nset, pc[off + i] = v1 for i < nset, other

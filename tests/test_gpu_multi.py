@@ -221,3 +221,45 @@ def test_topk_full_sort_small_n(n):
         assert sw.sw_topk_dev(d, None, n, k, ti, ts) == k
         ei, es = oracle.topk(x, k)
         assert np.array_equal(ti.cpu().numpy(), ei) and np.array_equal(ts.cpu().numpy(), es), (n, k)
+
+
+def test_topk_dev_is_stream_ordered_and_serialised():
+    """sw_topk_dev returns once enqueued (swdb.h): several calls on two side
+    streams, back to back with no synchronisation in between, each read only
+    after its own stream; the shared key scratch is ordered by the library."""
+    rng = np.random.default_rng(7)
+    n = 300_000
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    xs = [rng.integers(0, 500, n).astype(np.int32) for _ in range(4)]
+    ds = [torch.from_numpy(x).cuda() for x in xs]
+    torch.cuda.synchronize()
+    outs = []
+    for i, (x, d) in enumerate(zip(xs, ds)):
+        st = s1 if i % 2 == 0 else s2
+        k = (10, 33, 100, 32)[i]
+        ti = torch.empty(k, dtype=torch.int64, device="cuda")
+        ts = torch.empty(k, dtype=torch.int32, device="cuda")
+        assert sw.sw_topk_dev(d, None, n, k, ti, ts, st) == k
+        outs.append((x, k, ti, ts, st))
+    for x, k, ti, ts, st in outs:
+        st.synchronize()
+        ei, es = oracle.topk(x, k)
+        assert np.array_equal(ti.cpu().numpy(), ei) and np.array_equal(ts.cpu().numpy(), es), k
+
+
+def test_timing_history_matches_last_timing():
+    """sw_timing_history: the pass-kernel time of each of the last searches,
+    oldest first, from the events sw_last_timing reads for the last one."""
+    w = si.config0()
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    d = torch.empty(w.db.count, dtype=torch.int32, device="cuda")
+    st = torch.cuda.Stream()
+    qs = [w.queries[0], si.rr_residues(si.rng_for(0, 99), 300), si.rr_residues(si.rng_for(0, 98), 700)]
+    for q in qs:
+        sw.sw_search_dev(q, BLOSUM62, 10, 2, d, st)
+    h = sw.sw_timing_history(3)
+    last = sw.sw_last_timing()["pass_kernels_ms"]
+    assert len(h) == 3 and all(x > 0 for x in h)
+    assert abs(h[-1] - last) < 1e-6
+    assert len(sw.sw_timing_history(1000)) <= 64
+    assert (d.cpu().numpy() == oracle.batch(qs[-1], w.db.residues, w.db.offsets, BLOSUM62, 10, 2)).all()
