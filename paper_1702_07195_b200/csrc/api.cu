@@ -184,7 +184,13 @@ struct State {
   uint16_t *h_stream = nullptr; // pinned host image: 16-bit column words (1 B per residue)
   uint8_t *h_res = nullptr;     // pinned, mapped host copy of the residues (s32 re-scoring)
   DevBuf<uint32_t> cbuf[2];     // device chunk buffers (double-buffered), 32-bit column words
-  DevBuf<uint16_t> cbuf16[2];   // their compact copies as they arrive over the host link
+  DevBuf<uint16_t> cbuf16[2];
+  // chunk k of a search uses buffer (k + buf_parity) & 1; at the end of a
+  // search chunk 0 of the next one is copied into the buffer the last chunk
+  // did not use (the database does not change between searches), so its copy
+  // overlaps the last chunk's passes instead of opening the next search
+  int buf_parity = 0;
+  bool chunk0_staged = false;   // their compact copies as they arrive over the host link
   DevBuf<int32_t> cseq_idx;     // sequences grouped by chunk
   DevBuf<int64_t> cseq_endcol;  // their END columns (global image columns)
   cudaStream_t copy_st = nullptr;
@@ -206,6 +212,8 @@ struct State {
     copy_st = nullptr;
     chunks.clear();
     streamed = false;
+    buf_parity = 0;
+    chunk0_staged = false;
   }
 
   void release_all() {
@@ -692,16 +700,18 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     const Item *items = I.items.p;
     int nitems = I.num_items;
     int64_t base = 0;
-    const int b = k & 1;
+    const int b = (k + (strm ? g.buf_parity : 0)) & 1;
     if (strm) {
       const State::Chunk &c = g.chunks[k];
-      // the buffer is free once the passes of the chunk that used it last are done
-      CUDA_TRY(cudaStreamWaitEvent(g.copy_st, g.ev_free[b], 0));
-      // the 16-bit image crosses the host link (2 B per column, 1 B per
-      // residue) and is expanded to 32-bit column words on the device
-      CUDA_TRY(cudaMemcpyAsync(g.cbuf16[b].p, g.h_stream + c.col_begin, (size_t)(c.col_end - c.col_begin) * 2,
-                               cudaMemcpyHostToDevice, g.copy_st));
-      CUDA_TRY(cudaEventRecord(g.ev_copied[b], g.copy_st));
+      if (k > 0 || !g.chunk0_staged) {
+        // the buffer is free once the passes of the chunk that used it last are done
+        CUDA_TRY(cudaStreamWaitEvent(g.copy_st, g.ev_free[b], 0));
+        // the 16-bit image crosses the host link (2 B per column, 1 B per
+        // residue) and is expanded to 32-bit column words on the device
+        CUDA_TRY(cudaMemcpyAsync(g.cbuf16[b].p, g.h_stream + c.col_begin, (size_t)(c.col_end - c.col_begin) * 2,
+                                 cudaMemcpyHostToDevice, g.copy_st));
+        CUDA_TRY(cudaEventRecord(g.ev_copied[b], g.copy_st));
+      }
       CUDA_TRY(cudaStreamWaitEvent(st, g.ev_copied[b], 0));
       CUDA_TRY(launch_expand_columns(g.cbuf16[b].p, c.col_end - c.col_begin, g.cbuf[b].p, st));
       base = c.col_begin;
@@ -787,6 +797,18 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       }
     }
     if (strm) CUDA_TRY(cudaEventRecord(g.ev_free[b], st));
+  }
+  if (strm && !wave) {
+    // the next search's chunk 0 into the buffer this search's last chunk did not use
+    g.chunk0_staged = false;
+    const int nb = (g.buf_parity + nch) & 1;
+    const State::Chunk &c0 = g.chunks[0];
+    CUDA_TRY(cudaStreamWaitEvent(g.copy_st, g.ev_free[nb], 0));
+    CUDA_TRY(cudaMemcpyAsync(g.cbuf16[nb].p, g.h_stream + c0.col_begin, (size_t)(c0.col_end - c0.col_begin) * 2,
+                             cudaMemcpyHostToDevice, g.copy_st));
+    CUDA_TRY(cudaEventRecord(g.ev_copied[nb], g.copy_st));
+    g.buf_parity = nb;
+    g.chunk0_staged = true;
   }
   CUDA_TRY(cudaEventRecord(g.ev[2], st));
   if (strm || wave || P >= 255)

@@ -18,3 +18,5 @@ tail -2 gpurun_out/n_ncu_full.log
 timeout 1800 python tests/report_configs.py 0 1 2 4 --reps 5 > gpurun_out/n_configs.jsonl 2> gpurun_out/n_configs.err; cat gpurun_out/n_configs.jsonl; tail -2 gpurun_out/n_configs.err
 timeout 2400 python tests/report_configs.py 3 --reps 5 --batch > gpurun_out/n_cfg3.jsonl 2> gpurun_out/n_cfg3.err; tail -3 gpurun_out/n_cfg3.jsonl; tail -2 gpurun_out/n_cfg3.err
 timeout 900 python tools/run_streamed.py 2 128,256,1024 > gpurun_out/n_streamed.jsonl 2>&1; cat gpurun_out/n_streamed.jsonl
+timeout 900 python tools/rows_perf.py > gpurun_out/n_rows_mode.jsonl 2>&1; tail -2 gpurun_out/n_rows_mode.jsonl | cut -c1-300
+timeout 900 python tools/lat_calibrate.py > gpurun_out/n_lat_calibration.jsonl 2>&1; grep cfg0 gpurun_out/n_lat_calibration.jsonl | head -2
