@@ -53,6 +53,9 @@
 #ifndef SW_LATROWS
 #define SW_LATROWS 1   // EARLY tiles: Eq. 3 with a one-instruction vertical chain (Goe >= Ge)
 #endif
+#ifndef SW_SHFLORD
+#define SW_SHFLORD 0   // 1: shuffle the chain values before the descriptor words (experiment)
+#endif
 #ifndef SW_SCEND
 #define SW_SCEND 0   // 1: lane G-1 stores the score chain at separator columns only (experiment)
 #endif
@@ -540,6 +543,16 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       // ---- this column's inputs from lane t-1 (lane 0: from lane G-1)
+#if SW_SHFLORD
+      // (experiment) the chain values first, then the descriptor words
+      const uint32_t hu = __shfl_sync(0xffffffffu, hout, src);
+      uint32_t F = __shfl_sync(0xffffffffu, fout, src);
+      if (!EARLY) w0 = __shfl_sync(0xffffffffu, w0, src);
+      ngoe = __shfl_sync(0xffffffffu, ngoe, src);
+      nge = __shfl_sync(0xffffffffu, nge, src);
+      knext = __shfl_sync(0xffffffffu, knext, src);
+      const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
+#else
       if (!EARLY) w0 = __shfl_sync(0xffffffffu, w0, src);
       ngoe = __shfl_sync(0xffffffffu, ngoe, src);
       nge = __shfl_sync(0xffffffffu, nge, src);
@@ -547,6 +560,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
       const uint32_t hu = __shfl_sync(0xffffffffu, hout, src);
       uint32_t F = __shfl_sync(0xffffffffu, fout, src);
       const uint32_t sc_in = __shfl_sync(0xffffffffu, sc, src);
+#endif
       // EARLY: the next column's profile offsets (lane G-1 sends lane 0's next
       // column's) and its profile chunks, loaded during this column's rows
       if (EARLY) {
