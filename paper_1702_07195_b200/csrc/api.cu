@@ -117,7 +117,6 @@ struct State {
   DevBuf<uint8_t> flagged, flagged2;
   DevBuf<int32_t> flag_list, flag_list2;
   DevBuf<int> fcounters;    // 32-bit re-scoring: (count, cursor) per (pass, query of a pair)
-  DevBuf<int> pcounters;    // per (chunk, pass) item cursors
   const uint8_t *res_dev = nullptr;  // residues for s32 re-scoring (device or mapped host)
   DevBuf<int64_t> cells32;
   // per-search inputs in one device buffer: matrix (576 B), query, query 2
@@ -221,7 +220,7 @@ struct State {
     img[0].release(); img[1].release();
     sc_out.release(); res.release(); offs.release();
     scores.release(); bscores.release(); flagged.release(); flagged2.release(); flag_list.release();
-    flag_list2.release(); fcounters.release(); pcounters.release(); cells32.release(); progress.release();
+    flag_list2.release(); fcounters.release(); cells32.release(); progress.release();
     qin.release(); qp.release(); desc.release(); qp32.release();
     qp32b.release(); bnd.release(); skip.release(); item_hot.release();
     rows_wrap.release(); rows_prog.release();
@@ -518,7 +517,35 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   g.last_thresh = thresh - kBias16;  // in score units
   const int goe = gap_open + gap_extend, ge = gap_extend;
 
-  const size_t in_bytes = (size_t)kAlpha * kAlpha + (size_t)m + (pair ? (size_t)m2 : 0);
+  // Item cursors per (chunk, pass), then the solo cursors: the leading,
+  // chain-bound items of a chunk (the whole resident image is one chunk) are
+  // claimed only by the first group of warps 0-3 of a CTA, one per SM
+  // sub-partition, whose partner warps then claim nothing, so the long item
+  // streams without competing for issue slots.  Latency tiles
+  // only (the model chose them because a chain bounds the pass; in the
+  // throughput tiles the claim code alone measured 1.7-2.3% slower: register
+  // allocation of the main loop).  Rows mode: the pass kernel starts claiming
+  // after the long items.
+  const int nchk = g.streamed ? (int)g.chunks.size() : 1;
+  const int first = rowsm ? I0.n_long : 0;
+  std::vector<int> solo_n((size_t)nchk, 0);
+  if (solo_enabled() && lat && T.G == 32 && !pair && !use_sp && !wave) {
+    for (int k = 0; k < nchk; ++k) {
+      const int ib = g.streamed ? g.chunks[k].item_begin : first;
+      const int ie = g.streamed ? g.chunks[k].item_end : I0.num_items;
+      if (ie <= ib) continue;
+      const int64_t thr = std::max<int64_t>(512, I0.item_ncols[ib] / 2);   // half the chunk's longest item
+      int n = 0;
+      while (ib + n < ie && n < 4 * g.num_sms && I0.item_ncols[ib + n] >= thr) ++n;   // one per sub-partition
+      solo_n[k] = n;
+    }
+  }
+
+  // pc[k * P + pass]: item cursor, pc[nchk * P + k * P + pass]: solo cursor
+  // (item indices relative to the chunk's first item); copied with the inputs
+  const size_t pc_off = ((size_t)kAlpha * kAlpha + (size_t)m + (pair ? (size_t)m2 : 0) + 15) & ~(size_t)15;
+  const size_t npc = (size_t)2 * nchk * P;
+  const size_t in_bytes = pc_off + npc * sizeof(int);
   CUDA_TRY(g.qin.ensure(in_bytes));
   const int slot = g_stage.next;
   g_stage.next = (slot + 1) % Staging::kSlots;
@@ -535,6 +562,17 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   std::memcpy(g_stage.h[slot], matrix, (size_t)kAlpha * kAlpha);
   std::memcpy(g_stage.h[slot] + kAlpha * kAlpha, q, (size_t)m);
   if (pair) std::memcpy(g_stage.h[slot] + kAlpha * kAlpha + m, q2, (size_t)m2);
+  {
+    int *hpc = reinterpret_cast<int *>(g_stage.h[slot] + pc_off);
+    for (int k = 0; k < nchk; ++k) {
+      const int start = g.streamed ? 0 : first;
+      for (int pass = 0; pass < P; ++pass) {
+        hpc[(size_t)k * P + pass] = start + solo_n[(size_t)k];
+        hpc[(size_t)nchk * P + (size_t)k * P + pass] = start;
+      }
+    }
+  }
+  int *const pc = reinterpret_cast<int *>(g.qin.p + pc_off);
   g.mat_d = reinterpret_cast<const int8_t *>(g.qin.p);
   g.q_d = g.qin.p + kAlpha * kAlpha;
   g.q2_d = pair ? g.q_d + m : nullptr;
@@ -554,24 +592,9 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(g.fcounters.ensure((size_t)4 * (P + 1)));
   const int32_t *item_of = pair ? nullptr : g.img[0].item_of.p;
   if (!pair) CUDA_TRY(g.item_hot.ensure((size_t)std::max(1, g.img[0].num_items)));
-  // Item cursors per (chunk, pass), then per pass the solo cursors (latency
-  // tiles, resident: the leading items of at least solo_cols columns are
-  // claimed only by warps 0-3 of a CTA, one per SM sub-partition, whose
-  // partner warp then claims nothing: the chain-bound item streams alone).
-  // Rows mode: the pass kernel starts claiming after the long items.
-  const int nchk = g.streamed ? (int)g.chunks.size() : 1;
-  const int first = rowsm ? I0.n_long : 0;
-  int solo_cols = 0, n_solo = 0;
-  if (lat && !g.streamed && T.G == 32 && solo_enabled()) {
-    solo_cols = (int)std::max<int64_t>(512, Im.max_item_cols / 2);
-    while (first + n_solo < I0.num_items && n_solo < 4 * g.num_sms && I0.item_ncols[first + n_solo] >= solo_cols)
-      ++n_solo;   // at most one per SM sub-partition
-    if (n_solo == 0) solo_cols = 0;
-  }
-  CUDA_TRY(g.pcounters.ensure((size_t)nchk * P + P));
   CUDA_TRY(launch_search_init(g.fcounters.p, 4 * (P + 1), g.flagged.p, pair ? g.flagged2.p : nullptr, g.count,
                               g.cells32.p, pair ? nullptr : g.item_hot.p, pair ? 0 : std::max(1, g.img[0].num_items),
-                              g.pcounters.p, nchk * P + P, P, first + n_solo, nchk * P, first, st));
+                              nullptr, 0, 0, 0, 0, 0, st));
   if (!g.ev[0])
     for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g.ev[i]));
   // a batch's timing spans all of its searches (sw_last_timing)
@@ -663,7 +686,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     p.stream = I.stream.p;
     p.items = I.items.p;
     p.num_items = I.num_items;
-    p.counter = g.pcounters.p;
+    p.counter = pc;
     p.qp = reinterpret_cast<const uint4 *>(g.qp.p);
     p.desc = g.desc.p;
     p.bnd_in = nullptr;
@@ -679,7 +702,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     p.zero = 0u;
     p.one = 1u;
     p.npass = P;
-    p.pcounters = g.pcounters.p;
+    p.pcounters = pc;
     p.progress = g.progress.p;
     p.bndbuf[0] = g.bnd.p;
     p.bndbuf[1] = g.bnd.p + span;
@@ -724,7 +747,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       p.stream = stream_base;
       p.items = items;
       p.num_items = nitems;
-      p.counter = g.pcounters.p + (size_t)k * P + pass;
+      p.counter = pc + (size_t)k * P + pass;
       p.qp = reinterpret_cast<const uint4 *>(g.qp.p);
       p.desc = g.desc.p;
       p.bnd_in = pass == 0 ? nullptr : g.bnd.p + (size_t)((pass - 1) & 1) * span - base;
@@ -745,10 +768,9 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       p.skip = (skipping && pass > 0) ? g.skip.p : nullptr;
       p.query = g.q_d;
       p.m = m;
-      // latency tiles: the solo items [first, first + n_solo) (
-      // SWDB_SOLO=0 turns it off for experiments)
-      p.solo_counter = (solo_cols && k == 0) ? g.pcounters.p + (size_t)nchk * P + pass : nullptr;
-      p.solo_end = first + n_solo;
+      // the chunk's solo items (SWDB_SOLO=0 turns them off for experiments)
+      p.solo_counter = solo_n[(size_t)k] ? pc + (size_t)nchk * P + (size_t)k * P + pass : nullptr;
+      p.solo_end = (strm ? 0 : first) + solo_n[(size_t)k];
       const int pe = pev0 + 2 * npl++;   // event slots: this search's pass launches in order
       CUDA_TRY(pass_event(pe + 1));
       CUDA_TRY(cudaEventRecord(pev[pe], st));
