@@ -43,6 +43,8 @@ for _k in ("SW_QPTAIL", "SW_TAILADDR", "SW_ROWS_TRACE"):   # profile tail layout
         NVCC_FLAGS = NVCC_FLAGS + [f"-D{_k}=" + os.environ[_k]]
 if os.environ.get("SW_DEFS"):     # experiment macros: SW_DEFS="SW_X=1 SW_Y=0"
     NVCC_FLAGS = NVCC_FLAGS + ["-D" + d for d in os.environ["SW_DEFS"].split()]
+if os.environ.get("SW_PTXAS"):    # experiment: extra ptxas options, SW_PTXAS="-O2 --allow-expensive-optimizations=true"
+    NVCC_FLAGS = NVCC_FLAGS + ["-Xptxas", ",".join(os.environ["SW_PTXAS"].split())]
 if os.environ.get("SW_DEBUG"):    # device-side bounds checks (slow; debug builds)
     NVCC_FLAGS = NVCC_FLAGS + ["-DSW_DEBUG=1"]
 

@@ -1787,50 +1787,52 @@ TileEntry g_tiles[] = {
 constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
 
 // Measured full-row throughput (GCUPS) of each tile's pass kernel on one
-// B200, biased arithmetic (configs[1] at 0.3 scale; tools/calibrate_tiles.py,
-// profiles/r01_tile_calibration_biased.jsonl): eff0 = first pass (query of G*R;
-// mean of two runs), eff1 = a pass reading the previous pass's boundary (2*G*R
-// minus G*R; measured after the boundary ring was dropped from that variant).
-// The tile choice predicts time ~ G*R * (1/eff0 + (P-1)/eff1).
+// B200, biased-unsigned arithmetic, configs[1] at FULL size (round 2,
+// tools/calibrate_tiles.py 1.0, profiles/r02b_tile_calibration_full.jsonl;
+// round 1's table came from a 0.3-scale database and ran 2-5% lower): eff0 =
+// first pass (query of G*R), eff1 = a pass reading the previous pass's
+// boundary (2*G*R minus G*R).  The tile choice predicts time
+// ~ G*R * (1/eff0 + (P-1)/eff1).
 struct TileEff { int G, R; float eff0, eff1; };
 const TileEff kTileEff[] = {
-    {8, 8, 4220.0f, 3476.3f},
-    {8, 12, 4904.7f, 4338.7f},
-    {8, 16, 5189.6f, 4876.9f},
-    {8, 18, 5389.9f, 4978.0f},
-    {8, 20, 5486.9f, 5131.1f},
-    {8, 22, 5527.5f, 5230.0f},
-    {8, 24, 5580.8f, 5323.5f},
-    {8, 26, 5643.8f, 5434.3f},
-    {8, 28, 5677.0f, 5468.9f},
-    {8, 29, 5748.0f, 5488.7f},
-    {8, 30, 5748.6f, 5465.4f},
-    {8, 32, 5789.5f, 5431.1f},
-    {16, 8, 4316.1f, 3671.4f},
-    {16, 12, 4962.9f, 4472.8f},
-    {16, 16, 5249.9f, 4964.5f},
-    {16, 18, 5428.1f, 5047.1f},
-    {16, 20, 5525.2f, 5188.2f},
-    {16, 22, 5564.0f, 5299.8f},
-    {16, 24, 5612.9f, 5354.9f},
-    {16, 26, 5678.6f, 5478.5f},
-    {16, 28, 5709.1f, 5491.1f},
-    {16, 29, 5787.8f, 5524.9f},
-    {16, 30, 5779.9f, 5492.1f},
-    {16, 32, 5826.2f, 5454.0f},
-    {32, 8, 4274.6f, 3776.3f},
-    {32, 12, 4914.3f, 4575.2f},
-    {32, 15, 5127.2f, 4816.1f},
-    {32, 16, 5177.9f, 4822.6f},
-    {32, 18, 5394.9f, 5005.7f},
-    {32, 20, 5450.8f, 5187.7f},
-    {32, 22, 5460.6f, 5261.3f},
-    {32, 24, 5479.5f, 5377.5f},
-    {32, 26, 5574.1f, 5332.9f},
-    {32, 28, 5517.0f, 5410.3f},
-    {32, 29, 5564.6f, 5387.9f},
-    {32, 30, 5568.9f, 5423.8f},
-    {32, 32, 5717.9f, 5473.8f}};
+    {8, 8, 4376.3f, 3593.6f},
+    {8, 12, 5146.3f, 4495.5f},
+    {8, 16, 5407.8f, 5036.3f},
+    {8, 18, 5592.9f, 5133.4f},
+    {8, 20, 5685.7f, 5314.9f},
+    {8, 22, 5719.6f, 5419.0f},
+    {8, 24, 5768.3f, 5492.2f},
+    {8, 26, 5826.4f, 5607.1f},
+    {8, 28, 5813.4f, 5628.1f},
+    {8, 29, 5961.6f, 5669.2f},
+    {8, 30, 5925.9f, 5679.4f},
+    {8, 32, 5950.9f, 5665.6f},
+    {16, 8, 4427.5f, 3821.6f},
+    {16, 12, 5161.6f, 4621.5f},
+    {16, 16, 5423.4f, 5110.5f},
+    {16, 18, 5592.2f, 5184.4f},
+    {16, 20, 5681.2f, 5332.0f},
+    {16, 22, 5720.7f, 5430.1f},
+    {16, 24, 5770.8f, 5496.6f},
+    {16, 26, 5832.3f, 5621.2f},
+    {16, 28, 5811.6f, 5639.8f},
+    {16, 29, 5961.9f, 5675.6f},
+    {16, 30, 5921.1f, 5683.7f},
+    {16, 32, 5962.1f, 5679.4f},
+    {32, 8, 4493.4f, 3963.9f},
+    {32, 12, 5038.6f, 4772.3f},
+    {32, 15, 5356.8f, 5017.0f},
+    {32, 16, 5370.9f, 5026.1f},
+    {32, 18, 5623.4f, 5231.5f},
+    {32, 20, 5649.6f, 5403.7f},
+    {32, 22, 5678.4f, 5474.4f},
+    {32, 24, 5719.5f, 5587.0f},
+    {32, 26, 5768.8f, 5550.7f},
+    {32, 28, 5690.3f, 5626.9f},
+    {32, 29, 5835.2f, 5608.6f},
+    {32, 30, 5802.5f, 5648.2f},
+    {32, 32, 5961.3f, 5666.6f},
+};
 
 // Latency tiles (EARLY + LROWS, 256 threads, one CTA per SM;
 // tools/lat_calibrate.py, profiles/r02_lat_calibration_early.jsonl): SM cycles

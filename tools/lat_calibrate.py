@@ -68,8 +68,8 @@ def main():
         print(json.dumps({"kind": "cfg0", "forced": [G, R, lat], "tile": [s["G"], s["R"]], "lat": s["lat"],
                           "passes": s["passes"], "ms": round(ms, 4), "pass_ms": round(pms, 4),
                           "gcups": round(cells / (ms * 1e6), 1)}), flush=True)
-    # (3) bulk throughput of the LAT tiles relative to the throughput tiles (cfg1 at 0.2 scale)
-    w = si.config1(scale=0.2)
+    # (3) bulk throughput of the LAT tiles relative to the throughput tiles (cfg1 at full size)
+    w = si.config1(scale=1.0)
     sw.sw_db_load(w.db.residues, w.db.offsets)
     d = torch.empty(w.db.count, dtype=torch.int32, device="cuda")
     for G, R, lat in [(32, 8, 0), (32, 16, 0)] + [t for t in tiles if t[2]]:
