@@ -5,8 +5,8 @@ Each trial draws a database (count, length mix, alphabet use), a query or a
 query pair, a scoring matrix (BLOSUM62, random symmetric, random asymmetric,
 extreme int8), gap penalties (including 0 and very large), a tile (default or
 any compiled one: throughput, latency or score-profile tiles), the cross-pass
-wavefront (off / auto / forced), the latency-tile mode and the substitution
-profile (query / score profile), and a path (resident single, resident query
+wavefront (off / auto / forced), the latency-tile mode, the substitution
+profile (query / score profile), rows mode (never / auto / on request), and a path (resident single, resident query
 pair, streamed), then compares every score and the top-k (k up to 200: both
 sorting paths) with the oracle.
 
@@ -111,6 +111,8 @@ def main():
         sw.sw_set_latency_mode(lat)
         prof = int(rng.choice([0, 1, 2]))       # substitution scores: auto / query profile / score profile
         sw.sw_set_profile(prof)
+        rows = int(rng.choice([-1, 0, 0, 1]))   # rows mode for the long items: never / auto / on request
+        sw.sw_set_rows_mode(rows)
         if (args.only and trials != args.only) or trials < args.start:
             continue
         if args.dump:
@@ -119,7 +121,7 @@ def main():
         if args.verbose:
             print(json.dumps({"trial": trials, "count": db.count, "max_len": int(db.lengths().max(initial=0)),
                               "alpha": alpha, "matrix": mname, "gaps": [go, ge], "m": m, "path": path,
-                              "tile": tile, "wave": wave, "lat": lat, "profile": prof}), flush=True)
+                              "tile": tile, "wave": wave, "lat": lat, "profile": prof, "rows": rows}), flush=True)
         try:
             if path == "streamed":
                 sw.sw_db_load_streamed(db.residues, db.offsets, chunk)
@@ -138,7 +140,7 @@ def main():
                 if bad.size:
                     ok = False
                     print(json.dumps({"trial": trials, "path": path, "tile": tile, "wave": wave, "lat": lat,
-                                      "profile": prof, "matrix": mname, "gaps": [go, ge],
+                                      "profile": prof, "rows": rows, "matrix": mname, "gaps": [go, ge],
                                       "m": len(qq), "count": db.count, "mismatches": int(bad.size),
                                       "first": bad[:5].tolist(), "got": g[bad[:5]].tolist(),
                                       "exp": exp[bad[:5]].tolist()}), flush=True)
@@ -159,6 +161,7 @@ def main():
     sw.sw_set_wave(0)
     sw.sw_set_latency_mode(0)
     sw.sw_set_profile(0)
+    sw.sw_set_rows_mode(0)
     print(json.dumps({"trials": trials, "failures": fails, "cells": cells, "seconds": args.seconds}), flush=True)
     sys.exit(1 if fails else 0)
 
