@@ -234,12 +234,9 @@ struct State {
 State g;
 constexpr int kMaxPass = 4096;
 
-bool solo_enabled() {
-  static const bool on = [] {
-    const char *e = std::getenv("SWDB_SOLO");
-    return !(e && e[0] == '0');
-  }();
-  return on;
+bool solo_enabled() {   // SWDB_SOLO=0 turns solo items off (experiments; read per search)
+  const char *e = std::getenv("SWDB_SOLO");
+  return !(e && e[0] == '0');
 }
 
 // The per-search inputs (matrix, query, query 2) cross the host link in ONE
@@ -536,7 +533,8 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       if (ie <= ib) continue;
       const int64_t thr = std::max<int64_t>(512, I0.item_ncols[ib] / 2);   // half the chunk's longest item
       int n = 0;
-      while (ib + n < ie && n < 4 * g.num_sms && I0.item_ncols[ib + n] >= thr) ++n;   // one per sub-partition
+      // at most one per SM: each idles the other warps of its sub-partition
+      while (ib + n < ie && n < g.num_sms && I0.item_ncols[ib + n] >= thr) ++n;
       solo_n[k] = n;
     }
   }

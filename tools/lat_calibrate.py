@@ -72,6 +72,7 @@ def main():
     w = si.config1(scale=1.0)
     sw.sw_db_load(w.db.residues, w.db.offsets)
     d = torch.empty(w.db.count, dtype=torch.int32, device="cuda")
+    os.environ["SWDB_SOLO"] = "0"   # the latency tiles' bulk rate without solo items (read per search)
     for G, R, lat in [(32, 8, 0), (32, 16, 0)] + [t for t in tiles if t[2]]:
         sw.sw_set_latency_mode(1 if lat else -1)
         sw.sw_set_tile(G, R)
@@ -81,6 +82,7 @@ def main():
                           "gcups": round(G * R * w.db.total_residues / (pms * 1e6), 1)}), flush=True)
     sw.sw_set_tile(0)
     sw.sw_set_latency_mode(0)
+    os.environ.pop("SWDB_SOLO", None)
 
 
 if __name__ == "__main__":
