@@ -87,9 +87,13 @@ int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count);
  * sw_db_load, plus
  *   chunk_bytes : >= 1, the device memory budget of one chunk of the stream
  *                 image (two chunk buffers are allocated).
- * The sequence-pair image is kept in pinned HOST memory and split into chunks
- * of consecutive work items; every search copies chunk k+1 host->device on a
- * separate stream while the pass kernels run on chunk k.  Residues for 32-bit
+ * The sequence-pair image is kept in pinned HOST memory (16-bit column words,
+ * 1 B per residue on the link) and split into chunks of consecutive work
+ * items; every search copies chunk k+1 host->device on a separate stream while
+ * the pass kernels run on chunk k (expanded to 32-bit words on the device),
+ * and at its end copies the next search's chunk 0 while its last chunk runs.
+ * Device memory: 2 x chunk_bytes of 32-bit words + 2 x chunk_bytes / 2 of
+ * 16-bit copies, plus the per-column score chain of one chunk.  Residues for 32-bit
  * re-scoring are read from mapped host memory.  sw_search / sw_search_dev /
  * sw_topk work unchanged; sw_search_batch(_dev) returns SW_EINVAL (it needs a
  * resident database).  Per-sequence arrays (scores, offsets) stay on the
@@ -127,7 +131,10 @@ int sw_search(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t 
 
 /*
  * sw_search_dev -- same as sw_search but stream-ordered and device-resident:
- *   query, matrix : host pointers (copied, < 6 KB).
+ *   query, matrix : host pointers, read during the call (copied into a pinned
+ *                   staging slot and sent to the device in one copy together
+ *                   with the search's item cursors; the host does not wait
+ *                   for the stream unless all 4 staging slots are in flight).
  *   d_scores      : DEVICE pointer, int32[count], written in original order.
  *   cuda_stream   : cudaStream_t to order the work on (NULL = legacy default).
  * Returns once all work is enqueued; results are final when the stream
