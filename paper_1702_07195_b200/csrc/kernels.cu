@@ -1835,13 +1835,17 @@ const TileEff kTileEff[] = {
 };
 
 // Latency tiles (EARLY + LROWS, 256 threads, one CTA per SM;
-// tools/lat_calibrate.py, profiles/r02_lat_calibration_early.jsonl): SM cycles
+// tools/lat_calibrate.py, profiles/r02b_lat_calibration.jsonl): SM cycles
 // per column step of a group running alone (one 12,000-residue sequence) and
-// bulk GCUPS (configs[1] at 0.2 scale, one pass).
+// bulk GCUPS (configs[1] at full size, one pass, solo items off).
 struct LatEff { int G, R; float step, bulk; };
 const LatEff kLatEff[] = {
-    {32, 3, 104.8f, 2476.9f}, {32, 4, 130.2f, 2899.2f}, {32, 5, 129.2f, 3073.5f},
-    {32, 6, 164.7f, 3277.4f}, {32, 8, 188.5f, 3597.0f}, {16, 9, 202.4f, 3773.3f},
+    {32, 3, 115.5f, 2432.3f},
+    {32, 4, 136.5f, 2933.0f},
+    {32, 5, 150.3f, 3066.8f},
+    {32, 6, 168.6f, 3354.4f},
+    {32, 8, 199.8f, 3723.9f},
+    {16, 9, 211.8f, 3839.1f},
 };
 
 TileEff tile_eff(int G, int R) {

@@ -444,6 +444,33 @@ def test_streamed_database_matches_resident_and_oracle():
             oracle.batch(queries[1], db.residues, db.offsets, BLOSUM62, 10, 2)).all()
 
 
+def test_streamed_back_to_back_searches_prefetch():
+    """Out-of-core database, searches enqueued back to back on one stream with
+    no synchronisation: each search's chunk 0 was copied during the previous
+    search's last chunk, into the buffer that chunk did not use (odd and even
+    chunk counts), with different queries per search."""
+    import torch
+    rng = np.random.default_rng(556)
+    seqs = [si.rr_residues(rng, int(L)) for L in rng.integers(0, 500, 2500)] + [si.rr_residues(rng, 6000)]
+    db = _db(seqs)
+    st = torch.cuda.Stream()
+    queries = [si.rr_residues(rng, int(m)) for m in (60, 300, 144, 1000, 37)]
+    exps = [oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2) for q in queries]
+    seen = set()
+    for budget in (48 * 1024, 64 * 1024, 96 * 1024, 160 * 1024):
+        sw.sw_db_load_streamed(db.residues, db.offsets, budget)
+        seen.add(sw.sw_db_chunks() % 2)
+        outs = [torch.empty(db.count, dtype=torch.int32, device="cuda") for _ in queries]
+        for q, d in zip(queries, outs):
+            sw.sw_search_dev(q, BLOSUM62, 10, 2, d, st)
+        st.synchronize()
+        for q, d, exp in zip(queries, outs, exps):
+            got = d.cpu().numpy()
+            assert (got == exp).all(), (budget, len(q), int((got != exp).sum()))
+    assert seen == {0, 1}, seen   # both chunk-count parities were exercised
+    sw.sw_db_load(db.residues, db.offsets)
+
+
 def test_shard_count_invariance_sequential_shards():
     """Multi-GPU without a multi-GPU box (SPEC.md:409 analogue): the
     database is residue-balanced into G shards (parallel.shard_database), each
