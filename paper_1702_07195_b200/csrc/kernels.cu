@@ -60,7 +60,10 @@
 #define SW_SCEND 0   // 1: lane G-1 stores the score chain at separator columns only (experiment)
 #endif
 #ifndef SW_DESCADDR
-#define SW_DESCADDR 0   // 1: lane G-1's descriptor address from s_qp instead of s_desc (experiment)
+// lane G-1's descriptor address from its own s_qp (1) or from the shared base s_desc (0),
+// per kernel instantiation from a calibration (-1, kernels.cu desc_from_qp); 0 / 1 force
+// every instantiation (the calibration builds)
+#define SW_DESCADDR -1
 #endif
 #ifndef SW_TAILADDR
 #define SW_TAILADDR 0   // narrow-tail address: 0 = IMAD from the profile offset, 1 = from the chunk address
@@ -246,7 +249,7 @@ __device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on
 //   outgoing registers with lane 0's next-column inputs, including the
 //   previous pass's boundary (prefetched U columns ahead).  No per-lane
 //   selects at lane 0.
-template <int R, int G, bool BIN, int QPM, int NT, int U, bool WAVE = false>
+template <int R, int G, bool BIN, int QPM, int NT, int U, bool WAVE = false, bool DA = false>
 __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   static_assert(!WAVE || BIN, "the wavefront kernel reads boundaries (from pass 1 on)");
   static_assert(U == 1 || U == 2 || U == 4, "U: columns per unrolled block / prefetch distance");
@@ -753,11 +756,13 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
         // s_desc + dnext, written from lane G-1's own s_qp (t = G-1): a register
         // the loop keeps anyway (s_desc itself is rematerialised per column
         // from SR_CgaCtaId under the register cap: 4 instructions)
-#if SW_DESCADDR
-        const DescWords d = EARLY ? dq[u & 1] : load_desc(s_qp + dnext - (uint32_t)(DESC_U4 * 16 + (G - 1) * 16));
-#else
-        const DescWords d = EARLY ? dq[u & 1] : load_desc(s_desc + dnext);
-#endif
+        // DA (per instantiation, desc_from_qp): the same address from lane G-1's
+        // own s_qp; the two forms compile to different register allocations
+        // of the main loop, worth -1..+2% by tile (profiles/r02b_descaddr_calibration.jsonl)
+        constexpr bool DAx = SW_DESCADDR >= 0 ? SW_DESCADDR == 1 : DA;
+        const DescWords d = EARLY ? dq[u & 1]
+                                  : load_desc(DAx ? s_qp + dnext - (uint32_t)(DESC_U4 * 16 + (G - 1) * 16)
+                                                  : s_desc + dnext);
         if (!EARLY) w0 = d.w0;   // (EARLY: word 0 went to lane 0 one step ago)
         ngoe = d.ngoe;
         nge = d.nge;
@@ -1727,6 +1732,22 @@ constexpr int smem_of() {
   return kNL * kNL * 16 + (QPM == 1 ? kSPBytes : kNL * qp_letter_bytes(G, R));
 }
 
+// Per (tile, boundary input, profile mode): 1 when the descriptor address from
+// lane G-1's s_qp measured faster than from the shared base (both forms are
+// the same instructions; the register allocation of the main loop differs).
+// From tools/calibrate_tiles.py under SW_DESCADDR=0 and =1 builds
+// (profiles/r02b_descaddr_calibration.jsonl); query-profile throughput tiles only.
+struct DescPick { int G, R; bool bin; };
+constexpr DescPick kDescFromQp[] = {
+    {0, 0, false},   // (filled by the calibration)
+};
+constexpr bool desc_from_qp(int G, int R, bool bin, int qpm) {
+  if (qpm != 0) return false;
+  for (const DescPick &d : kDescFromQp)
+    if (d.G == G && d.R == R && d.bin == bin) return true;
+  return false;
+}
+
 struct TileEntry {
   int G, R, qpm, nt, smem;
   PassFn fn0, fn1;   // pass 0 / passes > 0 (boundary input)
@@ -1736,18 +1757,20 @@ struct TileEntry {
   int lat;           // 1: latency tile (256 threads, one CTA per SM), for critical-path-bound launches
 };
 
-#define SW_TILE_NTU(G_, R_, M_, NT_, U_)                                                     \
-  {G_, R_, M_, NT_, smem_of<R_, G_, M_>(), sw16_pass_kernel<R_, G_, false, M_, NT_, U_>,   \
-   sw16_pass_kernel<R_, G_, true, M_, NT_, U_>, 0, nullptr, 0, 0}
+#define SW_TILE_NTU(G_, R_, M_, NT_, U_)                                                          \
+  {G_, R_, M_, NT_, smem_of<R_, G_, M_>(),                                                      \
+   sw16_pass_kernel<R_, G_, false, M_, NT_, U_, false, desc_from_qp(G_, R_, false, M_)>,        \
+   sw16_pass_kernel<R_, G_, true, M_, NT_, U_, false, desc_from_qp(G_, R_, true, M_)>, 0, nullptr, 0, 0}
 // latency tiles (single query): small R, 256 threads, launched
 // with one CTA per SM, for passes bounded by one long item's critical path
 #define SW_TILE_LAT(G_, R_)                                                                    \
   {G_, R_, 0, 256, smem_of<R_, G_, 0>(), sw16_pass_kernel<R_, G_, false, 0, 256, SW_UNROLL>, \
    sw16_pass_kernel<R_, G_, true, 0, 256, SW_UNROLL>, 0, nullptr, 0, 1}
 // tiles that also have a wavefront kernel (single-query mode)
-#define SW_TILE_W(G_, R_)                                                                     \
-  {G_, R_, 0, 512, smem_of<R_, G_, 0>(), sw16_pass_kernel<R_, G_, false, 0, 512, SW_UNROLL>, \
-   sw16_pass_kernel<R_, G_, true, 0, 512, SW_UNROLL>, 0,                                      \
+#define SW_TILE_W(G_, R_)                                                                       \
+  {G_, R_, 0, 512, smem_of<R_, G_, 0>(),                                                        \
+   sw16_pass_kernel<R_, G_, false, 0, 512, SW_UNROLL, false, desc_from_qp(G_, R_, false, 0)>,   \
+   sw16_pass_kernel<R_, G_, true, 0, 512, SW_UNROLL, false, desc_from_qp(G_, R_, true, 0)>, 0,  \
    sw16_pass_kernel<R_, G_, true, 0, 512, SW_UNROLL, true>, 0, 0}
 #ifndef SW_UNROLL
 #define SW_UNROLL 4   // columns per unrolled block = lane G-1's prefetch distance
