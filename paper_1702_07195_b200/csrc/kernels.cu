@@ -1735,11 +1735,68 @@ constexpr int smem_of() {
 // Per (tile, boundary input, profile mode): 1 when the descriptor address from
 // lane G-1's s_qp measured faster than from the shared base (both forms are
 // the same instructions; the register allocation of the main loop differs).
-// From tools/calibrate_tiles.py under SW_DESCADDR=0 and =1 builds
-// (profiles/r02b_descaddr_calibration.jsonl); query-profile throughput tiles only.
+// From tools/calibrate_tiles.py under SW_DESCADDR=0 and =1 builds, >= 0.5%
+// faster (profiles/r02b_descaddr_calibration.jsonl, tools/descaddr_table.py);
+// query-profile throughput tiles only.
 struct DescPick { int G, R; bool bin; };
 constexpr DescPick kDescFromQp[] = {
-    {0, 0, false},   // (filled by the calibration)
+    {8, 8, false},
+    {8, 8, true},
+    {8, 12, false},
+    {8, 12, true},
+    {8, 16, false},
+    {8, 16, true},
+    {8, 18, false},
+    {8, 18, true},
+    {8, 20, false},
+    {8, 20, true},
+    {8, 22, false},
+    {8, 22, true},
+    {8, 24, false},
+    {8, 24, true},
+    {8, 26, false},
+    {8, 26, true},
+    {8, 28, false},
+    {8, 28, true},
+    {8, 29, true},
+    {8, 30, false},
+    {8, 30, true},
+    {16, 8, false},
+    {16, 8, true},
+    {16, 12, false},
+    {16, 12, true},
+    {16, 16, false},
+    {16, 16, true},
+    {16, 18, false},
+    {16, 18, true},
+    {16, 20, false},
+    {16, 20, true},
+    {16, 22, false},
+    {16, 22, true},
+    {16, 24, false},
+    {16, 24, true},
+    {16, 26, false},
+    {16, 26, true},
+    {16, 28, false},
+    {16, 28, true},
+    {16, 30, false},
+    {16, 30, true},
+    {32, 8, false},
+    {32, 12, false},
+    {32, 12, true},
+    {32, 15, false},
+    {32, 15, true},
+    {32, 16, false},
+    {32, 16, true},
+    {32, 20, false},
+    {32, 22, false},
+    {32, 22, true},
+    {32, 24, false},
+    {32, 26, true},
+    {32, 28, false},
+    {32, 29, true},
+    {32, 30, false},
+    {32, 32, false},
 };
 constexpr bool desc_from_qp(int G, int R, bool bin, int qpm) {
   if (qpm != 0) return false;
@@ -1810,51 +1867,53 @@ TileEntry g_tiles[] = {
 constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
 
 // Measured full-row throughput (GCUPS) of each tile's pass kernel on one
-// B200, biased-unsigned arithmetic, configs[1] at FULL size (round 2,
-// tools/calibrate_tiles.py 1.0, profiles/r02b_tile_calibration_full.jsonl;
-// round 1's table came from a 0.3-scale database and ran 2-5% lower): eff0 =
+// B200, biased-unsigned arithmetic, configs[1] at FULL size, in the
+// descriptor-address form kDescFromQp picks (round 2, tools/calibrate_tiles.py
+// 1.0 under both forms, profiles/r02b_descaddr_calibration.jsonl,
+// tools/descaddr_table.py; round 1's table came from a 0.3-scale database and
+// ran 2-5% lower): eff0 =
 // first pass (query of G*R), eff1 = a pass reading the previous pass's
 // boundary (2*G*R minus G*R).  The tile choice predicts time
 // ~ G*R * (1/eff0 + (P-1)/eff1).
 struct TileEff { int G, R; float eff0, eff1; };
 const TileEff kTileEff[] = {
-    {8, 8, 4376.3f, 3593.6f},
-    {8, 12, 5146.3f, 4495.5f},
-    {8, 16, 5407.8f, 5036.3f},
-    {8, 18, 5592.9f, 5133.4f},
-    {8, 20, 5685.7f, 5314.9f},
-    {8, 22, 5719.6f, 5419.0f},
-    {8, 24, 5768.3f, 5492.2f},
-    {8, 26, 5826.4f, 5607.1f},
-    {8, 28, 5813.4f, 5628.1f},
-    {8, 29, 5961.6f, 5669.2f},
-    {8, 30, 5925.9f, 5679.4f},
-    {8, 32, 5950.9f, 5665.6f},
-    {16, 8, 4427.5f, 3821.6f},
-    {16, 12, 5161.6f, 4621.5f},
-    {16, 16, 5423.4f, 5110.5f},
-    {16, 18, 5592.2f, 5184.4f},
-    {16, 20, 5681.2f, 5332.0f},
-    {16, 22, 5720.7f, 5430.1f},
-    {16, 24, 5770.8f, 5496.6f},
-    {16, 26, 5832.3f, 5621.2f},
-    {16, 28, 5811.6f, 5639.8f},
-    {16, 29, 5961.9f, 5675.6f},
-    {16, 30, 5921.1f, 5683.7f},
-    {16, 32, 5962.1f, 5679.4f},
-    {32, 8, 4493.4f, 3963.9f},
-    {32, 12, 5038.6f, 4772.3f},
-    {32, 15, 5356.8f, 5017.0f},
-    {32, 16, 5370.9f, 5026.1f},
-    {32, 18, 5623.4f, 5231.5f},
-    {32, 20, 5649.6f, 5403.7f},
-    {32, 22, 5678.4f, 5474.4f},
-    {32, 24, 5719.5f, 5587.0f},
-    {32, 26, 5768.8f, 5550.7f},
-    {32, 28, 5690.3f, 5626.9f},
-    {32, 29, 5835.2f, 5608.6f},
-    {32, 30, 5802.5f, 5648.2f},
-    {32, 32, 5961.3f, 5666.6f},
+    {8, 8, 4409.6f, 3640.3f},
+    {8, 12, 5194.2f, 4528.7f},
+    {8, 16, 5532.6f, 5106.0f},
+    {8, 18, 5731.3f, 5230.7f},
+    {8, 20, 5754.7f, 5425.0f},
+    {8, 22, 5803.6f, 5549.9f},
+    {8, 24, 5834.0f, 5555.0f},
+    {8, 26, 5904.2f, 5678.3f},
+    {8, 28, 5900.0f, 5697.6f},
+    {8, 29, 5962.4f, 5701.8f},
+    {8, 30, 6014.1f, 5754.4f},
+    {8, 32, 5952.3f, 5670.9f},
+    {16, 8, 4464.6f, 3866.3f},
+    {16, 12, 5210.4f, 4672.4f},
+    {16, 16, 5530.1f, 5173.0f},
+    {16, 18, 5738.4f, 5309.7f},
+    {16, 20, 5754.6f, 5439.7f},
+    {16, 22, 5804.3f, 5568.1f},
+    {16, 24, 5834.1f, 5557.7f},
+    {16, 26, 5909.3f, 5683.3f},
+    {16, 28, 5894.1f, 5702.9f},
+    {16, 29, 5963.0f, 5673.9f},
+    {16, 30, 6015.9f, 5761.3f},
+    {16, 32, 5963.1f, 5679.4f},
+    {32, 8, 4573.4f, 3964.3f},
+    {32, 12, 5291.5f, 4821.0f},
+    {32, 15, 5411.5f, 5071.9f},
+    {32, 16, 5527.3f, 5123.4f},
+    {32, 18, 5619.7f, 5229.0f},
+    {32, 20, 5796.1f, 5403.9f},
+    {32, 22, 5741.6f, 5535.5f},
+    {32, 24, 5829.3f, 5590.2f},
+    {32, 26, 5768.7f, 5604.8f},
+    {32, 28, 5747.0f, 5626.4f},
+    {32, 29, 5835.5f, 5734.1f},
+    {32, 30, 5841.2f, 5648.3f},
+    {32, 32, 5998.9f, 5666.6f},
 };
 
 // Latency tiles (EARLY + LROWS, 256 threads, one CTA per SM;
