@@ -42,7 +42,7 @@
 #define SW_BRING 0   // 1: boundary prefetch ring in every boundary-reading kernel (experiment)
 #endif
 #ifndef SW_ROWAHEAD
-#define SW_ROWAHEAD 1
+#define SW_ROWAHEAD -1   // -1: per kernel instantiation (kRowPlain); 0 / 1 force every one
 #endif
 #ifndef SW_ROWS_TRACE
 #define SW_ROWS_TRACE 0   // 1: the rows kernel prints per-pass cycle counts of item 0 (experiments)
@@ -249,7 +249,7 @@ __device__ __forceinline__ T *ptr_add(T *p, uint32_t n) {  // p + n elements, on
 //   outgoing registers with lane 0's next-column inputs, including the
 //   previous pass's boundary (prefetched U columns ahead).  No per-lane
 //   selects at lane 0.
-template <int R, int G, bool BIN, int QPM, int NT, int U, bool WAVE = false, bool DA = false>
+template <int R, int G, bool BIN, int QPM, int NT, int U, bool WAVE = false, bool DA = false, bool RA = true>
 __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
   static_assert(!WAVE || BIN, "the wavefront kernel reads boundaries (from pass 1 on)");
   static_assert(U == 1 || U == 2 || U == 4, "U: columns per unrolled block / prefetch distance");
@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           F = haddmax(F, nge, hg);                    // Eq. 3 (next row)
           tcur = tnext;
         }
-      } else if (kBiased && SW_ROWAHEAD && SW_ABLATE == 0) {
+      } else if (kBiased && (SW_ROWAHEAD >= 0 ? (SW_ROWAHEAD == 1 || EARLY) : RA) && SW_ABLATE == 0) {
         // Biased rows with the diagonal add one row ahead: t(r+1) = H_old[r] + P(r+1)
         // is formed before H[r] is overwritten, so the new H can take the old H's
         // register (no per-column rotation of the H registers, which otherwise
@@ -1804,6 +1804,18 @@ constexpr bool desc_from_qp(int G, int R, bool bin, int qpm) {
     if (d.G == G && d.R == R && d.bin == bin) return true;
   return false;
 }
+// Per (tile, boundary input): the plain row order of the biased cell loop
+// (the diagonal add after the row) instead of one row ahead, where it measured
+// >= 0.5% faster (profiles/r02b_variant_calibration.jsonl).
+constexpr DescPick kRowPlain[] = {
+    {0, 0, false},   // (filled by the calibration)
+};
+constexpr bool row_ahead(int G, int R, bool bin, int qpm) {
+  if (qpm != 0) return true;
+  for (const DescPick &d : kRowPlain)
+    if (d.G == G && d.R == R && d.bin == bin) return false;
+  return true;
+}
 
 struct TileEntry {
   int G, R, qpm, nt, smem;
@@ -1816,8 +1828,10 @@ struct TileEntry {
 
 #define SW_TILE_NTU(G_, R_, M_, NT_, U_)                                                          \
   {G_, R_, M_, NT_, smem_of<R_, G_, M_>(),                                                      \
-   sw16_pass_kernel<R_, G_, false, M_, NT_, U_, false, desc_from_qp(G_, R_, false, M_)>,        \
-   sw16_pass_kernel<R_, G_, true, M_, NT_, U_, false, desc_from_qp(G_, R_, true, M_)>, 0, nullptr, 0, 0}
+   sw16_pass_kernel<R_, G_, false, M_, NT_, U_, false, desc_from_qp(G_, R_, false, M_),          \
+                    row_ahead(G_, R_, false, M_)>,                                              \
+   sw16_pass_kernel<R_, G_, true, M_, NT_, U_, false, desc_from_qp(G_, R_, true, M_),            \
+                    row_ahead(G_, R_, true, M_)>, 0, nullptr, 0, 0}
 // latency tiles (single query): small R, 256 threads, launched
 // with one CTA per SM, for passes bounded by one long item's critical path
 #define SW_TILE_LAT(G_, R_)                                                                    \
@@ -1826,8 +1840,10 @@ struct TileEntry {
 // tiles that also have a wavefront kernel (single-query mode)
 #define SW_TILE_W(G_, R_)                                                                       \
   {G_, R_, 0, 512, smem_of<R_, G_, 0>(),                                                        \
-   sw16_pass_kernel<R_, G_, false, 0, 512, SW_UNROLL, false, desc_from_qp(G_, R_, false, 0)>,   \
-   sw16_pass_kernel<R_, G_, true, 0, 512, SW_UNROLL, false, desc_from_qp(G_, R_, true, 0)>, 0,  \
+   sw16_pass_kernel<R_, G_, false, 0, 512, SW_UNROLL, false, desc_from_qp(G_, R_, false, 0),     \
+                    row_ahead(G_, R_, false, 0)>,                                               \
+   sw16_pass_kernel<R_, G_, true, 0, 512, SW_UNROLL, false, desc_from_qp(G_, R_, true, 0),       \
+                    row_ahead(G_, R_, true, 0)>, 0,                                             \
    sw16_pass_kernel<R_, G_, true, 0, 512, SW_UNROLL, true>, 0, 0}
 #ifndef SW_UNROLL
 #define SW_UNROLL 4   // columns per unrolled block = lane G-1's prefetch distance
