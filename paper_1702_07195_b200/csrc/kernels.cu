@@ -1808,7 +1808,10 @@ constexpr bool desc_from_qp(int G, int R, bool bin, int qpm) {
 // (the diagonal add after the row) instead of one row ahead, where it measured
 // >= 0.5% faster (profiles/r02b_variant_calibration.jsonl).
 constexpr DescPick kRowPlain[] = {
-    {0, 0, false},   // (filled by the calibration)
+    {8, 20, false}, {8, 20, true}, {8, 22, false}, {8, 24, false}, {8, 28, false}, {8, 28, true},
+    {8, 32, true}, {16, 20, false}, {16, 20, true}, {16, 22, false}, {16, 24, false}, {16, 28, false},
+    {16, 28, true}, {32, 8, true}, {32, 15, false}, {32, 16, false}, {32, 16, true}, {32, 18, true},
+    {32, 22, false}, {32, 24, false}, {32, 26, true}, {32, 28, false}, {32, 29, false}, {32, 30, false},
 };
 constexpr bool row_ahead(int G, int R, bool bin, int qpm) {
   if (qpm != 0) return true;
@@ -1886,50 +1889,51 @@ constexpr int kNumTiles = sizeof(g_tiles) / sizeof(g_tiles[0]);
 // B200, biased-unsigned arithmetic, configs[1] at FULL size, in the
 // descriptor-address form kDescFromQp picks (round 2, tools/calibrate_tiles.py
 // 1.0 under both forms, profiles/r02b_descaddr_calibration.jsonl,
-// tools/descaddr_table.py; round 1's table came from a 0.3-scale database and
-// ran 2-5% lower): eff0 =
+// tools/descaddr_table.py) and the row order kRowPlain picks (the same tool
+// under SW_ROWAHEAD=1 / =0 builds, profiles/r02b_variant_calibration.jsonl);
+// round 1's table came from a 0.3-scale database and ran 2-5% lower: eff0 =
 // first pass (query of G*R), eff1 = a pass reading the previous pass's
 // boundary (2*G*R minus G*R).  The tile choice predicts time
 // ~ G*R * (1/eff0 + (P-1)/eff1).
 struct TileEff { int G, R; float eff0, eff1; };
 const TileEff kTileEff[] = {
-    {8, 8, 4409.6f, 3640.3f},
-    {8, 12, 5194.2f, 4528.7f},
-    {8, 16, 5532.6f, 5106.0f},
-    {8, 18, 5731.3f, 5230.7f},
-    {8, 20, 5754.7f, 5425.0f},
-    {8, 22, 5803.6f, 5549.9f},
-    {8, 24, 5834.0f, 5555.0f},
-    {8, 26, 5904.2f, 5678.3f},
-    {8, 28, 5900.0f, 5697.6f},
-    {8, 29, 5962.4f, 5701.8f},
-    {8, 30, 6014.1f, 5754.4f},
-    {8, 32, 5952.3f, 5670.9f},
-    {16, 8, 4464.6f, 3866.3f},
-    {16, 12, 5210.4f, 4672.4f},
-    {16, 16, 5530.1f, 5173.0f},
-    {16, 18, 5738.4f, 5309.7f},
-    {16, 20, 5754.6f, 5439.7f},
-    {16, 22, 5804.3f, 5568.1f},
-    {16, 24, 5834.1f, 5557.7f},
-    {16, 26, 5909.3f, 5683.3f},
-    {16, 28, 5894.1f, 5702.9f},
-    {16, 29, 5963.0f, 5673.9f},
-    {16, 30, 6015.9f, 5761.3f},
-    {16, 32, 5963.1f, 5679.4f},
-    {32, 8, 4573.4f, 3964.3f},
-    {32, 12, 5291.5f, 4821.0f},
-    {32, 15, 5411.5f, 5071.9f},
-    {32, 16, 5527.3f, 5123.4f},
-    {32, 18, 5619.7f, 5229.0f},
-    {32, 20, 5796.1f, 5403.9f},
-    {32, 22, 5741.6f, 5535.5f},
-    {32, 24, 5829.3f, 5590.2f},
-    {32, 26, 5768.7f, 5604.8f},
-    {32, 28, 5747.0f, 5626.4f},
-    {32, 29, 5835.5f, 5734.1f},
-    {32, 30, 5841.2f, 5648.3f},
-    {32, 32, 5998.9f, 5666.6f},
+    {8, 8, 4411.0f, 3628.2f},
+    {8, 12, 5202.2f, 4507.4f},
+    {8, 16, 5541.1f, 5106.0f},
+    {8, 18, 5726.3f, 5238.0f},
+    {8, 20, 5804.8f, 5466.5f},
+    {8, 22, 5843.1f, 5553.7f},
+    {8, 24, 5892.6f, 5561.9f},
+    {8, 26, 5919.6f, 5690.1f},
+    {8, 28, 5958.2f, 5760.4f},
+    {8, 29, 5967.1f, 5699.0f},
+    {8, 30, 6021.9f, 5760.6f},
+    {8, 32, 5953.8f, 5709.2f},
+    {16, 8, 4463.2f, 3861.8f},
+    {16, 12, 5214.1f, 4665.8f},
+    {16, 16, 5540.1f, 5174.5f},
+    {16, 18, 5744.9f, 5308.0f},
+    {16, 20, 5806.9f, 5480.4f},
+    {16, 22, 5844.3f, 5566.4f},
+    {16, 24, 5885.6f, 5563.7f},
+    {16, 26, 5915.7f, 5692.7f},
+    {16, 28, 5953.1f, 5764.5f},
+    {16, 29, 5968.5f, 5674.4f},
+    {16, 30, 6022.5f, 5759.0f},
+    {16, 32, 5968.2f, 5684.4f},
+    {32, 8, 4575.3f, 3969.8f},
+    {32, 12, 5296.1f, 4816.8f},
+    {32, 15, 5468.5f, 5072.6f},
+    {32, 16, 5582.6f, 5170.8f},
+    {32, 18, 5628.5f, 5265.4f},
+    {32, 20, 5800.9f, 5405.9f},
+    {32, 22, 5804.2f, 5542.8f},
+    {32, 24, 5912.1f, 5592.2f},
+    {32, 26, 5773.9f, 5672.4f},
+    {32, 28, 5817.2f, 5631.1f},
+    {32, 29, 5888.3f, 5738.4f},
+    {32, 30, 5894.1f, 5650.3f},
+    {32, 32, 6004.0f, 5672.6f},
 };
 
 // Latency tiles (EARLY + LROWS, 256 threads, one CTA per SM;

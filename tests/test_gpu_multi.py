@@ -263,3 +263,91 @@ def test_timing_history_matches_last_timing():
     assert abs(h[-1] - last) < 1e-6
     assert len(sw.sw_timing_history(1000)) <= 64
     assert (d.cpu().numpy() == oracle.batch(qs[-1], w.db.residues, w.db.offsets, BLOSUM62, 10, 2)).all()
+
+
+# ---------------------------------------------------------------------------
+# The bench's sharded step at world size 2 with the real kernels: two ranks
+# (gloo process group, both on cuda:0, each with its own library state) build
+# their shards with bench.Work, run the search and the shard top-k in
+# libswdb.so, and rank 0 assembles every score in original order and merges
+# the top-k with the library's scatter / top-k kernels.  gloo gathers only CPU
+# tensors, so ShardedSearch runs on CPU buffers and the backend stages each
+# call's operands through device copies; the ranks' kernels never wait on one
+# another (no device-side exchange), so one GPU is a faithful stand-in for
+# the data each rank computes.  Expected: the oracle over the whole database.
+# ---------------------------------------------------------------------------
+class _StagedLibBackend:
+    def __init__(self):
+        from paper_1702_07195_b200.parallel import LibBackend
+        self.lib = LibBackend(sw)
+
+    def search(self, queries, M, go, ge, d_out, stream):
+        d = torch.zeros(d_out.numel(), dtype=torch.int32, device="cuda")
+        n = self.lib.search(queries, M, go, ge, d, None)
+        torch.cuda.synchronize()
+        d_out.copy_(d.cpu())
+        return n
+
+    def topk(self, d_scores, d_index, n, k, d_idx_out, d_score_out, stream):
+        s = d_scores[:n].cuda()
+        i = d_index[:n].cuda() if d_index is not None else None
+        oi = torch.empty(k, dtype=torch.int64, device="cuda")
+        os_ = torch.empty(k, dtype=torch.int32, device="cuda")
+        r = self.lib.topk(s, i, n, k, oi, os_, None)
+        torch.cuda.synchronize()
+        d_idx_out[:k].copy_(oi.cpu())
+        d_score_out[:k].copy_(os_.cpu())
+        return r
+
+    def scatter(self, d_src, d_index, n, d_dst, dst_count, stream):
+        dst = d_dst.cuda()
+        self.lib.scatter(d_src[:n].cuda(), d_index[:n].cuda(), n, dst, dst_count, None)
+        torch.cuda.synchronize()
+        d_dst.copy_(dst.cpu())
+
+
+def _world2_worker(rank, world, port, cfg, scale, nq, result_path):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    sys.path.insert(0, ROOT)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from paper_1702_07195_b200.parallel import ShardedSearch
+    w = bench.Work(cfg, scale, world, rank)
+    sw.sw_db_load(w.db.residues, w.db.offsets)
+    queries = w.queries[:nq]
+    ss = ShardedSearch(_StagedLibBackend(), w.gidx, w.count_global, len(queries), 10, torch.device("cpu"),
+                       dist=dist, world=world, rank=rank)
+    for _ in range(2):    # a second step over the same buffers: the assembly is repeatable
+        ss.step(queries, w.matrix, w.gap_open, w.gap_extend, None)
+    if rank == 0:
+        full, ti, ts = ss.result()
+        np.savez(result_path, full=full.numpy(), ti=ti.numpy(), ts=ts.numpy(), ng=w.count_global,
+                 res=w.residues_global, mine=w.db.count)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,scale,nq", [(2, 0.003, 1), (3, 0.002, 3), (4, 0.01, 1), (0, 0.2, 1)])
+def test_bench_sharded_step_world2_real_kernels(tmp_path, cfg, scale, nq):
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    path = str(tmp_path / "res.npz")
+    mp.spawn(_world2_worker, args=(2, port, cfg, scale, nq, path), nprocs=2, join=True)
+    r = np.load(path)
+    gscale = scale * (2 if cfg in (0, 1) else 1)
+    wfull = si.make_config(cfg, scale=gscale)
+    assert int(r["ng"]) == wfull.db.count and int(r["res"]) == wfull.db.total_residues
+    assert 0 < int(r["mine"]) < wfull.db.count          # rank 0 held a proper shard
+    qs = wfull.queries[:nq]
+    for k, q in enumerate(qs):
+        exp = oracle.batch(q, wfull.db.residues, wfull.db.offsets, wfull.matrix, wfull.gap_open,
+                           wfull.gap_extend)
+        assert np.array_equal(r["full"][k], exp), (cfg, k, int(np.sum(r["full"][k] != exp)))
+        ei, es = oracle.topk(exp, 10)
+        assert np.array_equal(r["ti"][k], ei) and np.array_equal(r["ts"][k], es)
