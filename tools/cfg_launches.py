@@ -1,4 +1,4 @@
-"""Launch list of cfg0 searches (run under ncu --metrics gpu__time_duration.sum):
+"""Launch list of configs[CFG] searches (default cfg0) (run under ncu --metrics gpu__time_duration.sum):
 where the non-pass-kernel time of a small search goes.  Without ncu it prints
 the single-search and back-to-back event times and the pass-kernel time."""
 import json, os, sys
@@ -7,7 +7,8 @@ import numpy as np, torch
 import sw_inputs as si
 import paper_1702_07195_b200 as sw
 
-w = si.config0()
+CFG = int(os.environ.get("CFG", "0"))
+w = si.make_config(CFG)
 sw.sw_db_load(w.db.residues, w.db.offsets)
 d = torch.empty(w.db.count, dtype=torch.int32, device="cuda")
 st = torch.cuda.Stream()
@@ -24,7 +25,7 @@ for _ in range(int(os.environ.get("REPS", "5"))):
     st.synchronize()
     one.append(e0.elapsed_time(e1))
     pk.append(sw.sw_last_timing()["pass_kernels_ms"])
-n = 50
+n = int(os.environ.get("B2B", "50"))
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(st)
 for _ in range(n):
