@@ -648,6 +648,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     q.offs = g.offs.p;
     q.qp32 = k ? g.qp32b.p : g.qp32.p;
     q.m = mm;
+    q.len = len;
     q.row0 = row0;
     q.passes = (len - row0 + 32 * kSW32Rows - 1) / (32 * kSW32Rows);
     q.neg_goe = -goe;

@@ -33,6 +33,7 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <type_traits>
 #include <climits>
 #include <cstdio>
 
@@ -1179,8 +1180,6 @@ __global__ void sw16_update_kernel(const int64_t *__restrict__ endcol, int64_t c
 // ---------------------------------------------------------------------------
 template <int R>
 __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) {
-  constexpr int K4 = R / 4;
-  constexpr int SLICE_U4 = kNL * K4 * 32;
   extern __shared__ uint4 sq[];
   __shared__ int s_base;
   const int lane = threadIdx.x & 31;
@@ -1222,24 +1221,31 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
       col0 = (e >> 1) - n;                   // the sequence's first stream column
       half = p.half >= 0 ? p.half : (int)(e & 1);
     }
-    for (int pass = 0; pass < p.passes; ++pass) {
+    // One query pass of RR rows per lane (RR = R, or a narrower last pass:
+    // only the rows the query still has are computed, no phantom rows beyond
+    // the next multiple of 32 * RR).  CTA-uniform: staging synchronises.
+    int64_t rows_done = 0;
+    auto run_pass = [&](int pass, auto rr_c) {
+      constexpr int RR = decltype(rr_c)::value;
+      constexpr int KR = RR / 4;
       __syncthreads();
       // stage this pass's profile slice [letter][4-row chunk][lane][4] from the
-      // plain [letter][m] profile, rows row0 + pass*32*R ...
-      for (int i = threadIdx.x; i < SLICE_U4 * 4; i += blockDim.x) {
+      // plain [letter][m] profile, rows row0 + pass*32*R + lane*RR ...
+      for (int i = threadIdx.x; i < kNL * KR * 32 * 4; i += blockDim.x) {
         const int e4 = i & 3, ln = (i >> 2) & 31, rest = i >> 7;
-        const int kk = rest % K4, c = rest / K4;
-        const int row = p.row0 + pass * 32 * R + ln * R + kk * 4 + e4;
+        const int kk = rest % KR, c = rest / KR;
+        const int row = p.row0 + pass * 32 * R + ln * RR + kk * 4 + e4;
         reinterpret_cast<int32_t *>(sq)[i] = row < p.m ? p.qp32[(int64_t)c * p.m + row] : -(1 << 30);
       }
       __syncthreads();
-      if (!active) continue;
+      rows_done += 32 * RR;
+      if (!active) return;
       const uint2 *bin = pass == 0 ? nullptr : ((pass & 1) ? buf0 : buf1);
       const uint2 *b16 = (pass == 0 && p.row0 > 0) ? p.bnd16 + col0 : nullptr;
       uint2 *bout = pass == p.passes - 1 ? nullptr : ((pass & 1) ? buf1 : buf0);
-      int H[R], E[R];
+      int H[RR], E[RR];
 #pragma unroll
-      for (int r = 0; r < R; ++r) { H[r] = 0; E[r] = 0; }
+      for (int r = 0; r < RR; ++r) { H[r] = 0; E[r] = 0; }
       int S = 0, hout = 0, fout = 0, hprev = 0, code = kNul;
       // Lane 0's column inputs (letter, boundary H and F of the row above) are
       // fetched 32 columns at a time, one column per lane, coalesced and one
@@ -1287,11 +1293,11 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
           code = first ? rc : code_up;
           const int hu = hu_up * nfirst + bh;
           int F = fu_up * nfirst + bf;
-          const uint32_t qa = sbase + (uint32_t)code * (K4 * 32 * 16);
+          const uint32_t qa = sbase + (uint32_t)code * (KR * 32 * 16);
           int hd = hprev;
           hprev = hu;
 #pragma unroll
-          for (int kk = 0; kk < K4; ++kk) {
+          for (int kk = 0; kk < KR; ++kk) {
             const uint4 a = lds128(qa + kk * 32 * 16);
             const int av[4] = {(int)a.x, (int)a.y, (int)a.z, (int)a.w};
 #pragma unroll
@@ -1308,14 +1314,28 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
             }
           }
 #pragma unroll
-          for (int r = 0; r + 1 < R; r += 2) S = __vimax3_s32(S, H[r], H[r + 1]);
-          hout = H[R - 1];
+          for (int r = 0; r + 1 < RR; r += 2) S = __vimax3_s32(S, H[r], H[r + 1]);
+          hout = H[RR - 1];
           fout = F;
           if (last && bout) bout[c - 31] = make_uint2((uint32_t)hout, (uint32_t)fout);
         }
       }
       best = max(best, S);
       __syncwarp();
+    };
+    for (int pass = 0; pass < p.passes; ++pass) {
+      if constexpr (R % 12 == 0) {
+        const int left = p.len - p.row0 - pass * 32 * R;   // query rows from this pass on
+        if (pass == p.passes - 1 && left <= 32 * (R / 3)) {
+          run_pass(pass, std::integral_constant<int, R / 3>{});
+          continue;
+        }
+        if (pass == p.passes - 1 && left <= 32 * (2 * R / 3)) {
+          run_pass(pass, std::integral_constant<int, 2 * R / 3>{});
+          continue;
+        }
+      }
+      run_pass(pass, std::integral_constant<int, R>{});
     }
     if (active) {
 #pragma unroll
@@ -1323,7 +1343,7 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
       if (first) {
         p.scores[orig] = best;
         if (p.cells) atomicAdd(reinterpret_cast<unsigned long long *>(p.cells),
-                               (unsigned long long)n * (unsigned long long)(p.passes * 32 * R));
+                               (unsigned long long)n * (unsigned long long)rows_done);
       }
     }
   }

@@ -136,6 +136,8 @@ struct SW32Params {
   const int64_t *offs;
   const int32_t *qp32;      // plain int32 profile [kNL][m] (-2^30 for separator letters)
   int m;                    // query length (rows of qp32)
+  int len;                  // rows of this query (<= m; a pair's shorter query); the last pass
+                            // runs R/3 or 2R/3 rows per lane when that covers the rest
   int row0;                 // first query row to compute (rows < row0 were exact in 16 bit)
   int passes;               // ceil((m - row0) / (32 * R))
   int neg_goe, neg_ge;      // -(open+extend), -extend  (>= -2^30)

@@ -176,6 +176,32 @@ def test_saturation_boundary_and_rescoring():
     assert _flags_ok(st, [11 * n for n in ns])
 
 
+def test_rescoring_narrow_last_pass():
+    """The 32-bit kernel's last query pass runs R/3 or 2R/3 rows per lane when
+    that covers the rows left (no phantom rows past the next multiple of 32 rows
+    per lane width).  One W^3000 sequence flags in the 16-bit pass holding row
+    ~2,978 (8x8 tile: 64 rows per pass, re-scoring from row 2,944); the query
+    length sets the rows left at and around every width edge (256 / 512 / 768
+    rows per pass of the 24-row kernel).  cells32 pins the rows computed."""
+    db = _db([encode("W" * 3000)])
+    sw.sw_db_load(db.residues, db.offsets)
+    sw.sw_set_tile(8, 8)
+    try:
+        for k in (40, 255, 256, 257, 511, 512, 513, 767, 768, 769, 1280, 1281, 1537):
+            q = encode("W" * (2944 + k))
+            got = sw.sw_search(q, BLOSUM62, 10, 2)
+            assert int(got[0]) == 33000, k
+            st = sw.sw_last_stats()
+            assert st["flagged"] == 1, k
+            rows = 2944 + k - 2944
+            passes = -(-rows // 768)
+            left = rows - (passes - 1) * 768
+            last = 256 if left <= 256 else (512 if left <= 512 else 768)
+            assert st["cells32"] == 3000 * ((passes - 1) * 768 + last), (k, st["cells32"])
+    finally:
+        sw.sw_set_tile(0)
+
+
 def test_rescoring_seeded_from_pass_boundaries():
     """Sequences flagged in a later 16-bit pass are re-scored in 32 bit from that
     pass's first row, seeded with its exact input boundary.  A
