@@ -512,6 +512,12 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   for (int i = 0; i < kAlpha * kAlpha; ++i) smax = std::max(smax, (int)matrix[i]);
   const int thresh = kHalfTop - smax;   // stored 16-bit units (R7)
   g.last_thresh = thresh - kBias16;  // in score units
+  // A local alignment pairs at most min(m, n) residues, each scoring <= smax,
+  // so no score reaches the flag threshold when smax * min(m, longest
+  // sequence) is below it (configs[0-3]): the search then launches no flag
+  // detection, no flag compaction, no item skipping and no 32-bit re-scoring.
+  const bool can_flag = (int64_t)smax * std::min<int64_t>(mm, std::max<int64_t>(g.max_len, 1)) >=
+                        (int64_t)g.last_thresh;
   const int goe = gap_open + gap_extend, ge = gap_extend;
 
   // Item cursors per (chunk, pass), then the solo cursors: the leading,
@@ -714,7 +720,8 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     g.hnpev[g.hslot] = g.npev;
     // the score chain was carried through the passes: one gather of the maxima
     CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p, nullptr, nullptr, 0,
-                                thresh, st, nullptr, item_of, g.item_hot.p));
+                                thresh, st, nullptr, item_of, g.item_hot.p, nullptr, nullptr, nullptr, nullptr, 0,
+                                can_flag));
   }
   int npl = 0;   // pass launches so far (per-pass path)
   for (int k = 0; k < (wave ? 0 : nch); ++k) {
@@ -763,7 +770,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
       p.one = 1u;
       // resident single-query passes after the first start each item behind
       // its leading run of flagged sequences (item_skip_kernel below)
-      const bool skipping = !strm && !pair && P > 1;
+      const bool skipping = !strm && !pair && P > 1 && can_flag;
       p.skip = (skipping && pass > 0) ? g.skip.p : nullptr;
       p.query = g.q_d;
       p.m = m;
@@ -801,16 +808,17 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
         const State::Chunk &c = g.chunks[k];
         CUDA_TRY(launch_sw16_gather(g.cseq_endcol.p + c.seq_begin, c.seq_end - c.seq_begin, g.sc_out.p - base,
                                     d_scores, g.flagged.p, nullptr, nullptr, pass, thresh, st,
-                                    g.cseq_idx.p + c.seq_begin, item_of, g.item_hot.p));
+                                    g.cseq_idx.p + c.seq_begin, item_of, g.item_hot.p, nullptr, nullptr, nullptr,
+                                    nullptr, 0, can_flag));
       } else {
         // the update launch also compacts the sequences first flagged in this
         // pass for the 32-bit kernel (passes < 254; flag byte pass + 1)
-        const bool fuse = pass + 1 < 255;
+        const bool fuse = pass + 1 < 255 && can_flag;
         CUDA_TRY(launch_sw16_gather(I.endcol.p, g.count, g.sc_out.p, d_scores, g.flagged.p,
                                     pair ? d_scores2 : nullptr, pair ? g.flagged2.p : nullptr, pass, thresh, st,
                                     nullptr, item_of, pair ? nullptr : g.item_hot.p, g.flag_list.p,
                                     g.fcounters.p + 4 * pass, pair ? g.flag_list2.p : nullptr,
-                                    g.fcounters.p + 4 * pass + 2, fuse ? pass + 1 : 0));
+                                    g.fcounters.p + 4 * pass + 2, fuse ? pass + 1 : 0, can_flag));
         if (fuse)
           for (int k = 0; k < (pair ? 2 : 1); ++k) CUDA_TRY(rescore(k, pass, p.bnd_in, true));
         if (skipping && pass + 1 < P)
@@ -832,7 +840,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     g.chunk0_staged = true;
   }
   CUDA_TRY(cudaEventRecord(g.ev[2], st));
-  if (strm || wave || P >= 255)
+  if ((strm || wave || P >= 255) && can_flag)
     for (int k = 0; k < (pair ? 2 : 1); ++k) CUDA_TRY(rescore(k, (strm || wave) ? -1 : 254, nullptr));
   CUDA_TRY(cudaEventRecord(g.ev[3], st));
 

@@ -2063,10 +2063,11 @@ cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint3
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
                                cudaStream_t st, const int32_t *seq_idx, const int32_t *item_of,
                                uint8_t *item_hot, int32_t *list, int *nlist, int32_t *list2, int *nlist2,
-                               int want) {
+                               int want, bool detect) {
   if (count <= 0) return cudaSuccess;
-  ++g_launches;
-  sw16_detect_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, flagged, flagged2,
+  if (detect) ++g_launches;
+  if (detect)
+    sw16_detect_kernel<<<grid_for(count, 256), 256, 0, st>>>(endcol, count, sc_out, flagged, flagged2,
                                                             scores2 != nullptr, pass, thresh, seq_idx, item_of,
                                                             item_hot);
   ++g_launches;

@@ -197,7 +197,8 @@ cudaError_t launch_sw16_gather(const int64_t *endcol, int64_t count, const uint3
                                uint8_t *flagged, int32_t *scores2, uint8_t *flagged2, int pass, int thresh,
                                cudaStream_t st, const int32_t *seq_idx, const int32_t *item_of,
                                uint8_t *item_hot, int32_t *list = nullptr, int *nlist = nullptr,
-                               int32_t *list2 = nullptr, int *nlist2 = nullptr, int want = 0);
+                               int32_t *list2 = nullptr, int *nlist2 = nullptr, int want = 0,
+                               bool detect = true);   // false: no score can reach thresh (no flag pass)
 // want > 0: the update launch also compacts the sequences with flag byte ==
 // want (those first flagged in this pass) into list / list2 (counts nlist /
 // nlist2, zeroed by the caller), as launch_flag_compact would.

@@ -149,9 +149,20 @@ def test_launch_counter_counts_library_kernels():
     sw.sw_search(w.queries[0], BLOSUM62, 10, 2)
     n1 = sw.sw_launch_count()
     st = sw.sw_last_stats()
-    assert n1 - n0 >= 1 + 4 * st["passes"]
+    # 144 x 11 < the flag threshold: no score can flag, so the search is the
+    # init, profile, pass and update launches only (no detect, no 32-bit kernel)
+    assert st["passes"] == 1 and n1 - n0 == 4
     sw.sw_topk(10)
     assert sw.sw_launch_count() - n1 == 3
+    # a query whose scores can reach the threshold: init + profile, then per
+    # pass the pass, detect, update and 32-bit launches (plus item skipping)
+    db = si.database_from_list([encode("W" * 3000), encode("A" * 40)])
+    sw.sw_db_load(db.residues, db.offsets)
+    n2 = sw.sw_launch_count()
+    got = sw.sw_search(encode("W" * 3100), BLOSUM62, 10, 2)
+    st = sw.sw_last_stats()
+    assert int(got[0]) == 33000 and st["flagged"] >= 1
+    assert sw.sw_launch_count() - n2 >= 2 + 4 * st["passes"]
 
 
 def _run(args, env=None):
