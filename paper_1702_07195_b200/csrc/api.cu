@@ -596,9 +596,9 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   CUDA_TRY(g.fcounters.ensure((size_t)4 * (P + 1)));
   const int32_t *item_of = pair ? nullptr : g.img[0].item_of.p;
   if (!pair) CUDA_TRY(g.item_hot.ensure((size_t)std::max(1, g.img[0].num_items)));
-  CUDA_TRY(launch_search_init(g.fcounters.p, 4 * (P + 1), g.flagged.p, pair ? g.flagged2.p : nullptr, g.count,
-                              g.cells32.p, pair ? nullptr : g.item_hot.p, pair ? 0 : std::max(1, g.img[0].num_items),
-                              nullptr, 0, 0, 0, 0, 0, st));
+  // zeroed by the profile launch below
+  const SearchInit zinit{g.fcounters.p, 4 * (P + 1), g.flagged.p, pair ? g.flagged2.p : nullptr, g.count,
+                         g.cells32.p, pair ? nullptr : g.item_hot.p, pair ? 0 : std::max(1, g.img[0].num_items)};
   if (!g.ev[0])
     for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreate(&g.ev[i]));
   // a batch's timing spans all of its searches (sw_last_timing)
@@ -623,7 +623,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   const int pev0 = 2 * g.npev;
   CUDA_TRY(launch_qp_build(g.q_d, m, pair ? g.q2_d : nullptr, m2, g.mat_d, T.G, T.R, P, g.qp.p,
                            g.desc.p, g.qp32.p, pair ? g.qp32b.p : nullptr,
-                           goe, ge, st, use_sp ? 1 : 0));
+                           goe, ge, st, use_sp ? 1 : 0, zinit));
 
   const int grid = g.num_sms * (lat ? 1 : std::max(1, tile_ctas_per_sm(ti)));
   // Exact s32 re-scoring ("recalculated using the next wider

@@ -1349,13 +1349,34 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
   }
 }
 
+// Per-search zeroing (replaces four memsets; done by the profile launch).  16-B stores for
+// the byte arrays' aligned bulk.
+__device__ __forceinline__ void zero_bytes(uint8_t *p, int64_t n, int64_t tid, int64_t nth) {
+  if (!p || n <= 0) return;
+  const int64_t mis = (16 - (int64_t)(reinterpret_cast<uintptr_t>(p) & 15)) & 15;
+  const int64_t head = n < mis ? n : mis;
+  const int64_t n16 = (n - head) >> 4;
+  uint4 *q = reinterpret_cast<uint4 *>(p + head);
+  for (int64_t i = tid; i < n16; i += nth) q[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int64_t i = tid; i < head; i += nth) p[i] = 0;
+  for (int64_t i = head + 16 * n16 + tid; i < n; i += nth) p[i] = 0;
+}
+__device__ __forceinline__ void search_init(const SearchInit &z, int64_t tid, int64_t nth) {
+  for (int64_t i = tid; i < z.nfc; i += nth) z.fcounters[i] = 0;
+  if (tid == 0 && z.cells32) *z.cells32 = 0;
+  zero_bytes(z.flagged, z.count, tid, nth);
+  zero_bytes(z.flagged2, z.count, tid, nth);
+  zero_bytes(z.item_hot, z.nitems, tid, nth);
+}
+
 // ---------------------------------------------------------------------------
 // Query profile ("auxiliary two-dimensional array of size
 // |q| x |Sigma|"), built per query in the layouts the kernels read.
 // ---------------------------------------------------------------------------
 __global__ void qp_build_kernel(const uint8_t *__restrict__ q, int m, const uint8_t *__restrict__ q2, int m2,
                                 const int8_t *__restrict__ M, int G, int R, int P, uint32_t *qp, uint4 *desc,
-                                int32_t *qp32, int32_t *qp32b, int goe, int ge, int sp) {
+                                int32_t *qp32, int32_t *qp32b, int goe, int ge, int sp, const SearchInit ini) {
+  search_init(ini, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
   // q2 == nullptr: one query (QPM 0); q2 != nullptr: query pair (QPM 3).  See
   // the profile-mode notes above the pass kernel for the word formats.
   // slice layout: kernels.cuh (qp_letter_bytes): full chunks, then a narrow tail block
@@ -1456,30 +1477,6 @@ __global__ void item_skip_kernel(const Item *__restrict__ items, int nitems, con
   }
 }
 
-// Per-search zeroing (replaces four memsets: one launch).  16-B stores for
-// the byte arrays' aligned bulk.
-__device__ __forceinline__ void zero_bytes(uint8_t *p, int64_t n, int64_t tid, int64_t nth) {
-  if (!p || n <= 0) return;
-  const int64_t mis = (16 - (int64_t)(reinterpret_cast<uintptr_t>(p) & 15)) & 15;
-  const int64_t head = n < mis ? n : mis;
-  const int64_t n16 = (n - head) >> 4;
-  uint4 *q = reinterpret_cast<uint4 *>(p + head);
-  for (int64_t i = tid; i < n16; i += nth) q[i] = make_uint4(0u, 0u, 0u, 0u);
-  for (int64_t i = tid; i < head; i += nth) p[i] = 0;
-  for (int64_t i = head + 16 * n16 + tid; i < n; i += nth) p[i] = 0;
-}
-__global__ void search_init_kernel(int *fcounters, int nfc, uint8_t *flagged, uint8_t *flagged2, int64_t count,
-                                   int64_t *cells32, uint8_t *item_hot, int64_t nitems, int *pc, int npc, int nset,
-                                   int v0, int off, int v1) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = tid; i < nfc; i += nth) fcounters[i] = 0;
-  for (int64_t i = tid; i < npc; i += nth)
-    pc[i] = i < nset ? v0 : (i >= off && i < off + nset ? v1 : 0);
-  if (tid == 0 && cells32) *cells32 = 0;
-  zero_bytes(flagged, count, tid, nth);
-  zero_bytes(flagged2, count, tid, nth);
-  zero_bytes(item_hot, nitems, tid, nth);
-}
 
 // 16-bit column words -> 32-bit words (device image upload, out-of-core
 // chunks as they arrive over the host link).
@@ -2037,14 +2034,15 @@ size_t qp_bytes(int G, int R, int P, int qpm) {
 
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,
                             int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
-                            int goe, int ge, cudaStream_t st, int sp) {
+                            int goe, int ge, cudaStream_t st, int sp, const SearchInit &init) {
   const int mm = d_query2 ? (m > m2 ? m : m2) : m;
   const int64_t total = (sp ? (int64_t)kSPBytes / 4 : (int64_t)P * kNL * (qp_letter_bytes(G, R) / 4)) +
                         kNL * kNL + (int64_t)kNL * mm;
+  const int64_t zero = std::max<int64_t>(std::max<int64_t>(init.count, init.nitems) / 16, init.nfc) + 1;
   ++g_launches;
-  qp_build_kernel<<<grid_for(total, 256), 256, 0, st>>>(d_query, m, d_query2, m2, d_matrix, G, R, P,
-                                                         reinterpret_cast<uint32_t *>(d_qp), d_desc, d_qp32,
-                                                         d_qp32b, goe, ge, sp);
+  qp_build_kernel<<<grid_for(std::max(total, zero), 256), 256, 0, st>>>(
+      d_query, m, d_query2, m2, d_matrix, G, R, P, reinterpret_cast<uint32_t *>(d_qp), d_desc, d_qp32, d_qp32b, goe,
+      ge, sp, init);
   return cudaGetLastError();
 }
 
@@ -2164,15 +2162,6 @@ cudaError_t launch_sw16_rows(int grid, const RowsParams &p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_search_init(int *fcounters, int nfc, uint8_t *flagged, uint8_t *flagged2, int64_t count,
-                               int64_t *cells32, uint8_t *item_hot, int64_t nitems, int *pc, int npc, int nset,
-                               int v0, int off, int v1, cudaStream_t st) {
-  ++g_launches;
-  const int64_t work = std::max<int64_t>(std::max<int64_t>(count, nitems) / 16, (int64_t)std::max(nfc, npc)) + 1;
-  search_init_kernel<<<grid_for(work, 256), 256, 0, st>>>(fcounters, nfc, flagged, flagged2, count, cells32,
-                                                             item_hot, nitems, pc, npc, nset, v0, off, v1);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_expand_columns(const uint16_t *in, int64_t n, uint32_t *out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;

@@ -180,10 +180,22 @@ int tile_ctas_per_sm(int i);
 // Threads per CTA of tile i's kernel.
 int tile_threads(int i);
 
+// Per-search zeroing of the re-scoring counters, the flag bytes, the 32-bit
+// cell counter and the per-item carry marks (null / 0 = skip), done by the
+// profile launch (one launch fewer per search).
+struct SearchInit {
+  int *fcounters;
+  int nfc;
+  uint8_t *flagged, *flagged2;
+  int64_t count;
+  int64_t *cells32;
+  uint8_t *item_hot;
+  int64_t nitems;
+};
 // d_query2 != nullptr: query-pair profile (QPM 3) and a second s32 profile.
 cudaError_t launch_qp_build(const uint8_t *d_query, int m, const uint8_t *d_query2, int m2, const int8_t *d_matrix,
                             int G, int R, int P, uint8_t *d_qp, uint4 *d_desc, int32_t *d_qp32, int32_t *d_qp32b,
-                            int goe, int ge, cudaStream_t st, int sp = 0);
+                            int goe, int ge, cudaStream_t st, int sp, const SearchInit &init);
 // sp = 1: d_qp receives the score profile (QPM 1) and the descriptors its pair offsets.
 // goe = gap open + extend, ge = gap extend (>= 0; the descriptor penalty words clamp at 32767)
 cudaError_t launch_sw16_pass(int tile_index, int grid, const SW16Params &p, cudaStream_t st);
@@ -223,13 +235,7 @@ cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st);
 // 16-bit column words (host image, streamed chunks) -> the pass kernel's
 // 32-bit words: out[i] = in[i] for i < n.
 cudaError_t launch_expand_columns(const uint16_t *in, int64_t n, uint32_t *out, cudaStream_t st);
-// Per-search zeroing of the flag bytes, the re-scoring counters, the 32-bit
-// cell counter and the per-item carry marks in one launch (null / 0 = skip).
-// Item cursors: pc[i] = v0 for i < nset, pc[off + i] = v1 for i < nset, other
-// entries < npc zero.
-cudaError_t launch_search_init(int *fcounters, int nfc, uint8_t *flagged, uint8_t *flagged2, int64_t count,
-                               int64_t *cells32, uint8_t *item_hot, int64_t nitems, int *pc, int npc, int nset,
-                               int v0, int off, int v1, cudaStream_t st);
+
 
 // Sorting stage.
 cudaError_t launch_make_keys(const int32_t *scores, const int64_t *index, int64_t n,
