@@ -1194,13 +1194,26 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
   const int nflag = *p.flag_count;
   const uint32_t one = p.one;
 
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_base = atomicAdd(p.cursor, nw);
-    __syncthreads();
-    const int base = s_base;
-    if (base >= nflag) break;                      // CTA-uniform
-    const int idx = base + warp;
+  // First round: a static round-robin share of at most one sequence per warp
+  // (CTA b takes b, b + grid, ...: every CTA, and so every SM, gets the same
+  // number of sequences when fewer are flagged than there are warps -- with
+  // CTA-wide claims of nw sequences, the first CTAs to arrive took them all
+  // and a third of the SMs ran one CTA or none).  Later rounds: dynamic
+  // claims of nw sequences (uneven lengths).
+  const int share = min(nw, (nflag + (int)gridDim.x - 1) / (int)gridDim.x);
+  for (int round = 0;; ++round) {
+    int idx;
+    if (round == 0) {
+      if ((int)blockIdx.x >= nflag) continue;     // CTA-uniform: nothing static for this CTA
+      idx = warp < share ? (int)blockIdx.x + warp * (int)gridDim.x : nflag;
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) s_base = share * (int)gridDim.x + atomicAdd(p.cursor, nw);
+      __syncthreads();
+      const int base = s_base;
+      if (base >= nflag) break;                    // CTA-uniform
+      idx = base + warp;
+    }
     const bool active = idx < nflag;
     int orig = 0, n = 0;
     const uint8_t *res = p.res;
