@@ -159,11 +159,22 @@ def test_launch_counter_counts_library_kernels():
     # pass the pass, detect, update and 32-bit launches (plus item skipping)
     db = si.database_from_list([encode("W" * 3000), encode("A" * 40)])
     sw.sw_db_load(db.residues, db.offsets)
-    n2 = sw.sw_launch_count()
-    got = sw.sw_search(encode("W" * 3100), BLOSUM62, 10, 2)
-    st = sw.sw_last_stats()
-    assert int(got[0]) == 33000 and st["flagged"] >= 1
-    assert sw.sw_launch_count() - n2 >= 1 + 4 * st["passes"]
+    try:
+        sw.sw_set_wave(-1)     # per-pass launches (two items would pick the wavefront)
+        n2 = sw.sw_launch_count()
+        got = sw.sw_search(encode("W" * 3100), BLOSUM62, 10, 2)
+        st = sw.sw_last_stats()
+        assert int(got[0]) == 33000 and st["flagged"] >= 1 and st["wave"] == 0
+        assert sw.sw_launch_count() - n2 >= 1 + 4 * st["passes"]
+        # the wavefront: profile, one pass launch, detect + update, flag
+        # compaction + 32-bit kernel at the end
+        sw.sw_set_wave(1)
+        n3 = sw.sw_launch_count()
+        got = sw.sw_search(encode("W" * 3100), BLOSUM62, 10, 2)
+        assert int(got[0]) == 33000 and sw.sw_last_stats()["wave"] == 1
+        assert sw.sw_launch_count() - n3 == 6
+    finally:
+        sw.sw_set_wave(0)
 
 
 def _run(args, env=None):
