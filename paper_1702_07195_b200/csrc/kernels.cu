@@ -1201,12 +1201,6 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
   // and a third of the SMs ran one CTA or none).  Later rounds: dynamic
   // claims of nw sequences (uneven lengths).
   const int share = min(nw, (nflag + (int)gridDim.x - 1) / (int)gridDim.x);
-  // A warp's column step is bound by the F recurrence through its R rows (3
-  // dependent DPX per row, ~14 cycles each) unless enough warps share the SM:
-  // with at most 3 flagged sequences per SM sub-partition (12 per SM) the
-  // one-instruction chain form (more ALU work, a third of the chain) is faster.
-  const bool chain_form = SW_S32CHAIN >= 0 ? SW_S32CHAIN == 1
-                                            : (int64_t)nflag * 4 <= (int64_t)gridDim.x * nw * 3;
   for (int round = 0;; ++round) {
     int idx;
     if (round == 0) {
@@ -1244,9 +1238,8 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
     // only the rows the query still has are computed, no phantom rows beyond
     // the next multiple of 32 * RR).  CTA-uniform: staging synchronises.
     int64_t rows_done = 0;
-    auto run_pass = [&](int pass, auto rr_c, auto lr_c) {
+    auto run_pass = [&](int pass, auto rr_c) {
       constexpr int RR = decltype(rr_c)::value;
-      constexpr bool LR = decltype(lr_c)::value;
       constexpr int KR = RR / 4;
       __syncthreads();
       // stage this pass's profile slice [letter][4-row chunk][lane][4] from the
@@ -1325,27 +1318,12 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
               const int r = kk * 4 + e;
               // H_diag + SM as an IMAD on the FMA pipe; E, F >= 0 make the 0 of
               // Eq. 1 implicit, so Eq. 1 is one VIMNMX3 (4.5 ALU per cell, not 5.5)
-              if (LR) {
-                // Eq. 3 with a one-instruction chain through the rows (as the
-                // 16-bit latency tiles): F' = max(F - Ge, max(max(t, E) - Goe, 0)),
-                // equal to max(F - Ge, max(H - Goe, 0)) since Goe >= Ge; two more
-                // ALU instructions per cell, off the chain
-                const int a = max((int)imad((uint32_t)hd, one, (uint32_t)av[e]), E[r]);
-                const int uu = __viaddmax_s32_relu(a, p.neg_goe, 0);
-                const int h = max(a, F);
-                hd = H[r];
-                H[r] = h;
-                const int hg = __viaddmax_s32_relu(h, p.neg_goe, 0);
-                E[r] = __viaddmax_s32(E[r], p.neg_ge, hg);
-                F = __viaddmax_s32(F, p.neg_ge, uu);
-              } else {
-                const int h = __vimax3_s32((int)imad((uint32_t)hd, one, (uint32_t)av[e]), E[r], F);
-                hd = H[r];
-                H[r] = h;
-                const int hg = __viaddmax_s32_relu(h, p.neg_goe, 0);
-                E[r] = __viaddmax_s32(E[r], p.neg_ge, hg);
-                F = __viaddmax_s32(F, p.neg_ge, hg);
-              }
+              const int h = __vimax3_s32((int)imad((uint32_t)hd, one, (uint32_t)av[e]), E[r], F);
+              hd = H[r];
+              H[r] = h;
+              const int hg = __viaddmax_s32_relu(h, p.neg_goe, 0);
+              E[r] = __viaddmax_s32(E[r], p.neg_ge, hg);
+              F = __viaddmax_s32(F, p.neg_ge, hg);
             }
           }
 #pragma unroll
@@ -1358,24 +1336,20 @@ __global__ void __launch_bounds__(kSW32Threads) sw32_kernel(const SW32Params p) 
       best = max(best, S);
       __syncwarp();
     };
-    auto run_passes = [&](auto lr_c) {
-      for (int pass = 0; pass < p.passes; ++pass) {
-        if constexpr (R % 12 == 0) {
-          const int left = p.len - p.row0 - pass * 32 * R;   // query rows from this pass on
-          if (pass == p.passes - 1 && left <= 32 * (R / 3)) {
-            run_pass(pass, std::integral_constant<int, R / 3>{}, lr_c);
-            continue;
-          }
-          if (pass == p.passes - 1 && left <= 32 * (2 * R / 3)) {
-            run_pass(pass, std::integral_constant<int, 2 * R / 3>{}, lr_c);
-            continue;
-          }
+    for (int pass = 0; pass < p.passes; ++pass) {
+      if constexpr (R % 12 == 0) {
+        const int left = p.len - p.row0 - pass * 32 * R;   // query rows from this pass on
+        if (pass == p.passes - 1 && left <= 32 * (R / 3)) {
+          run_pass(pass, std::integral_constant<int, R / 3>{});
+          continue;
         }
-        run_pass(pass, std::integral_constant<int, R>{}, lr_c);
+        if (pass == p.passes - 1 && left <= 32 * (2 * R / 3)) {
+          run_pass(pass, std::integral_constant<int, 2 * R / 3>{});
+          continue;
+        }
       }
-    };
-    if (chain_form) run_passes(std::true_type{});
-    else run_passes(std::false_type{});
+      run_pass(pass, std::integral_constant<int, R>{});
+    }
     if (active) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));

@@ -228,9 +228,6 @@ cudaError_t launch_item_skip(const Item *items, int nitems, const int32_t *slots
 #ifndef SW_S32ROWS
 #define SW_S32ROWS 24
 #endif
-#ifndef SW_S32CHAIN
-#define SW_S32CHAIN -1   // s32 row-chain form: -1 by flagged count (kernels.cu), 0 / 1 force (experiments)
-#endif
 constexpr int kSW32Rows = SW_S32ROWS;  // rows per lane of the 32-bit kernel
 constexpr int kSW32Threads = 256;
 cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st);
