@@ -313,13 +313,22 @@ def run_reference(args):
             "ms_per_step": round(1e3 * total / max(1, len(times)), 3), "higher_is_better": True,
             "scaling": "weak" if args.config in WEAK_CONFIGS else "strong", "vs_baseline": None, "dtype": "i64",
             "data": "synthetic",
-            "config": {"workload": w.name, "query_len": len(q), "db_sequences": w.count_global,
+            "config": {"workload": workload_text(w, [q]), "query_len": len(q), "db_sequences": w.count_global,
                        "db_residues": w.residues_global},
             "cpu_baseline": {"value": round(val, 3), "unit": "GCUPS", "cores": cores, "cpu_model": cpu_model(),
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": round(val, 3), "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def workload_text(w, queries):
+    """The `config.workload` string, the same in both arms (the reference arm
+    scores query 0 of the configuration only)."""
+    nq = len(queries)
+    qres = sum(len(q) for q in queries)
+    return (f"{w.name}: {nq} quer{'y' if nq == 1 else 'ies'} ({qres} residues) vs "
+            f"{w.count_global} synthetic sequences ({w.residues_global} residues), BLOSUM62, gaps 10/2")
 
 
 def run_ours(args):
@@ -521,9 +530,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": "weak" if w.weak else "strong", "vs_baseline": None,
             "dtype": "i16", "data": "synthetic",
-            "config": {"workload": f"{w.name}: {nq} quer{'y' if nq == 1 else 'ies'} ({w.qres} residues) vs "
-                                   f"{w.count_global} synthetic sequences ({w.residues_global} residues), "
-                                   f"BLOSUM62, gaps 10/2",
+            "config": {"workload": workload_text(w, w.queries),
                        "query_len": qlens[0] if nq == 1 else qlens, "db_sequences": w.count_global,
                        "db_residues": w.residues_global, "per_gpu_db_residues": local_res, "topk": TOPK,
                        "tile_G_R": [st["G"], st["R"]], "passes": st["passes"],
