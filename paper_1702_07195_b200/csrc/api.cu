@@ -960,7 +960,11 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
       try {
         // streamed: items of at most a quarter of a chunk's share per group,
         // so each chunk's launch keeps the 8-lane tiles' 2 x target_groups busy
-        const int64_t cap = strm ? std::max<int64_t>(256, (chunk_bytes / 4) / (4 * target_groups)) : 0;
+        // streamed: at least 4 items per group per chunk, and at most 4,096
+        // columns per item: a chunk is one launch, whose drain is about one
+        // item long (measured on cfg2, m = 144, 1 GiB chunks: cap 14,170 ->
+        // 4,096 takes the three pass kernels from 36.6 to 34.0 ms)
+        const int64_t cap = strm ? std::max<int64_t>(256, std::min<int64_t>(4096, (chunk_bytes / 4) / (4 * target_groups))) : 0;
         // rows mode (resident pair image): sequences longer than 4x the
         // average columns per lane group are the long pairs
         const int64_t avg = (offsets[count] + 2 * count) / 2 / std::max<int64_t>(1, target_groups);
@@ -1062,13 +1066,37 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
     // chunk of its own
     std::vector<int32_t> item_chunk(H.items.size());
     int64_t span = 0;
+    // Balanced chunks: the greedy split fixes the chunk count; the limit is
+    // then lowered to the smallest one that still gives that count, so the
+    // last chunk is not a short one (a short last chunk cannot hide the copy
+    // of the next search's first chunk, and the copy before it idles).
+    auto count_chunks = [&](int64_t limit) {
+      int64_t n = 0;
+      for (size_t b = 0; b < H.items.size(); ++n) {
+        const int64_t c0 = H.items[b].col_begin - kItemPad;
+        size_t e = b + 1;
+        while (e < H.items.size() && H.items[e].col_begin + H.items[e].ncols + kItemPad - c0 <= limit) ++e;
+        b = e;
+      }
+      return n;
+    };
+    int64_t limit = chunk_cols;
+    {
+      const int64_t n0 = count_chunks(chunk_cols);
+      int64_t lo_l = 1, hi_l = chunk_cols;   // count_chunks(hi_l) == n0; find the smallest such limit
+      while (lo_l < hi_l) {
+        const int64_t mid = lo_l + (hi_l - lo_l) / 2;
+        if (count_chunks(mid) <= n0) hi_l = mid; else lo_l = mid + 1;
+      }
+      limit = hi_l;
+    }
     for (size_t b = 0; b < H.items.size();) {
       State::Chunk c;
       c.item_begin = (int)b;
       c.col_begin = H.items[b].col_begin - kItemPad;
       size_t e = b + 1;
       while (e < H.items.size() &&
-             H.items[e].col_begin + H.items[e].ncols + kItemPad - c.col_begin <= chunk_cols)
+             H.items[e].col_begin + H.items[e].ncols + kItemPad - c.col_begin <= limit)
         ++e;
       c.item_end = (int)e;
       c.col_end = H.items[e - 1].col_begin + H.items[e - 1].ncols + kItemPad;
