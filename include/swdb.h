@@ -89,7 +89,9 @@ int sw_db_load(const uint8_t *residues, const int64_t *offsets, int64_t count);
  *                 image (two chunk buffers are allocated).
  * The sequence-pair image is kept in pinned HOST memory (16-bit column words,
  * 1 B per residue on the link) and split into chunks of consecutive work
- * items; every search copies chunk k+1 host->device on a separate stream while
+ * items (as few chunks as chunk_bytes allows, then equal in size: the column
+ * limit is lowered to the smallest one giving that count); every search
+ * copies chunk k+1 host->device on a separate stream while
  * the pass kernels run on chunk k (expanded to 32-bit words on the device),
  * and at its end copies the next search's chunk 0 while its last chunk runs.
  * Device memory: 2 x chunk_bytes of 32-bit words + 2 x chunk_bytes / 2 of
