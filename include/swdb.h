@@ -106,6 +106,18 @@ int sw_db_load_streamed(const uint8_t *residues, const int64_t *offsets, int64_t
 /* Number of chunks of a streamed database (0 for a resident one). */
 int64_t sw_db_chunks(void);
 
+/* Columns of a streamed database's resident head (0: none, or a resident
+ * database).  The head is the run of leading -- longest -- work items within a
+ * quarter of chunk_bytes (at least the first item), kept on the device when
+ * more than one chunk of items follows it: every search scores it on a second,
+ * high-priority stream beside the streamed chunks, so that a very long
+ * sequence's chain of column steps is hidden by the whole search instead of
+ * bounding the chunk that would hold it ("minimize workload
+ * imbalances").  It is not counted by sw_db_chunks and costs
+ * 8 B per column of device memory (+ 16 B per column for multi-pass queries).
+ * SWDB_STREAM_HEAD=0 in the environment at load time turns it off. */
+int64_t sw_db_head_columns(void);
+
 /* Frees the database and all device buffers.  Safe to call at any time. */
 void sw_db_free(void);
 

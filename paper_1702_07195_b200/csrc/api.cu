@@ -194,6 +194,16 @@ struct State {
   DevBuf<int64_t> cseq_endcol;  // their END columns (global image columns)
   cudaStream_t copy_st = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  // Resident head: the leading (longest) work items stay on
+  // the device and run on a second, high-priority compute stream beside the
+  // streamed chunks, so a long sequence's chain is hidden by the whole search
+  // instead of bounding the one chunk that holds it.
+  bool has_head = false;
+  Chunk head{};
+  DevBuf<uint32_t> head_buf, head_sc;
+  DevBuf<uint2> head_bnd;
+  cudaStream_t head_st = nullptr;
+  cudaEvent_t ev_head = nullptr;
 
   void release_streamed() {
     if (h_stream) cudaFreeHost(h_stream);
@@ -209,6 +219,12 @@ struct State {
     }
     if (copy_st) cudaStreamDestroy(copy_st);
     copy_st = nullptr;
+    if (head_st) cudaStreamDestroy(head_st);
+    head_st = nullptr;
+    if (ev_head) cudaEventDestroy(ev_head);
+    ev_head = nullptr;
+    head_buf.release(); head_sc.release(); head_bnd.release();
+    has_head = false;
     chunks.clear();
     streamed = false;
     buf_parity = 0;
@@ -529,13 +545,15 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // throughput tiles the claim code alone measured 1.7-2.3% slower: register
   // allocation of the main loop).  Rows mode: the pass kernel starts claiming
   // after the long items.
-  const int nchk = g.streamed ? (int)g.chunks.size() : 1;
+  // streamed: the chunks, then the resident head (cursor index nchk - 1)
+  const int nchk = g.streamed ? (int)g.chunks.size() + (g.has_head ? 1 : 0) : 1;
+  auto chunk_at = [&](int k) -> const State::Chunk & { return k < (int)g.chunks.size() ? g.chunks[k] : g.head; };
   const int first = rowsm ? I0.n_long : 0;
   std::vector<int> solo_n((size_t)nchk, 0);
   if (solo_enabled() && lat && T.G == 32 && !pair && !use_sp && !wave) {
     for (int k = 0; k < nchk; ++k) {
-      const int ib = g.streamed ? g.chunks[k].item_begin : first;
-      const int ie = g.streamed ? g.chunks[k].item_end : I0.num_items;
+      const int ib = g.streamed ? chunk_at(k).item_begin : first;
+      const int ie = g.streamed ? chunk_at(k).item_end : I0.num_items;
       if (ie <= ib) continue;
       const int64_t thr = std::max<int64_t>(512, I0.item_ncols[ib] / 2);   // half the chunk's longest item
       int n = 0;
@@ -724,6 +742,55 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
                                 can_flag));
   }
   int npl = 0;   // pass launches so far (per-pass path)
+  // Streamed database with a resident head: its passes and gathers run on
+  // head_st (high priority: its CTAs take the first SMs that free up) beside
+  // the chunks below; the search stream joins it after the last chunk.
+  const bool head = strm && !wave && g.has_head;
+  if (head) {
+    const State::Chunk &c = g.head;
+    const int kh = nch;   // cursor index of the head
+    const int64_t hc = c.col_end - c.col_begin, base = c.col_begin;
+    if (P > 1) CUDA_TRY(g.head_bnd.ensure((size_t)hc * 2));
+    CUDA_TRY(cudaStreamWaitEvent(g.head_st, g.ev[1], 0));   // the profile and the cursors are ready
+    for (int pass = 0; pass < P; ++pass) {
+      SW16Params p{};
+      p.stream = g.head_buf.p - base;
+      p.items = I.items.p + c.item_begin;
+      p.num_items = c.item_end - c.item_begin;
+      p.counter = pc + (size_t)kh * P + pass;
+      p.qp = reinterpret_cast<const uint4 *>(g.qp.p);
+      p.desc = g.desc.p;
+      p.bnd_in = pass == 0 ? nullptr : g.head_bnd.p + (size_t)((pass - 1) & 1) * hc - base;
+      p.bnd_out = pass == P - 1 ? nullptr : g.head_bnd.p + (size_t)(pass & 1) * hc - base;
+      p.dummy = g.dummy.p;
+      p.nul_stream = g.nulcols.p;
+      p.col_lo = base;
+      p.col_hi = c.col_end;
+      p.zero_bnd = g.zerocols.p;
+      p.sc_out = g.head_sc.p - base;
+      p.pass = pass;
+      p.thresh = thresh;
+      p.zero = 0u;
+      p.one = 1u;
+      p.skip = nullptr;
+      p.query = g.q_d;
+      p.m = m;
+      p.solo_counter = solo_n[(size_t)kh] ? pc + (size_t)nchk * P + (size_t)kh * P + pass : nullptr;
+      p.solo_end = solo_n[(size_t)kh];
+      const int pe = pev0 + 2 * npl++;
+      CUDA_TRY(pass_event(pe + 1));
+      CUDA_TRY(cudaEventRecord(pev[pe], g.head_st));
+      CUDA_TRY(launch_sw16_pass(ti, grid, p, g.head_st));
+      CUDA_TRY(cudaEventRecord(pev[pe + 1], g.head_st));
+      g.npev = pe / 2 + 1;
+      g.hnpev[g.hslot] = g.npev;
+      CUDA_TRY(launch_sw16_gather(g.cseq_endcol.p + c.seq_begin, c.seq_end - c.seq_begin, g.head_sc.p - base,
+                                  d_scores, g.flagged.p, nullptr, nullptr, pass, thresh, g.head_st,
+                                  g.cseq_idx.p + c.seq_begin, item_of, g.item_hot.p, nullptr, nullptr, nullptr,
+                                  nullptr, 0, can_flag));
+    }
+    CUDA_TRY(cudaEventRecord(g.ev_head, g.head_st));
+  }
   for (int k = 0; k < (wave ? 0 : nch); ++k) {
     const uint32_t *stream_base = I.stream.p;
     const Item *items = I.items.p;
@@ -827,6 +894,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     }
     if (strm) CUDA_TRY(cudaEventRecord(g.ev_free[b], st));
   }
+  if (head) CUDA_TRY(cudaStreamWaitEvent(st, g.ev_head, 0));
   if (strm && !wave) {
     // the next search's chunk 0 into the buffer this search's last chunk did not use
     g.chunk0_staged = false;
@@ -1070,9 +1138,33 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
     // then lowered to the smallest one that still gives that count, so the
     // last chunk is not a short one (a short last chunk cannot hide the copy
     // of the next search's first chunk, and the copy before it idles).
+    // Resident head: the leading items within a quarter of a chunk (at least
+    // the first item), when at least two chunks' worth of items follow.
+    size_t head_end = 0;
+    {
+      const char *e = std::getenv("SWDB_STREAM_HEAD");
+      if (!(e && e[0] == '0') && H.items.size() > 1) {
+        const int64_t c0 = H.items[0].col_begin - kItemPad;
+        size_t e1 = 1;
+        while (e1 < H.items.size() && H.items[e1].col_begin + H.items[e1].ncols + kItemPad - c0 <= chunk_cols / 4) ++e1;
+        const int64_t rest = e1 < H.items.size()
+                                 ? H.items.back().col_begin + H.items.back().ncols - H.items[e1].col_begin : 0;
+        if (rest > chunk_cols) head_end = e1;
+      }
+    }
+    std::vector<State::Chunk> all;
+    if (head_end > 0) {
+      State::Chunk c;
+      c.item_begin = 0;
+      c.item_end = (int)head_end;
+      c.col_begin = H.items[0].col_begin - kItemPad;
+      c.col_end = H.items[head_end - 1].col_begin + H.items[head_end - 1].ncols + kItemPad;
+      for (size_t i = 0; i < head_end; ++i) item_chunk[i] = 0;
+      all.push_back(c);
+    }
     auto count_chunks = [&](int64_t limit) {
       int64_t n = 0;
-      for (size_t b = 0; b < H.items.size(); ++n) {
+      for (size_t b = head_end; b < H.items.size(); ++n) {
         const int64_t c0 = H.items[b].col_begin - kItemPad;
         size_t e = b + 1;
         while (e < H.items.size() && H.items[e].col_begin + H.items[e].ncols + kItemPad - c0 <= limit) ++e;
@@ -1090,7 +1182,7 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
       }
       limit = hi_l;
     }
-    for (size_t b = 0; b < H.items.size();) {
+    for (size_t b = head_end; b < H.items.size();) {
       State::Chunk c;
       c.item_begin = (int)b;
       c.col_begin = H.items[b].col_begin - kItemPad;
@@ -1100,16 +1192,16 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
         ++e;
       c.item_end = (int)e;
       c.col_end = H.items[e - 1].col_begin + H.items[e - 1].ncols + kItemPad;
-      for (size_t i = b; i < e; ++i) item_chunk[i] = (int32_t)g.chunks.size();
+      for (size_t i = b; i < e; ++i) item_chunk[i] = (int32_t)all.size();
       span = std::max(span, c.col_end - c.col_begin);
-      g.chunks.push_back(c);
+      all.push_back(c);
       b = e;
     }
     g.chunk_span = span;
-    // per chunk: its sequences (original index) and their END columns
-    std::vector<int64_t> cnt(g.chunks.size() + 1, 0);
+    // per chunk (the head first): its sequences (original index) and their END columns
+    std::vector<int64_t> cnt(all.size() + 1, 0);
     for (size_t i = 0; i < H.items.size(); ++i) cnt[item_chunk[i] + 1] += H.items[i].nA + H.items[i].nB;
-    for (size_t k = 0; k < g.chunks.size(); ++k) cnt[k + 1] += cnt[k];
+    for (size_t k = 0; k < all.size(); ++k) cnt[k + 1] += cnt[k];
     std::vector<int32_t> idx((size_t)count);
     std::vector<int64_t> ecol((size_t)count);
     std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
@@ -1122,10 +1214,13 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
         ecol[pos] = H.endcol[orig];
       }
     }
-    for (size_t k = 0; k < g.chunks.size(); ++k) {
-      g.chunks[k].seq_begin = cnt[k];
-      g.chunks[k].seq_end = cnt[k + 1];
+    for (size_t k = 0; k < all.size(); ++k) {
+      all[k].seq_begin = cnt[k];
+      all[k].seq_end = cnt[k + 1];
     }
+    g.has_head = head_end > 0;
+    if (g.has_head) g.head = all[0];
+    g.chunks.assign(all.begin() + (g.has_head ? 1 : 0), all.end());
     CUDA_TRY(g.cseq_idx.ensure((size_t)count));
     CUDA_TRY(g.cseq_endcol.ensure((size_t)count));
     CUDA_TRY(cudaMemcpy(g.cseq_idx.p, idx.data(), idx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -1140,6 +1235,23 @@ int load_impl_body(const uint8_t *residues, const int64_t *offsets, int64_t coun
     }
     CUDA_TRY(cudaStreamCreateWithFlags(&g.copy_st, cudaStreamNonBlocking));
     CUDA_TRY(g.sc_out.ensure((size_t)span));
+    if (g.has_head) {   // the head's columns, expanded once
+      const int64_t hc = g.head.col_end - g.head.col_begin;
+      int lo_p = 0, hi_p = 0;
+      CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
+      CUDA_TRY(cudaStreamCreateWithPriority(&g.head_st, cudaStreamNonBlocking, hi_p));
+      CUDA_TRY(cudaEventCreateWithFlags(&g.ev_head, cudaEventDisableTiming));
+      CUDA_TRY(g.head_buf.ensure((size_t)hc));
+      CUDA_TRY(g.head_sc.ensure((size_t)hc));
+      DevBuf<uint16_t> tmp;
+      cudaError_t e = tmp.ensure((size_t)hc + 8);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(tmp.p, g.h_stream + g.head.col_begin, (size_t)hc * 2, cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) e = launch_expand_columns(tmp.p, hc, g.head_buf.p, nullptr);
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      tmp.release();
+      CUDA_TRY(e);
+    }
     // residues for the (rare) s32 re-scoring: read over the host link
     CUDA_TRY(cudaHostAlloc(&g.h_res, std::max<size_t>((size_t)g.total_res, 1), cudaHostAllocMapped));
     if (g.total_res > 0) std::memcpy(g.h_res, residues, (size_t)g.total_res);
@@ -1223,6 +1335,10 @@ int sw_db_load_streamed(const uint8_t *residues, const int64_t *offsets, int64_t
 }
 
 int64_t sw_db_chunks(void) { return g.loaded && g.streamed ? (int64_t)g.chunks.size() : 0; }
+
+int64_t sw_db_head_columns(void) {
+  return g.loaded && g.streamed && g.has_head ? g.head.col_end - g.head.col_begin : 0;
+}
 
 int sw_search_dev(const uint8_t *query, int32_t qlen, const int8_t *matrix, int32_t gap_open,
                   int32_t gap_extend, int32_t *d_scores, void *cuda_stream) {

@@ -19,7 +19,7 @@ SW_OK, SW_EINVAL, SW_ENOMEM, SW_ECUDA, SW_ENODB, SW_ESTATE = 0, -1, -2, -3, -4, 
 _NAMES = {SW_EINVAL: "SW_EINVAL", SW_ENOMEM: "SW_ENOMEM", SW_ECUDA: "SW_ECUDA",
           SW_ENODB: "SW_ENODB", SW_ESTATE: "SW_ESTATE"}
 
-EXPORTS = ["sw_db_load", "sw_db_load_streamed", "sw_db_chunks", "sw_db_free", "sw_db_count", "sw_db_residues", "sw_search",
+EXPORTS = ["sw_db_load", "sw_db_load_streamed", "sw_db_chunks", "sw_db_head_columns", "sw_db_free", "sw_db_count", "sw_db_residues", "sw_search",
            "sw_search_dev", "sw_search_batch", "sw_search_batch_dev", "sw_topk", "sw_topk_dev", "sw_scatter_dev", "sw_last_stats", "sw_last_timing", "sw_timing_history", "sw_set_tile",
            "sw_tile_supported", "sw_set_wave", "sw_set_latency_mode", "sw_set_profile", "sw_set_rows_mode", "sw_last_error", "sw_version", "sw_launch_count"]
 
@@ -51,6 +51,7 @@ def load_library():
         "sw_db_load": (ctypes.c_int, [p, p, i64]),
         "sw_db_load_streamed": (ctypes.c_int, [p, p, i64, i64]),
         "sw_db_chunks": (i64, []),
+        "sw_db_head_columns": (i64, []),
         "sw_db_free": (None, []),
         "sw_db_count": (i64, []),
         "sw_db_residues": (i64, []),
@@ -150,6 +151,11 @@ def sw_db_load_streamed(residues, offsets, chunk_bytes: int) -> None:
 
 def sw_db_chunks() -> int:
     return int(load_library().sw_db_chunks())
+
+
+def sw_db_head_columns() -> int:
+    """Columns of a streamed database's resident head, 0 if none (swdb.h)."""
+    return int(load_library().sw_db_head_columns())
 
 
 def sw_db_free() -> None:

@@ -453,6 +453,7 @@ def test_streamed_database_matches_resident_and_oracle():
     queries = [si.rr_residues(rng, 300), si.rr_residues(rng, 1700), encode("W" * 3100)]
     sw.sw_db_load_streamed(db.residues, db.offsets, 64 * 1024)     # many small chunks
     assert sw.sw_db_chunks() > 4
+    assert sw.sw_db_head_columns() >= 9000 // 2    # the resident head holds the 9,000-residue sequence's item
     for q in queries:
         got = sw.sw_search(q, BLOSUM62, 10, 2)
         exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
@@ -468,6 +469,42 @@ def test_streamed_database_matches_resident_and_oracle():
     assert sw.sw_db_chunks() == 0
     assert (sw.sw_search(queries[1], BLOSUM62, 10, 2) ==
             oracle.batch(queries[1], db.residues, db.offsets, BLOSUM62, 10, 2)).all()
+
+
+def test_streamed_resident_head_on_and_off(monkeypatch):
+    """Streamed database: the resident head (the leading, longest work items,
+    scored on a second stream beside the chunks; swdb.h sw_db_head_columns)
+    against the same database streamed without it and against the oracle:
+    single- and multi-pass queries, flagged sequences in the head and in the
+    chunks (32-bit re-scoring after both streams joined), heads of one long
+    item and of many items, searches back to back without a synchronize."""
+    import torch
+    rng = np.random.default_rng(557)
+    seqs = [si.rr_residues(rng, int(L)) for L in rng.integers(1, 400, 4000)]
+    seqs += [si.rr_residues(rng, 12000), si.rr_residues(rng, 7000), encode("W" * 3200), encode("W" * 3050),
+             encode("W" * 200)]
+    db = _db(seqs)
+    queries = [si.rr_residues(rng, 144), si.rr_residues(rng, 1300), encode("W" * 3100), si.rr_residues(rng, 40)]
+    exps = [oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2) for q in queries]
+    assert exps[2].max() >= 32_757
+    st = torch.cuda.Stream()
+    for budget in (64 * 1024, 512 * 1024):
+        for head in ("1", "0"):
+            monkeypatch.setenv("SWDB_STREAM_HEAD", head)
+            sw.sw_db_load_streamed(db.residues, db.offsets, budget)
+            assert (sw.sw_db_head_columns() > 0) == (head == "1"), (budget, head)
+            assert sw.sw_db_chunks() >= 2
+            for rep in range(2):
+                outs = [torch.empty(db.count, dtype=torch.int32, device="cuda") for _ in queries]
+                for q, d in zip(queries, outs):
+                    sw.sw_search_dev(q, BLOSUM62, 10, 2, d, st)
+                st.synchronize()
+                for q, d, exp in zip(queries, outs, exps):
+                    got = d.cpu().numpy()
+                    assert (got == exp).all(), (budget, head, len(q), int((got != exp).sum()))
+    monkeypatch.delenv("SWDB_STREAM_HEAD")
+    sw.sw_db_load(db.residues, db.offsets)
+    assert sw.sw_db_head_columns() == 0
 
 
 def test_streamed_back_to_back_searches_prefetch():
