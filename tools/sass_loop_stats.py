@@ -40,9 +40,13 @@ def main():
                                                                           os.path.join(B.CSRC, "kernels.cu")]
         subprocess.run(cmd, check=True)
         sass = subprocess.run(["cuobjdump", "-sass", cub], check=True, capture_output=True, text=True).stdout
-    name = f"16sw16_pass_kernelILi{args.R}ELi{args.G}ELb{args.bin}ELi0ELi512ELi{U}ELb0EE"
+    # sw16_pass_kernel<R, G, BIN, QPM = 0, NT = 512, U, WAVE = false, DA, RA>: the
+    # non-wavefront instantiation of the tile, whatever its DA / RA forms
+    name = f"16sw16_pass_kernelILi{args.R}ELi{args.G}ELb{args.bin}ELi0ELi512ELi{U}ELb0ELb"
     lines = sass.split("\n")
-    st = next(i for i, l in enumerate(lines) if "Function :" in l and name in l)
+    st = next((i for i, l in enumerate(lines) if "Function :" in l and name in l), None)
+    if st is None:
+        sys.exit(f"no instantiation matching {name}* in the cubin")
     en = next((i for i in range(st + 1, len(lines)) if "Function :" in lines[i]), len(lines))
     ins = []
     for l in lines[st:en]:
