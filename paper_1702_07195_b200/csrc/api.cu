@@ -607,7 +607,21 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // is shared by every search: order this search's device work after the
   // previous one's, whatever stream that ran on (ev[3] marks its end).
   if (g.has_search && g.ev[3]) CUDA_TRY(cudaStreamWaitEvent(st, g.ev[3], 0));
-  CUDA_TRY(cudaMemcpyAsync(g.qin.p, g_stage.h[slot], in_bytes, cudaMemcpyHostToDevice, st));
+  // Streamed database: the copy engine is busy with chunk copies of several
+  // ms each, and a small copy queues behind them (measured: ~5 ms between
+  // back-to-back searches on cfg2 with 1 GiB chunks), so a kernel reads the
+  // pinned slot over the link instead.  SWDB_STAGE_KERNEL=0/1 forces either.
+  static const int stage_kernel_env = [] {
+    const char *e = std::getenv("SWDB_STAGE_KERNEL");
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  if (stage_kernel_env == 1 || (stage_kernel_env < 0 && g.streamed)) {
+    void *hdev = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer(&hdev, g_stage.h[slot], 0));
+    CUDA_TRY(launch_stage_copy(hdev, g.qin.p, in_bytes, st));
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(g.qin.p, g_stage.h[slot], in_bytes, cudaMemcpyHostToDevice, st));
+  }
   CUDA_TRY(cudaEventRecord(g_stage.ev[slot], st));
   // 32-bit re-scoring counters: (count, cursor) per (pass, query of the pair),
   // plus one set for the end-of-search launch; flags; carry marks

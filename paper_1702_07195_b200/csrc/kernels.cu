@@ -1506,6 +1506,14 @@ __global__ void expand_columns_kernel(const uint16_t *__restrict__ in, int64_t n
     out[i] = in[i];
 }
 
+// Per-search inputs (matrix, query, item cursors) read straight from the
+// pinned, mapped staging slot: used instead of a copy-engine memcpy when the
+// copy engine is busy with a streamed database's chunks (a small H2D copy
+// queues behind a chunk copy of several ms).
+__global__ void stage_copy_kernel(const uint32_t *__restrict__ host_src, uint32_t *__restrict__ dst, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = host_src[i];
+}
+
 __global__ void flag_compact_kernel(const uint8_t *__restrict__ flagged, int64_t count, int32_t *list,
                                     int *n, int want) {
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < count;
@@ -2180,6 +2188,15 @@ cudaError_t launch_expand_columns(const uint16_t *in, int64_t n, uint32_t *out, 
   if (n <= 0) return cudaSuccess;
   ++g_launches;
   expand_columns_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, st>>>(in, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage_copy(const void *host_src_dev, void *dst, size_t bytes, cudaStream_t st) {
+  const int n = (int)((bytes + 3) / 4);
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  stage_copy_kernel<<<std::min(8, (n + 255) / 256), 256, 0, st>>>(reinterpret_cast<const uint32_t *>(host_src_dev),
+                                                                  reinterpret_cast<uint32_t *>(dst), n);
   return cudaGetLastError();
 }
 

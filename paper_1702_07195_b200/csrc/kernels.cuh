@@ -235,6 +235,8 @@ cudaError_t launch_sw32(int grid, const SW32Params &p, cudaStream_t st);
 // 16-bit column words (host image, streamed chunks) -> the pass kernel's
 // 32-bit words: out[i] = in[i] for i < n.
 cudaError_t launch_expand_columns(const uint16_t *in, int64_t n, uint32_t *out, cudaStream_t st);
+// bytes (rounded up to 4) from a pinned, mapped host buffer (its device pointer) to device memory
+cudaError_t launch_stage_copy(const void *host_src_dev, void *dst, size_t bytes, cudaStream_t st);
 
 
 // Sorting stage.
