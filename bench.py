@@ -513,6 +513,20 @@ def run_ours(args):
         roof["frac_measured_ipipe"] = round(achieved / (nsm * f_max * 1e6 * ALU_LANE_OPS_PER_CLK_PER_SM / ipipe / 1e9), 4)
         roof["ipipe_alu_per_cell"] = ipipe
     roof["frac_vs_2.75_dpx_per_cell"] = round(achieved / (nsm * f_max * 1e6 * ALU_LANE_OPS_PER_CLK_PER_SM / 2.75 / 1e9), 4)
+    # HBM as the non-binding limit (north_star): algorithmic bytes per launch
+    # (one pass over the shard: 1 B per residue + 4 B per score)
+    # and the ncu DRAM traffic of the same launch against the measured copy bandwidth
+    alg_bytes = int(local_res + 4 * w.db.count)
+    hbm_peak = float(peaks.get("hbm_gbs", 0.0)) or None
+    # the committed capture is of the default workload on one GPU
+    tr = roof["traffic"] if (args.config == CONFIG_INDEX and world == 1 and args.scale == 1.0) else None
+    roof["hbm"] = {"algorithmic_bytes": alg_bytes,
+                   "algorithmic_GBps": round(alg_bytes / (kms * 1e6), 1),
+                   "traffic_GBps": round(tr / (kms * 1e6), 1) if tr else None,
+                   "peak_GBps": hbm_peak,
+                   "frac": round(tr / (kms * 1e6) / hbm_peak, 4) if (tr and hbm_peak) else None,
+                   "traffic_over_algorithmic": round(tr / alg_bytes, 2) if tr else None,
+                   "traffic_is": "ncu dram bytes of the default workload's pass-kernel launch (profiles/ncu_summary.json)"}
 
     clk_all = None
     if dist:

@@ -25,6 +25,10 @@ def test_bench_line_small():
               "clocks", "gpu_launches", "config"):
         assert k in d
     assert d["value"] > 0 and d["roofline"]["bound"] == "alu" and d["gpu_launches"] > 0
+    # HBM as the non-binding limit: algorithmic bytes always, the committed ncu
+    # traffic only for the default full-size workload (not this scaled one)
+    hbm = d["roofline"]["hbm"]
+    assert hbm["algorithmic_bytes"] > 0 and hbm["algorithmic_GBps"] > 0 and hbm["traffic_GBps"] is None
 
 
 def test_bench_nccl_gather_path_world1():
