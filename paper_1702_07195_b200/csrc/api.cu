@@ -475,7 +475,7 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
   // wavefront runs the query passes of an item on several groups at once.
   // Auto rule, from a tile sweep on databases of 10-4,000 items of 1-35 k
   // residues (profiles/r01b_wavefront_tiles.jsonl): below half as many items
-  // as 32-lane groups, 32x8 tiles when the query makes >= 8 passes of them and
+  // as 32-lane groups, 32x8 tiles when the query makes >= 4 passes of them and
   // the units (items x passes) do not overfill the groups 1.5 times, else 32x16
   // tiles when their units exceed half the groups.  Forced mode (1) uses the
   // forced or chosen tile when it has a wavefront kernel, else 32x16 / 32x8.
@@ -491,7 +491,10 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     } else if (!g.force_G && t8 >= 0 && t16 >= 0 && tile_has_wave(t8) && tile_has_wave(t16)) {
       const double groups32 = (double)g.num_sms * std::max(1, tile_ctas_per_sm(t8)) * 512.0 / 32.0;
       if (items < 0.5 * groups32) {
-        if (passes_of(t8) >= 8 && items * passes_of(t8) <= 1.5 * groups32) tw = t8;
+        // >= 4 passes since the last session of round 2 (tools/wave_small.py, 1-100
+        // items of 20-35 k residues: m = 1000 runs 1.3-1.7x faster as 4 chained
+        // 32x8 passes than as one 32x32 pass; 2-3 passes are slower or mixed)
+        if (passes_of(t8) >= 4 && items * passes_of(t8) <= 1.5 * groups32) tw = t8;
         else if (passes_of(t16) >= 2 && items * passes_of(t16) > 0.5 * groups32) tw = t16;
       }
     }
