@@ -339,8 +339,11 @@ int sw_set_latency_mode(int32_t mode);
  * a resident database: one launch runs every query pass, an
  * item's pass p trailing its pass p-1 through the boundary buffer, so several
  * lane groups work on one long sequence at once (intra-task parallelism,
- * PAPER.md:32).  mode 0 (default): used when a pass has fewer work items than
- * lane groups; 1: always (when the query needs more than one pass); -1: never.
+ * PAPER.md:32).  mode 0 (default): used when a pass has fewer than half as many
+ * work items as lane groups and the query makes at least 4 passes of the 32x8
+ * tile (or 2 of the 32x16 tile with enough units); with few units only as many
+ * lane groups per CTA claim as spreads them over all SMs; 1: always (when the
+ * query needs more than one pass); -1: never.
  * In wavefront mode flagged sequences are re-scored in 32 bit from row 0.
  * Returns SW_OK or SW_EINVAL.
  */

@@ -749,7 +749,20 @@ int search_core(const uint8_t *q, int32_t m, const uint8_t *q2, int32_t m2, cons
     CUDA_TRY(pass_event(pev0 + 1));
     CUDA_TRY(cudaEventRecord(pev[pev0], st));
     // every CTA must be resident: a wavefront CTA may wait on another's progress
-    CUDA_TRY(launch_sw16_pass(ti, g.num_sms * tile_wave_ctas_per_sm(ti), p, st));
+    const int wgrid = g.num_sms * tile_wave_ctas_per_sm(ti);
+    {
+      // few units: spread them, at most ceil(units / CTAs) groups per CTA claim
+      // (all units are still claimed at once: the limit times the grid covers them)
+      const int64_t units = (int64_t)std::max(1, I.num_items) * P;
+      const int64_t lim = (units + wgrid - 1) / wgrid;
+      // measured (tools/wave_small.py, 1-100 items of 20-35 k residues): up to 4
+      // groups per CTA the spread is 1.2-1.3x faster (100 items x 4 passes 12.9 ->
+      // 10.4 ms, 10-30 items 10.9 -> 8.3-8.5), at 6 (100 items x 8 passes) slower
+      // (13.3 -> 15.8 ms), so it is used up to 4
+      p.group_limit = (lim <= 4 && lim < 512 / T.G) ? (int)lim : 0;
+      if (const char *e = std::getenv("SWDB_WAVE_SPREAD")) if (e[0] == '0') p.group_limit = 0;
+    }
+    CUDA_TRY(launch_sw16_pass(ti, wgrid, p, st));
     CUDA_TRY(cudaEventRecord(pev[pev0 + 1], st));
     g.npev = pev0 / 2 + 1;
     g.hnpev[g.hslot] = g.npev;

@@ -448,6 +448,9 @@ __global__ void __launch_bounds__(NT, 1) sw16_pass_kernel(const SW16Params p) {
           } else {
             it = solo_idle ? INT_MAX : atomicAdd(counter, 1);
           }
+        } else if (WAVE && p.group_limit > 0 &&
+                   (int)(threadIdx.x >> 5) + (NT / 32) * (int)((threadIdx.x & 31) / G) >= p.group_limit) {
+          it = INT_MAX;   // this group sits the launch out (few units: one or two per SM)
         } else {
           it = atomicAdd(counter, 1);
         }

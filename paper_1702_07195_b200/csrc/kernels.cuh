@@ -98,6 +98,11 @@ struct SW16Params {
   // partner's first item is one of them claims nothing (null: off).
   int *solo_counter;
   int solo_end;
+  // Wavefront launches with fewer units (items x passes) than lane groups: only
+  // the first group_limit groups of a CTA (counted across its warps first)
+  // claim, so the units spread over all SMs instead of filling the CTAs that
+  // reach the cursor first (0: every group claims).
+  int group_limit;
 };
 
 // Rows mode (long database sequences along the rows, kernels.cu).
