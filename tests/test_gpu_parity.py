@@ -571,6 +571,41 @@ def test_shard_count_invariance_sequential_shards():
         assert mi.tolist() == eidx.tolist() and ms.tolist() == esc.tolist(), G
 
 
+def test_wavefront_auto_from_four_passes_and_spread_units(monkeypatch):
+    """Few long work items: auto mode takes the 32x8 cross-pass wavefront from 4
+    passes on (m >= 769) and keeps the single pass below; with few units only
+    ceil(units / CTAs) <= 4 lane groups per CTA claim (the units spread over the
+    SMs; SWDB_WAVE_SPREAD=0 lets every group claim).  Scores equal the oracle's
+    either way, from 1 item (every CTA but a few sits the launch out) to more
+    items than the limit covers, with saturating sequences re-scored in 32 bit."""
+    rng = np.random.default_rng(4242)
+    cases = [[si.rr_residues(rng, 9000)],
+             [si.rr_residues(rng, int(L)) for L in rng.integers(2000, 7000, 7)] + [encode("W" * 3300)] * 2,
+             [si.rr_residues(rng, int(L)) for L in rng.integers(600, 1500, 900)]]
+    queries = [si.rr_residues(rng, 600), si.rr_residues(rng, 1000), encode("W" * 3100 + "A" * 20)]
+    try:
+        sw.sw_set_tile(0)
+        sw.sw_set_wave(0)
+        for ci, seqs in enumerate(cases):
+            db = _db(seqs)
+            sw.sw_db_load(db.residues, db.offsets)
+            for q in queries:
+                exp = oracle.batch(q, db.residues, db.offsets, BLOSUM62, 10, 2)
+                for spread in ("1", "0"):
+                    monkeypatch.setenv("SWDB_WAVE_SPREAD", spread)
+                    got = sw.sw_search(q, BLOSUM62, 10, 2)
+                    st = sw.sw_last_stats()
+                    assert (got == exp).all(), (ci, len(q), spread, st, np.nonzero(got != exp)[0][:5])
+                    if len(q) < 769:
+                        assert st["wave"] == 0, (ci, len(q), st)
+                    elif ci < 2:
+                        assert st["wave"] == 1 and (st["G"], st["R"]) == (32, 8), (ci, len(q), st)
+    finally:
+        monkeypatch.delenv("SWDB_WAVE_SPREAD", raising=False)
+        sw.sw_set_tile(0)
+        sw.sw_set_wave(0)
+
+
 def test_cross_pass_wavefront_matches_oracle():
     """The cross-pass wavefront (one launch runs every query pass; an item's
     pass p trails pass p-1 through the boundary buffer and the score chain,
